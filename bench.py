@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native SlabLU engine on BASELINE.json's metric.
+
+metric: factorization DOF/s (N / T_factor) of the dense SlabLU path on
+configs[2] = 4000x4000 variable-coefficient (bump) Helmholtz, b = 150,
+kappa = kappa_from_ppw(10, 4000) (N = 16M), plus solve ms/RHS.
+
+A "step" is one factorization of that operator.  `value` is timed on the
+device (CUDA events inside the engine, CSR already resident in HBM);
+`e2e` times the public host API (pinned host CSR -> factorize -> solve one
+RHS -> host solution).  Inputs and factors (~100 GB) exceed the 126 MB L2,
+so no L2 flush is needed between steps.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config cfg3]
+
+--impl reference times the reference's CPU path (the oracle port, all host
+threads) on a bounded sample of the same workload and prints the same JSON
+line with "impl": "reference".
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (kind, n1, n2, b, ppw or None for poisson, description)
+    "cfg1": (0, 255, 255, 31, None, "5-point FD Poisson 255x255, b=31"),
+    "cfg2": (1, 1000, 1000, 60, 10.0, "5-point FD Helmholtz 1000x1000, 10 ppw, b=60 (dense)"),
+    "cfg3": (2, 4000, 4000, 150, 10.0, "5-point FD bump Helmholtz 4000x4000 (N=16M), 10 ppw, b=150 (dense)"),
+    "cfg4": (1, 2000, 2000, 100, 10.0, "5-point FD Helmholtz 2000x2000 (rectangle stand-in), 10 ppw, b=100, 64 RHS"),
+}
+FP64_PEAK_TFLOPS = 37.067  # measured DMMA peak on this pool's B200 (profiles/fp64_peak_r01.json)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def geometry(n1, n2, b):
+    """Strip widths and interface count exactly as partition.hpp:70-91."""
+    ints, col, t, nifc = [], 0, 1, 0
+    while col < n1:
+        ifc = t * (b + 1) - 1
+        stop = min(ifc, n1)
+        if stop > col:
+            ints.append(stop - col)
+        col = stop
+        if col == ifc and col < n1:
+            nifc += 1
+            col += 1
+        t += 1
+    return ints, nifc
+
+
+def algorithmic_flops(n1, n2, b):
+    """F_factor = sum 2 w^3 n2 + sum 3 c w^2 n2^2 + ((k-1) 14/3 + 2/3) n2^3."""
+    widths, k = geometry(n1, n2, b)
+    band = sum(2.0 * w ** 3 * n2 for w in widths)
+    schur = 0.0
+    for s, w in enumerate(widths):
+        c = (1 if s > 0 else 0) + (1 if s < k else 0)
+        schur += 3.0 * c * w * w * n2 * n2
+    sweep = ((k - 1) * 14.0 / 3.0 + 2.0 / 3.0) * n2 ** 3
+    return band, schur, sweep
+
+
+def solve_bytes(n1, n2, b, nrhs):
+    widths, k = geometry(n1, n2, b)
+    band = sum((3 * w + 1) * w * n2 for w in widths)
+    return 8.0 * (2 * band + (4 * k - 3) * n2 * n2) + nrhs * 8.0 * 3 * n1 * n2
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self):
+        self.rows, self.proc = [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200", "-i", os.environ.get("LOCAL_RANK", "0")],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sms.append(float(r[1]))
+                mx = float(r[2])
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": float(np.median(sms)) if sms else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def problem(cfg):
+    import paper_2211_07572_b200 as S
+    kind, n1, n2, b, ppw, _ = CONFIGS[cfg]
+    kappa = 0.0 if ppw is None else S.kappa_from_ppw(ppw, n2)
+    spec = (S.poisson_log_problem(n1, n2) if kind == 0 else
+            S.helmholtz_problem(n1, n2, kappa) if kind == 1 else S.helmholtz_bump_problem(n1, n2, kappa))
+    return spec, kappa
+
+
+def cpu_sample(cfg, threads, budget_s=20.0):
+    """Bounded CPU-baseline sample of the reference path (oracle port), extrapolated to T_factor."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    kind, n1, n2, b, ppw, _ = CONFIGS[cfg]
+    kappa = 0.0 if ppw is None else O.kappa_from_ppw(ppw, n2)
+    O.set_blas_threads(threads)
+    sysm = O.assemble_canned(kind, n1, n2, kappa)
+    widths, k = geometry(n1, n2, b)
+    full = max(range(len(widths)), key=lambda s: widths[s] if 0 < s < k else -1)
+    nrhs = 8
+    t_trf, t_trs = O.time_slab_sample(sysm, b, full, nrhs)
+    while t_trs < 0.5 and nrhs < n2:  # grow the RHS sample to a measurable size
+        nrhs = min(n2, nrhs * 4)
+        t_trf, t_trs = O.time_slab_sample(sysm, b, full, nrhs)
+    per_col = t_trs / nrhs
+    w_full = widths[full]
+    t1 = 0.0
+    for s, w in enumerate(widths):
+        calls = (2 if (s > 0 and s < k) else 1) + (2 if (s > 0 and s < k) else 0)  # build_reduced dgbtrs calls
+        scale = (w / w_full)
+        t1 += t_trf * scale + calls * n2 * per_col * scale  # band ops ~ n w^2, per column ~ n w
+    t_step = O.time_sweep_step(n2) if k > 1 else 0.0
+    t2 = max(k - 1, 0) * t_step + (t_step / 4.0 if k > 0 else 0.0)
+    T = t1 + t2
+    return {"T_factor_s": T, "dof_s": n1 * n2 / T, "sample": (
+        f"oracle port (OpenBLAS {threads} threads): one full strip (w={w_full}) dgbtrf + dgbtrs with {nrhs} of "
+        f"{n2} identity RHS, and one stage-two step at n2={n2}; extrapolated over {len(widths)} strips "
+        f"x build_reduced call counts and {k - 1} sweep steps"), "t_trf": t_trf, "t_trs_per_rhs": per_col,
+        "t_sweep_step": t_step}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    kind, n1, n2, b, ppw, desc = CONFIGS[args.config]
+    vals = []
+    t0 = time.perf_counter()
+    for step in range(args.warmup + args.steps):
+        r = cpu_sample(args.config, threads)
+        if step >= args.warmup:
+            vals.append(r["dof_s"])
+        if time.perf_counter() - t0 > 240:
+            break
+    v = float(np.median(vals)) if vals else r["dof_s"]
+    line = {"metric": "factorization DOF/s (dense SlabLU, N=16M FD bump Helmholtz)" if args.config == "cfg3" else
+            f"factorization DOF/s ({desc})", "value": v, "unit": "DOF/s", "n_gpus": args.gpus, "steps": len(vals),
+            "warmup": args.warmup, "ms_per_step": n1 * n2 / v * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic canned problem)",
+            "config": {"workload": desc, "n1": n1, "n2": n2, "b": b, "N": n1 * n2}, "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "DOF/s", "cores": threads, "kind": "port", "sample": r["sample"]},
+            "e2e": {"value": v, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import paper_2211_07572_b200 as S
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    kind, n1, n2, b, ppw, desc = CONFIGS[args.config]
+    spec, kappa = problem(args.config)
+    t_asm = time.perf_counter()
+    sysm = S.assemble_fd5(spec)
+    log(f"[bench] assembled {desc}: N={sysm.dim()}, nnz={len(sysm.values)} in {time.perf_counter() - t_asm:.1f}s")
+    N = sysm.dim()
+    cfgS = S.SolverConfig(b=b, compression=S.CompressionChoice.dense, device=local)
+    dev = torch.device("cuda", local)
+    d_rp = torch.from_numpy(sysm.row_ptr).to(dev)
+    d_ci = torch.from_numpy(sysm.col_idx).to(dev)
+    d_v = torch.from_numpy(sysm.values).to(dev)
+    # pinned host inputs for the end-to-end leg
+    h_rp = torch.from_numpy(sysm.row_ptr).pin_memory()
+    h_ci = torch.from_numpy(sysm.col_idx).pin_memory()
+    h_v = torch.from_numpy(sysm.values).pin_memory()
+    h_f = torch.from_numpy(sysm.rhs).pin_memory()
+    h_u = torch.empty(N, dtype=torch.float64).pin_memory()
+    sysp = S.SparseSystem(h_rp.numpy(), h_ci.numpy(), h_v.numpy(), h_f.numpy(), n1, n2, sysm.h)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    for w in range(args.warmup):
+        f = S.factorize_device(n1, n2, d_rp, d_ci, d_v, cfgS)
+        log(f"[bench] warmup {w}: T_factor {f.t_stage1 + f.t_stage2:.3f}s (chain {f.stats.t_chain:.3f}, "
+            f"schur {f.stats.t_schur:.3f}, asm {f.stats.t_assemble:.3f}, stage2 {f.t_stage2:.3f})")
+        f.close()
+    clocks = ClockSampler()
+    clocks.start()
+    barrier()
+    t_fac, t_schur, t_chain, t_st2, launches = [], [], [], [], []
+    wall0 = time.perf_counter()
+    fact = None
+    for s in range(args.steps):
+        if fact is not None:
+            fact.close()
+        fact = S.factorize_device(n1, n2, d_rp, d_ci, d_v, cfgS)
+        t_fac.append(fact.t_stage1 + fact.t_stage2)
+        t_schur.append(fact.stats.t_schur)
+        t_chain.append(fact.stats.t_chain)
+        t_st2.append(fact.t_stage2)
+        launches.append(fact.stats.gpu_launches)
+    barrier()
+    wall = time.perf_counter() - wall0
+    # solve: 1 RHS (device-resident), then a 64-RHS block for ms/RHS
+    d_f = torch.from_numpy(sysm.rhs).to(dev).reshape(1, N)
+    d_u = torch.empty_like(d_f)
+    S.solve_device(fact, d_f, d_u)
+    st = fact.refresh_stats()
+    t_solve1 = st.t_solve_last
+    t_solve1_strips = st.t_solve_strips
+    nrhs = 64 if args.config in ("cfg4", "cfg2", "cfg1") else 8
+    d_F = torch.randn(nrhs, N, dtype=torch.float64, device=dev)
+    d_U = torch.empty_like(d_F)
+    S.solve_device(fact, d_F, d_U)
+    st = fact.refresh_stats()
+    t_solveB = st.t_solve_last
+    clk = clocks.stop()
+    # parity of this run (size-independent): residual of the 1-RHS solve
+    u = d_u.reshape(N).cpu().numpy()
+    res = float(np.linalg.norm(sysm.matvec(u) - sysm.rhs) / np.linalg.norm(sysm.rhs))
+    fact.close()
+    # end-to-end leg: pinned host CSR -> factorize -> solve -> host u
+    t_e2e = []
+    for s in range(max(1, min(args.steps, 2))):
+        barrier()
+        t0 = time.perf_counter()
+        fe = S.factorize(sysp, cfgS)
+        u_h = S.solve(fe, h_f.numpy())
+        h_u.numpy()[:] = u_h[:, 0]
+        barrier()
+        t_e2e.append(time.perf_counter() - t0)
+        fe.close()
+    h2d = sysm.row_ptr.nbytes + sysm.col_idx.nbytes + sysm.values.nbytes + sysm.rhs.nbytes
+    d2h = N * 8
+    T = float(np.mean(t_fac))
+    if dist is not None:
+        tt = torch.tensor([T, float(np.mean(t_e2e))], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        T, te = float(tt[0]), float(tt[1])
+    else:
+        te = float(np.mean(t_e2e))
+    band, schur, sweep = algorithmic_flops(n1, n2, b)
+    T_schur = float(np.mean(t_schur))
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            cpu = cpu_sample(args.config, os.cpu_count() or 1)
+        except Exception as e:  # reported, not fatal
+            log(f"[bench] cpu baseline failed: {e}")
+    if rank != 0:
+        return
+    line = {
+        "metric": "factorization DOF/s (dense SlabLU, N=16M FD bump Helmholtz)" if args.config == "cfg3"
+        else f"factorization DOF/s ({desc})",
+        "value": world * N / T, "unit": "DOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": T * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (deterministic canned problem, inputs resident in HBM; factors > L2 so no flush needed)",
+        "config": {"workload": desc, "n1": n1, "n2": n2, "b": b, "kappa": kappa, "N": N,
+                   "parallelism": "replicas" if world > 1 else "single-gpu", "l2": "inputs+factors >> 126 MB L2"},
+        "T_factor_s": T, "T_stage1_s": T - float(np.mean(t_st2)), "T_stage2_s": float(np.mean(t_st2)),
+        "phases_s": {"chain": float(np.mean(t_chain)), "schur": T_schur},
+        "solve_ms_per_rhs": t_solve1 * 1e3, "solve_ms_per_rhs_batched": t_solveB / nrhs * 1e3, "solve_batch": nrhs,
+        "solve_strip_sweeps_ms": t_solve1_strips * 1e3,
+        "relerr_res": res,
+        "gpu_launches": int(np.mean(launches)),
+        "e2e": {"value": world * N / te, "unit": "DOF/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h,
+                "seconds": te},
+        "roofline": {"bound": "tensor", "kernel": "schur_kernel (slab Schur sweeps)",
+                     "achieved": schur / T_schur / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": schur / T_schur / 1e12 / FP64_PEAK_TFLOPS, "traffic": None,
+                     "peak_source": "FP64 DMMA measured on this pool (profiles/fp64_peak_r01.json); "
+                                    "MEASURED_PEAKS.json has no FP64 entry",
+                     "factor_frac": (band + schur + sweep) / T / 1e12 / FP64_PEAK_TFLOPS,
+                     "solve_frac_of_hbm": solve_bytes(n1, n2, b, 1) / t_solve1 / 1e9 / 6553.3},
+        "clocks": clk, "wall_s": wall,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = {"value": cpu["dof_s"], "unit": "DOF/s", "cores": os.cpu_count(), "kind": "port",
+                                "sample": cpu["sample"], "T_factor_s": cpu["T_factor_s"]}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,149 @@
+/*
+ * slablu_gpu.h — C ABI of the B200-native SlabLU engine (libslablu_gpu.so).
+ *
+ * Drop-in boundary for the reference's dense-mode factorize/solve path
+ * (arxiv/paper_2211_07572, /root/reference/proj/include/slablu/):
+ *
+ *   slablu_gpu_assemble_fd5*   <- assemble_fd5            (problem.hpp:78-132)
+ *   slablu_gpu_choose_b        <- choose_b                (driver.hpp:55-66)
+ *   slablu_gpu_partition       <- partition               (partition.hpp:70-91)
+ *   slablu_gpu_factorize       <- factorize               (driver.hpp:115-167)
+ *   slablu_gpu_solve           <- solve                   (driver.hpp:171-179)
+ *   slablu_gpu_stats           <- Factorization fields    (driver.hpp:72-87)
+ *   slablu_gpu_T_block         <- ReducedSystem blocks    (stage_one.hpp:303-338, staged parity)
+ *   slablu_gpu_reduce_rhs      <- reduce_rhs              (stage_one.hpp:415-433, staged parity)
+ *   slablu_gpu_destroy         <- ~Factorization
+ *
+ * Conventions (mirroring the reference):
+ *   - matrices are column major; the operator is the reference's CSR
+ *     (Eigen RowMajor compressed: int32 row_ptr[n+1], int32 col_idx[nnz],
+ *     double val[nnz]), unknown (i, j) at index i*n2 + j.
+ *   - errors are returned as a status; code SLABLU_ERR_CONFIG maps to
+ *     ConfigError, SLABLU_ERR_SINGULAR to SingularMatrixError(index), every
+ *     other nonzero code to Error (common.hpp:32-60).
+ *   - a factorization is immutable after slablu_gpu_factorize and owns all of
+ *     its device memory; solves are const and may be issued repeatedly.
+ *   - there is no CPU fallback: without a usable CUDA device every compute
+ *     entry point returns SLABLU_ERR_CUDA.
+ */
+#ifndef SLABLU_GPU_H
+#define SLABLU_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SLABLU_OK = 0,
+  SLABLU_ERR_GENERIC = 1,     /* Error */
+  SLABLU_ERR_CONFIG = 2,      /* ConfigError */
+  SLABLU_ERR_SINGULAR = 3,    /* SingularMatrixError; index = strip or block */
+  SLABLU_ERR_CUDA = 4,        /* CUDA runtime failure or no device */
+  SLABLU_ERR_OOM = 5,         /* device memory exhausted */
+  SLABLU_ERR_UNSUPPORTED = 6  /* valid input outside the engine's envelope */
+};
+
+/* SolverConfig (driver.hpp:41-50). compression: 0 automatic, 1 dense, 2 hbs.
+ * The engine implements the dense path; automatic resolves to dense and hbs
+ * is rejected with SLABLU_ERR_UNSUPPORTED. */
+typedef struct {
+  int64_t b;          /* explicit slab width; 0 derives it from c */
+  double c;           /* b ~ c * n2^(2/3), c in (0, 2] */
+  int compression;
+  uint64_t seed;
+  int threads;        /* accepted, unused (as in the reference) */
+  int device;         /* CUDA device ordinal */
+  int keep_T;         /* keep a copy of the reduced blocks for slablu_gpu_T_block */
+} slablu_gpu_config;
+
+typedef struct {
+  int code;
+  int64_t index;
+  char msg[256];
+} slablu_gpu_status;
+
+typedef struct {
+  int64_t n1, n2, b;
+  int64_t interfaces;     /* k */
+  int64_t strips;
+  int64_t padded_width;   /* Wp */
+  int single_slab;        /* degenerate whole-grid path */
+  int symmetric_strips;   /* strips that took the symmetric Schur shortcut */
+  double t_stage1;        /* seconds, device time (CUDA events) */
+  double t_stage2;
+  int64_t storage_stage1; /* reference-equivalent scalars (driver.hpp:153-159) */
+  int64_t storage_stage2; /* (stage_two.hpp:191-198) */
+  int64_t device_bytes;   /* bytes held by the factorization */
+  int64_t gpu_launches;   /* kernels launched by the last factorize */
+  int64_t solve_launches; /* kernels launched by the last solve */
+  double t_chain;         /* stage one: block band LU of all slabs (s, CUDA events) */
+  double t_schur;         /* stage one: Schur sweep kernel (s, CUDA events) */
+  double t_assemble;      /* stage one: T assembly + validation (s) */
+  double t_solve_last;    /* device time of the last solve (s) */
+  double t_solve_strips;  /* ... of which the two slab sweeps (reduce + recover) */
+} slablu_gpu_stats_t;
+
+typedef struct slablu_gpu_fact slablu_gpu_fact;
+
+/* ---- problem assembly (host) ------------------------------------------- */
+typedef double (*slablu_field_fn)(double x, double y, void* user);
+/* Generic ProblemSpec: coefficient b(x), Dirichlet data g, body load f. Fills
+ * caller buffers row_ptr[n+1], col_idx[5n], val[5n], rhs[n]; *nnz receives
+ * the entry count. */
+slablu_gpu_status slablu_gpu_assemble_fd5(int64_t n1, int64_t n2, double h, double kappa,
+                                          slablu_field_fn coefficient, slablu_field_fn dirichlet,
+                                          slablu_field_fn load, void* user, int32_t* row_ptr,
+                                          int32_t* col_idx, double* val, double* rhs,
+                                          int64_t* nnz);
+/* Canned problems (problem.hpp:210-261): 0 poisson_log, 1 helmholtz, 2 helmholtz_bump. */
+slablu_gpu_status slablu_gpu_assemble_canned(int kind, int64_t n1, int64_t n2, double kappa,
+                                             int32_t* row_ptr, int32_t* col_idx, double* val,
+                                             double* rhs, int64_t* nnz);
+/* Manufactured solution of a canned problem sampled on the grid (problem.hpp:199-206). */
+slablu_gpu_status slablu_gpu_sample_solution(int kind, int64_t n1, int64_t n2, double kappa,
+                                             double* out);
+double slablu_gpu_kappa_from_ppw(double ppw, int64_t n2);
+double slablu_gpu_bessel_j0(double t);
+/* gaussian_matrix (common.hpp:72-79): mt19937_64(seed) + normal_distribution. */
+void slablu_gpu_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out);
+
+/* ---- geometry ---------------------------------------------------------------- */
+slablu_gpu_status slablu_gpu_choose_b(int64_t n1, int64_t n2, int64_t b, double c, int64_t* out);
+/* interior/interface strips as (first_col, width) pairs; cap = pairs available. */
+slablu_gpu_status slablu_gpu_partition(int64_t n1, int64_t n2, int64_t b, int64_t* n_interiors,
+                                       int64_t* interiors, int64_t* n_interfaces,
+                                       int64_t* interfaces, int64_t cap);
+
+/* ---- factorize / solve ------------------------------------------------------ */
+/* Host CSR. */
+slablu_gpu_status slablu_gpu_factorize(int64_t n1, int64_t n2, const int32_t* row_ptr,
+                                       const int32_t* col_idx, const double* val,
+                                       const slablu_gpu_config* config, slablu_gpu_fact** out);
+/* Device-resident CSR (pointers into device memory of config->device). */
+slablu_gpu_status slablu_gpu_factorize_device(int64_t n1, int64_t n2, int64_t nnz,
+                                              const int32_t* d_row_ptr, const int32_t* d_col_idx,
+                                              const double* d_val, const slablu_gpu_config* config,
+                                              slablu_gpu_fact** out);
+/* u (n x nrhs, ld ldu) = A^{-1} f (n x nrhs, ld ldf); host buffers. */
+slablu_gpu_status slablu_gpu_solve(const slablu_gpu_fact* fact, const double* f, int64_t ldf,
+                                   int64_t nrhs, double* u, int64_t ldu);
+/* Same with device buffers; stream 0 of the factorization's device. */
+slablu_gpu_status slablu_gpu_solve_device(const slablu_gpu_fact* fact, const double* d_f,
+                                          int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu);
+slablu_gpu_status slablu_gpu_stats(const slablu_gpu_fact* fact, slablu_gpu_stats_t* out);
+/* Reduced block before stage two (needs config.keep_T): which 0 diag[j], 1 super[j], 2 sub[j]. */
+slablu_gpu_status slablu_gpu_T_block(const slablu_gpu_fact* fact, int which, int64_t j, double* out);
+/* Staged reduce_rhs: out (k*n2 x nrhs) from host f (n x nrhs, ld n). */
+slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* fact, const double* f, int64_t nrhs,
+                                        double* out);
+void slablu_gpu_destroy(slablu_gpu_fact* fact);
+
+/* Device count visible to the engine (0 when CUDA is unusable). */
+int slablu_gpu_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLABLU_GPU_H */

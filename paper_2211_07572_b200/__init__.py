@@ -1,0 +1,15 @@
+"""B200-native SlabLU engine (arXiv 2211.07572) — dense-mode factorize/solve.
+
+Drop-in for the reference's C++ solver API (assemble_fd5 -> factorize ->
+solve); compute runs in hand-written sm_100a kernels behind the C ABI in
+include/slablu_gpu.h (libslablu_gpu.so, built in-tree).
+"""
+from .slablu import (  # noqa: F401
+    CompressionChoice, ConfigError, Error, ErrorReport, Factorization, GridStrip, ProblemSpec,
+    SingularMatrixError, SlabPartition, SolverConfig, SparseSystem, UnsupportedError, assemble_fd5,
+    bessel_j0, choose_b, device_count, error_report, factorize, factorize_device, gaussian_matrix,
+    helmholtz_bump_problem, helmholtz_problem, kappa_from_ppw, partition, poisson_log_problem,
+    run_problem, sample_field, sample_solution, solve, solve_device, true_solution_helmholtz,
+    true_solution_poisson,
+)
+from ._lib import LIB_PATH, EXPORTS  # noqa: F401

@@ -1,0 +1,97 @@
+"""ctypes loader for libslablu_gpu.so (the engine's C ABI, include/slablu_gpu.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2211_07572_b200/csrc``).  There is no CPU fallback: if the
+library is missing the import fails loudly.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libslablu_gpu.so")
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+D = ctypes.c_double
+I = ctypes.c_int
+
+
+class Status(ctypes.Structure):
+    _fields_ = [("code", I), ("index", I64), ("msg", ctypes.c_char * 256)]
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("b", I64), ("c", D), ("compression", I), ("seed", ctypes.c_uint64),
+                ("threads", I), ("device", I), ("keep_T", I)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("n1", I64), ("n2", I64), ("b", I64), ("interfaces", I64), ("strips", I64),
+                ("padded_width", I64), ("single_slab", I), ("symmetric_strips", I),
+                ("t_stage1", D), ("t_stage2", D), ("storage_stage1", I64), ("storage_stage2", I64),
+                ("device_bytes", I64), ("gpu_launches", I64), ("solve_launches", I64),
+                ("t_chain", D), ("t_schur", D), ("t_assemble", D), ("t_solve_last", D),
+                ("t_solve_strips", D)]
+
+
+FIELD_FN = ctypes.CFUNCTYPE(D, D, D, P)
+
+# exported symbols of include/slablu_gpu.h (checked by tests/test_abi.py)
+EXPORTS = [
+    "slablu_gpu_assemble_fd5", "slablu_gpu_assemble_canned", "slablu_gpu_sample_solution",
+    "slablu_gpu_kappa_from_ppw", "slablu_gpu_bessel_j0", "slablu_gpu_gaussian_matrix",
+    "slablu_gpu_choose_b", "slablu_gpu_partition", "slablu_gpu_factorize",
+    "slablu_gpu_factorize_device", "slablu_gpu_solve", "slablu_gpu_solve_device",
+    "slablu_gpu_stats", "slablu_gpu_T_block", "slablu_gpu_reduce_rhs", "slablu_gpu_destroy",
+    "slablu_gpu_device_count",
+]
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the CUDA engine with __graft_entry__.build() "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    St = Status
+    L.slablu_gpu_assemble_fd5.restype = St
+    L.slablu_gpu_assemble_fd5.argtypes = [I64, I64, D, D, FIELD_FN, FIELD_FN, FIELD_FN, P, P, P, P, P, P]
+    L.slablu_gpu_assemble_canned.restype = St
+    L.slablu_gpu_assemble_canned.argtypes = [I, I64, I64, D, P, P, P, P, P]
+    L.slablu_gpu_sample_solution.restype = St
+    L.slablu_gpu_sample_solution.argtypes = [I, I64, I64, D, P]
+    L.slablu_gpu_kappa_from_ppw.restype = D
+    L.slablu_gpu_kappa_from_ppw.argtypes = [D, I64]
+    L.slablu_gpu_bessel_j0.restype = D
+    L.slablu_gpu_bessel_j0.argtypes = [D]
+    L.slablu_gpu_gaussian_matrix.restype = None
+    L.slablu_gpu_gaussian_matrix.argtypes = [I64, I64, ctypes.c_uint64, P]
+    L.slablu_gpu_choose_b.restype = St
+    L.slablu_gpu_choose_b.argtypes = [I64, I64, I64, D, P]
+    L.slablu_gpu_partition.restype = St
+    L.slablu_gpu_partition.argtypes = [I64, I64, I64, P, P, P, P, I64]
+    L.slablu_gpu_factorize.restype = St
+    L.slablu_gpu_factorize.argtypes = [I64, I64, P, P, P, P, P]
+    L.slablu_gpu_factorize_device.restype = St
+    L.slablu_gpu_factorize_device.argtypes = [I64, I64, I64, P, P, P, P, P]
+    L.slablu_gpu_solve.restype = St
+    L.slablu_gpu_solve.argtypes = [P, P, I64, I64, P, I64]
+    L.slablu_gpu_solve_device.restype = St
+    L.slablu_gpu_solve_device.argtypes = [P, P, I64, I64, P, I64]
+    L.slablu_gpu_stats.restype = St
+    L.slablu_gpu_stats.argtypes = [P, P]
+    L.slablu_gpu_T_block.restype = St
+    L.slablu_gpu_T_block.argtypes = [P, I, I64, P]
+    L.slablu_gpu_reduce_rhs.restype = St
+    L.slablu_gpu_reduce_rhs.argtypes = [P, P, I64, P]
+    L.slablu_gpu_destroy.restype = None
+    L.slablu_gpu_destroy.argtypes = [P]
+    L.slablu_gpu_device_count.restype = I
+    L.slablu_gpu_device_count.argtypes = []
+    _lib = L
+    return L

@@ -1,0 +1,59 @@
+// Shared device helpers for the SlabLU B200 engine (sm_100a).
+//
+// FP64 tensor math on sm_100a is the warp-level mma.sync f64 path, which
+// lowers to SASS DMMA.8x8x4 (tcgen05 has no f64 kind).  Everything here is
+// written for that pipe: m8n8k4 fragments, cp.async staging, padded shared
+// tiles (row stride == 4 mod 16 doubles so a fragment load is 2 wavefronts).
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define SLB_CUDA_CHECK(expr)                                                        \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess) throw ::slb::CudaFailure(_e, #expr, __FILE__, __LINE__); \
+  } while (0)
+
+namespace slb {
+
+struct CudaFailure {
+  cudaError_t err;
+  const char* expr;
+  const char* file;
+  int line;
+  CudaFailure(cudaError_t e, const char* x, const char* f, int l) : err(e), expr(x), file(f), line(l) {}
+};
+
+// D(8x8) += A(8x4) * B(4x8).  Fragments (lane = 4*g + t):
+//   a = A[g][t], b = B[t][g], d0/d1 = D[g][2t], D[g][2t+1].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 8-byte async copy global -> shared; zero-fills when !pred.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const int bytes = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes));
+}
+// 16-byte async copy (both addresses 16-byte aligned); zero-fills when !pred.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const int bytes = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+
+}  // namespace slb

@@ -1,0 +1,849 @@
+// Engine orchestration and the C ABI (include/slablu_gpu.h).
+//
+// factorize (proj/include/slablu/driver.hpp:115-167):
+//   stage one  = coupling/level extraction from the CSR, the level-by-level
+//                block band LU of every slab (band_lu.cu, all slabs batched),
+//                the Schur sweep (schur.cu) and T assembly;
+//   stage two  = sweeping block LU of the reduced block tridiagonal system
+//                (stage_two.hpp:131-150) with dense LU on the device
+//                (dense.cu); each S_j is kept as its explicit inverse so the
+//                stage-two solve is bandwidth-bound GEMV.
+// solve (driver.hpp:171-179): reduce_rhs -> sweep solve -> recover_interiors,
+// all on the device.
+#include <algorithm>
+#include <array>
+#include <memory>
+#include <atomic>
+#include <chrono>
+#include <climits>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "host.h"
+#include "kernels.h"
+
+namespace slb {
+
+std::atomic<int64_t> g_launches{0};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Exact-size caching device allocator (repeated factorizations of the same
+// problem reuse their buffers instead of paying cudaMalloc/cudaFree).
+struct DevPool {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> free_blocks;
+  size_t cached_bytes(int dev) {
+    std::lock_guard<std::mutex> g(mu);
+    size_t s = 0;
+    for (auto& kv : free_blocks)
+      if (kv.first.first == dev) s += kv.first.second;
+    return s;
+  }
+  void* get(int dev, size_t bytes) {
+    if (bytes == 0) return nullptr;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = free_blocks.find({dev, bytes});
+      if (it != free_blocks.end()) {
+        void* p = it->second;
+        free_blocks.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      trim(dev);
+      e = cudaMalloc(&p, bytes);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw HostError(SLABLU_ERR_OOM, "device memory exhausted (" + std::to_string(bytes >> 20) + " MiB)");
+      }
+    }
+    return p;
+  }
+  void put(int dev, size_t bytes, void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(mu);
+    free_blocks.insert({{dev, bytes}, p});
+  }
+  void trim(int dev) {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto it = free_blocks.begin(); it != free_blocks.end();) {
+      if (it->first.first == dev) {
+        cudaFree(it->second);
+        it = free_blocks.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+};
+DevPool& pool() {
+  static DevPool* p = new DevPool;  // never destroyed (process exit frees device memory)
+  return *p;
+}
+
+template <class T>
+struct DBuf {
+  int dev = 0;
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  void alloc(int d, size_t count) {
+    release();
+    dev = d;
+    n = count;
+    p = static_cast<T*>(pool().get(d, count * sizeof(T)));
+  }
+  void release() {
+    if (p) pool().put(dev, n * sizeof(T), p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+  ~DBuf() { release(); }
+};
+
+// ---------------------------------------------------------------------------
+__global__ void gather_ifc_kernel(const double* f, int64_t ldf, int64_t nrhs, int nifc, const int64_t* off,
+                                  int64_t n2, double* out, int64_t K) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= K * nrhs) return;
+  const int64_t c = idx / K, r = idx % K, j = r / n2, q = r % n2;
+  out[idx] = f[c * ldf + off[j] + q];
+}
+__global__ void scatter_ifc_kernel(const double* u_ifc, int64_t K, int64_t nrhs, const int64_t* off, int64_t n2,
+                                   double* u, int64_t ldu) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= K * nrhs) return;
+  const int64_t c = idx / K, r = idx % K, j = r / n2, q = r % n2;
+  u[c * ldu + off[j] + q] = u_ifc[idx];
+}
+// red_j = (f_j - contrib[strip j][R]) - contrib[strip j+1][L]  (stage_one.hpp:423-432 order)
+__global__ void combine_reduce_kernel(double* red, int64_t K, int64_t nrhs, int64_t n2, int nstrips,
+                                      const StripDesc* strips, const double* contrib) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= K * nrhs) return;
+  const int64_t c = idx / K, r = idx % K, j = r / n2, q = r % n2;
+  double v = red[idx];
+  if (j < nstrips && strips[j].right == j) v -= contrib[((int64_t)(j * 2 + 1) * nrhs + c) * n2 + q];
+  if (j + 1 < nstrips && strips[j + 1].left == j) v -= contrib[((int64_t)((j + 1) * 2 + 0) * nrhs + c) * n2 + q];
+  red[idx] = v;
+}
+__global__ void copy2d_kernel(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < rows * cols;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx % rows, c = idx / rows;
+    dst[c * ldd + r] = src[c * lds + r];
+  }
+}
+
+void copy2d(cudaStream_t st, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols) {
+  if (rows <= 0 || cols <= 0) return;
+  copy2d_kernel<<<(unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 8192), 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
+  SLB_CUDA_CHECK(cudaGetLastError());
+  g_launches++;
+}
+
+int sm_count(int dev) {
+  int v = 0;
+  SLB_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+  return v;
+}
+
+}  // namespace
+
+
+}  // namespace slb
+
+using namespace slb;
+
+struct slablu_gpu_fact {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n1 = 0, n2 = 0, N = 0, b = 0;
+  bool single = false;
+  int S = 0, K = 0, Wp = 0;
+  std::vector<StripDesc> strips_h;
+  std::vector<int64_t> ifc_off_h;
+  std::vector<int32_t> sym_h;
+  DBuf<StripDesc> strips;
+  DBuf<int64_t> ifc_off;
+  DBuf<double> fac;
+  DBuf<int32_t> perm;
+  DBuf<double> cpl;
+  DBuf<int32_t> sym;
+  DBuf<double> T;       // [diag k | super k-1 | sub k-1] blocks, n2 x n2; diag holds S_j^{-1}
+  DBuf<double> Tkeep;   // optional copy of the reduced blocks
+  DBuf<DevStatus> status;
+  int64_t sF = 0, sP = 0, sCPL = 0;
+  double t1 = 0, t2 = 0, t_chain = 0, t_schur = 0, t_asm = 0;
+  mutable double t_solve = 0, t_solve_strips = 0;
+  int64_t storage1 = 0, storage2 = 0;
+  int64_t launches_factor = 0;
+  mutable int64_t launches_solve = 0;
+  mutable std::mutex solve_mu;
+  double* Tdiag() const { return T.p; }
+  double* Tsup() const { return T.p + (size_t)K * n2 * n2; }
+  double* Tsub() const { return T.p + (size_t)(2 * K - 1) * n2 * n2; }
+  ~slablu_gpu_fact() {
+    if (stream) {
+      cudaSetDevice(device);
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+  }
+};
+
+namespace {
+
+void throw_status(const DevStatus& st) {
+  if (st.flags & ERR_OUT_OF_BAND) throw HostError(SLABLU_ERR_GENERIC, "BandedMatrix::at: index outside band");
+  if (st.flags & ERR_PAST_INTERFACE)
+    throw HostError(SLABLU_ERR_GENERIC, "factor_one_interior: interior couples past its adjacent interfaces");
+  if (st.flags & ERR_COUPLING_LEVEL)
+    throw HostError(SLABLU_ERR_UNSUPPORTED, "interior/interface coupling outside the five-point level structure");
+  if (st.flags & ERR_IFC_STRUCTURE)
+    throw HostError(SLABLU_ERR_UNSUPPORTED, "interface row couples outside its adjacent strips/interfaces");
+}
+
+int64_t cfg_device(const slablu_gpu_config* c) { return c ? c->device : 0; }
+
+// Factorize with the CSR already on the device.
+slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32_t* rp, const int32_t* ci,
+                                const double* v, const slablu_gpu_config* cfg) {
+  if (n1 * n2 == 0) throw HostError(SLABLU_ERR_CONFIG, "factorize: empty system");
+  slablu_gpu_config c{};
+  c.c = 0.6;
+  if (cfg) c = *cfg;
+  if (c.compression == 2)
+    throw HostError(SLABLU_ERR_UNSUPPORTED, "factorize: hbs compression is not implemented by the GPU engine");
+  const int64_t launches0 = g_launches.load();
+  auto F = std::make_unique<slablu_gpu_fact>();
+  F->device = c.device;
+  SLB_CUDA_CHECK(cudaSetDevice(c.device));
+  SLB_CUDA_CHECK(cudaStreamCreateWithFlags(&F->stream, cudaStreamNonBlocking));
+  cudaStream_t st = F->stream;
+  F->n1 = n1;
+  F->n2 = n2;
+  F->N = n1 * n2;
+  F->b = c.b > 0 ? c.b : choose_b(n1, n2, 0, c.c);
+  const int dev = c.device;
+
+  // geometry (driver.hpp:134-139: degenerate whole-grid path)
+  std::vector<GridStrip> ints;
+  std::vector<GridStrip> ifcs;
+  if (F->b > n1 - 2 || n1 < 3) {
+    F->single = true;
+    ints.push_back({0, n1});
+  } else {
+    Partition p = partition(n1, n2, F->b);
+    ints = p.interiors;
+    ifcs = p.interfaces;
+  }
+  F->S = (int)ints.size();
+  F->K = (int)ifcs.size();
+  int64_t wmax = 0;
+  for (auto& s : ints) wmax = std::max(wmax, s.width);
+  F->Wp = (int)round_up(wmax, 8);
+  if (F->Wp > 160)
+    throw HostError(SLABLU_ERR_UNSUPPORTED, "factorize: slab width " + std::to_string(wmax) + " exceeds the engine's 160-column envelope");
+  const int Wp = F->Wp, S = F->S, K = F->K;
+  for (int s = 0; s < S; s++) {
+    StripDesc d;
+    d.col0 = (int32_t)ints[s].first_col;
+    d.w = (int32_t)ints[s].width;
+    d.left = s > 0 ? s - 1 : -1;
+    d.right = s < K ? s : -1;
+    d.left_off = d.left >= 0 ? ifcs[d.left].first_col * n2 : -1;
+    d.right_off = d.right >= 0 ? ifcs[d.right].first_col * n2 : -1;
+    F->strips_h.push_back(d);
+  }
+  for (auto& f : ifcs) F->ifc_off_h.push_back(f.first_col * n2);
+
+  cudaEvent_t e0, e1, e2, ec, es;
+  SLB_CUDA_CHECK(cudaEventCreate(&e0));
+  SLB_CUDA_CHECK(cudaEventCreate(&e1));
+  SLB_CUDA_CHECK(cudaEventCreate(&e2));
+  SLB_CUDA_CHECK(cudaEventCreate(&ec));
+  SLB_CUDA_CHECK(cudaEventCreate(&es));
+  SLB_CUDA_CHECK(cudaEventRecord(e0, st));
+
+  F->strips.alloc(dev, S);
+  SLB_CUDA_CHECK(cudaMemcpyAsync(F->strips.p, F->strips_h.data(), S * sizeof(StripDesc), cudaMemcpyHostToDevice, st));
+  if (K > 0) {
+    F->ifc_off.alloc(dev, K);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(F->ifc_off.p, F->ifc_off_h.data(), K * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  }
+  F->status.alloc(dev, 1);
+  DevStatus st0{0, INT_MAX, INT_MAX, 0};
+  SLB_CUDA_CHECK(cudaMemcpyAsync(F->status.p, &st0, sizeof(DevStatus), cudaMemcpyHostToDevice, st));
+  CsrDev A{rp, ci, v, F->N};
+
+  // ---- stage one: couplings + level chain ---------------------------------------
+  const int64_t lvl = 4LL * Wp * Wp;
+  F->sF = n2 * lvl;
+  F->sP = n2 * 2 * Wp;
+  F->sCPL = 4 * n2 * Wp;
+  F->fac.alloc(dev, (size_t)S * F->sF);
+  F->perm.alloc(dev, (size_t)S * F->sP);
+  F->cpl.alloc(dev, (size_t)S * F->sCPL);
+  F->sym.alloc(dev, S);
+  {
+    std::vector<int32_t> ones(S, 1);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(F->sym.p, ones.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  }
+  extract_couplings(st, A, F->strips.p, S, n2, Wp, F->cpl.p, F->sCPL, F->sym.p, F->status.p);
+  g_launches++;
+
+  const int64_t LCH = std::min<int64_t>(n2, 64);
+  const int64_t sNX = LCH * 3 * Wp * Wp;
+  DBuf<double> nx, sv, scr, gath;
+  nx.alloc(dev, (size_t)S * sNX);
+  sv.alloc(dev, (size_t)2 * S * 2 * Wp * Wp);
+  scr.alloc(dev, (size_t)S * lvl);        // [Ainv | Fbot | H] col-major per strip
+  gath.alloc(dev, (size_t)S * 3 * Wp * Wp);  // [Bsel | R1]
+  const int64_t sSV = 2LL * Wp * Wp, sScr = lvl, sG3 = 3LL * Wp * Wp;
+  double* svb[2] = {sv.p, sv.p + (size_t)S * sSV};
+  extract_levels(st, A, F->strips.p, S, n2, Wp, 0, LCH, nx.p, sNX, F->status.p);
+  init_sv(st, S, Wp, nx.p, sNX, svb[0], sSV);
+  g_launches += 2;
+  int cur = 0;
+  for (int64_t l = 0; l < n2; l++) {
+    const int64_t nxt = l + 1;
+    const bool has_next = nxt < n2;
+    if (has_next && nxt % LCH == 0) {
+      extract_levels(st, A, F->strips.p, S, n2, Wp, nxt, std::min(LCH, n2 - nxt), nx.p, sNX, F->status.p);
+      g_launches++;
+    }
+    LevelArgs la;
+    la.Wp = Wp;
+    la.nstrips = S;
+    la.has_next = has_next;
+    la.sv_in = svb[cur];
+    la.sSV = sSV;
+    la.nx = has_next ? nx.p + (nxt % LCH) * 3 * Wp * Wp : nullptr;
+    la.sNX = sNX;
+    la.sv_out = svb[1 - cur];
+    la.ainv = scr.p;
+    la.sF = sScr;
+    la.perm = F->perm.p + l * 2 * Wp;
+    la.sP = F->sP;
+    la.bsel = gath.p;
+    la.r1 = gath.p + (size_t)Wp * Wp;
+    la.sScr = sG3;
+    la.status = F->status.p;
+    la.level = (int32_t)l;
+    level_panel(st, la);
+    g_launches++;
+    double* ainv = scr.p;
+    double* fbot = scr.p + (size_t)Wp * Wp;
+    double* hh = scr.p + (size_t)2 * Wp * Wp;
+    if (has_next) {
+      dgemm_batched(st, Wp, 2 * Wp, Wp, 1.0, ainv, Wp, sScr, la.r1, Wp, sG3, 0.0, hh, Wp, sScr, S);
+      dgemm_batched(st, Wp, Wp, Wp, -1.0, la.bsel, Wp, sG3, ainv, Wp, sScr, 0.0, fbot, Wp, sScr, S);
+      dgemm_batched(st, Wp, 2 * Wp, Wp, -1.0, la.bsel, Wp, sG3, hh, Wp, sScr, 1.0, svb[1 - cur], Wp, sSV, S);
+      g_launches += 3;
+    } else {
+      for (int s = 0; s < S; s++)
+        SLB_CUDA_CHECK(cudaMemsetAsync(fbot + s * sScr, 0, 3 * Wp * Wp * sizeof(double), st));
+    }
+    pack_level(st, S, Wp, ainv, fbot, hh, sScr, F->fac.p + l * lvl, F->sF);
+    g_launches++;
+    cur = 1 - cur;
+  }
+  SLB_CUDA_CHECK(cudaEventRecord(ec, st));
+  nx.release();
+  sv.release();
+  scr.release();
+  gath.release();
+  {
+    DevStatus hs;
+    SLB_CUDA_CHECK(cudaMemcpyAsync(&hs, F->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+    SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+    throw_status(hs);
+    if (hs.flags & ERR_SINGULAR) {
+      if (F->single) throw HostError(SLABLU_ERR_SINGULAR, "BandedLU: exactly singular pivot", hs.singular_strip);
+      throw HostError(SLABLU_ERR_SINGULAR, "factor_one_interior: singular slab interior", hs.singular_strip);
+    }
+    F->sym_h.resize(S);
+    SLB_CUDA_CHECK(cudaMemcpy(F->sym_h.data(), F->sym.p, S * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  }
+
+  if (!F->single) {
+    // ---- Schur sweep ----------------------------------------------------------------
+    std::vector<int32_t> tasks;
+    std::vector<std::array<int64_t, 4>> order;  // (-work, q0, strip, side)
+    for (int s = 0; s < S; s++)
+      for (int side = 0; side < 2; side++) {
+        if ((side == 0 ? F->strips_h[s].left : F->strips_h[s].right) < 0) continue;
+        for (int64_t q0 = 0; q0 < n2; q0 += kSweepChunk) {
+          const int64_t l0 = q0 > 0 ? q0 - 1 : 0;
+          const int64_t work = (n2 - l0) + (F->sym_h[s] ? n2 - q0 : n2);
+          order.push_back({-work, q0, s, side});
+        }
+      }
+    std::sort(order.begin(), order.end());
+    for (auto& o : order) {
+      tasks.push_back((int32_t)o[2]);
+      tasks.push_back((int32_t)o[3]);
+      tasks.push_back((int32_t)o[1]);
+    }
+    const int ntasks = (int)order.size();
+    DBuf<int32_t> dtasks, counter;
+    dtasks.alloc(dev, tasks.size());
+    counter.alloc(dev, 1);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    SLB_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
+    const int64_t sG = 4 * n2 * n2;
+    DBuf<double> gbuf, ybuf;
+    gbuf.alloc(dev, (size_t)S * sG);
+    SLB_CUDA_CHECK(cudaMemsetAsync(gbuf.p, 0, gbuf.bytes(), st));
+    const int64_t sY = n2 * Wp * kSweepChunk;
+    int nslots = std::min(sm_count(dev), ntasks);
+    {
+      size_t fr = 0, tot = 0;
+      SLB_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+      fr += pool().cached_bytes(dev);  // cached blocks are reusable (trimmed on demand)
+      const size_t reserve = (size_t)(3 * K) * n2 * n2 * sizeof(double) + (size_t)(4LL << 30);
+      const size_t per = (size_t)sY * sizeof(double);
+      if (fr > reserve) nslots = (int)std::max<int64_t>(1, std::min<int64_t>(nslots, (fr - reserve) / per));
+      else nslots = 1;
+    }
+    ybuf.alloc(dev, (size_t)nslots * sY);
+    SchurArgs sa{};
+    sa.Wp = Wp;
+    sa.n2 = n2;
+    sa.nstrips = S;
+    sa.strips = F->strips.p;
+    sa.fac = F->fac.p;
+    sa.sF = F->sF;
+    sa.perm = F->perm.p;
+    sa.sP = F->sP;
+    sa.cpl = F->cpl.p;
+    sa.sCPL = F->sCPL;
+    sa.sym = F->sym.p;
+    sa.gbuf = gbuf.p;
+    sa.sG = sG;
+    sa.ybuf = ybuf.p;
+    sa.sY = sY;
+    sa.task_counter = counter.p;
+    sa.ntasks = ntasks;
+    sa.tasks = dtasks.p;
+    sa.mode = SWEEP_SCHUR;
+    sweep(st, sa, nslots);
+    g_launches++;
+    SLB_CUDA_CHECK(cudaEventRecord(es, st));
+    ybuf.release();
+    // ---- T assembly --------------------------------------------------------------------
+    F->T.alloc(dev, (size_t)(3 * K - 2) * n2 * n2);
+    assemble_T(st, n2, K, S, F->strips.p, F->sym.p, gbuf.p, sG, F->Tdiag(), F->Tsup(), F->Tsub(), A,
+               F->ifc_off.p, F->status.p);
+    g_launches += 2;
+    check_finite(st, F->T.p, (int64_t)(3 * K - 2) * n2 * n2, F->status.p);
+    g_launches++;
+    if (c.keep_T) {
+      F->Tkeep.alloc(dev, F->T.n);
+      SLB_CUDA_CHECK(cudaMemcpyAsync(F->Tkeep.p, F->T.p, F->T.bytes(), cudaMemcpyDeviceToDevice, st));
+    }
+    gbuf.release();
+    SLB_CUDA_CHECK(cudaEventRecord(e1, st));
+
+    // ---- stage two: sweeping block LU (stage_two.hpp:131-150) --------------------------
+    const int64_t bs = n2 * n2;
+    DBuf<double> X, I;
+    DBuf<int32_t> ipiv;
+    X.alloc(dev, bs);
+    I.alloc(dev, bs);
+    ipiv.alloc(dev, n2);
+    for (int j = 0; j < K; j++) {
+      double* Sj = F->Tdiag() + j * bs;
+      if (j > 0) {
+        dgemm_batched(st, n2, n2, n2, 1.0, F->Tdiag() + (j - 1) * bs, n2, 0, F->Tsup() + (j - 1) * bs, n2, 0, 0.0,
+                      X.p, n2, 0, 1);
+        dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X.p, n2, 0, 1.0, Sj, n2, 0, 1);
+        g_launches += 2;
+      }
+      dgetrf(st, n2, Sj, ipiv.p, nullptr, F->status.p, j);
+      dset_identity(st, I.p, n2);
+      dgetrs(st, n2, n2, Sj, ipiv.p, I.p, n2, nullptr);
+      SLB_CUDA_CHECK(cudaMemcpyAsync(Sj, I.p, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      g_launches += 4;
+    }
+  } else {
+    SLB_CUDA_CHECK(cudaEventRecord(es, st));
+    SLB_CUDA_CHECK(cudaEventRecord(e1, st));
+  }
+  SLB_CUDA_CHECK(cudaEventRecord(e2, st));
+  SLB_CUDA_CHECK(cudaEventSynchronize(e2));
+  {
+    DevStatus hs;
+    SLB_CUDA_CHECK(cudaMemcpy(&hs, F->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost));
+    throw_status(hs);
+    if (hs.flags & ERR_NONFINITE) throw HostError(SLABLU_ERR_GENERIC, "BlockTridiagonal: non-finite block entry");
+    if (hs.flags & ERR_SINGULAR)
+      throw HostError(SLABLU_ERR_SINGULAR, "sweep_build: singular Schur complement block", hs.singular_block);
+  }
+  float ms1 = 0, ms2 = 0, msc = 0, mss = 0, msa = 0;
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&ms1, e0, e1));
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&ms2, e1, e2));
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&msc, e0, ec));
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&mss, ec, es));
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&msa, es, e1));
+  F->t_chain = msc * 1e-3;
+  F->t_schur = mss * 1e-3;
+  F->t_asm = msa * 1e-3;
+  for (cudaEvent_t ev : {e0, e1, e2, ec, es}) cudaEventDestroy(ev);
+  F->t1 = ms1 * 1e-3;
+  F->t2 = ms2 * 1e-3;
+  // reference-equivalent storage (driver.hpp:153-159; stage_two.hpp:191-198)
+  for (auto& s : F->strips_h) {
+    const int64_t w = s.w;
+    if (F->single) {
+      F->storage1 += (3 * n2 + 1) * F->N;  // BandedLU(n, n2, n2) in the reference
+    } else {
+      F->storage1 += (3 * w + 1) * w * n2 + (s.left >= 0 ? 2 * n2 : 0) + (s.right >= 0 ? 2 * n2 : 0);
+    }
+  }
+  if (!F->single) F->storage2 = (int64_t)(K + 2 * (K - 1)) * n2 * n2;
+  F->launches_factor = g_launches.load() - launches0;
+  return F.release();
+}
+
+void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu) {
+  std::lock_guard<std::mutex> guard(F->solve_mu);
+  const int64_t launches0 = g_launches.load();
+  SLB_CUDA_CHECK(cudaSetDevice(F->device));
+  cudaStream_t st = F->stream;
+  const int dev = F->device;
+  const int64_t n2 = F->n2, N = F->N, K = (int64_t)F->K * n2;
+  const int S = F->S;
+  // compact f (ld N)
+  DBuf<double> f;
+  const double* fp = d_f;
+  if (ldf != N) {
+    f.alloc(dev, (size_t)N * nrhs);
+    copy2d(st, d_f, ldf, f.p, N, N, nrhs);
+    fp = f.p;
+  }
+  DBuf<double> u;
+  double* up = d_u;
+  if (ldu != N) {
+    u.alloc(dev, (size_t)N * nrhs);
+    up = u.p;
+  }
+  cudaEvent_t s0, s1, s2, s3, s4;
+  for (cudaEvent_t* ev : {&s0, &s1, &s2, &s3, &s4}) SLB_CUDA_CHECK(cudaEventCreate(ev));
+  SLB_CUDA_CHECK(cudaEventRecord(s0, st));
+  SLB_CUDA_CHECK(cudaEventRecord(s1, st));
+  SLB_CUDA_CHECK(cudaEventRecord(s2, st));
+  SLB_CUDA_CHECK(cudaEventRecord(s3, st));
+  const int64_t nch = cdiv(nrhs, kSweepChunk);
+  std::vector<int32_t> tasks;
+  for (int s = 0; s < S; s++)
+    for (int64_t cch = 0; cch < nch; cch++) {
+      tasks.push_back(s);
+      tasks.push_back(0);
+      tasks.push_back((int32_t)(cch * kSweepChunk));
+    }
+  const int ntasks = (int)(tasks.size() / 3);
+  DBuf<int32_t> dtasks, counter;
+  dtasks.alloc(dev, tasks.size());
+  counter.alloc(dev, 1);
+  SLB_CUDA_CHECK(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  const int nslots = std::min(sm_count(dev), ntasks);
+  const int64_t sY = n2 * F->Wp * kSweepChunk;
+  DBuf<double> ybuf;
+  ybuf.alloc(dev, (size_t)nslots * sY);
+  SchurArgs sa{};
+  sa.Wp = F->Wp;
+  sa.n2 = n2;
+  sa.nstrips = S;
+  sa.strips = F->strips.p;
+  sa.fac = F->fac.p;
+  sa.sF = F->sF;
+  sa.perm = F->perm.p;
+  sa.sP = F->sP;
+  sa.cpl = F->cpl.p;
+  sa.sCPL = F->sCPL;
+  sa.sym = F->sym.p;
+  sa.ybuf = ybuf.p;
+  sa.sY = sY;
+  sa.task_counter = counter.p;
+  sa.ntasks = ntasks;
+  sa.tasks = dtasks.p;
+  sa.N = N;
+  sa.K = K;
+  sa.nrhs = nrhs;
+  sa.f = fp;
+
+  if (F->single) {
+    SLB_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
+    sa.mode = SWEEP_RECOVER;
+    sa.u_ifc = nullptr;
+    sa.out = up;
+    sweep(st, sa, nslots);
+    g_launches++;
+  } else {
+    DBuf<double> red, uifc, contrib, tmp, part;
+    red.alloc(dev, (size_t)K * nrhs);
+    uifc.alloc(dev, (size_t)K * nrhs);
+    contrib.alloc(dev, (size_t)S * 2 * nrhs * n2);
+    tmp.alloc(dev, (size_t)n2 * nrhs);
+    part.alloc(dev, (size_t)8 * n2 * nrhs);
+    const unsigned gb = (unsigned)cdiv(K * nrhs, 256);
+    // reduce_rhs (stage_one.hpp:415-433)
+    gather_ifc_kernel<<<gb, 256, 0, st>>>(fp, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K);
+    SLB_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
+    sa.mode = SWEEP_REDUCE;
+    sa.out = contrib.p;
+    sweep(st, sa, nslots);
+    SLB_CUDA_CHECK(cudaEventRecord(s1, st));
+    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, S, F->strips.p, contrib.p);
+    g_launches += 3;
+    // sweep solve (stage_two.hpp:170-188) with S_j^{-1}
+    const int64_t bs = n2 * n2;
+    for (int j = 0; j < F->K; j++) {
+      double* rj = red.p + j * n2;
+      if (j > 0) dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j - 1) * bs, n2, uifc.p + (j - 1) * n2, K,
+                                   1.0, rj, K, part.p);
+      dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tdiag() + j * bs, n2, rj, K, 0.0, uifc.p + j * n2, K, part.p);
+      g_launches += j > 0 ? 4 : 2;
+    }
+    for (int j = F->K - 2; j >= 0; j--) {
+      dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tsup() + j * bs, n2, uifc.p + (j + 1) * n2, K, 0.0, tmp.p, n2,
+                        part.p);
+      dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tdiag() + j * bs, n2, tmp.p, n2, 1.0, uifc.p + j * n2, K, part.p);
+      g_launches += 4;
+    }
+    // recover_interiors (stage_one.hpp:438-462)
+    SLB_CUDA_CHECK(cudaEventRecord(s2, st));
+    SLB_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
+    sa.mode = SWEEP_RECOVER;
+    sa.u_ifc = uifc.p;
+    sa.out = up;
+    sweep(st, sa, nslots);
+    SLB_CUDA_CHECK(cudaEventRecord(s3, st));
+    scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc.p, K, nrhs, F->ifc_off.p, n2, up, N);
+    g_launches += 2;
+    SLB_CUDA_CHECK(cudaGetLastError());
+    SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+  if (up != d_u) copy2d(st, up, N, d_u, ldu, N, nrhs);
+  SLB_CUDA_CHECK(cudaEventRecord(s4, st));
+  SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+  float a = 0, b = 0, c = 0;
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&a, s0, s4));
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&b, s0, s1));
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&c, s2, s3));
+  F->t_solve = a * 1e-3;
+  F->t_solve_strips = F->single ? a * 1e-3 : (b + c) * 1e-3;
+  for (cudaEvent_t ev : {s0, s1, s2, s3, s4}) cudaEventDestroy(ev);
+  F->launches_solve = g_launches.load() - launches0;
+}
+
+slablu_gpu_status status_from(const HostError& e) { return make_status(e.code, e.what(), e.index); }
+slablu_gpu_status status_from(const CudaFailure& e) {
+  const int code = e.err == cudaErrorMemoryAllocation ? SLABLU_ERR_OOM : SLABLU_ERR_CUDA;
+  return make_status(code, std::string("CUDA error: ") + cudaGetErrorString(e.err) + " at " + e.file + ":" +
+                               std::to_string(e.line) + " (" + e.expr + ")", -1);
+}
+
+#define ABI_TRY(...)                                   \
+  try {                                                \
+    __VA_ARGS__;                                       \
+    return make_status(SLABLU_OK, "", -1);             \
+  } catch (const HostError& e) {                       \
+    return status_from(e);                             \
+  } catch (const CudaFailure& e) {                     \
+    return status_from(e);                             \
+  } catch (const std::bad_alloc&) {                    \
+    return make_status(SLABLU_ERR_OOM, "host allocation failed", -1); \
+  }
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw HostError(SLABLU_ERR_CUDA, "no CUDA device available (the engine has no CPU fallback)");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int slablu_gpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+slablu_gpu_status slablu_gpu_factorize(int64_t n1, int64_t n2, const int32_t* row_ptr, const int32_t* col_idx,
+                                       const double* val, const slablu_gpu_config* config, slablu_gpu_fact** out) {
+  ABI_TRY({
+    require_device();
+    *out = nullptr;
+    const int dev = (int)cfg_device(config);
+    SLB_CUDA_CHECK(cudaSetDevice(dev));
+    const int64_t n = n1 * n2;
+    if (n == 0) throw HostError(SLABLU_ERR_CONFIG, "factorize: empty system");
+    const int64_t nnz = row_ptr[n];
+    DBuf<int32_t> rp, ci;
+    DBuf<double> v;
+    rp.alloc(dev, n + 1);
+    ci.alloc(dev, nnz);
+    v.alloc(dev, nnz);
+    SLB_CUDA_CHECK(cudaMemcpy(rp.p, row_ptr, (n + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
+    SLB_CUDA_CHECK(cudaMemcpy(ci.p, col_idx, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+    SLB_CUDA_CHECK(cudaMemcpy(v.p, val, nnz * sizeof(double), cudaMemcpyHostToDevice));
+    *out = factorize_impl(n1, n2, nnz, rp.p, ci.p, v.p, config);
+  })
+}
+
+slablu_gpu_status slablu_gpu_factorize_device(int64_t n1, int64_t n2, int64_t nnz, const int32_t* d_row_ptr,
+                                              const int32_t* d_col_idx, const double* d_val,
+                                              const slablu_gpu_config* config, slablu_gpu_fact** out) {
+  ABI_TRY({
+    require_device();
+    *out = nullptr;
+    *out = factorize_impl(n1, n2, nnz, d_row_ptr, d_col_idx, d_val, config);
+  })
+}
+
+slablu_gpu_status slablu_gpu_solve(const slablu_gpu_fact* fact, const double* f, int64_t ldf, int64_t nrhs,
+                                   double* u, int64_t ldu) {
+  ABI_TRY({
+    if (!fact) throw HostError(SLABLU_ERR_GENERIC, "solve: null factorization");
+    if (nrhs < 0 || ldf < fact->N || ldu < fact->N)
+      throw HostError(SLABLU_ERR_GENERIC, "solve: rhs length must equal the grid size");
+    if (nrhs == 0) return make_status(SLABLU_OK, "", -1);
+    SLB_CUDA_CHECK(cudaSetDevice(fact->device));
+    const int64_t N = fact->N;
+    DBuf<double> df, du;
+    df.alloc(fact->device, (size_t)N * nrhs);
+    du.alloc(fact->device, (size_t)N * nrhs);
+    SLB_CUDA_CHECK(cudaMemcpy2DAsync(df.p, N * sizeof(double), f, ldf * sizeof(double), N * sizeof(double), nrhs,
+                                     cudaMemcpyHostToDevice, fact->stream));
+    solve_impl(fact, df.p, N, nrhs, du.p, N);
+    SLB_CUDA_CHECK(cudaMemcpy2DAsync(u, ldu * sizeof(double), du.p, N * sizeof(double), N * sizeof(double), nrhs,
+                                     cudaMemcpyDeviceToHost, fact->stream));
+    SLB_CUDA_CHECK(cudaStreamSynchronize(fact->stream));
+  })
+}
+
+slablu_gpu_status slablu_gpu_solve_device(const slablu_gpu_fact* fact, const double* d_f, int64_t ldf, int64_t nrhs,
+                                          double* d_u, int64_t ldu) {
+  ABI_TRY({
+    if (!fact) throw HostError(SLABLU_ERR_GENERIC, "solve: null factorization");
+    if (nrhs < 0 || ldf < fact->N || ldu < fact->N)
+      throw HostError(SLABLU_ERR_GENERIC, "solve: rhs length must equal the grid size");
+    if (nrhs == 0) return make_status(SLABLU_OK, "", -1);
+    solve_impl(fact, d_f, ldf, nrhs, d_u, ldu);
+  })
+}
+
+slablu_gpu_status slablu_gpu_stats(const slablu_gpu_fact* F, slablu_gpu_stats_t* o) {
+  ABI_TRY({
+    if (!F) throw HostError(SLABLU_ERR_GENERIC, "stats: null factorization");
+    o->n1 = F->n1;
+    o->n2 = F->n2;
+    o->b = F->b;
+    o->interfaces = F->K;
+    o->strips = F->S;
+    o->padded_width = F->Wp;
+    o->single_slab = F->single ? 1 : 0;
+    o->symmetric_strips = 0;
+    for (int v : F->sym_h) o->symmetric_strips += v ? 1 : 0;
+    o->t_stage1 = F->t1;
+    o->t_stage2 = F->t2;
+    o->storage_stage1 = F->storage1;
+    o->storage_stage2 = F->storage2;
+    o->device_bytes = (int64_t)(F->fac.bytes() + F->perm.bytes() + F->cpl.bytes() + F->T.bytes() + F->Tkeep.bytes());
+    o->gpu_launches = F->launches_factor;
+    o->solve_launches = F->launches_solve;
+    o->t_chain = F->t_chain;
+    o->t_schur = F->t_schur;
+    o->t_assemble = F->t_asm;
+    o->t_solve_last = F->t_solve;
+    o->t_solve_strips = F->t_solve_strips;
+  })
+}
+
+slablu_gpu_status slablu_gpu_T_block(const slablu_gpu_fact* F, int which, int64_t j, double* out) {
+  ABI_TRY({
+    if (!F || !F->Tkeep.p) throw HostError(SLABLU_ERR_GENERIC, "T_block: factorization was not built with keep_T");
+    const int64_t nb = which == 0 ? F->K : F->K - 1;
+    if (j < 0 || j >= nb || which < 0 || which > 2) throw HostError(SLABLU_ERR_GENERIC, "T_block: index out of range");
+    const int64_t base = which == 0 ? j : which == 1 ? F->K + j : 2 * F->K - 1 + j;
+    SLB_CUDA_CHECK(cudaSetDevice(F->device));
+    SLB_CUDA_CHECK(cudaMemcpy(out, F->Tkeep.p + base * F->n2 * F->n2, F->n2 * F->n2 * sizeof(double),
+                              cudaMemcpyDeviceToHost));
+  })
+}
+
+slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* F, const double* f, int64_t nrhs, double* out) {
+  ABI_TRY({
+    if (!F || F->single) throw HostError(SLABLU_ERR_GENERIC, "reduce_rhs: no partition");
+    std::lock_guard<std::mutex> guard(F->solve_mu);
+    SLB_CUDA_CHECK(cudaSetDevice(F->device));
+    cudaStream_t st = F->stream;
+    const int dev = F->device;
+    const int64_t n2 = F->n2, N = F->N, K = (int64_t)F->K * n2;
+    DBuf<double> df, red, contrib, ybuf;
+    DBuf<int32_t> dtasks, counter;
+    df.alloc(dev, (size_t)N * nrhs);
+    SLB_CUDA_CHECK(cudaMemcpy(df.p, f, N * nrhs * sizeof(double), cudaMemcpyHostToDevice));
+    red.alloc(dev, (size_t)K * nrhs);
+    contrib.alloc(dev, (size_t)F->S * 2 * nrhs * n2);
+    std::vector<int32_t> tasks;
+    for (int s = 0; s < F->S; s++)
+      for (int64_t c0 = 0; c0 < nrhs; c0 += kSweepChunk) {
+        tasks.push_back(s);
+        tasks.push_back(0);
+        tasks.push_back((int32_t)c0);
+      }
+    dtasks.alloc(dev, tasks.size());
+    counter.alloc(dev, 1);
+    SLB_CUDA_CHECK(cudaMemcpy(dtasks.p, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    SLB_CUDA_CHECK(cudaMemset(counter.p, 0, sizeof(int32_t)));
+    const int ntasks = (int)(tasks.size() / 3);
+    const int nslots = std::min(sm_count(dev), ntasks);
+    const int64_t sY = n2 * F->Wp * kSweepChunk;
+    ybuf.alloc(dev, (size_t)nslots * sY);
+    SchurArgs sa{};
+    sa.Wp = F->Wp; sa.n2 = n2; sa.nstrips = F->S; sa.strips = F->strips.p; sa.fac = F->fac.p; sa.sF = F->sF;
+    sa.perm = F->perm.p; sa.sP = F->sP; sa.cpl = F->cpl.p; sa.sCPL = F->sCPL; sa.sym = F->sym.p;
+    sa.ybuf = ybuf.p; sa.sY = sY; sa.task_counter = counter.p; sa.ntasks = ntasks; sa.tasks = dtasks.p;
+    sa.N = N; sa.K = K; sa.nrhs = nrhs; sa.f = df.p; sa.mode = SWEEP_REDUCE; sa.out = contrib.p;
+    const unsigned gb = (unsigned)cdiv(K * nrhs, 256);
+    gather_ifc_kernel<<<gb, 256, 0, st>>>(df.p, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K);
+    sweep(st, sa, nslots);
+    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, F->S, F->strips.p, contrib.p);
+    SLB_CUDA_CHECK(cudaGetLastError());
+    SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+    SLB_CUDA_CHECK(cudaMemcpy(out, red.p, K * nrhs * sizeof(double), cudaMemcpyDeviceToHost));
+  })
+}
+
+void slablu_gpu_destroy(slablu_gpu_fact* fact) {
+  if (!fact) return;
+  try {
+    delete fact;
+  } catch (...) {
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,141 @@
+// Internal launcher declarations for the SlabLU B200 engine.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace slb {
+
+// ---- gemm.cu -------------------------------------------------------------
+void dgemm_batched(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                   int64_t lda, int64_t sA, const double* B, int64_t ldb, int64_t sB, double beta,
+                   double* C, int64_t ldc, int64_t sC, int64_t batch, const int32_t* brow = nullptr,
+                   int64_t sBrow = 0);
+void dscale_batched(cudaStream_t st, int64_t M, int64_t N, double beta, double* C, int64_t ldc,
+                    int64_t sC, int64_t batch);
+
+// ---- strips ----------------------------------------------------------------
+// One interior strip (slab) of the partition, with its adjacent interfaces.
+struct StripDesc {
+  int32_t col0;       // first grid column
+  int32_t w;          // real width (<= Wp)
+  int32_t left;       // left interface id or -1
+  int32_t right;      // right interface id or -1
+  int64_t left_off;   // global index of the left interface's first unknown, -1
+  int64_t right_off;  // same for the right interface
+};
+
+// Error flags raised by the extraction / factor kernels (bitmask).
+enum ErrBits : int32_t {
+  ERR_OUT_OF_BAND = 1,        // interior entry outside the kl=ku=w band
+  ERR_PAST_INTERFACE = 2,     // interior couples past its adjacent interfaces
+  ERR_COUPLING_LEVEL = 4,     // interior<->interface coupling across levels
+  ERR_SINGULAR = 8,           // exactly singular pivot
+  ERR_IFC_STRUCTURE = 16,     // interface row couples outside adjacent strips/interfaces
+  ERR_NONFINITE = 32,         // non-finite reduced block entry
+};
+struct DevStatus {
+  int32_t flags;
+  int32_t singular_strip;  // lowest strip index with a singular pivot (or INT_MAX)
+  int32_t singular_block;  // lowest sweep block index with a singular pivot
+  int32_t pad;
+};
+
+// ---- band_lu.cu --------------------------------------------------------------
+struct CsrDev {
+  const int32_t* rp;
+  const int32_t* ci;
+  const double* v;
+  int64_t n;
+};
+
+// Extract per-level dense blocks [Lsub | D | Usup] (Wp x 3Wp, ld Wp) for levels
+// [L0, L0+nl) of every strip into nx (stride per strip sNX, per level 3*Wp*Wp).
+void extract_levels(cudaStream_t st, CsrDev A, const StripDesc* strips, int nstrips, int64_t n2,
+                    int Wp, int64_t L0, int64_t nl, double* nx, int64_t sNX, DevStatus* status);
+// Per-level coupling vectors fromL/fromR/toL/toR (n2 x Wp each per strip).
+void extract_couplings(cudaStream_t st, CsrDev A, const StripDesc* strips, int nstrips, int64_t n2,
+                       int Wp, double* cpl, int64_t sCPL, int32_t* sym_flags, DevStatus* status);
+// SV(level 0) = [D_0 | Usup_0] from the level-0 extracted blocks.
+void init_sv(cudaStream_t st, int nstrips, int Wp, const double* nx0, int64_t sNX, double* sv,
+             int64_t sSV);
+// One level step of the block band LU for all strips (see band_lu.cu).
+struct LevelArgs {
+  int Wp;
+  int nstrips;
+  int has_next;          // level l+1 exists
+  const double* sv_in;   // Wp x 2Wp per strip  [S | V]
+  int64_t sSV;
+  const double* nx;      // Wp x 3Wp per strip  [Lsub | D | Usup] of level l+1
+  int64_t sNX;
+  double* sv_out;        // Wp x 2Wp per strip: receives R2 (prefill for the update)
+  double* ainv;          // Wp x Wp  (factor storage, level l)
+  int64_t sF;            // per-strip stride of factor storage
+  int32_t* perm;         // 2Wp      (factor storage, level l)
+  int64_t sP;
+  double* bsel;          // Wp x Wp scratch: pivot-ordered bottom panel rows
+  double* r1;            // Wp x 2Wp scratch: pivot-ordered top rows of [V 0; D Usup]
+  int64_t sScr;
+  DevStatus* status;
+  int32_t level;
+};
+void level_panel(cudaStream_t st, const LevelArgs& a);
+
+// ---- schur.cu --------------------------------------------------------------------
+struct SchurArgs {
+  int Wp;
+  int64_t n2;
+  int nstrips;
+  const StripDesc* strips;
+  const double* fac;      // factor storage base (per strip stride sF; per level 4*Wp*Wp)
+  int64_t sF;
+  const int32_t* perm;    // per strip stride sP; per level 2*Wp
+  int64_t sP;
+  const double* cpl;      // coupling vectors (per strip sCPL): fromL, fromR, toL, toR (n2 x Wp each)
+  int64_t sCPL;
+  const int32_t* sym;     // per-strip symmetric flag
+  double* gbuf;           // per strip 4 * n2 * n2 (row-major [X][Y][p][q])
+  int64_t sG;
+  double* ybuf;           // per CTA slot: n2 * Wp * C
+  int64_t sY;
+  int32_t* task_counter;
+  int ntasks;
+  const int32_t* tasks;   // packed (strip, side, q0) triples (solve modes: side unused, q0 = rhs col0)
+  int mode;               // SweepMode
+  // solve modes
+  int64_t N, K, nrhs;
+  const double* f;        // N x nrhs (ld N), natural ordering
+  const double* u_ifc;    // K x nrhs (recover)
+  double* out;            // reduce: contrib[s][X][nrhs][n2]; recover: u (N x nrhs)
+};
+enum SweepMode { SWEEP_SCHUR = 0, SWEEP_REDUCE = 1, SWEEP_RECOVER = 2 };
+constexpr int kSweepChunk = 64;
+void sweep(cudaStream_t st, const SchurArgs& a, int nslots);
+
+// T block assembly from per-strip G buffers (reference order: direct, left strip, right strip).
+void assemble_T(cudaStream_t st, int64_t n2, int nifc, int nstrips, const StripDesc* strips,
+                const int32_t* sym, const double* gbuf, int64_t sG, double* Tdiag, double* Tsup,
+                double* Tsub, CsrDev A, const int64_t* ifc_off, DevStatus* status);
+
+// ---- dense.cu (stage two) -------------------------------------------------------
+// In-place LU with partial pivoting of an n x n column-major matrix (ld = n).
+void dgetrf(cudaStream_t st, int64_t n, double* a, int32_t* ipiv, double* work, DevStatus* status,
+            int block_index);
+// Solve A X = B with the dgetrf factors, B is n x nrhs (ld ldb), in place.
+void dgetrs(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const int32_t* ipiv,
+            double* b, int64_t ldb, double* work);
+void check_finite(cudaStream_t st, const double* a, int64_t count, DevStatus* status);
+
+// ---- solve.cu ---------------------------------------------------------------------
+
+// y = beta*y + alpha * A x  (A m x n col-major, x n x nrhs); part: 8*m*nrhs scratch
+void dgemv_batched_rhs(cudaStream_t st, int64_t m, int64_t n, int64_t nrhs, double alpha,
+                       const double* A, int64_t lda, const double* x, int64_t ldx, double beta,
+                       double* y, int64_t ldy, double* part);
+void dset_identity(cudaStream_t st, double* a, int64_t n);
+
+}  // namespace slb
+
+namespace slb {
+void pack_level(cudaStream_t st, int nstrips, int Wp, const double* ainv, const double* fbot,
+                const double* h, int64_t sScr, double* out, int64_t sF);
+}

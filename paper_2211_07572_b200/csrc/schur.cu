@@ -1,0 +1,446 @@
+// Stage one, part 2: dense Schur blocks T = A_JJ - A_JI A_II^{-1} A_IJ (sm_100a).
+//
+// Reference: build_reduced dense branch (proj/include/slablu/stage_one.hpp:
+// 357-411) applies apply_T_block (:258-299) to Identity(n2): one dgbtrs with
+// n2 right-hand sides per adjacent strip side (banded.hpp:116-128).
+//
+// Here every strip side Y in {L, R} contributes the n2 x n2 blocks
+//   C_XY[p][q] = to_X[p] . (A_ii^{-1} from_Y[:, q])[level p]     (X in {L, R})
+// computed by a persistent kernel: one task = (strip, side, C = 64 columns
+// starting at level q0).  Column q of from_Y lives on level q only, so the
+// forward sweep starts at level q0 - 1 (sparse start).  For symmetric strips
+// (A_ii = A_ii^T, to = from^T, detected at factorize time) C is symmetric over
+// (X,p)x(Y,q) and the backward sweep stops at level q0 (rows p >= q0 are the
+// only ones needed); the mirror half is filled in assemble_T.
+//
+// Per level, both sweeps are one FP64 GEMM on the DMMA pipe (mma.sync m8n8k4):
+//   forward  [y_l ; z_{l+1} - t_bot] = [Ainv ; Fbot] (2Wp x Wp) * t_top (Wp x C)
+//   backward x_l = y_l - H_l (Wp x 2Wp) * [x_{l+1} ; x_{l+2}] (2Wp x C)
+// A operands stream from HBM/L2 in fragment order (16-byte cp.async, 3-stage
+// ring, continuous across levels); B operands stay in shared memory; y_l is
+// spilled to a per-CTA HBM slab between the two sweeps.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace slb {
+namespace {
+
+constexpr int C = 64;       // RHS columns per task
+constexpr int NT = C / 8;   // n8 tiles
+constexpr int THREADS = 512;
+constexpr int STAGES = 3;
+
+__device__ __forceinline__ int swz(int r, int n) { return r * C + (n ^ ((r & 3) << 2)); }
+
+struct TaskGeom {
+  int s, side, q0, l0, lstop;
+  int64_t nf, nslices;  // forward slices, total slices
+};
+
+template <int MTMAX>
+__global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
+  extern __shared__ double sm[];
+  const int Wp = a.Wp;
+  const int64_t n2 = a.n2;
+  double* zb = sm;                       // forward: z      | backward: x buffer 0
+  double* tb = sm + Wp * C;              // forward: t_top  | backward: x buffer 1
+  double* stg = sm + 2 * Wp * C;         // STAGES slots of 16*Wp doubles
+  int* sperm = reinterpret_cast<int*>(stg + STAGES * 16 * Wp);
+  __shared__ int s_task;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int MTH = Wp / 8;                       // m8 tiles per Wp rows
+  const int MTPW = (MTH + 3) / 4;               // m tiles per m-warp (<= MTMAX)
+  const int fslice = 16 * Wp;                   // doubles per forward k8 slice
+  const int bslice = 8 * Wp;                    // doubles per backward k8 slice
+  const int64_t lvl_stride = 4LL * Wp * Wp;
+  const int kf = Wp / 8, kb = Wp / 4;           // slices per level (fwd, bwd)
+  double* ybase = a.ybuf + (int64_t)blockIdx.x * a.sY;
+
+  for (;;) {
+    if (tid == 0) s_task = atomicAdd(a.task_counter, 1);
+    __syncthreads();
+    const int task = s_task;
+    __syncthreads();
+    if (task >= a.ntasks) break;
+    TaskGeom T;
+    T.s = a.tasks[3 * task];
+    T.side = a.tasks[3 * task + 1];
+    T.q0 = a.tasks[3 * task + 2];
+    const bool schur = a.mode == SWEEP_SCHUR;
+    T.l0 = (schur && T.q0 > 0) ? T.q0 - 1 : 0;
+    T.lstop = (schur && a.sym[T.s]) ? T.q0 : 0;
+    T.nf = (n2 - T.l0) * kf;
+    T.nslices = T.nf + (n2 - T.lstop) * kb;
+    const StripDesc sd = a.strips[T.s];
+    const double* fac = a.fac + T.s * a.sF;
+    const int32_t* permg = a.perm + T.s * a.sP;
+    const double* cpl = a.cpl + T.s * a.sCPL;
+    const double* fromY = cpl + (T.side == 0 ? 0 : n2 * Wp);
+    const double* toL = cpl + 2 * n2 * Wp;
+    const double* toR = cpl + 3 * n2 * Wp;
+    double* gb = a.gbuf + T.s * a.sG;
+    const int64_t rem = schur ? n2 - T.q0 : a.nrhs - T.q0;
+    const int ncols = (int)(rem < C ? rem : C);
+    // dense right-hand side of level L (solve modes): b_L[i][n]
+    auto rhs_val = [&](int64_t L, int i, int n) -> double {
+      if (i >= sd.w || n >= ncols) return 0.0;
+      const int64_t col = T.q0 + n;
+      double v = a.f[col * a.N + (int64_t)(sd.col0 + i) * n2 + L];
+      if (a.mode == SWEEP_RECOVER) {
+        if (sd.left >= 0) v -= cpl[L * Wp + i] * a.u_ifc[col * a.K + (int64_t)sd.left * n2 + L];
+        if (sd.right >= 0) v -= cpl[n2 * Wp + L * Wp + i] * a.u_ifc[col * a.K + (int64_t)sd.right * n2 + L];
+      }
+      return v;
+    };
+
+    auto slice_src = [&](int64_t i) -> const double* {
+      if (i < T.nf) {
+        const int64_t l = T.l0 + i / kf, j = i % kf;
+        return fac + l * lvl_stride + j * fslice;
+      }
+      const int64_t ib = i - T.nf;
+      const int64_t l = n2 - 1 - ib / kb, j = ib % kb;
+      return fac + l * lvl_stride + 2LL * Wp * Wp + j * bslice;
+    };
+    auto issue = [&](int64_t i) {
+      if (i < T.nslices) {
+        const double* src = slice_src(i);
+        const int len = i < T.nf ? fslice : bslice;  // doubles
+        double* dst = stg + (i % STAGES) * fslice;
+        for (int c = tid; c < len / 2; c += THREADS) cp_async16(dst + 2 * c, src + 2 * c, true);
+      }
+      cp_async_commit();
+    };
+
+    int64_t slice = 0;
+    for (int i = 0; i < STAGES - 1; i++) issue(i);
+
+    // ---------------- forward sweep ----------------
+    for (int idx = tid; idx < Wp * C; idx += THREADS) zb[idx] = 0.0;
+    __syncthreads();
+    if (schur) {
+      if (T.q0 == 0)  // column 0 lives on level 0: z_0 = from_Y[level 0]
+        for (int i = tid; i < Wp; i += THREADS) zb[swz(i, 0)] = fromY[i];
+    } else {
+      for (int idx = tid; idx < Wp * C; idx += THREADS) {
+        const int r = idx / C, n = idx % C;
+        zb[swz(r, n)] = rhs_val(0, r, n);
+      }
+    }
+
+    const int half = warp >> 3;          // 0: Ainv rows (y), 1: Fbot rows (z')
+    const int fwm = (warp & 7) >> 1;     // m group
+    const int fwn = warp & 1;            // n group: tiles [4 fwn, 4 fwn + 4)
+    for (int64_t l = T.l0; l < n2; l++) {
+      const bool has_next = l + 1 < n2;
+      const int cstar = (schur && has_next) ? (int)(l + 1 - T.q0) : -1;  // column injected
+      const bool inj = cstar >= 0 && cstar < ncols;
+      const double* fvec = inj ? fromY + (l + 1) * Wp : nullptr;
+      for (int i = tid; i < 2 * Wp; i += THREADS) sperm[i] = permg[l * 2 * Wp + i];
+      __syncthreads();
+      auto vval = [&](int src, int n) -> double {
+        if (src < Wp) return zb[swz(src, n)];
+        if (!schur) return has_next ? rhs_val(l + 1, src - Wp, n) : 0.0;
+        return (inj && n == cstar) ? fvec[src - Wp] : 0.0;
+      };
+      for (int idx = tid; idx < Wp * C; idx += THREADS) {
+        const int r = idx / C, n = idx % C;
+        tb[swz(r, n)] = vval(sperm[r], n);
+      }
+      double acc[MTMAX][4][2];
+#pragma unroll
+      for (int mi = 0; mi < MTMAX; mi++)
+#pragma unroll
+        for (int nj = 0; nj < 4; nj++) {
+          acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+          const int mt = fwm * MTPW + mi;
+          if (half == 1 && mi < MTPW && mt < MTH) {
+            const int row = mt * 8 + g;
+            const int col = (fwn * 4 + nj) * 8 + 2 * t;
+            const int src = sperm[Wp + row];
+            acc[mi][nj][0] = vval(src, col);
+            acc[mi][nj][1] = vval(src, col + 1);
+          }
+        }
+      __syncthreads();
+      for (int j = 0; j < kf; j++, slice++) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        issue(slice + STAGES - 1);
+        const double* A = stg + (slice % STAGES) * fslice;
+#pragma unroll
+        for (int kk = 0; kk < 2; kk++) {
+          const int k = j * 8 + kk * 4 + t;  // B row
+          double bf[4];
+#pragma unroll
+          for (int nj = 0; nj < 4; nj++) bf[nj] = tb[swz(k, (fwn * 4 + nj) * 8 + g)];
+          const double* Ak = A + kk * (2 * MTH) * 32 + half * MTH * 32 + lane;
+#pragma unroll
+          for (int mi = 0; mi < MTMAX; mi++) {
+            const int mt = fwm * MTPW + mi;
+            if (mi < MTPW && mt < MTH) {
+              const double af = Ak[mt * 32];
+#pragma unroll
+              for (int nj = 0; nj < 4; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
+            }
+          }
+        }
+      }
+      // epilogue: y_l -> HBM slab (canonical tile order), z_{l+1} -> smem
+      double* ylev = ybase + (l - T.l0) * (int64_t)Wp * C;
+#pragma unroll
+      for (int mi = 0; mi < MTMAX; mi++) {
+        const int mt = fwm * MTPW + mi;
+        if (mi >= MTPW || mt >= MTH) continue;
+#pragma unroll
+        for (int nj = 0; nj < 4; nj++) {
+          const int nt = fwn * 4 + nj;
+          if (half == 0) {
+            double2* dst = reinterpret_cast<double2*>(ylev + ((int64_t)(mt * NT + nt) * 32 + lane) * 2);
+            *dst = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
+          } else {
+            const int row = mt * 8 + g, col = nt * 8 + 2 * t;
+            zb[swz(row, col)] = acc[mi][nj][0];
+            zb[swz(row, col + 1)] = acc[mi][nj][1];
+          }
+        }
+      }
+    }
+
+    // ---------------- backward sweep ----------------
+    __syncthreads();
+    for (int idx = tid; idx < 2 * Wp * C; idx += THREADS) sm[idx] = 0.0;  // x_{n2}, x_{n2+1} = 0
+    __syncthreads();
+    const int bwm = warp >> 2;        // m group
+    const int bwn = warp & 3;         // n tiles [2 bwn, 2 bwn + 2)
+    int p_buf = 0;                    // buffer holding x_{l+1}; the other holds x_{l+2}
+    for (int64_t l = n2 - 1; l >= T.lstop; l--) {
+      const double* ylev = ybase + (l - T.l0) * (int64_t)Wp * C;
+      double acc[MTMAX][2][2];
+#pragma unroll
+      for (int mi = 0; mi < MTMAX; mi++) {
+        const int mt = bwm * MTPW + mi;
+#pragma unroll
+        for (int nj = 0; nj < 2; nj++) {
+          acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+          if (mi < MTPW && mt < MTH) {
+            const int nt = bwn * 2 + nj;
+            const double2 v = *reinterpret_cast<const double2*>(ylev + ((int64_t)(mt * NT + nt) * 32 + lane) * 2);
+            acc[mi][nj][0] = -v.x;  // accumulate -x, negate at the end
+            acc[mi][nj][1] = -v.y;
+          }
+        }
+      }
+      const double* xp = sm + p_buf * Wp * C;        // x_{l+1}
+      const double* xq = sm + (1 - p_buf) * Wp * C;  // x_{l+2}
+      for (int j = 0; j < kb; j++, slice++) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        issue(slice + STAGES - 1);
+        const double* A = stg + (slice % STAGES) * fslice;
+        const double* xs = (j * 8 < Wp) ? xp : xq;
+        const int kbase = (j * 8 < Wp) ? j * 8 : j * 8 - Wp;
+#pragma unroll
+        for (int kk = 0; kk < 2; kk++) {
+          const int k = kbase + kk * 4 + t;
+          double bf[2];
+#pragma unroll
+          for (int nj = 0; nj < 2; nj++) bf[nj] = xs[swz(k, (bwn * 2 + nj) * 8 + g)];
+          const double* Ak = A + kk * MTH * 32 + lane;
+#pragma unroll
+          for (int mi = 0; mi < MTMAX; mi++) {
+            const int mt = bwm * MTPW + mi;
+            if (mi < MTPW && mt < MTH) {
+              const double af = Ak[mt * 32];
+#pragma unroll
+              for (int nj = 0; nj < 2; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
+            }
+          }
+        }
+      }
+      __syncthreads();  // everyone done reading x_{l+2}
+      double* xo = sm + (1 - p_buf) * Wp * C;  // x_l overwrites x_{l+2}
+#pragma unroll
+      for (int mi = 0; mi < MTMAX; mi++) {
+        const int mt = bwm * MTPW + mi;
+        if (mi >= MTPW || mt >= MTH) continue;
+#pragma unroll
+        for (int nj = 0; nj < 2; nj++) {
+          const int row = mt * 8 + g, col = (bwn * 2 + nj) * 8 + 2 * t;
+          xo[swz(row, col)] = -acc[mi][nj][0];
+          xo[swz(row, col + 1)] = -acc[mi][nj][1];
+        }
+      }
+      __syncthreads();
+      if (a.mode == SWEEP_RECOVER) {
+        for (int idx = tid; idx < sd.w * ncols; idx += THREADS) {
+          const int i = idx % sd.w, n = idx / sd.w;
+          a.out[(T.q0 + n) * a.N + (int64_t)(sd.col0 + i) * n2 + l] = xo[swz(i, n)];
+        }
+      } else {
+        // boundary extraction: C_XY[l][q0 + n] = to_X[l] . x_l[:, n]
+        const int X = tid >> 8;            // 0: L, 1: R
+        const int n = (tid >> 2) & 63;     // column
+        const int part = tid & 3;
+        const double* tv = (X == 0 ? toL : toR) + l * Wp;
+        double sum = 0.0;
+        for (int i = part; i < Wp; i += 4) sum = fma(tv[i], xo[swz(i, n)], sum);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        const bool has = X == 0 ? sd.left >= 0 : sd.right >= 0;
+        if (part == 0 && has && n < ncols) {
+          if (schur) gb[((int64_t)(X * 2 + T.side) * n2 + l) * n2 + T.q0 + n] = sum;
+          else a.out[((int64_t)(T.s * 2 + X) * a.nrhs + T.q0 + n) * n2 + l] = sum;  // contrib[s][X][col][l]
+        }
+      }
+      p_buf = 1 - p_buf;
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+void sweep(cudaStream_t st, const SchurArgs& a, int nslots) {
+  const int Wp = a.Wp;
+  const size_t smem = (size_t)(2 * Wp * C + STAGES * 16 * Wp) * sizeof(double) + 2 * Wp * sizeof(int);
+  const int mtpw = (Wp / 8 + 3) / 4;
+  auto launch = [&](auto kern) {
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<nslots, THREADS, smem, st>>>(a);
+  };
+  if (mtpw <= 1) launch(schur_kernel<1>);
+  else if (mtpw <= 2) launch(schur_kernel<2>);
+  else if (mtpw <= 3) launch(schur_kernel<3>);
+  else if (mtpw <= 4) launch(schur_kernel<4>);
+  else if (mtpw <= 5) launch(schur_kernel<5>);
+  else throw CudaFailure(cudaErrorInvalidValue, "sweep: slab width > 160 unsupported", __FILE__, __LINE__);
+  SLB_CUDA_CHECK(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// T assembly (reference order: direct term, then the strip left of the
+// interface (its right side), then the strip right of it (its left side);
+// inc/stage_one.hpp:284-297).  T blocks are n2 x n2 column major.
+namespace {
+
+__device__ __forceinline__ double cval(const double* gb, int64_t n2, int sym, int X, int Y, int64_t p,
+                                       int64_t q) {
+  if (sym && p < q) return gb[((int64_t)(Y * 2 + X) * n2 + q) * n2 + p];
+  return gb[((int64_t)(X * 2 + Y) * n2 + p) * n2 + q];
+}
+
+// grid (ceil(n2/32), ceil(n2/32), nblocks) with blocks ordered diag j (k), super j (k-1), sub j (k-1)
+__global__ void assemble_T_kernel(int64_t n2, int nifc, int nstrips, const int32_t* sym,
+                                  const double* gbuf, int64_t sG, double* Tdiag, double* Tsup,
+                                  double* Tsub) {
+  __shared__ double tile[32][33];
+  const int b = blockIdx.z;
+  int kind, j;
+  if (b < nifc) {
+    kind = 0;
+    j = b;
+  } else if (b < 2 * nifc - 1) {
+    kind = 1;
+    j = b - nifc;
+  } else {
+    kind = 2;
+    j = b - (2 * nifc - 1);
+  }
+  double* T = (kind == 0 ? Tdiag : kind == 1 ? Tsup : Tsub) + (int64_t)j * n2 * n2;
+  const int64_t p0 = (int64_t)blockIdx.x * 32, q0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  // The two (or one) strip terms, each (strip, X, Y):
+  //  diag j: strip j (X=R,Y=R), strip j+1 (X=L,Y=L) if it exists
+  //  super j (T_{j,j+1}): strip j+1 (X=L, Y=R);  sub j (T_{j+1,j}): strip j+1 (X=R, Y=L)
+  int ns = 0, st_[2], X_[2], Y_[2];
+  if (kind == 0) {
+    st_[ns] = j; X_[ns] = 1; Y_[ns] = 1; ns++;
+    if (j + 1 < nstrips) { st_[ns] = j + 1; X_[ns] = 0; Y_[ns] = 0; ns++; }
+  } else if (kind == 1) {
+    st_[ns] = j + 1; X_[ns] = 0; Y_[ns] = 1; ns++;
+  } else {
+    st_[ns] = j + 1; X_[ns] = 1; Y_[ns] = 0; ns++;
+  }
+  // element (p, q) of T at T[q*n2 + p]; thread (tx, ty..) handles p = p0 + tx, q = q0 + ty + 8r
+  double val[4];
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    const int64_t p = p0 + tx, q = q0 + ty + 8 * r;
+    val[r] = (p < n2 && q < n2) ? T[q * n2 + p] : 0.0;
+  }
+  for (int e = 0; e < ns; e++) {
+    const double* gb = gbuf + st_[e] * sG;
+    const int sy = sym[st_[e]];
+    // coalesced path: load the 32x32 tile with q fastest (row-major gbuf) then transpose
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      const int64_t p = p0 + ty + 8 * r, q = q0 + tx;
+      tile[ty + 8 * r][tx] = (p < n2 && q < n2) ? cval(gb, n2, sy, X_[e], Y_[e], p, q) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; r++) val[r] -= tile[tx][ty + 8 * r];
+  }
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    const int64_t p = p0 + tx, q = q0 + ty + 8 * r;
+    if (p < n2 && q < n2) T[q * n2 + p] = val[r];
+  }
+}
+
+// Direct interface blocks from the CSR: grid = nifc, each block scans the
+// interface's rows and scatters into the zeroed T blocks.
+__global__ void direct_T_kernel(CsrDev A, int64_t n2, int nifc, const int64_t* ifc_off,
+                                const StripDesc* strips, int nstrips, double* Tdiag, double* Tsup,
+                                double* Tsub, DevStatus* status) {
+  const int j = blockIdx.x;
+  const int64_t off = ifc_off[j];
+  for (int64_t p = threadIdx.x; p < n2; p += blockDim.x) {
+    const int64_t r = off + p;
+    for (int32_t e = A.rp[r]; e < A.rp[r + 1]; e++) {
+      const int64_t c = A.ci[e];
+      const double v = A.v[e];
+      if (c >= off && c < off + n2) {
+        Tdiag[(int64_t)j * n2 * n2 + (c - off) * n2 + p] = v;
+      } else if (j + 1 < nifc && c >= ifc_off[j + 1] && c < ifc_off[j + 1] + n2) {
+        Tsup[(int64_t)j * n2 * n2 + (c - ifc_off[j + 1]) * n2 + p] = v;
+      } else if (j > 0 && c >= ifc_off[j - 1] && c < ifc_off[j - 1] + n2) {
+        Tsub[(int64_t)(j - 1) * n2 * n2 + (c - ifc_off[j - 1]) * n2 + p] = v;
+      } else {
+        // must belong to the strip left (j) or right (j+1) of the interface
+        bool ok = false;
+        for (int s = j; s <= j + 1 && s < nstrips; s++) {
+          const int64_t b0 = (int64_t)strips[s].col0 * n2, b1 = b0 + (int64_t)strips[s].w * n2;
+          if (c >= b0 && c < b1) ok = true;
+        }
+        if (!ok) atomicOr(&status->flags, ERR_IFC_STRUCTURE);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void assemble_T(cudaStream_t st, int64_t n2, int nifc, int nstrips, const StripDesc* strips,
+                const int32_t* sym, const double* gbuf, int64_t sG, double* Tdiag, double* Tsup,
+                double* Tsub, CsrDev A, const int64_t* ifc_off, DevStatus* status) {
+  const int64_t bsz = n2 * n2 * sizeof(double);
+  SLB_CUDA_CHECK(cudaMemsetAsync(Tdiag, 0, bsz * nifc, st));
+  if (nifc > 1) {
+    SLB_CUDA_CHECK(cudaMemsetAsync(Tsup, 0, bsz * (nifc - 1), st));
+    SLB_CUDA_CHECK(cudaMemsetAsync(Tsub, 0, bsz * (nifc - 1), st));
+  }
+  direct_T_kernel<<<nifc, 256, 0, st>>>(A, n2, nifc, ifc_off, strips, nstrips, Tdiag, Tsup, Tsub, status);
+  SLB_CUDA_CHECK(cudaGetLastError());
+  const int nblocks = 3 * nifc - 2;
+  dim3 grid((unsigned)cdiv(n2, 32), (unsigned)cdiv(n2, 32), (unsigned)nblocks);
+  assemble_T_kernel<<<grid, dim3(32, 8), 0, st>>>(n2, nifc, nstrips, sym, gbuf, sG, Tdiag, Tsup, Tsub);
+  SLB_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace slb

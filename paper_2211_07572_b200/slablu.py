@@ -1,0 +1,443 @@
+"""Python mirror of the reference's solver API on top of the C ABI.
+
+Names, argument meaning and error behaviour follow the reference library
+(/root/reference/proj/include/slablu/):
+
+    ProblemSpec, poisson_log_problem, helmholtz_problem,
+    helmholtz_bump_problem, kappa_from_ppw         problem.hpp:35-48, 153-157, 210-261
+    SparseSystem, assemble_fd5                     problem.hpp:52-64, 78-132
+    error_report, sample_field                     problem.hpp:160-206
+    SolverConfig, CompressionChoice, choose_b      driver.hpp:37-66
+    GridStrip, SlabPartition, partition            partition.hpp:27-91
+    Factorization, factorize, solve                driver.hpp:72-179
+    Error, ConfigError, SingularMatrixError        common.hpp:32-60
+
+Compute runs on the B200 through libslablu_gpu.so; this module only
+marshals arguments (numpy for host data, torch CUDA tensors for the
+device-resident entry points).
+"""
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import lib
+
+
+# ---------------------------------------------------------------------------
+# errors (common.hpp:32-60)
+class Error(RuntimeError):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class SingularMatrixError(Error):
+    def __init__(self, what, index):
+        super().__init__(f"{what} (index {index})")
+        self.index = index
+
+
+class UnsupportedError(Error):
+    pass
+
+
+def _check(st):
+    if st.code == 0:
+        return
+    msg = st.msg.decode(errors="replace")
+    if st.code == 2:
+        raise ConfigError(msg)
+    if st.code == 3:
+        raise SingularMatrixError(msg, int(st.index))
+    if st.code == 6:
+        raise UnsupportedError(msg)
+    if st.code == 5:
+        raise MemoryError(msg)
+    raise Error(msg)
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def device_count():
+    return lib().slablu_gpu_device_count()
+
+
+# ---------------------------------------------------------------------------
+# problems (problem.hpp)
+ScalarField = Callable[[float, float], float]
+
+
+@dataclass
+class ProblemSpec:
+    n1: int = 0
+    n2: int = 0
+    h: float = 0.0
+    kappa: float = 0.0
+    coefficient_field: ScalarField = field(default=lambda x, y: 1.0)
+    dirichlet_data: ScalarField = field(default=lambda x, y: 0.0)
+    body_load: ScalarField = field(default=lambda x, y: 0.0)
+    canned: Optional[int] = None  # 0 poisson_log, 1 helmholtz, 2 helmholtz_bump (native fast path)
+
+
+def kappa_from_ppw(ppw, n2):
+    if not (ppw > 0.0):
+        raise ConfigError("kappa_from_ppw: ppw must be positive")
+    if n2 < 2:
+        raise ConfigError("kappa_from_ppw: n2 must be at least 2")
+    return lib().slablu_gpu_kappa_from_ppw(float(ppw), int(n2))
+
+
+def bessel_j0(t):
+    return lib().slablu_gpu_bessel_j0(float(t))
+
+
+def true_solution_poisson(x, y):
+    r = np.hypot(x + 0.1, y - 0.5)
+    if r == 0.0:
+        raise Error("true_solution_poisson: evaluated at the source point")
+    return float(np.log(r))
+
+
+def true_solution_helmholtz(x, y, kappa):
+    if kappa < 0.0:
+        raise Error("true_solution_helmholtz: kappa must be nonnegative")
+    return bessel_j0(kappa * np.hypot(x + 0.1, y - 0.5))
+
+
+def poisson_log_problem(n1, n2):
+    return ProblemSpec(n1, n2, 1.0 / (n2 + 1), 0.0, lambda x, y: 1.0,
+                       true_solution_poisson, lambda x, y: 0.0, canned=0)
+
+
+def helmholtz_problem(n1, n2, kappa):
+    return ProblemSpec(n1, n2, 1.0 / (n2 + 1), kappa, lambda x, y: 1.0,
+                       lambda x, y: true_solution_helmholtz(x, y, kappa), lambda x, y: 0.0, canned=1)
+
+
+def helmholtz_bump_problem(n1, n2, kappa):
+    def coef(x, y):
+        h = 1.0 / (n2 + 1)
+        cx, cy = 0.5 * (n1 + 1) * h, 0.5
+        return 1.0 - 0.9 * np.exp(-64.0 * ((x - cx) ** 2 + (y - cy) ** 2))
+    return ProblemSpec(n1, n2, 1.0 / (n2 + 1), kappa, coef,
+                       lambda x, y: true_solution_helmholtz(x, y, kappa), lambda x, y: 0.0, canned=2)
+
+
+@dataclass
+class SparseSystem:
+    """Assembled A u = f: CSR (Eigen RowMajor compressed form) + rhs."""
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+    rhs: np.ndarray
+    n1: int
+    n2: int
+    h: float
+
+    def dim(self):
+        return self.n1 * self.n2
+
+    def node_index(self, i, j):
+        return i * self.n2 + j
+
+    def node_coords(self):
+        i, j = np.divmod(np.arange(self.dim()), self.n2)
+        return (i + 1) * self.h, (j + 1) * self.h
+
+    def matvec(self, x):
+        """A @ x for x of shape (N,) or (N, nrhs) (host, validation only)."""
+        import scipy.sparse as sp
+        a = sp.csr_matrix((self.values, self.col_idx, self.row_ptr), shape=(self.dim(), self.dim()))
+        x = np.asarray(x, np.float64)
+        return np.asarray(a @ x.reshape(self.dim(), -1)).reshape(x.shape)
+
+
+def assemble_fd5(spec: ProblemSpec) -> SparseSystem:
+    """Five-point assembly (problem.hpp:78-132), bit-identical to the reference."""
+    n = spec.n1 * spec.n2
+    rp = np.zeros(max(n, 0) + 1, np.int32)
+    ci = np.zeros(max(5 * n, 1), np.int32)
+    v = np.zeros(max(5 * n, 1), np.float64)
+    rhs = np.zeros(max(n, 1), np.float64)
+    nnz = ctypes.c_int64()
+    if spec.canned is not None:
+        st = lib().slablu_gpu_assemble_canned(int(spec.canned), int(spec.n1), int(spec.n2), float(spec.kappa),
+                                              _p(rp), _p(ci), _p(v), _p(rhs), ctypes.byref(nnz))
+    else:
+        errs = []
+
+        def wrap(fn):
+            def cb(x, y, _u):
+                try:
+                    return float(fn(x, y))
+                except Exception as e:  # surfaced after the call
+                    errs.append(e)
+                    return float("nan")
+            return _lib.FIELD_FN(cb)
+        cbs = [wrap(spec.coefficient_field), wrap(spec.dirichlet_data), wrap(spec.body_load)]
+        st = lib().slablu_gpu_assemble_fd5(int(spec.n1), int(spec.n2), float(spec.h), float(spec.kappa),
+                                           cbs[0], cbs[1], cbs[2], None, _p(rp), _p(ci), _p(v), _p(rhs),
+                                           ctypes.byref(nnz))
+        if errs:
+            raise errs[0]
+    _check(st)
+    k = nnz.value
+    return SparseSystem(rp, ci[:k].copy(), v[:k].copy(), rhs[:n].copy(), int(spec.n1), int(spec.n2), float(spec.h))
+
+
+def sample_field(system: SparseSystem, fn: ScalarField) -> np.ndarray:
+    x, y = system.node_coords()
+    return np.array([fn(a, b) for a, b in zip(x, y)], np.float64)
+
+
+def sample_solution(kind, n1, n2, kappa=0.0):
+    out = np.zeros(n1 * n2)
+    _check(lib().slablu_gpu_sample_solution(int(kind), int(n1), int(n2), float(kappa), _p(out)))
+    return out
+
+
+def gaussian_matrix(rows, cols, seed):
+    """mt19937_64 + normal_distribution (common.hpp:72-79), column major."""
+    out = np.empty((cols, rows), np.float64)
+    lib().slablu_gpu_gaussian_matrix(int(rows), int(cols), int(seed), _p(out))
+    return out.T
+
+
+@dataclass
+class ErrorReport:
+    relerr_res: float = 0.0
+    relerr_true: float = 0.0
+    n_rhs: int = 0
+    residual_norm_is_absolute: bool = False
+    solution_norm_is_absolute: bool = False
+
+
+def error_report(system, u_calc, u_true, f=None) -> ErrorReport:
+    """problem.hpp:160-190."""
+    n = system.dim()
+    u_calc = np.asarray(u_calc).reshape(n, -1)
+    u_true = np.asarray(u_true).reshape(n, -1)
+    f = system.rhs.reshape(n, -1) if f is None else np.asarray(f).reshape(n, -1)
+    if u_calc.shape != u_true.shape or u_calc.shape[1] != f.shape[1] or u_calc.shape[1] < 1:
+        raise Error("error_report: column counts must agree")
+    rep = ErrorReport(n_rhs=u_calc.shape[1])
+    res = np.linalg.norm(system.matvec(u_calc) - f)
+    fn = np.linalg.norm(f)
+    if fn > 0:
+        rep.relerr_res = res / fn
+    else:
+        rep.relerr_res, rep.residual_norm_is_absolute = res, True
+    err = np.linalg.norm(u_calc - u_true)
+    un = np.linalg.norm(u_true)
+    if un > 0:
+        rep.relerr_true = err / un
+    else:
+        rep.relerr_true, rep.solution_norm_is_absolute = err, True
+    return rep
+
+
+# ---------------------------------------------------------------------------
+# configuration and geometry (driver.hpp:37-66, partition.hpp)
+class CompressionChoice(enum.IntEnum):
+    automatic = 0
+    dense = 1
+    hbs = 2
+
+
+@dataclass
+class SolverConfig:
+    b: int = 0
+    c: float = 0.6
+    compression: CompressionChoice = CompressionChoice.automatic
+    hbs_tol: float = 1e-11
+    hbs_trunc_rel: float = 1e-13
+    hbs_leaf_size: int = 64
+    seed: int = 0
+    threads: int = 1
+    device: int = 0
+    keep_T: bool = False
+
+    def _c(self):
+        return _lib.Config(int(self.b), float(self.c), int(self.compression), int(self.seed),
+                           int(self.threads), int(self.device), int(bool(self.keep_T)))
+
+
+def choose_b(n1, n2, config: SolverConfig = SolverConfig()):
+    out = ctypes.c_int64()
+    _check(lib().slablu_gpu_choose_b(int(n1), int(n2), int(config.b), float(config.c), ctypes.byref(out)))
+    return out.value
+
+
+@dataclass
+class GridStrip:
+    first_col: int
+    width: int
+
+
+@dataclass
+class SlabPartition:
+    n1: int
+    n2: int
+    b: int
+    interfaces: List[GridStrip]
+    interiors: List[GridStrip]
+
+    def interface_count(self):
+        return len(self.interfaces)
+
+    def interior_count(self):
+        return len(self.interiors)
+
+    def dim(self):
+        return self.n1 * self.n2
+
+    def interface_offset(self, j):
+        return self.interfaces[j].first_col * self.n2
+
+    def interior_offset(self, i):
+        return self.interiors[i].first_col * self.n2
+
+    def interior_size(self, i):
+        return self.interiors[i].width * self.n2
+
+    def left_interior(self, j):
+        return j
+
+    def right_interior(self, j):
+        return j + 1 if j + 1 < self.interior_count() else -1
+
+
+def partition(n1, n2, b) -> SlabPartition:
+    cap = max(int(n1) + 2, 4)
+    ints = np.zeros(2 * cap, np.int64)
+    ifcs = np.zeros(2 * cap, np.int64)
+    ni, nf = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().slablu_gpu_partition(int(n1), int(n2), int(b), ctypes.byref(ni), _p(ints), ctypes.byref(nf),
+                                      _p(ifcs), cap))
+    return SlabPartition(int(n1), int(n2), int(b),
+                         [GridStrip(int(ifcs[2 * k]), int(ifcs[2 * k + 1])) for k in range(nf.value)],
+                         [GridStrip(int(ints[2 * k]), int(ints[2 * k + 1])) for k in range(ni.value)])
+
+
+# ---------------------------------------------------------------------------
+# factorize / solve (driver.hpp:72-179)
+class Factorization:
+    """Immutable two-stage factorization held on the GPU."""
+
+    def __init__(self, handle, config):
+        self._h = ctypes.c_void_p(handle)
+        st = _lib.Stats()
+        _check(lib().slablu_gpu_stats(self._h, ctypes.byref(st)))
+        self.n1, self.n2, self.b = int(st.n1), int(st.n2), int(st.b)
+        self.config = SolverConfig(**{**config.__dict__, "b": int(st.b),
+                                      "compression": CompressionChoice.dense})
+        self.t_stage1, self.t_stage2 = float(st.t_stage1), float(st.t_stage2)
+        self.storage_stage1, self.storage_stage2 = int(st.storage_stage1), int(st.storage_stage2)
+        self.hbs_max_rank = 0
+        self.stats = st
+        self.part = None if st.single_slab else partition(self.n1, self.n2, self.b)
+
+    def single_slab(self):
+        return bool(self.stats.single_slab)
+
+    def storage_scalars(self):
+        return self.storage_stage1 + self.storage_stage2
+
+    def refresh_stats(self):
+        st = _lib.Stats()
+        _check(lib().slablu_gpu_stats(self._h, ctypes.byref(st)))
+        self.stats = st
+        return st
+
+    def T_block(self, which, j):
+        n2 = self.n2
+        out = np.empty((n2, n2), order="F")
+        _check(lib().slablu_gpu_T_block(self._h, {"diag": 0, "super": 1, "sub": 2}[which], int(j), _p(out)))
+        return out
+
+    def reduce_rhs(self, f):
+        n = self.n1 * self.n2
+        f = np.asfortranarray(np.asarray(f, np.float64).reshape(n, -1))
+        k = self.stats.interfaces
+        out = np.empty((k * self.n2, f.shape[1]), order="F")
+        _check(lib().slablu_gpu_reduce_rhs(self._h, _p(f), f.shape[1], _p(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().slablu_gpu_destroy(self._h)
+            self._h = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def factorize(system: SparseSystem, config: SolverConfig = SolverConfig()) -> Factorization:
+    if system.dim() == 0:
+        raise ConfigError("factorize: empty system")
+    h = ctypes.c_void_p()
+    cfg = config._c()
+    rp = np.ascontiguousarray(system.row_ptr, np.int32)
+    ci = np.ascontiguousarray(system.col_idx, np.int32)
+    v = np.ascontiguousarray(system.values, np.float64)
+    _check(lib().slablu_gpu_factorize(system.n1, system.n2, _p(rp), _p(ci), _p(v), ctypes.byref(cfg),
+                                      ctypes.byref(h)))
+    return Factorization(h.value, config)
+
+
+def factorize_device(n1, n2, row_ptr, col_idx, values, config: SolverConfig = SolverConfig()) -> Factorization:
+    """CSR already resident on the GPU (torch CUDA tensors int32/int32/float64)."""
+    h = ctypes.c_void_p()
+    cfg = config._c()
+    _check(lib().slablu_gpu_factorize_device(int(n1), int(n2), int(values.numel()), row_ptr.data_ptr(),
+                                             col_idx.data_ptr(), values.data_ptr(), ctypes.byref(cfg),
+                                             ctypes.byref(h)))
+    return Factorization(h.value, config)
+
+
+def solve(fact: Factorization, f) -> np.ndarray:
+    """u = A^{-1} f for host f of shape (N,) or (N, nrhs); returns (N, nrhs)."""
+    n = fact.n1 * fact.n2
+    f = np.asarray(f, np.float64)
+    if f.shape[0] != n:
+        raise Error("solve: rhs length must equal the grid size")
+    f2 = np.asfortranarray(f.reshape(n, -1))
+    u = np.empty_like(f2, order="F")
+    _check(lib().slablu_gpu_solve(fact._h, _p(f2), n, f2.shape[1], _p(u), n))
+    return u
+
+
+def solve_device(fact: Factorization, f, u):
+    """Device-resident solve: f, u are torch CUDA float64 tensors of shape (nrhs, N) (column-major N x nrhs)."""
+    n = fact.n1 * fact.n2
+    nrhs = f.shape[0] if f.dim() == 2 else 1
+    _check(lib().slablu_gpu_solve_device(fact._h, f.data_ptr(), n, nrhs, u.data_ptr(), n))
+    return u
+
+
+def run_problem(spec: ProblemSpec, config: SolverConfig = SolverConfig()):
+    """driver.hpp:268-292: assemble, factorize, solve, error report (GPU times)."""
+    import time
+    system = assemble_fd5(spec)
+    fact = factorize(system, config)
+    t0 = time.perf_counter()
+    u = solve(fact, system.rhs)
+    t_solve = time.perf_counter() - t0
+    u_true = (sample_solution(spec.canned, spec.n1, spec.n2, spec.kappa) if spec.canned is not None
+              else sample_field(system, spec.dirichlet_data))
+    rep = error_report(system, u, u_true)
+    return {"N": system.dim(), "n1": spec.n1, "n2": spec.n2, "b": fact.b, "kappa": spec.kappa,
+            "T_factor_stage1_s": fact.t_stage1, "T_factor_stage2_s": fact.t_stage2, "T_solve_s": t_solve,
+            "M_factor_scalars": fact.storage_scalars(), "relerr_res": rep.relerr_res,
+            "relerr_true": rep.relerr_true, "hbs_max_rank": 0, "seed": config.seed}
