@@ -9,12 +9,11 @@
 // Wp-padded blocks (Wp = round_up(b, 8); padded unknowns are decoupled
 // identity rows that never win a pivot):
 //
-//   panel  P_l = [S_l ; Lsub_{l+1}]  (2Wp x Wp)      -> perm_l (window pivots)
-//   A11 = (perm_l P_l)_top, B = (perm_l P_l)_bot
-//   Ainv_l = A11^{-1}   (Gauss-Jordan, pivots known)
-//   Fbot_l = -B Ainv_l
-//   R  = perm_l [V_l 0 ; D_{l+1} Usup_{l+1}] = [R1 ; R2]
-//   H_l = Ainv_l R1,  [S_{l+1} | V_{l+1}] = R2 - B H_l
+//   panel  perm_l [S_l ; Lsub_{l+1}] = [L11 ; L21] U11   (window pivots, 2Wp x Wp)
+//   R = perm_l [V_l 0 ; D_{l+1} Usup_{l+1}] = [R1 ; R2]
+//   U1213 = L11^{-1} R1,  [S_{l+1} | V_{l+1}] = R2 - L21 U1213      (the chain)
+// and, after the chain, for every level in parallel (convert_levels):
+//   Ainv_l = U11^{-1} L11^{-1},  Fbot_l = -L21 L11^{-1},  H_l = U11^{-1} U1213
 //
 // so that A_ii^{-1} b is the pure-GEMM sweep
 //   forward  t = perm_l [z_l ; b_{l+1}],  y_l = Ainv_l t_top,  z_{l+1} = t_bot + Fbot_l t_top
@@ -142,38 +141,45 @@ __global__ void init_sv_kernel(int Wp, const double* nx0, int64_t sNX, double* s
 }
 
 // ---------------------------------------------------------------------------
-// One level step for every strip: window-pivoted panel LU (pivot order only),
-// Gauss-Jordan inverse of the pivot block, and the gathers feeding the GEMMs.
-// grid = nstrips, block = 1024.
-__global__ void __launch_bounds__(1024) level_panel_kernel(LevelArgs a) {
+// One level step for every strip: LU with partial pivoting of the panel
+// P_l = [S_l ; Lsub_{l+1}] (2Wp x Wp) restricted to dgbtrf's window (rows
+// k..k+Wp at column k; a circular buffer of Wp+1 rows in shared memory).
+// Outputs into the level slot (LU form, converted later by convert_levels):
+//   LU11 (row-major Wp x Wp: unit-lower multipliers + U11), L21 (row-major),
+//   U1213 <- R1 = top rows of perm_l [V_l 0 ; D_{l+1} Usup_{l+1}] (col-major Wp x 2Wp),
+// and sv_out <- R2 = bottom rows.  The chain then forms
+//   U1213 = L11^{-1} R1 (trsm_small_batched) and [S|V]_{l+1} = R2 - L21 U1213 (GEMM).
+// grid = nstrips, block = 512.
+__global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   extern __shared__ double smem[];
   const int Wp = a.Wp, NW = Wp + 1, RS = Wp + 1;
   double* win = smem;            // NW * RS
   double* prow = win + NW * RS;  // Wp + 1
-  double* fcol = prow + Wp + 1;  // Wp + 1
-  int* perm = reinterpret_cast<int*>(fcol + Wp + 1);  // 2 Wp
-  __shared__ int s_piv;
+  int* perm = reinterpret_cast<int*>(prow + Wp + 1);  // 2 Wp
   __shared__ int s_sing;
 
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const double* SV = a.sv_in + s * a.sSV;
   const double* NX = a.has_next ? a.nx + s * a.sNX : nullptr;
+  double* slot = a.slot + s * a.sF;
+  double* LU11 = slot;
+  double* L21 = slot + (int64_t)Wp * Wp;
+  double* U1213 = slot + 2LL * Wp * Wp;
   const int rows_total = a.has_next ? 2 * Wp : Wp;
+  auto slot_of = [&](int pos) { return pos < NW ? pos : pos - NW; };
   auto Pval = [&](int p, int j) -> double {
     return p < Wp ? SV[(int64_t)j * Wp + p] : NX[(int64_t)j * Wp + (p - Wp)];
   };
   if (tid == 0) s_sing = 0;
 
-  // ---- phase 1: window LU, pivot order only --------------------------------
   const int init_rows = rows_total < NW ? rows_total : NW;
   for (int idx = tid; idx < init_rows * Wp; idx += blockDim.x) {
     const int j = idx / init_rows, p = idx % init_rows;
     win[p * RS + j] = Pval(p, j);
   }
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm[p] = p;
-  // register prefetch of the next entering bottom row (position Wp + 1 + k -> bottom row k + 1)
-  double nextv = 0.0;
+  double nextv = 0.0;  // register prefetch of the next entering bottom row
   if (a.has_next && tid < Wp && Wp > 1) nextv = NX[(int64_t)tid * Wp + 1];
   __syncthreads();
 
@@ -181,9 +187,9 @@ __global__ void __launch_bounds__(1024) level_panel_kernel(LevelArgs a) {
     const int hi = min(k + Wp, rows_total - 1);
     if (warp == 0) {
       double best = -1.0;
-      int bpos = INT_MAX;
+      int bpos = 0x7fffffff;
       for (int pos = k + lane; pos <= hi; pos += 32) {
-        const double v = fabs(win[(pos % NW) * RS + k]);
+        const double v = fabs(win[slot_of(pos) * RS + k]);
         if (v > best) {
           best = v;
           bpos = pos;
@@ -199,13 +205,13 @@ __global__ void __launch_bounds__(1024) level_panel_kernel(LevelArgs a) {
         }
       }
       int r = bpos;
-      if (!(best > 0.0)) {  // exactly singular (or NaN) column
+      if (!(best > 0.0)) {
         r = k;
         if (lane == 0) s_sing = 1;
       }
+      double* rk = win + slot_of(k) * RS;
       if (r != k) {
-        double* rk = win + (k % NW) * RS;
-        double* rr = win + (r % NW) * RS;
+        double* rr = win + slot_of(r) * RS;
         for (int j = lane; j < Wp; j += 32) {
           const double t = rk[j];
           rk[j] = rr[j];
@@ -218,88 +224,94 @@ __global__ void __launch_bounds__(1024) level_panel_kernel(LevelArgs a) {
         }
         __syncwarp();
       }
-      const double* rk = win + (k % NW) * RS;
       for (int j = lane; j < Wp; j += 32) prow[j] = rk[j];
     }
     __syncthreads();
+    // retire position k (a final LU11 row), scale + update rows below
+    for (int j = tid; j < Wp; j += blockDim.x) LU11[(int64_t)k * Wp + j] = prow[j];
     const double pv = prow[k];
     const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
     for (int pos = k + 1 + warp; pos <= hi; pos += nwarps) {
-      double* row = win + (pos % NW) * RS;
+      double* row = win + slot_of(pos) * RS;
       const double m = row[k] * inv;
+      __syncwarp();
+      if (lane == 0) row[k] = m;
       if (m != 0.0)
         for (int j = k + 1 + lane; j < Wp; j += 32) row[j] = fma(-m, prow[j], row[j]);
     }
     // entering row: position k + Wp + 1 = bottom row k + 1, into the freed slot of position k
-    if (k + Wp + 1 < rows_total) {
-      if (tid < Wp) win[(k % NW) * RS + tid] = nextv;
-      if (tid < Wp && k + 2 < Wp) nextv = NX[(int64_t)tid * Wp + (k + 2)];
+    if (k + Wp + 1 < rows_total && tid < Wp) {
+      win[slot_of(k) * RS + tid] = nextv;
+      if (k + 2 < Wp) nextv = NX[(int64_t)tid * Wp + (k + 2)];
     }
     __syncthreads();
   }
 
-  // ---- gathers: perm, Bsel, R1, R2 (-> sv_out) ---------------------------------
   int32_t* perm_out = a.perm + s * a.sP;
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm_out[p] = perm[p];
   if (a.has_next) {
+    // L21: positions Wp..2Wp-1
+    for (int idx = tid; idx < Wp * Wp; idx += blockDim.x) {
+      const int i = idx / Wp, j = idx % Wp;
+      L21[idx] = win[slot_of(Wp + i) * RS + j];
+    }
     const double* V = SV + (int64_t)Wp * Wp;
     auto Rval = [&](int p, int c) -> double {
       if (p < Wp) return c < Wp ? V[(int64_t)c * Wp + p] : 0.0;
-      return NX[(int64_t)(Wp + c) * Wp + (p - Wp)];  // [D | Usup] columns Wp..3Wp-1 of NX
+      return NX[(int64_t)(Wp + c) * Wp + (p - Wp)];  // [D | Usup] = NX columns Wp..3Wp-1
     };
-    double* bsel = a.bsel + s * a.sScr;
-    double* r1 = a.r1 + s * a.sScr;
     double* r2 = a.sv_out + s * a.sSV;
-    for (int idx = tid; idx < Wp * Wp; idx += blockDim.x) {
-      const int j = idx / Wp, i = idx % Wp;
-      bsel[idx] = Pval(perm[Wp + i], j);
-    }
     for (int idx = tid; idx < 2 * Wp * Wp; idx += blockDim.x) {
       const int c = idx / Wp, i = idx % Wp;
-      r1[idx] = Rval(perm[i], c);
+      U1213[idx] = Rval(perm[i], c);
       r2[idx] = Rval(perm[Wp + i], c);
     }
-  }
-  // A11 = pivot-ordered top rows of the original panel, row-major in win
-  for (int idx = tid; idx < Wp * Wp; idx += blockDim.x) {
-    const int j = idx / Wp, i = idx % Wp;
-    win[i * RS + j] = Pval(perm[i], j);
-  }
-  __syncthreads();
-
-  // ---- phase 2: in-place Gauss-Jordan inverse of A11 (pivots known) -------------
-  for (int k = 0; k < Wp; k++) {
-    const double piv = win[k * RS + k];
-    const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
-    if (piv == 0.0 && tid == 0) s_sing = 1;
-    if (tid < Wp) fcol[tid] = tid == k ? 0.0 : win[tid * RS + k];
-    else if (tid < 2 * Wp) {
-      const int j = tid - Wp;
-      prow[j] = (j == k ? 1.0 : win[k * RS + j]) * ip;
-    }
-    __syncthreads();
-    for (int i = warp; i < Wp; i += nwarps) {
-      double* row = win + i * RS;
-      if (i == k) {
-        for (int j = lane; j < Wp; j += 32) row[j] = prow[j];
-      } else {
-        const double f = fcol[i];
-        for (int j = lane; j < Wp; j += 32) {
-          const double base = j == k ? 0.0 : row[j];
-          row[j] = fma(-f, prow[j], base);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  double* ainv = a.ainv + s * a.sF;
-  for (int idx = tid; idx < Wp * Wp; idx += blockDim.x) {
-    const int j = idx / Wp, i = idx % Wp;
-    ainv[idx] = win[i * RS + j];
+  } else {
+    for (int idx = tid; idx < 3 * Wp * Wp; idx += blockDim.x) L21[idx] = 0.0;  // L21 and U1213
   }
   if (tid == 0 && s_sing) {
     atomicOr(&a.status->flags, ERR_SINGULAR);
     atomicMin(&a.status->singular_strip, s);
+  }
+}
+
+// Conversion helpers (per strip, all levels batched): X = [I | U1213] and
+// the final packing of [Ainv | H] and Fbot into DMMA fragment order.
+__global__ void convert_init_kernel(int Wp, const double* slots, int64_t lvl, double* X, int64_t sX) {
+  const int64_t l = blockIdx.y;
+  const double* U = slots + l * lvl + 2LL * Wp * Wp;
+  double* x = X + l * sX;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 3 * Wp * Wp; idx += gridDim.x * blockDim.x) {
+    const int c = idx / Wp, r = idx % Wp;
+    x[idx] = c < Wp ? (r == c ? 1.0 : 0.0) : U[(int64_t)(c - Wp) * Wp + r];
+  }
+}
+
+// out (per level, 4 Wp^2): F = [Ainv ; Fbot] (2Wp x Wp) then H (Wp x 2Wp), fragment order
+__global__ void convert_pack_kernel(int Wp, const double* X, int64_t sX, const double* Fb, int64_t sFb,
+                                    double* slots, int64_t lvl) {
+  const int64_t l = blockIdx.y;
+  const double* AH = X + l * sX;    // [Ainv | H] col-major Wp x 3Wp
+  const double* F1 = Fb + l * sFb;  // Fbot col-major Wp x Wp
+  double* o = slots + l * lvl;
+  const int64_t nF = 2LL * Wp * Wp;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * nF;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(idx & 31);
+    const int g = lane >> 2, t = lane & 3;
+    if (idx < nF) {
+      const int64_t q = idx >> 5;
+      const int MT = 2 * Wp / 8;
+      const int mt = (int)(q % MT), ks = (int)(q / MT);
+      const int m = mt * 8 + g, k = ks * 4 + t;
+      o[idx] = m < Wp ? AH[(int64_t)k * Wp + m] : F1[(int64_t)k * Wp + (m - Wp)];
+    } else {
+      const int64_t q = (idx - nF) >> 5;
+      const int MT = Wp / 8;
+      const int mt = (int)(q % MT), ks = (int)(q / MT);
+      const int m = mt * 8 + g, k = ks * 4 + t;
+      o[idx] = AH[(int64_t)(Wp + k) * Wp + m];
+    }
   }
 }
 
@@ -327,61 +339,31 @@ void init_sv(cudaStream_t st, int nstrips, int Wp, const double* nx0, int64_t sN
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
-void level_panel(cudaStream_t st, const LevelArgs& a) {
+void level_lu(cudaStream_t st, const LevelArgs& a) {
   const int Wp = a.Wp;
-  const size_t smem = (size_t)((Wp + 1) * (Wp + 1) + 2 * (Wp + 1)) * sizeof(double) + 2 * Wp * sizeof(int);
+  const size_t smem = (size_t)((Wp + 1) * (Wp + 1) + (Wp + 1)) * sizeof(double) + 2 * Wp * sizeof(int);
   static size_t attr = 0;
   if (smem > attr) {
-    SLB_CUDA_CHECK(cudaFuncSetAttribute(level_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  level_panel_kernel<<<a.nstrips, 1024, smem, st>>>(a);
+  level_lu_kernel<<<a.nstrips, 512, smem, st>>>(a);
+  SLB_CUDA_CHECK(cudaGetLastError());
+}
+
+// LU form -> GEMM form for levels [0, nl) of one strip (slots at stride lvl):
+//   Linv = L11^{-1};  Fbot = -L21 Linv;  [Ainv | H] = U11^{-1} [Linv | U1213];  pack.
+void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* X, double* Fb) {
+  const int64_t sX = 3LL * Wp * Wp, sFb = (int64_t)Wp * Wp;
+  convert_init_kernel<<<dim3((unsigned)cdiv(3 * Wp * Wp, 256), (unsigned)nl), 256, 0, st>>>(Wp, slots, lvl, X, sX);
+  SLB_CUDA_CHECK(cudaGetLastError());
+  trsm_small_batched(st, true, Wp, slots, Wp, lvl, X, Wp, sX, Wp, nl);
+  dgemm_batched(st, Wp, Wp, Wp, -1.0, slots + (int64_t)Wp * Wp, Wp, lvl, X, Wp, sX, 0.0, Fb, Wp, sFb, nl, true);
+  trsm_small_batched(st, false, Wp, slots, Wp, lvl, X, Wp, sX, 3 * Wp, nl);
+  convert_pack_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(4LL * Wp * Wp, 256), 64), (unsigned)nl), 256, 0, st>>>(
+      Wp, X, sX, Fb, sFb, slots, lvl);
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
 }  // namespace slb
 
-// ---------------------------------------------------------------------------
-// Pack one level's col-major factors into the DMMA fragment order used by
-// the sweeps (schur.cu, solve.cu).  Per level (4 Wp^2 doubles):
-//   F = [Ainv ; Fbot]  (2Wp x Wp):  [k4 step][m8 tile][lane]  (lane = 4g + t -> F[8mt+g][4ks+t])
-//   H                  (Wp x 2Wp):  same order, at offset 2 Wp^2
-namespace slb {
-namespace {
-__global__ void pack_level_kernel(int Wp, const double* ainv, const double* fbot, const double* h,
-                                  int64_t sScr, double* out, int64_t sF) {
-  const int s = blockIdx.y;
-  const double* A0 = ainv + s * sScr;
-  const double* F1 = fbot + s * sScr;
-  const double* H = h + s * sScr;
-  double* o = out + s * sF;
-  const int64_t nF = 2LL * Wp * Wp;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * nF;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int lane = (int)(idx & 31);
-    const int g = lane >> 2, t = lane & 3;
-    if (idx < nF) {
-      const int64_t q = idx >> 5;
-      const int MT = 2 * Wp / 8;
-      const int mt = (int)(q % MT), ks = (int)(q / MT);
-      const int m = mt * 8 + g, k = ks * 4 + t;
-      o[idx] = m < Wp ? A0[(int64_t)k * Wp + m] : F1[(int64_t)k * Wp + (m - Wp)];
-    } else {
-      const int64_t q = (idx - nF) >> 5;
-      const int MT = Wp / 8;
-      const int mt = (int)(q % MT), ks = (int)(q / MT);
-      const int m = mt * 8 + g, k = ks * 4 + t;
-      o[idx] = H[(int64_t)k * Wp + m];
-    }
-  }
-}
-}  // namespace
-
-void pack_level(cudaStream_t st, int nstrips, int Wp, const double* ainv, const double* fbot,
-                const double* h, int64_t sScr, double* out, int64_t sF) {
-  const int64_t total = 4LL * Wp * Wp;
-  dim3 grid((unsigned)std::min<int64_t>(cdiv(total, 256), 64), (unsigned)nstrips);
-  pack_level_kernel<<<grid, 256, 0, st>>>(Wp, ainv, fbot, h, sScr, out, sF);
-  SLB_CUDA_CHECK(cudaGetLastError());
-}
-}  // namespace slb

@@ -175,46 +175,6 @@ __global__ void laswp_kernel(double* A, int64_t lda, int64_t c0, int64_t c1, con
   }
 }
 
-// Leaf triangular solve: L (m x m, m <= 64) against B (m x ncols), one
-// thread per column.  lower: unit-lower forward; else upper (non-unit) backward.
-template <bool LOWER>
-__global__ void trsm_leaf_kernel(const double* L, int64_t ldl, int m, double* B, int64_t ldb,
-                                 int64_t ncols) {
-  __shared__ double sL[64][65];
-  for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-    const int c = idx / m, rr = idx % m;
-    sL[rr][c] = L[c * ldl + rr];
-  }
-  __syncthreads();
-  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= ncols) return;
-  double x[64];
-  double* b = B + col * ldb;
-#pragma unroll
-  for (int rr = 0; rr < 64; rr++) x[rr] = rr < m ? b[rr] : 0.0;
-  if (LOWER) {
-#pragma unroll
-    for (int c = 0; c < 64; c++) {
-      if (c >= m) break;
-#pragma unroll
-      for (int rr = c + 1; rr < 64; rr++)
-        if (rr < m) x[rr] = fma(-sL[rr][c], x[c], x[rr]);
-    }
-  } else {
-#pragma unroll
-    for (int c = 63; c >= 0; c--) {
-      if (c >= m) continue;
-      x[c] = x[c] / sL[c][c];
-#pragma unroll
-      for (int rr = 0; rr < 64; rr++)
-        if (rr < c) x[rr] = fma(-sL[rr][c], x[c], x[rr]);
-    }
-  }
-#pragma unroll
-  for (int rr = 0; rr < 64; rr++)
-    if (rr < m) b[rr] = x[rr];
-}
-
 __global__ void finite_kernel(const double* a, int64_t count, DevStatus* status) {
   bool bad = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
@@ -265,10 +225,8 @@ void laswp(cudaStream_t st, double* A, int64_t lda, int64_t c0, int64_t c1, cons
 void trsm(cudaStream_t st, bool lower, const double* L, int64_t ldl, int64_t m, double* B, int64_t ldb,
           int64_t ncols) {
   if (m <= 0 || ncols <= 0) return;
-  if (m <= 64) {
-    if (lower) trsm_leaf_kernel<true><<<(unsigned)cdiv(ncols, 128), 128, 0, st>>>(L, ldl, (int)m, B, ldb, ncols);
-    else trsm_leaf_kernel<false><<<(unsigned)cdiv(ncols, 128), 128, 0, st>>>(L, ldl, (int)m, B, ldb, ncols);
-    SLB_CUDA_CHECK(cudaGetLastError());
+  if (m <= 128) {
+    trsm_small_batched(st, lower, (int)m, L, ldl, 0, B, ldb, 0, ncols, 1, /*rowmajor=*/false);
     return;
   }
   const int64_t h = round_up(m / 2, 64) < m ? round_up(m / 2, 64) : m / 2;

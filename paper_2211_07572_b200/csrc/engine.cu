@@ -307,12 +307,10 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
 
   const int64_t LCH = std::min<int64_t>(n2, 64);
   const int64_t sNX = LCH * 3 * Wp * Wp;
-  DBuf<double> nx, sv, scr, gath;
+  DBuf<double> nx, sv;
   nx.alloc(dev, (size_t)S * sNX);
   sv.alloc(dev, (size_t)2 * S * 2 * Wp * Wp);
-  scr.alloc(dev, (size_t)S * lvl);        // [Ainv | Fbot | H] col-major per strip
-  gath.alloc(dev, (size_t)S * 3 * Wp * Wp);  // [Bsel | R1]
-  const int64_t sSV = 2LL * Wp * Wp, sScr = lvl, sG3 = 3LL * Wp * Wp;
+  const int64_t sSV = 2LL * Wp * Wp;
   double* svb[2] = {sv.p, sv.p + (size_t)S * sSV};
   extract_levels(st, A, F->strips.p, S, n2, Wp, 0, LCH, nx.p, sNX, F->status.p);
   init_sv(st, S, Wp, nx.p, sNX, svb[0], sSV);
@@ -334,38 +332,37 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     la.nx = has_next ? nx.p + (nxt % LCH) * 3 * Wp * Wp : nullptr;
     la.sNX = sNX;
     la.sv_out = svb[1 - cur];
-    la.ainv = scr.p;
-    la.sF = sScr;
+    la.slot = F->fac.p + l * lvl;
+    la.sF = F->sF;
     la.perm = F->perm.p + l * 2 * Wp;
     la.sP = F->sP;
-    la.bsel = gath.p;
-    la.r1 = gath.p + (size_t)Wp * Wp;
-    la.sScr = sG3;
     la.status = F->status.p;
     la.level = (int32_t)l;
-    level_panel(st, la);
+    level_lu(st, la);
     g_launches++;
-    double* ainv = scr.p;
-    double* fbot = scr.p + (size_t)Wp * Wp;
-    double* hh = scr.p + (size_t)2 * Wp * Wp;
     if (has_next) {
-      dgemm_batched(st, Wp, 2 * Wp, Wp, 1.0, ainv, Wp, sScr, la.r1, Wp, sG3, 0.0, hh, Wp, sScr, S);
-      dgemm_batched(st, Wp, Wp, Wp, -1.0, la.bsel, Wp, sG3, ainv, Wp, sScr, 0.0, fbot, Wp, sScr, S);
-      dgemm_batched(st, Wp, 2 * Wp, Wp, -1.0, la.bsel, Wp, sG3, hh, Wp, sScr, 1.0, svb[1 - cur], Wp, sSV, S);
-      g_launches += 3;
-    } else {
-      for (int s = 0; s < S; s++)
-        SLB_CUDA_CHECK(cudaMemsetAsync(fbot + s * sScr, 0, 3 * Wp * Wp * sizeof(double), st));
+      double* LU11 = la.slot;
+      double* L21 = la.slot + (size_t)Wp * Wp;
+      double* U1213 = la.slot + (size_t)2 * Wp * Wp;
+      trsm_small_batched(st, true, Wp, LU11, Wp, F->sF, U1213, Wp, F->sF, 2 * Wp, S);
+      dgemm_batched(st, Wp, 2 * Wp, Wp, -1.0, L21, Wp, F->sF, U1213, Wp, F->sF, 1.0, svb[1 - cur], Wp, sSV, S, true);
+      g_launches += 2;
     }
-    pack_level(st, S, Wp, ainv, fbot, hh, sScr, F->fac.p + l * lvl, F->sF);
-    g_launches++;
     cur = 1 - cur;
   }
-  SLB_CUDA_CHECK(cudaEventRecord(ec, st));
   nx.release();
   sv.release();
-  scr.release();
-  gath.release();
+  // LU form -> GEMM-form sweep operators, all levels in parallel (per strip)
+  {
+    DBuf<double> X, Fb;
+    X.alloc(dev, (size_t)n2 * 3 * Wp * Wp);
+    Fb.alloc(dev, (size_t)n2 * Wp * Wp);
+    for (int s = 0; s < S; s++) {
+      convert_levels(st, Wp, F->fac.p + s * F->sF, lvl, n2, X.p, Fb.p);
+      g_launches += 5;
+    }
+  }
+  SLB_CUDA_CHECK(cudaEventRecord(ec, st));
   {
     DevStatus hs;
     SLB_CUDA_CHECK(cudaMemcpyAsync(&hs, F->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
@@ -836,6 +833,56 @@ slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* F, const double* 
     SLB_CUDA_CHECK(cudaStreamSynchronize(st));
     SLB_CUDA_CHECK(cudaMemcpy(out, red.p, K * nrhs * sizeof(double), cudaMemcpyDeviceToHost));
   })
+}
+
+// Micro-benchmark of the stage-two building blocks at block size n (device
+// time, CUDA events): out[0] GEMM n^3, out[1] getrf, out[2] inverse via getrs(I).
+int slablu_gpu_debug_dense_bench(int64_t n, int device, double* out) {
+  try {
+    SLB_CUDA_CHECK(cudaSetDevice(device));
+    cudaStream_t st;
+    SLB_CUDA_CHECK(cudaStreamCreate(&st));
+    DBuf<double> A, B, C;
+    DBuf<int32_t> ipiv;
+    DBuf<DevStatus> status;
+    A.alloc(device, n * n);
+    B.alloc(device, n * n);
+    C.alloc(device, n * n);
+    ipiv.alloc(device, n);
+    status.alloc(device, 1);
+    DevStatus st0{0, INT_MAX, INT_MAX, 0};
+    SLB_CUDA_CHECK(cudaMemcpy(status.p, &st0, sizeof(st0), cudaMemcpyHostToDevice));
+    std::vector<double> h(n * n);
+    uint64_t x = 88172645463325252ULL;
+    for (auto& v : h) {
+      x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+      v = (double)(x >> 11) / 9007199254740992.0 - 0.5;
+    }
+    for (int64_t i = 0; i < n; i++) h[i * n + i] += 0.0;  // general (pivoting exercised)
+    SLB_CUDA_CHECK(cudaMemcpy(A.p, h.data(), n * n * sizeof(double), cudaMemcpyHostToDevice));
+    SLB_CUDA_CHECK(cudaMemcpy(B.p, h.data(), n * n * sizeof(double), cudaMemcpyHostToDevice));
+    cudaEvent_t ev[4];
+    for (auto& e0 : ev) SLB_CUDA_CHECK(cudaEventCreate(&e0));
+    SLB_CUDA_CHECK(cudaEventRecord(ev[0], st));
+    dgemm_batched(st, n, n, n, 1.0, A.p, n, 0, B.p, n, 0, 0.0, C.p, n, 0, 1);
+    SLB_CUDA_CHECK(cudaEventRecord(ev[1], st));
+    dgetrf(st, n, A.p, ipiv.p, nullptr, status.p, 0);
+    SLB_CUDA_CHECK(cudaEventRecord(ev[2], st));
+    dset_identity(st, B.p, n);
+    dgetrs(st, n, n, A.p, ipiv.p, B.p, n, nullptr);
+    SLB_CUDA_CHECK(cudaEventRecord(ev[3], st));
+    SLB_CUDA_CHECK(cudaEventSynchronize(ev[3]));
+    float ms;
+    for (int i = 0; i < 3; i++) {
+      SLB_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      out[i] = ms * 1e-3;
+    }
+    for (auto& e0 : ev) cudaEventDestroy(e0);
+    cudaStreamDestroy(st);
+    return 0;
+  } catch (...) {
+    return 1;
+  }
 }
 
 void slablu_gpu_destroy(slablu_gpu_fact* fact) {

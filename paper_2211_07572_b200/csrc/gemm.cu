@@ -1,7 +1,7 @@
 // Batched FP64 GEMM on the DMMA pipe (sm_100a):
 //   C[b] = alpha * A[b] * B[b] + beta * C[b]     (column major, strided batch)
-// Optional row gather on B (B row r read from row brow[r]) lets the
-// band-LU level step apply its panel permutation for free.
+// A may be stored transposed (transA: element (m, k) at A[m * lda + k]),
+// which is how the band-LU chain keeps its row-major L factors.
 //
 // Tiling: 128x128x16 CTA tile, 8 warps each owning 64x32 (8x4 m8n8 DMMA
 // tiles), 3-stage cp.async pipeline, padded smem (stride = 4 mod 16 doubles).
@@ -25,8 +25,7 @@ struct GemmArgs {
   int64_t ldb, sB;
   double* C;
   int64_t ldc, sC;
-  const int32_t* brow;  // optional row map for B (per batch stride sBrow)
-  int64_t sBrow;
+  int transA;
 };
 
 __global__ void __launch_bounds__(THREADS) dgemm_kernel(GemmArgs p) {
@@ -37,7 +36,6 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(GemmArgs p) {
   const double* A = p.A + bz * p.sA;
   const double* B = p.B + bz * p.sB;
   double* C = p.C + bz * p.sC;
-  const int32_t* brow = p.brow ? p.brow + bz * p.sBrow : nullptr;
   const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -46,13 +44,24 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(GemmArgs p) {
   auto load_stage = [&](int stage, int64_t k0) {
     double* a = sA + stage * BK * SA;
     double* b = sB + stage * BN * SB;
+    if (!p.transA) {
 #pragma unroll
-    for (int r = 0; r < (BM * BK) / THREADS; r++) {
-      const int idx = tid + r * THREADS;
-      const int k = idx / BM, m = idx % BM;
-      const int64_t gm = m0 + m, gk = k0 + k;
-      const bool ok = gm < p.M && gk < p.K;
-      cp_async8(a + k * SA + m, ok ? A + gk * p.lda + gm : A, ok);
+      for (int r = 0; r < (BM * BK) / THREADS; r++) {
+        const int idx = tid + r * THREADS;
+        const int k = idx / BM, m = idx % BM;
+        const int64_t gm = m0 + m, gk = k0 + k;
+        const bool ok = gm < p.M && gk < p.K;
+        cp_async8(a + k * SA + m, ok ? A + gk * p.lda + gm : A, ok);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < (BM * BK) / THREADS; r++) {
+        const int idx = tid + r * THREADS;
+        const int m = idx / BK, k = idx % BK;
+        const int64_t gm = m0 + m, gk = k0 + k;
+        const bool ok = gm < p.M && gk < p.K;
+        cp_async8(a + k * SA + m, ok ? A + gm * p.lda + gk : A, ok);
+      }
     }
 #pragma unroll
     for (int r = 0; r < (BN * BK) / THREADS; r++) {
@@ -60,8 +69,7 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(GemmArgs p) {
       const int n = idx / BK, k = idx % BK;
       const int64_t gn = n0 + n, gk = k0 + k;
       const bool ok = gn < p.N && gk < p.K;
-      const int64_t row = ok ? (brow ? (int64_t)brow[gk] : gk) : 0;
-      cp_async8(b + n * SB + k, ok ? B + gn * p.ldb + row : B, ok);
+      cp_async8(b + n * SB + k, ok ? B + gn * p.ldb + gk : B, ok);
     }
   };
 
@@ -121,8 +129,7 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(GemmArgs p) {
 
 void dgemm_batched(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                    int64_t lda, int64_t sA, const double* B, int64_t ldb, int64_t sB, double beta,
-                   double* C, int64_t ldc, int64_t sC, int64_t batch, const int32_t* brow,
-                   int64_t sBrow) {
+                   double* C, int64_t ldc, int64_t sC, int64_t batch, bool transA) {
   if (M <= 0 || N <= 0 || batch <= 0) return;
   static bool attr = false;
   const size_t smem = SMEM_DOUBLES * sizeof(double);
@@ -134,10 +141,14 @@ void dgemm_batched(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alph
     dscale_batched(st, M, N, beta, C, ldc, sC, batch);
     return;
   }
-  GemmArgs p{M, N, K, alpha, beta, A, lda, sA, B, ldb, sB, C, ldc, sC, brow, sBrow};
-  dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN), (unsigned)batch);
-  dgemm_kernel<<<grid, THREADS, smem, st>>>(p);
-  SLB_CUDA_CHECK(cudaGetLastError());
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = std::min<int64_t>(65535, batch - b0);
+    GemmArgs p{M, N, K, alpha, beta, A + b0 * sA, lda, sA, B + b0 * sB, ldb, sB, C + b0 * sC, ldc, sC,
+               transA ? 1 : 0};
+    dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN), (unsigned)nb);
+    dgemm_kernel<<<grid, THREADS, smem, st>>>(p);
+    SLB_CUDA_CHECK(cudaGetLastError());
+  }
 }
 
 namespace {

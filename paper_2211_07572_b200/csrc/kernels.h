@@ -8,8 +8,12 @@ namespace slb {
 // ---- gemm.cu -------------------------------------------------------------
 void dgemm_batched(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                    int64_t lda, int64_t sA, const double* B, int64_t ldb, int64_t sB, double beta,
-                   double* C, int64_t ldc, int64_t sC, int64_t batch, const int32_t* brow = nullptr,
-                   int64_t sBrow = 0);
+                   double* C, int64_t ldc, int64_t sC, int64_t batch, bool transA = false);
+// Batched triangular solve X = T^{-1} B in place, T m x m (m <= 160) stored
+// ROW-major (T[r][c] at T[r * ldt + c]); lower => unit-lower forward,
+// else upper (non-unit) backward.  B is m x ncols column major.
+void trsm_small_batched(cudaStream_t st, bool lower, int m, const double* T, int64_t ldt, int64_t sT,
+                        double* B, int64_t ldb, int64_t sB, int64_t ncols, int64_t batch, bool rowmajor = true);
 void dscale_batched(cudaStream_t st, int64_t M, int64_t N, double beta, double* C, int64_t ldc,
                     int64_t sC, int64_t batch);
 
@@ -68,17 +72,15 @@ struct LevelArgs {
   const double* nx;      // Wp x 3Wp per strip  [Lsub | D | Usup] of level l+1
   int64_t sNX;
   double* sv_out;        // Wp x 2Wp per strip: receives R2 (prefill for the update)
-  double* ainv;          // Wp x Wp  (factor storage, level l)
+  double* slot;          // level slot (4 Wp^2): [LU11 | L21 | U1213]
   int64_t sF;            // per-strip stride of factor storage
   int32_t* perm;         // 2Wp      (factor storage, level l)
   int64_t sP;
-  double* bsel;          // Wp x Wp scratch: pivot-ordered bottom panel rows
-  double* r1;            // Wp x 2Wp scratch: pivot-ordered top rows of [V 0; D Usup]
-  int64_t sScr;
   DevStatus* status;
   int32_t level;
 };
-void level_panel(cudaStream_t st, const LevelArgs& a);
+void level_lu(cudaStream_t st, const LevelArgs& a);
+void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* X, double* Fb);
 
 // ---- schur.cu --------------------------------------------------------------------
 struct SchurArgs {
@@ -134,8 +136,3 @@ void dgemv_batched_rhs(cudaStream_t st, int64_t m, int64_t n, int64_t nrhs, doub
 void dset_identity(cudaStream_t st, double* a, int64_t n);
 
 }  // namespace slb
-
-namespace slb {
-void pack_level(cudaStream_t st, int nstrips, int Wp, const double* ainv, const double* fbot,
-                const double* h, int64_t sScr, double* out, int64_t sF);
-}

@@ -195,8 +195,9 @@ def test_cfg2_scale_properties():
     u = S.solve(fact, f)
     res = np.linalg.norm(sys_g.matvec(u) - f) / np.linalg.norm(f)
     fwd = relerr(u, w)
-    print(f"cfg2: residual {res:.3e}, forward error {fwd:.3e}")
-    assert res < 1e-10                      # backward stable
+    eta0 = backward_error(sys_g, u[:, 0], f[:, 0])
+    print(f"cfg2: residual {res:.3e}, forward error {fwd:.3e}, backward error {eta0:.3e}")
+    assert eta0 < 1e-13                     # backward stable
     assert fwd < 1e-4                       # conditioning-limited at 10 ppw (cond ~1e9)
     u1 = S.solve(fact, sys_g.rhs)[:, 0]
     rep = S.error_report(sys_g, u1, S.sample_solution(1, n, n, kappa))
