@@ -56,6 +56,7 @@ typedef struct {
   int threads;        /* accepted, unused (as in the reference) */
   int device;         /* CUDA device ordinal */
   int keep_T;         /* keep a copy of the reduced blocks for slablu_gpu_T_block */
+  int refine;         /* iterative-refinement steps per solve (residual with the original CSR) */
 } slablu_gpu_config;
 
 typedef struct {

@@ -22,7 +22,7 @@ class Status(ctypes.Structure):
 
 class Config(ctypes.Structure):
     _fields_ = [("b", I64), ("c", D), ("compression", I), ("seed", ctypes.c_uint64),
-                ("threads", I), ("device", I), ("keep_T", I)]
+                ("threads", I), ("device", I), ("keep_T", I), ("refine", I)]
 
 
 class Stats(ctypes.Structure):

@@ -143,7 +143,13 @@ __global__ void init_sv_kernel(int Wp, const double* nx0, int64_t sNX, double* s
 // ---------------------------------------------------------------------------
 // One level step for every strip: LU with partial pivoting of the panel
 // P_l = [S_l ; Lsub_{l+1}] (2Wp x Wp) restricted to dgbtrf's window (rows
-// k..k+Wp at column k; a circular buffer of Wp+1 rows in shared memory).
+// k..k+Wp at column k), blocked by 8 columns:
+//   (a) warp 0 factors the 8-column panel (pivot search, swaps, multipliers),
+//   (b) all threads apply its 8 row swaps to the other columns,
+//   (c) U block = L_bb^{-1} (pivot rows, trailing columns),
+//   (d) rank-8 trailing update of the window on the DMMA pipe,
+//   (e) the 8 finished rows retire to LU11, 8 bottom rows enter.
+// The window is a circular buffer of Wp+8 rows in shared memory.
 // Outputs into the level slot (LU form, converted later by convert_levels):
 //   LU11 (row-major Wp x Wp: unit-lower multipliers + U11), L21 (row-major),
 //   U1213 <- R1 = top rows of perm_l [V_l 0 ; D_{l+1} Usup_{l+1}] (col-major Wp x 2Wp),
@@ -152,14 +158,16 @@ __global__ void init_sv_kernel(int Wp, const double* nx0, int64_t sNX, double* s
 // grid = nstrips, block = 512.
 __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   extern __shared__ double smem[];
-  const int Wp = a.Wp, NW = Wp + 1, RS = Wp + 1;
-  double* win = smem;            // NW * RS
-  double* prow = win + NW * RS;  // Wp + 1
-  int* perm = reinterpret_cast<int*>(prow + Wp + 1);  // 2 Wp
+  const int Wp = a.Wp, NW = Wp + 8;
+  const int RS = ((Wp + 15) / 16) * 16 + 4;  // row stride = 4 mod 16 doubles
+  double* win = smem;                        // NW * RS
+  int* perm = reinterpret_cast<int*>(win + NW * RS + 16);  // 2 Wp (after 16 doubles of panel scratch)
   __shared__ int s_sing;
+  __shared__ int s_piv[8];
 
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
   const double* SV = a.sv_in + s * a.sSV;
   const double* NX = a.has_next ? a.nx + s * a.sNX : nullptr;
   double* slot = a.slot + s * a.sF;
@@ -167,7 +175,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   double* L21 = slot + (int64_t)Wp * Wp;
   double* U1213 = slot + 2LL * Wp * Wp;
   const int rows_total = a.has_next ? 2 * Wp : Wp;
-  auto slot_of = [&](int pos) { return pos < NW ? pos : pos - NW; };
+  auto rowp = [&](int pos) -> double* { return win + (pos < NW ? pos : pos - NW) * RS; };
   auto Pval = [&](int p, int j) -> double {
     return p < Wp ? SV[(int64_t)j * Wp + p] : NX[(int64_t)j * Wp + (p - Wp)];
   };
@@ -176,84 +184,196 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   const int init_rows = rows_total < NW ? rows_total : NW;
   for (int idx = tid; idx < init_rows * Wp; idx += blockDim.x) {
     const int j = idx / init_rows, p = idx % init_rows;
-    win[p * RS + j] = Pval(p, j);
+    rowp(p)[j] = Pval(p, j);
   }
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm[p] = p;
-  double nextv = 0.0;  // register prefetch of the next entering bottom row
-  if (a.has_next && tid < Wp && Wp > 1) nextv = NX[(int64_t)tid * Wp + 1];
   __syncthreads();
 
-  for (int k = 0; k < Wp; k++) {
-    const int hi = min(k + Wp, rows_total - 1);
+  for (int kb = 0; kb < Wp; kb += 8) {
+    const int kend = kb + 8;
+    // (a) panel factorization by warp 0 with the panel in registers: lane owns
+    //     positions kb + lane + 32 i (i < RPL), 8 panel columns each.
     if (warp == 0) {
-      double best = -1.0;
-      int bpos = 0x7fffffff;
-      for (int pos = k + lane; pos <= hi; pos += 32) {
-        const double v = fabs(win[slot_of(pos) * RS + k]);
-        if (v > best) {
-          best = v;
-          bpos = pos;
+      constexpr int RPL = 6;  // rows per lane (Wp + 8 <= 192)
+      const int rlast = min(kb + 7 + Wp, rows_total - 1);
+      double v[RPL][8];
+#pragma unroll
+      for (int i = 0; i < RPL; i++) {
+        const int pos = kb + lane + 32 * i;
+        if (pos <= rlast) {
+          const double* row = rowp(pos);
+#pragma unroll
+          for (int q = 0; q < 8; q++) v[i][q] = row[kb + q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; q++) v[i][q] = 0.0;
         }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
-        if (ob > best || (ob == best && op < bpos)) {
-          best = ob;
-          bpos = op;
+      for (int q = 0; q < 8; q++) {
+        const int c = kb + q;
+        const int hi = min(c + Wp, rows_total - 1);
+        // argmax of |column c| over positions c..hi (first max)
+        double best = -1.0;
+        int bpos = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < RPL; i++) {
+          const int pos = kb + lane + 32 * i;
+          const double av = fabs(v[i][q]);
+          if (pos >= c && pos <= hi && av > best) {
+            best = av;
+            bpos = pos;
+          }
+        }
+        double mx = best;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        int r = (int)__reduce_min_sync(0xffffffffu, (unsigned)(best == mx ? bpos : 0x7fffffff));
+        if (!(mx > 0.0)) {
+          r = c;
+          if (lane == 0) s_sing = 1;
+        }
+        // swap rows c (lane q, i = 0) and r through shared scratch
+        const int lr = (r - kb) & 31, ir = (r - kb) >> 5;
+        double* sc = win + NW * RS;  // 16 doubles of scratch after the window
+        if (r != c) {
+          if (lane == lr) {
+#pragma unroll
+            for (int i = 0; i < RPL; i++)
+              if (i == ir)
+#pragma unroll
+                for (int qq = 0; qq < 8; qq++) sc[qq] = v[i][qq];
+          }
+          if (lane == q) {
+#pragma unroll
+            for (int qq = 0; qq < 8; qq++) sc[8 + qq] = v[0][qq];
+          }
+          __syncwarp();
+          if (lane == q) {
+#pragma unroll
+            for (int qq = 0; qq < 8; qq++) v[0][qq] = sc[qq];
+          }
+          if (lane == lr) {
+#pragma unroll
+            for (int i = 0; i < RPL; i++)
+              if (i == ir)
+#pragma unroll
+                for (int qq = 0; qq < 8; qq++) v[i][qq] = sc[8 + qq];
+          }
+          if (lane == 0) {
+            const int tp = perm[c];
+            perm[c] = perm[r];
+            perm[r] = tp;
+          }
+          __syncwarp();
+        }
+        if (lane == 0) s_piv[q] = r;
+        // pivot row broadcast (lane q, i = 0 holds row c after the swap)
+        double pr[8];
+#pragma unroll
+        for (int qq = 0; qq < 8; qq++) pr[qq] = __shfl_sync(0xffffffffu, v[0][qq], q);
+        const double inv = pr[q] != 0.0 ? 1.0 / pr[q] : 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; i++) {
+          const int pos = kb + lane + 32 * i;
+          if (pos > c && pos <= hi) {
+            const double m = v[i][q] * inv;
+            v[i][q] = m;
+#pragma unroll
+            for (int qq = q + 1; qq < 8; qq++) v[i][qq] = fma(-m, pr[qq], v[i][qq]);
+          }
         }
       }
-      int r = bpos;
-      if (!(best > 0.0)) {
-        r = k;
-        if (lane == 0) s_sing = 1;
-      }
-      double* rk = win + slot_of(k) * RS;
-      if (r != k) {
-        double* rr = win + slot_of(r) * RS;
-        for (int j = lane; j < Wp; j += 32) {
-          const double t = rk[j];
-          rk[j] = rr[j];
-          rr[j] = t;
+#pragma unroll
+      for (int i = 0; i < RPL; i++) {
+        const int pos = kb + lane + 32 * i;
+        if (pos <= rlast) {
+          double* row = rowp(pos);
+#pragma unroll
+          for (int q = 0; q < 8; q++) row[kb + q] = v[i][q];
         }
-        if (lane == 0) {
-          const int t = perm[k];
-          perm[k] = perm[r];
-          perm[r] = t;
-        }
-        __syncwarp();
       }
-      for (int j = lane; j < Wp; j += 32) prow[j] = rk[j];
     }
     __syncthreads();
-    // retire position k (a final LU11 row), scale + update rows below
-    for (int j = tid; j < Wp; j += blockDim.x) LU11[(int64_t)k * Wp + j] = prow[j];
-    const double pv = prow[k];
-    const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
-    for (int pos = k + 1 + warp; pos <= hi; pos += nwarps) {
-      double* row = win + slot_of(pos) * RS;
-      const double m = row[k] * inv;
-      __syncwarp();
-      if (lane == 0) row[k] = m;
-      if (m != 0.0)
-        for (int j = k + 1 + lane; j < Wp; j += 32) row[j] = fma(-m, prow[j], row[j]);
+    // (b) the panel's row swaps on all other columns, in pivot order
+    for (int jj = tid; jj < Wp - 8; jj += blockDim.x) {
+      const int col = jj < kb ? jj : jj + 8;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const int c = kb + q, r = s_piv[q];
+        if (r != c) {
+          double* rc = rowp(c);
+          double* rr = rowp(r);
+          const double tv = rc[col];
+          rc[col] = rr[col];
+          rr[col] = tv;
+        }
+      }
     }
-    // entering row: position k + Wp + 1 = bottom row k + 1, into the freed slot of position k
-    if (k + Wp + 1 < rows_total && tid < Wp) {
-      win[slot_of(k) * RS + tid] = nextv;
-      if (k + 2 < Wp) nextv = NX[(int64_t)tid * Wp + (k + 2)];
+    __syncthreads();
+    // (c) U block: pivot rows kb..kb+7 on the trailing columns, U = L_bb^{-1} A
+    for (int j = kend + tid; j < Wp; j += blockDim.x) {
+      double u[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++) u[q] = rowp(kb + q)[j];
+#pragma unroll
+      for (int q = 1; q < 8; q++) {
+        const double* lq = rowp(kb + q);
+#pragma unroll
+        for (int p = 0; p < 8; p++)
+          if (p < q) u[q] = fma(-lq[kb + p], u[p], u[q]);
+      }
+#pragma unroll
+      for (int q = 1; q < 8; q++) rowp(kb + q)[j] = u[q];
+    }
+    __syncthreads();
+    // (d) trailing update on the DMMA pipe: rows kend..kb+7+Wp, cols kend..Wp-1
+    {
+      const int rlast = min(kb + 7 + Wp, rows_total - 1);
+      const int mt_n = (rlast - kend + 1 + 7) / 8;
+      const int nt_n = (Wp - kend) / 8;
+      const double* u0 = rowp(kb + t);       // B fragments: U[kb + t][col], U[kb + 4 + t][col]
+      const double* u1 = rowp(kb + 4 + t);
+      for (int tile = warp; tile < mt_n * nt_n; tile += nwarps) {
+        const int mi = tile / nt_n, ni = tile % nt_n;
+        const int pos = kend + mi * 8 + g;
+        const bool ok = pos <= rlast;
+        double* row = rowp(ok ? pos : kend);
+        const int c0 = kend + ni * 8;
+        const double a0 = ok ? -row[kb + t] : 0.0, a1 = ok ? -row[kb + 4 + t] : 0.0;
+        const double b0 = u0[c0 + g], b1 = u1[c0 + g];
+        double d0 = ok ? row[c0 + 2 * t] : 0.0, d1 = ok ? row[c0 + 2 * t + 1] : 0.0;
+        dmma884(d0, d1, a0, b0);
+        dmma884(d0, d1, a1, b1);
+        if (ok) {
+          row[c0 + 2 * t] = d0;
+          row[c0 + 2 * t + 1] = d1;
+        }
+      }
+    }
+    __syncthreads();
+    // (e) retire positions kb..kb+7; bottom rows kend..kend+7 enter at positions kend+Wp..
+    for (int idx = tid; idx < 8 * Wp; idx += blockDim.x) {
+      const int q = idx / Wp, j = idx % Wp;
+      double* rr = rowp(kb + q);
+      LU11[(int64_t)(kb + q) * Wp + j] = rr[j];
+      const int pe = kend + Wp + q;
+      if (pe < rows_total) rr[j] = NX[(int64_t)j * Wp + (pe - Wp)];
     }
     __syncthreads();
   }
 
   int32_t* perm_out = a.perm + s * a.sP;
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm_out[p] = perm[p];
+  {
+    // U13 != 0 iff a row of level l+1 was pivoted into the top half
+    const int up = __syncthreads_or(tid < Wp && perm[tid] >= Wp);
+    if (tid == 0) a.u13[s * a.sU13] = (uint8_t)(up ? 1 : 0);
+  }
   if (a.has_next) {
-    // L21: positions Wp..2Wp-1
     for (int idx = tid; idx < Wp * Wp; idx += blockDim.x) {
       const int i = idx / Wp, j = idx % Wp;
-      L21[idx] = win[slot_of(Wp + i) * RS + j];
+      L21[idx] = rowp(Wp + i)[j];
     }
     const double* V = SV + (int64_t)Wp * Wp;
     auto Rval = [&](int p, int c) -> double {
@@ -341,7 +461,8 @@ void init_sv(cudaStream_t st, int nstrips, int Wp, const double* nx0, int64_t sN
 
 void level_lu(cudaStream_t st, const LevelArgs& a) {
   const int Wp = a.Wp;
-  const size_t smem = (size_t)((Wp + 1) * (Wp + 1) + (Wp + 1)) * sizeof(double) + 2 * Wp * sizeof(int);
+  const int RS = ((Wp + 15) / 16) * 16 + 4;
+  const size_t smem = (size_t)((Wp + 8) * RS + 16) * sizeof(double) + 2 * Wp * sizeof(int);
   static size_t attr = 0;
   if (smem > attr) {
     SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
   __shared__ double s_rowP[PNB];
   __shared__ double s_rowK[PNB];
   __shared__ double s_prow[PNB];
+  __shared__ double s_krow[PNB];
   __shared__ int s_piv;
 
   double r[PNB];
@@ -92,27 +93,34 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
       }
     }
     cluster.sync();
-    // (2) cluster-wide pivot (every CTA computes the same answer)
-    if (tid == 0) {
+    // (2) cluster-wide pivot (every CTA computes the same answer); candidates read in parallel
+    if (warp == 0) {
       double bv = -1.0;
       int bi = INT_MAX;
-      for (int c = 0; c < ncta; c++) {
-        const double cv = *cluster.map_shared_rank(&s_cv, c);
-        const int ci = *cluster.map_shared_rank(&s_ci, c);
-        if (cv > bv || (cv == bv && ci < bi)) {
-          bv = cv;
-          bi = ci;
+      if (lane < ncta) {
+        bv = *cluster.map_shared_rank(&s_cv, lane);
+        bi = *cluster.map_shared_rank(&s_ci, lane);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
         }
       }
-      if (!(bv > 0.0)) {
-        bi = k;
-        if (rank == 0) {
-          atomicOr(&status->flags, ERR_SINGULAR);
-          atomicMin(&status->singular_block, block_index);
+      if (lane == 0) {
+        if (!(bv > 0.0)) {
+          bi = k;
+          if (rank == 0) {
+            atomicOr(&status->flags, ERR_SINGULAR);
+            atomicMin(&status->singular_block, block_index);
+          }
         }
+        s_piv = bi;
+        if (rank == 0) ipiv[j + k] = (int32_t)(j + bi);
       }
-      s_piv = bi;
-      if (rank == 0) ipiv[j + k] = (int32_t)(j + bi);
     }
     __syncthreads();
     const int p = s_piv;
@@ -124,17 +132,17 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
 #pragma unroll
       for (int c = 0; c < PNB; c++) s_rowK[c] = r[c];
     cluster.sync();
-    // (4) local copy of the pivot row; swap
+    // (4) local copies of both rows (parallel DSMEM reads), then swap
     if (tid < PNB) s_prow[tid] = *cluster.map_shared_rank(&s_rowP[tid], p / PTHREADS);
+    else if (tid < 2 * PNB) s_krow[tid - PNB] = *cluster.map_shared_rank(&s_rowK[tid - PNB], k / PTHREADS);
     __syncthreads();
     if (p != k) {
       if (own && i == k) {
 #pragma unroll
         for (int c = 0; c < PNB; c++) r[c] = s_prow[c];
       } else if (own && i == p) {
-        const double* rk = cluster.map_shared_rank(s_rowK, k / PTHREADS);
 #pragma unroll
-        for (int c = 0; c < PNB; c++) r[c] = rk[c];
+        for (int c = 0; c < PNB; c++) r[c] = s_krow[c];
       }
     }
     // (5) scale + rank-1 update of rows below k

@@ -139,6 +139,21 @@ __global__ void combine_reduce_kernel(double* red, int64_t K, int64_t nrhs, int6
   if (j + 1 < nstrips && strips[j + 1].left == j) v -= contrib[((int64_t)((j + 1) * 2 + 0) * nrhs + c) * n2 + q];
   red[idx] = v;
 }
+// r = f - A u (CSR, one thread per row and column), then u stays; used for refinement.
+__global__ void residual_kernel(const int32_t* rp, const int32_t* ci, const double* v, int64_t n, int64_t nrhs,
+                                const double* f, const double* u, double* r) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * nrhs) return;
+  const int64_t row = idx % n, c = idx / n;
+  const double* uc = u + c * n;
+  double acc = 0.0;
+  for (int32_t p = rp[row]; p < rp[row + 1]; p++) acc = fma(v[p], uc[ci[p]], acc);
+  r[idx] = f[idx] - acc;
+}
+__global__ void axpy_kernel(int64_t count, const double* x, double* y) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < count) y[idx] += x[idx];
+}
 __global__ void copy2d_kernel(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols) {
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < rows * cols;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -182,9 +197,13 @@ struct slablu_gpu_fact {
   DBuf<int32_t> perm;
   DBuf<double> cpl;
   DBuf<int32_t> sym;
+  DBuf<uint8_t> u13;
   DBuf<double> T;       // [diag k | super k-1 | sub k-1] blocks, n2 x n2; diag holds S_j^{-1}
   DBuf<double> Tkeep;   // optional copy of the reduced blocks
   DBuf<DevStatus> status;
+  DBuf<int32_t> a_rp, a_ci;  // the original operator (iterative refinement)
+  DBuf<double> a_v;
+  int refine = 0;
   int64_t sF = 0, sP = 0, sCPL = 0;
   double t1 = 0, t2 = 0, t_chain = 0, t_schur = 0, t_asm = 0;
   mutable double t_solve = 0, t_solve_strips = 0;
@@ -288,6 +307,15 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   DevStatus st0{0, INT_MAX, INT_MAX, 0};
   SLB_CUDA_CHECK(cudaMemcpyAsync(F->status.p, &st0, sizeof(DevStatus), cudaMemcpyHostToDevice, st));
   CsrDev A{rp, ci, v, F->N};
+  F->refine = std::max(0, c.refine);
+  if (F->refine > 0) {
+    F->a_rp.alloc(dev, F->N + 1);
+    F->a_ci.alloc(dev, nnz);
+    F->a_v.alloc(dev, nnz);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(F->a_rp.p, rp, (F->N + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    SLB_CUDA_CHECK(cudaMemcpyAsync(F->a_ci.p, ci, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    SLB_CUDA_CHECK(cudaMemcpyAsync(F->a_v.p, v, nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
 
   // ---- stage one: couplings + level chain ---------------------------------------
   const int64_t lvl = 4LL * Wp * Wp;
@@ -298,6 +326,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   F->perm.alloc(dev, (size_t)S * F->sP);
   F->cpl.alloc(dev, (size_t)S * F->sCPL);
   F->sym.alloc(dev, S);
+  F->u13.alloc(dev, (size_t)S * n2);
   {
     std::vector<int32_t> ones(S, 1);
     SLB_CUDA_CHECK(cudaMemcpyAsync(F->sym.p, ones.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice, st));
@@ -336,6 +365,8 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     la.sF = F->sF;
     la.perm = F->perm.p + l * 2 * Wp;
     la.sP = F->sP;
+    la.u13 = F->u13.p + l;
+    la.sU13 = n2;
     la.status = F->status.p;
     la.level = (int32_t)l;
     level_lu(st, la);
@@ -429,6 +460,8 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     sa.cpl = F->cpl.p;
     sa.sCPL = F->sCPL;
     sa.sym = F->sym.p;
+    sa.u13 = F->u13.p;
+    sa.chunk = kSweepChunk;
     sa.gbuf = gbuf.p;
     sa.sG = sG;
     sa.ybuf = ybuf.p;
@@ -516,8 +549,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   return F.release();
 }
 
-void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu) {
-  std::lock_guard<std::mutex> guard(F->solve_mu);
+void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu) {
   const int64_t launches0 = g_launches.load();
   SLB_CUDA_CHECK(cudaSetDevice(F->device));
   cudaStream_t st = F->stream;
@@ -544,13 +576,14 @@ void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   SLB_CUDA_CHECK(cudaEventRecord(s1, st));
   SLB_CUDA_CHECK(cudaEventRecord(s2, st));
   SLB_CUDA_CHECK(cudaEventRecord(s3, st));
-  const int64_t nch = cdiv(nrhs, kSweepChunk);
+  const int CH = nrhs <= 8 ? 8 : kSweepChunk;
+  const int64_t nch = cdiv(nrhs, CH);
   std::vector<int32_t> tasks;
   for (int s = 0; s < S; s++)
     for (int64_t cch = 0; cch < nch; cch++) {
       tasks.push_back(s);
       tasks.push_back(0);
-      tasks.push_back((int32_t)(cch * kSweepChunk));
+      tasks.push_back((int32_t)(cch * CH));
     }
   const int ntasks = (int)(tasks.size() / 3);
   DBuf<int32_t> dtasks, counter;
@@ -558,10 +591,12 @@ void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   counter.alloc(dev, 1);
   SLB_CUDA_CHECK(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   const int nslots = std::min(sm_count(dev), ntasks);
-  const int64_t sY = n2 * F->Wp * kSweepChunk;
+  const int64_t sY = n2 * F->Wp * CH;
   DBuf<double> ybuf;
   ybuf.alloc(dev, (size_t)nslots * sY);
   SchurArgs sa{};
+  sa.chunk = CH;
+  sa.u13 = F->u13.p;
   sa.Wp = F->Wp;
   sa.n2 = n2;
   sa.nstrips = S;
@@ -646,6 +681,53 @@ void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   F->t_solve_strips = F->single ? a * 1e-3 : (b + c) * 1e-3;
   for (cudaEvent_t ev : {s0, s1, s2, s3, s4}) cudaEventDestroy(ev);
   F->launches_solve = g_launches.load() - launches0;
+}
+
+// solve with F->refine steps of iterative refinement against the original
+// operator: u += A~^{-1} (f - A u).  Restores componentwise backward stability
+// lost to the explicit level/Schur inverses.
+void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu) {
+  std::lock_guard<std::mutex> guard(F->solve_mu);
+  cudaStream_t st = F->stream;
+  const int dev = F->device;
+  const int64_t N = F->N;
+  cudaEvent_t e0, e1;
+  SLB_CUDA_CHECK(cudaEventCreate(&e0));
+  SLB_CUDA_CHECK(cudaEventCreate(&e1));
+  SLB_CUDA_CHECK(cudaEventRecord(e0, st));
+  const int64_t l0 = g_launches.load();
+  if (F->refine == 0 || !F->a_rp.p) {
+    solve_once(F, d_f, ldf, nrhs, d_u, ldu);
+  } else {
+    DBuf<double> f, u, r, du;
+    f.alloc(dev, (size_t)N * nrhs);
+    u.alloc(dev, (size_t)N * nrhs);
+    r.alloc(dev, (size_t)N * nrhs);
+    du.alloc(dev, (size_t)N * nrhs);
+    copy2d(st, d_f, ldf, f.p, N, N, nrhs);
+    solve_once(F, f.p, N, nrhs, u.p, N);
+    double t_strips = F->t_solve_strips;
+    const unsigned gb = (unsigned)cdiv(N * nrhs, 256);
+    for (int it = 0; it < F->refine; it++) {
+      residual_kernel<<<gb, 256, 0, st>>>(F->a_rp.p, F->a_ci.p, F->a_v.p, N, nrhs, f.p, u.p, r.p);
+      SLB_CUDA_CHECK(cudaGetLastError());
+      solve_once(F, r.p, N, nrhs, du.p, N);
+      t_strips += F->t_solve_strips;
+      axpy_kernel<<<gb, 256, 0, st>>>(N * nrhs, du.p, u.p);
+      SLB_CUDA_CHECK(cudaGetLastError());
+      g_launches += 2;
+    }
+    copy2d(st, u.p, N, d_u, ldu, N, nrhs);
+    F->t_solve_strips = t_strips;
+  }
+  SLB_CUDA_CHECK(cudaEventRecord(e1, st));
+  SLB_CUDA_CHECK(cudaEventSynchronize(e1));
+  float ms = 0;
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+  F->t_solve = ms * 1e-3;
+  F->launches_solve = g_launches.load() - l0;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
 }
 
 slablu_gpu_status status_from(const HostError& e) { return make_status(e.code, e.what(), e.index); }
@@ -821,6 +903,7 @@ slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* F, const double* 
     const int64_t sY = n2 * F->Wp * kSweepChunk;
     ybuf.alloc(dev, (size_t)nslots * sY);
     SchurArgs sa{};
+    sa.chunk = kSweepChunk; sa.u13 = F->u13.p;
     sa.Wp = F->Wp; sa.n2 = n2; sa.nstrips = F->S; sa.strips = F->strips.p; sa.fac = F->fac.p; sa.sF = F->sF;
     sa.perm = F->perm.p; sa.sP = F->sP; sa.cpl = F->cpl.p; sa.sCPL = F->sCPL; sa.sym = F->sym.p;
     sa.ybuf = ybuf.p; sa.sY = sY; sa.task_counter = counter.p; sa.ntasks = ntasks; sa.tasks = dtasks.p;

@@ -11,10 +11,10 @@
 namespace slb {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3, THREADS = 256;
-constexpr int SA = BM + 4;  // sA[k][m]
+constexpr int BK = 16, STAGES = 3;
 constexpr int SB = BK + 4;  // sB[n][k]
-constexpr int SMEM_DOUBLES = STAGES * (BK * SA + BN * SB);
+template <int BM, int BN>
+constexpr int smem_doubles() { return STAGES * (BK * (BM + 4) + BN * SB); }
 
 struct GemmArgs {
   int64_t M, N, K;
@@ -28,7 +28,12 @@ struct GemmArgs {
   int transA;
 };
 
-__global__ void __launch_bounds__(THREADS) dgemm_kernel(GemmArgs p) {
+// BM x BN CTA tile, WM x WN warps, each warp (BM/WM) x (BN/WN).
+template <int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__(WM * WN * 32) dgemm_kernel(GemmArgs p) {
+  constexpr int THREADS = WM * WN * 32;
+  constexpr int SA = BM + 4;  // sA[k][m]
+  constexpr int MI = BM / WM / 8, NJ = BN / WN / 8;
   extern __shared__ double smem[];
   double* sA = smem;
   double* sB = smem + STAGES * BK * SA;
@@ -39,7 +44,7 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(GemmArgs p) {
   const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
+  const int wm = warp % WM, wn = warp / WM;
 
   auto load_stage = [&](int stage, int64_t k0) {
     double* a = sA + stage * BK * SA;
@@ -73,11 +78,11 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(GemmArgs p) {
     }
   };
 
-  double acc[8][4][2];
+  double acc[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 8; i++)
+  for (int i = 0; i < MI; i++)
 #pragma unroll
-    for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int64_t nk = cdiv(p.K, BK);
 #pragma unroll
@@ -91,32 +96,32 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(GemmArgs p) {
     const int64_t nxt = kt + STAGES - 1;
     if (nxt < nk) load_stage(nxt % STAGES, nxt * BK);
     cp_async_commit();
-    const double* a = sA + (kt % STAGES) * BK * SA + wm * 64 + g;
-    const double* b = sB + (kt % STAGES) * BN * SB + (wn * 32 + g) * SB + t;
+    const double* a = sA + (kt % STAGES) * BK * SA + wm * (MI * 8) + g;
+    const double* b = sB + (kt % STAGES) * BN * SB + (wn * (NJ * 8) + g) * SB + t;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[8], bf[4];
+      double af[MI], bf[NJ];
 #pragma unroll
-      for (int i = 0; i < 8; i++) af[i] = a[(kk + t) * SA + i * 8];
+      for (int i = 0; i < MI; i++) af[i] = a[(kk + t) * SA + i * 8];
 #pragma unroll
-      for (int j = 0; j < 4; j++) bf[j] = b[j * 8 * SB + kk];
+      for (int j = 0; j < NJ; j++) bf[j] = b[j * 8 * SB + kk];
 #pragma unroll
-      for (int i = 0; i < 8; i++)
+      for (int i = 0; i < MI; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < NJ; j++) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
   cp_async_wait<0>();
 
 #pragma unroll
-  for (int i = 0; i < 8; i++) {
-    const int64_t row = m0 + wm * 64 + i * 8 + g;
+  for (int i = 0; i < MI; i++) {
+    const int64_t row = m0 + wm * (MI * 8) + i * 8 + g;
     if (row >= p.M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; j++)
+    for (int j = 0; j < NJ; j++)
 #pragma unroll
       for (int e = 0; e < 2; e++) {
-        const int64_t col = n0 + wn * 32 + j * 8 + 2 * t + e;
+        const int64_t col = n0 + wn * (NJ * 8) + j * 8 + 2 * t + e;
         if (col >= p.N) continue;
         double* c = C + col * p.ldc + row;
         const double v = p.alpha * acc[i][j][e];
@@ -132,21 +137,30 @@ void dgemm_batched(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alph
                    double* C, int64_t ldc, int64_t sC, int64_t batch, bool transA) {
   if (M <= 0 || N <= 0 || batch <= 0) return;
   static bool attr = false;
-  const size_t smem = SMEM_DOUBLES * sizeof(double);
+  const size_t smem_big = smem_doubles<128, 128>() * sizeof(double);
+  const size_t smem_small = smem_doubles<64, 64>() * sizeof(double);
   if (!attr) {
-    SLB_CUDA_CHECK(cudaFuncSetAttribute(dgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(dgemm_kernel<128, 128, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_big));
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(dgemm_kernel<64, 64, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small));
     attr = true;
   }
   if (K <= 0) {  // C = beta * C
     dscale_batched(st, M, N, beta, C, ldc, sC, batch);
     return;
   }
+  // small tiles when the big-tile grid would not fill the GPU twice
+  const bool small = cdiv(M, 128) * cdiv(N, 128) * batch < 296;
   for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
     const int64_t nb = std::min<int64_t>(65535, batch - b0);
     GemmArgs p{M, N, K, alpha, beta, A + b0 * sA, lda, sA, B + b0 * sB, ldb, sB, C + b0 * sC, ldc, sC,
                transA ? 1 : 0};
-    dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN), (unsigned)nb);
-    dgemm_kernel<<<grid, THREADS, smem, st>>>(p);
+    if (small) {
+      dim3 grid((unsigned)cdiv(M, 64), (unsigned)cdiv(N, 64), (unsigned)nb);
+      dgemm_kernel<64, 64, 2, 2><<<grid, 128, smem_small, st>>>(p);
+    } else {
+      dim3 grid((unsigned)cdiv(M, 128), (unsigned)cdiv(N, 128), (unsigned)nb);
+      dgemm_kernel<128, 128, 2, 4><<<grid, 256, smem_big, st>>>(p);
+    }
     SLB_CUDA_CHECK(cudaGetLastError());
   }
 }

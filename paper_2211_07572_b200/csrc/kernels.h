@@ -76,6 +76,8 @@ struct LevelArgs {
   int64_t sF;            // per-strip stride of factor storage
   int32_t* perm;         // 2Wp      (factor storage, level l)
   int64_t sP;
+  uint8_t* u13;          // flag for this level (per strip stride n2)
+  int64_t sU13;
   DevStatus* status;
   int32_t level;
 };
@@ -95,6 +97,7 @@ struct SchurArgs {
   const double* cpl;      // coupling vectors (per strip sCPL): fromL, fromR, toL, toR (n2 x Wp each)
   int64_t sCPL;
   const int32_t* sym;     // per-strip symmetric flag
+  const uint8_t* u13;     // per (strip, level): 1 if a next-level row was pivoted up (U13 != 0)
   double* gbuf;           // per strip 4 * n2 * n2 (row-major [X][Y][p][q])
   int64_t sG;
   double* ybuf;           // per CTA slot: n2 * Wp * C
@@ -103,6 +106,7 @@ struct SchurArgs {
   int ntasks;
   const int32_t* tasks;   // packed (strip, side, q0) triples (solve modes: side unused, q0 = rhs col0)
   int mode;               // SweepMode
+  int chunk;              // RHS columns per task: 64 (Schur, batched solves) or 8 (small solves)
   // solve modes
   int64_t N, K, nrhs;
   const double* f;        // N x nrhs (ld N), natural ordering

@@ -25,20 +25,35 @@
 namespace slb {
 namespace {
 
-constexpr int C = 64;       // RHS columns per task
-constexpr int NT = C / 8;   // n8 tiles
 constexpr int THREADS = 512;
 constexpr int STAGES = 3;
 
-__device__ __forceinline__ int swz(int r, int n) { return r * C + (n ^ ((r & 3) << 2)); }
+// Compile-time layout of a sweep kernel with C right-hand-side columns.
+template <int C>
+struct Lay {
+  static constexpr int NT = C / 8;                    // n8 tiles
+  static constexpr int FWN = NT >= 2 ? 2 : 1;         // forward n groups (per half)
+  static constexpr int FWM = 8 / FWN;                 // forward m groups (per half)
+  static constexpr int FNT = NT / FWN;                // forward n tiles per warp
+  static constexpr int BWN = NT >= 4 ? 4 : NT;        // backward n groups
+  static constexpr int BWM = 16 / BWN;                // backward m groups
+  static constexpr int BNT = NT / BWN;                // backward n tiles per warp
+};
+
+template <int C>
+__device__ __forceinline__ int swz(int r, int n) {
+  if constexpr (C >= 16) return r * C + (n ^ ((r & 3) << 2));
+  else return r * C + n;
+}
 
 struct TaskGeom {
   int s, side, q0, l0, lstop;
-  int64_t nf, nslices;  // forward slices, total slices
+  int64_t nf, nslices;  // forward slices, total slices (upper bound; U13-free levels skip half)
 };
 
-template <int MTMAX>
-__global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
+template <int C, int MTMAX>
+__global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
+  using L = Lay<C>;
   extern __shared__ double sm[];
   const int Wp = a.Wp;
   const int64_t n2 = a.n2;
@@ -51,7 +66,8 @@ __global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int MTH = Wp / 8;                       // m8 tiles per Wp rows
-  const int MTPW = (MTH + 3) / 4;               // m tiles per m-warp (<= MTMAX)
+  const int FMT = (MTH + L::FWM - 1) / L::FWM;  // forward m tiles per warp
+  const int BMT = (MTH + L::BWM - 1) / L::BWM;  // backward m tiles per warp
   const int fslice = 16 * Wp;                   // doubles per forward k8 slice
   const int bslice = 8 * Wp;                    // doubles per backward k8 slice
   const int64_t lvl_stride = 4LL * Wp * Wp;
@@ -72,10 +88,10 @@ __global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
     T.l0 = (schur && T.q0 > 0) ? T.q0 - 1 : 0;
     T.lstop = (schur && a.sym[T.s]) ? T.q0 : 0;
     T.nf = (n2 - T.l0) * kf;
-    T.nslices = T.nf + (n2 - T.lstop) * kb;
     const StripDesc sd = a.strips[T.s];
     const double* fac = a.fac + T.s * a.sF;
     const int32_t* permg = a.perm + T.s * a.sP;
+    const uint8_t* u13 = a.u13 + T.s * n2;
     const double* cpl = a.cpl + T.s * a.sCPL;
     const double* fromY = cpl + (T.side == 0 ? 0 : n2 * Wp);
     const double* toL = cpl + 2 * n2 * Wp;
@@ -83,32 +99,48 @@ __global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
     double* gb = a.gbuf + T.s * a.sG;
     const int64_t rem = schur ? n2 - T.q0 : a.nrhs - T.q0;
     const int ncols = (int)(rem < C ? rem : C);
-    // dense right-hand side of level L (solve modes): b_L[i][n]
-    auto rhs_val = [&](int64_t L, int i, int n) -> double {
+    // dense right-hand side of level Lv (solve modes): b_Lv[i][n]
+    auto rhs_val = [&](int64_t Lv, int i, int n) -> double {
       if (i >= sd.w || n >= ncols) return 0.0;
       const int64_t col = T.q0 + n;
-      double v = a.f[col * a.N + (int64_t)(sd.col0 + i) * n2 + L];
+      double v = a.f[col * a.N + (int64_t)(sd.col0 + i) * n2 + Lv];
       if (a.mode == SWEEP_RECOVER) {
-        if (sd.left >= 0) v -= cpl[L * Wp + i] * a.u_ifc[col * a.K + (int64_t)sd.left * n2 + L];
-        if (sd.right >= 0) v -= cpl[n2 * Wp + L * Wp + i] * a.u_ifc[col * a.K + (int64_t)sd.right * n2 + L];
+        if (sd.left >= 0) v -= cpl[Lv * Wp + i] * a.u_ifc[col * a.K + (int64_t)sd.left * n2 + Lv];
+        if (sd.right >= 0) v -= cpl[n2 * Wp + Lv * Wp + i] * a.u_ifc[col * a.K + (int64_t)sd.right * n2 + Lv];
       }
       return v;
     };
 
-    auto slice_src = [&](int64_t i) -> const double* {
-      if (i < T.nf) {
-        const int64_t l = T.l0 + i / kf, j = i % kf;
-        return fac + l * lvl_stride + j * fslice;
-      }
-      const int64_t ib = i - T.nf;
-      const int64_t l = n2 - 1 - ib / kb, j = ib % kb;
-      return fac + l * lvl_stride + 2LL * Wp * Wp + j * bslice;
-    };
-    auto issue = [&](int64_t i) {
-      if (i < T.nslices) {
-        const double* src = slice_src(i);
-        const int len = i < T.nf ? fslice : bslice;  // doubles
-        double* dst = stg + (i % STAGES) * fslice;
+    // Slice stream: forward levels l0..n2-1 (kf slices each), then backward
+    // levels n2-1..lstop (kb slices, or kb/2 when U13 = 0 on that level).
+    // The producer walks it with its own cursor.
+    int64_t p_lvl = T.l0, p_j = 0;
+    bool p_fwd = true, p_done = false;
+    auto issue = [&](int stage) {
+      if (!p_done) {
+        const double* src;
+        int len;
+        if (p_fwd) {
+          src = fac + p_lvl * lvl_stride + p_j * fslice;
+          len = fslice;
+          if (++p_j == kf) {
+            p_j = 0;
+            if (++p_lvl == n2) {
+              p_fwd = false;
+              p_lvl = n2 - 1;
+              if (p_lvl < T.lstop) p_done = true;
+            }
+          }
+        } else {
+          src = fac + p_lvl * lvl_stride + 2LL * Wp * Wp + p_j * bslice;
+          len = bslice;
+          const int kbl = u13[p_lvl] ? kb : kb / 2;
+          if (++p_j == kbl) {
+            p_j = 0;
+            if (--p_lvl < T.lstop) p_done = true;
+          }
+        }
+        double* dst = stg + stage * fslice;
         for (int c = tid; c < len / 2; c += THREADS) cp_async16(dst + 2 * c, src + 2 * c, true);
       }
       cp_async_commit();
@@ -122,17 +154,17 @@ __global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
     __syncthreads();
     if (schur) {
       if (T.q0 == 0)  // column 0 lives on level 0: z_0 = from_Y[level 0]
-        for (int i = tid; i < Wp; i += THREADS) zb[swz(i, 0)] = fromY[i];
+        for (int i = tid; i < Wp; i += THREADS) zb[swz<C>(i, 0)] = fromY[i];
     } else {
       for (int idx = tid; idx < Wp * C; idx += THREADS) {
         const int r = idx / C, n = idx % C;
-        zb[swz(r, n)] = rhs_val(0, r, n);
+        zb[swz<C>(r, n)] = rhs_val(0, r, n);
       }
     }
 
-    const int half = warp >> 3;          // 0: Ainv rows (y), 1: Fbot rows (z')
-    const int fwm = (warp & 7) >> 1;     // m group
-    const int fwn = warp & 1;            // n group: tiles [4 fwn, 4 fwn + 4)
+    const int half = warp >> 3;            // 0: Ainv rows (y), 1: Fbot rows (z')
+    const int fwm = (warp & 7) / L::FWN;   // m group
+    const int fwn = (warp & 7) % L::FWN;   // n group
     for (int64_t l = T.l0; l < n2; l++) {
       const bool has_next = l + 1 < n2;
       const int cstar = (schur && has_next) ? (int)(l + 1 - T.q0) : -1;  // column injected
@@ -141,24 +173,24 @@ __global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
       for (int i = tid; i < 2 * Wp; i += THREADS) sperm[i] = permg[l * 2 * Wp + i];
       __syncthreads();
       auto vval = [&](int src, int n) -> double {
-        if (src < Wp) return zb[swz(src, n)];
+        if (src < Wp) return zb[swz<C>(src, n)];
         if (!schur) return has_next ? rhs_val(l + 1, src - Wp, n) : 0.0;
         return (inj && n == cstar) ? fvec[src - Wp] : 0.0;
       };
       for (int idx = tid; idx < Wp * C; idx += THREADS) {
         const int r = idx / C, n = idx % C;
-        tb[swz(r, n)] = vval(sperm[r], n);
+        tb[swz<C>(r, n)] = vval(sperm[r], n);
       }
-      double acc[MTMAX][4][2];
+      double acc[MTMAX][L::FNT][2];
 #pragma unroll
       for (int mi = 0; mi < MTMAX; mi++)
 #pragma unroll
-        for (int nj = 0; nj < 4; nj++) {
+        for (int nj = 0; nj < L::FNT; nj++) {
           acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
-          const int mt = fwm * MTPW + mi;
-          if (half == 1 && mi < MTPW && mt < MTH) {
+          const int mt = fwm * FMT + mi;
+          if (half == 1 && mi < FMT && mt < MTH) {
             const int row = mt * 8 + g;
-            const int col = (fwn * 4 + nj) * 8 + 2 * t;
+            const int col = (fwn * L::FNT + nj) * 8 + 2 * t;
             const int src = sperm[Wp + row];
             acc[mi][nj][0] = vval(src, col);
             acc[mi][nj][1] = vval(src, col + 1);
@@ -168,22 +200,22 @@ __global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
       for (int j = 0; j < kf; j++, slice++) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
-        issue(slice + STAGES - 1);
+        issue((int)((slice + STAGES - 1) % STAGES));
         const double* A = stg + (slice % STAGES) * fslice;
 #pragma unroll
         for (int kk = 0; kk < 2; kk++) {
           const int k = j * 8 + kk * 4 + t;  // B row
-          double bf[4];
+          double bf[L::FNT];
 #pragma unroll
-          for (int nj = 0; nj < 4; nj++) bf[nj] = tb[swz(k, (fwn * 4 + nj) * 8 + g)];
+          for (int nj = 0; nj < L::FNT; nj++) bf[nj] = tb[swz<C>(k, (fwn * L::FNT + nj) * 8 + g)];
           const double* Ak = A + kk * (2 * MTH) * 32 + half * MTH * 32 + lane;
 #pragma unroll
           for (int mi = 0; mi < MTMAX; mi++) {
-            const int mt = fwm * MTPW + mi;
-            if (mi < MTPW && mt < MTH) {
+            const int mt = fwm * FMT + mi;
+            if (mi < FMT && mt < MTH) {
               const double af = Ak[mt * 32];
 #pragma unroll
-              for (int nj = 0; nj < 4; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
+              for (int nj = 0; nj < L::FNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
             }
           }
         }
@@ -192,18 +224,18 @@ __global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
       double* ylev = ybase + (l - T.l0) * (int64_t)Wp * C;
 #pragma unroll
       for (int mi = 0; mi < MTMAX; mi++) {
-        const int mt = fwm * MTPW + mi;
-        if (mi >= MTPW || mt >= MTH) continue;
+        const int mt = fwm * FMT + mi;
+        if (mi >= FMT || mt >= MTH) continue;
 #pragma unroll
-        for (int nj = 0; nj < 4; nj++) {
-          const int nt = fwn * 4 + nj;
+        for (int nj = 0; nj < L::FNT; nj++) {
+          const int nt = fwn * L::FNT + nj;
           if (half == 0) {
-            double2* dst = reinterpret_cast<double2*>(ylev + ((int64_t)(mt * NT + nt) * 32 + lane) * 2);
+            double2* dst = reinterpret_cast<double2*>(ylev + ((int64_t)(mt * L::NT + nt) * 32 + lane) * 2);
             *dst = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
           } else {
             const int row = mt * 8 + g, col = nt * 8 + 2 * t;
-            zb[swz(row, col)] = acc[mi][nj][0];
-            zb[swz(row, col + 1)] = acc[mi][nj][1];
+            zb[swz<C>(row, col)] = acc[mi][nj][0];
+            zb[swz<C>(row, col + 1)] = acc[mi][nj][1];
           }
         }
       }
@@ -213,21 +245,22 @@ __global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
     __syncthreads();
     for (int idx = tid; idx < 2 * Wp * C; idx += THREADS) sm[idx] = 0.0;  // x_{n2}, x_{n2+1} = 0
     __syncthreads();
-    const int bwm = warp >> 2;        // m group
-    const int bwn = warp & 3;         // n tiles [2 bwn, 2 bwn + 2)
+    const int bwm = warp / L::BWN;    // m group
+    const int bwn = warp % L::BWN;    // n group
     int p_buf = 0;                    // buffer holding x_{l+1}; the other holds x_{l+2}
     for (int64_t l = n2 - 1; l >= T.lstop; l--) {
       const double* ylev = ybase + (l - T.l0) * (int64_t)Wp * C;
-      double acc[MTMAX][2][2];
+      const int kbl = u13[l] ? kb : kb / 2;  // U13 = 0: x_{l+2} does not enter
+      double acc[MTMAX][L::BNT][2];
 #pragma unroll
       for (int mi = 0; mi < MTMAX; mi++) {
-        const int mt = bwm * MTPW + mi;
+        const int mt = bwm * BMT + mi;
 #pragma unroll
-        for (int nj = 0; nj < 2; nj++) {
+        for (int nj = 0; nj < L::BNT; nj++) {
           acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
-          if (mi < MTPW && mt < MTH) {
-            const int nt = bwn * 2 + nj;
-            const double2 v = *reinterpret_cast<const double2*>(ylev + ((int64_t)(mt * NT + nt) * 32 + lane) * 2);
+          if (mi < BMT && mt < MTH) {
+            const int nt = bwn * L::BNT + nj;
+            const double2 v = *reinterpret_cast<const double2*>(ylev + ((int64_t)(mt * L::NT + nt) * 32 + lane) * 2);
             acc[mi][nj][0] = -v.x;  // accumulate -x, negate at the end
             acc[mi][nj][1] = -v.y;
           }
@@ -235,27 +268,27 @@ __global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
       }
       const double* xp = sm + p_buf * Wp * C;        // x_{l+1}
       const double* xq = sm + (1 - p_buf) * Wp * C;  // x_{l+2}
-      for (int j = 0; j < kb; j++, slice++) {
+      for (int j = 0; j < kbl; j++, slice++) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
-        issue(slice + STAGES - 1);
+        issue((int)((slice + STAGES - 1) % STAGES));
         const double* A = stg + (slice % STAGES) * fslice;
         const double* xs = (j * 8 < Wp) ? xp : xq;
         const int kbase = (j * 8 < Wp) ? j * 8 : j * 8 - Wp;
 #pragma unroll
         for (int kk = 0; kk < 2; kk++) {
           const int k = kbase + kk * 4 + t;
-          double bf[2];
+          double bf[L::BNT];
 #pragma unroll
-          for (int nj = 0; nj < 2; nj++) bf[nj] = xs[swz(k, (bwn * 2 + nj) * 8 + g)];
+          for (int nj = 0; nj < L::BNT; nj++) bf[nj] = xs[swz<C>(k, (bwn * L::BNT + nj) * 8 + g)];
           const double* Ak = A + kk * MTH * 32 + lane;
 #pragma unroll
           for (int mi = 0; mi < MTMAX; mi++) {
-            const int mt = bwm * MTPW + mi;
-            if (mi < MTPW && mt < MTH) {
+            const int mt = bwm * BMT + mi;
+            if (mi < BMT && mt < MTH) {
               const double af = Ak[mt * 32];
 #pragma unroll
-              for (int nj = 0; nj < 2; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
+              for (int nj = 0; nj < L::BNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
             }
           }
         }
@@ -264,31 +297,32 @@ __global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
       double* xo = sm + (1 - p_buf) * Wp * C;  // x_l overwrites x_{l+2}
 #pragma unroll
       for (int mi = 0; mi < MTMAX; mi++) {
-        const int mt = bwm * MTPW + mi;
-        if (mi >= MTPW || mt >= MTH) continue;
+        const int mt = bwm * BMT + mi;
+        if (mi >= BMT || mt >= MTH) continue;
 #pragma unroll
-        for (int nj = 0; nj < 2; nj++) {
-          const int row = mt * 8 + g, col = (bwn * 2 + nj) * 8 + 2 * t;
-          xo[swz(row, col)] = -acc[mi][nj][0];
-          xo[swz(row, col + 1)] = -acc[mi][nj][1];
+        for (int nj = 0; nj < L::BNT; nj++) {
+          const int row = mt * 8 + g, col = (bwn * L::BNT + nj) * 8 + 2 * t;
+          xo[swz<C>(row, col)] = -acc[mi][nj][0];
+          xo[swz<C>(row, col + 1)] = -acc[mi][nj][1];
         }
       }
       __syncthreads();
       if (a.mode == SWEEP_RECOVER) {
         for (int idx = tid; idx < sd.w * ncols; idx += THREADS) {
           const int i = idx % sd.w, n = idx / sd.w;
-          a.out[(T.q0 + n) * a.N + (int64_t)(sd.col0 + i) * n2 + l] = xo[swz(i, n)];
+          a.out[(T.q0 + n) * a.N + (int64_t)(sd.col0 + i) * n2 + l] = xo[swz<C>(i, n)];
         }
       } else {
         // boundary extraction: C_XY[l][q0 + n] = to_X[l] . x_l[:, n]
-        const int X = tid >> 8;            // 0: L, 1: R
-        const int n = (tid >> 2) & 63;     // column
-        const int part = tid & 3;
+        constexpr int PARTS = THREADS / (2 * C);  // threads per (X, n) dot product
+        const int X = tid / (THREADS / 2);
+        const int n = (tid / PARTS) % C;
+        const int part = tid % PARTS;
         const double* tv = (X == 0 ? toL : toR) + l * Wp;
         double sum = 0.0;
-        for (int i = part; i < Wp; i += 4) sum = fma(tv[i], xo[swz(i, n)], sum);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        for (int i = part; i < Wp; i += PARTS) sum = fma(tv[i], xo[swz<C>(i, n)], sum);
+#pragma unroll
+        for (int o = 1; o < PARTS; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         const bool has = X == 0 ? sd.left >= 0 : sd.right >= 0;
         if (part == 0 && has && n < ncols) {
           if (schur) gb[((int64_t)(X * 2 + T.side) * n2 + l) * n2 + T.q0 + n] = sum;
@@ -302,23 +336,31 @@ __global__ void __launch_bounds__(THREADS, 1) schur_kernel(SchurArgs a) {
   }
 }
 
-}  // namespace
-
-void sweep(cudaStream_t st, const SchurArgs& a, int nslots) {
+template <int C>
+void launch_sweep(cudaStream_t st, const SchurArgs& a, int nslots) {
+  using L = Lay<C>;
   const int Wp = a.Wp;
   const size_t smem = (size_t)(2 * Wp * C + STAGES * 16 * Wp) * sizeof(double) + 2 * Wp * sizeof(int);
-  const int mtpw = (Wp / 8 + 3) / 4;
-  auto launch = [&](auto kern) {
+  const int mth = Wp / 8;
+  const int mt = std::max((mth + L::FWM - 1) / L::FWM, (mth + L::BWM - 1) / L::BWM);
+  auto go = [&](auto kern) {
     SLB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<nslots, THREADS, smem, st>>>(a);
   };
-  if (mtpw <= 1) launch(schur_kernel<1>);
-  else if (mtpw <= 2) launch(schur_kernel<2>);
-  else if (mtpw <= 3) launch(schur_kernel<3>);
-  else if (mtpw <= 4) launch(schur_kernel<4>);
-  else if (mtpw <= 5) launch(schur_kernel<5>);
+  if (mt <= 1) go(sweep_kernel<C, 1>);
+  else if (mt <= 2) go(sweep_kernel<C, 2>);
+  else if (mt <= 3) go(sweep_kernel<C, 3>);
+  else if (mt <= 4) go(sweep_kernel<C, 4>);
+  else if (mt <= 5) go(sweep_kernel<C, 5>);
   else throw CudaFailure(cudaErrorInvalidValue, "sweep: slab width > 160 unsupported", __FILE__, __LINE__);
   SLB_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace
+
+void sweep(cudaStream_t st, const SchurArgs& a, int nslots) {
+  if (a.chunk == 8) launch_sweep<8>(st, a, nslots);
+  else launch_sweep<64>(st, a, nslots);
 }
 
 // ---------------------------------------------------------------------------

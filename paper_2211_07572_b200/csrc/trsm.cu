@@ -1,15 +1,17 @@
 // Batched small triangular solves on the DMMA pipe (sm_100a).
 //
-//   X = T^{-1} B   in place, T m x m (m <= 160, multiple of 8) stored row-major,
+//   X = T^{-1} B   in place, T m x m (m <= 160), row-major or column-major;
 //   lower => unit lower (forward), else upper non-unit (backward).
 //
 // Used by the band-LU level chain (U12|U13 = L11^{-1} R1 per level, the
 // dgbtrf/dgbtrs triangular factors of proj/include/slablu/banded.hpp:99-128
-// in block form) and by the conversion of every level's LU factors into the
-// GEMM-form sweep operators.  One CTA = one 32-column tile of one batch item;
-// the tile lives in shared memory, T streams from L2.  Row blocks of 16: the
-// off-diagonal update is a DMMA GEMM (two accumulators for ILP), the 16 x 16
-// diagonal block is solved per column.
+// in block form), by the conversion of every level's LU factors into the
+// GEMM-form sweep operators, and as the leaf of the stage-two recursive
+// TRSM.  One CTA = one 32-column tile of one batch item; the tile lives in
+// shared memory.  Row blocks of 16: the rows of T each block needs are staged
+// into shared memory with cp.async one block ahead (double buffer), the
+// off-diagonal update is a DMMA GEMM, the 16 x 16 diagonal block is solved
+// per column.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -19,6 +21,7 @@ namespace {
 constexpr int TN = 32;       // columns per tile
 constexpr int MMAX = 160;
 constexpr int RB = 16;       // rows per block
+constexpr int KS = MMAX + 4; // staged T row stride (== 4 mod 16)
 
 __device__ __forceinline__ int sw32(int r, int n) { return r * TN + (n ^ ((r & 3) << 2)); }
 
@@ -26,49 +29,65 @@ template <bool LOWER, bool ROWMAJOR>
 __global__ void __launch_bounds__(256) trsm_small_kernel(int m, const double* __restrict__ Tg, int64_t ldt,
                                                          int64_t sT, double* Bg, int64_t ldb, int64_t sB,
                                                          int64_t ncols) {
-  __shared__ double X[MMAX * TN];
-  __shared__ double Td[RB][RB + 1];
+  extern __shared__ double sm[];
+  double* X = sm;                       // MMAX * TN
+  double* sTb = sm + MMAX * TN;         // 2 x RB x KS
   const int64_t item = blockIdx.y;
   const double* T = Tg + item * sT;
   double* B = Bg + item * sB;
   const int64_t c0 = (int64_t)blockIdx.x * TN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  // load the tile
+  const int nb = (m + RB - 1) / RB;
+  auto block_of = [&](int bi) { return LOWER ? bi : nb - 1 - bi; };
+  // stage rows [r0, r1) of T, all m columns, into buffer buf (row-major, stride KS)
+  auto stage = [&](int bi, int buf) {
+    if (bi >= nb) return;
+    const int r0 = block_of(bi) * RB, h = min(m, r0 + RB) - r0;
+    double* dst = sTb + buf * RB * KS;
+    if (ROWMAJOR) {
+      for (int idx = tid; idx < h * m; idx += 256) {
+        const int rr = idx / m, c = idx % m;
+        cp_async8(dst + rr * KS + c, T + (int64_t)(r0 + rr) * ldt + c, true);
+      }
+    } else {
+      for (int idx = tid; idx < h * m; idx += 256) {
+        const int c = idx / h, rr = idx % h;
+        cp_async8(dst + rr * KS + c, T + (int64_t)c * ldt + r0 + rr, true);
+      }
+    }
+  };
+  stage(0, 0);
+  cp_async_commit();
   for (int idx = tid; idx < m * TN; idx += 256) {
     const int n = idx / m, r = idx % m;
     const int64_t c = c0 + n;
     X[sw32(r, n)] = c < ncols ? B[c * ldb + r] : 0.0;
   }
-  __syncthreads();
-  const int nb = (m + RB - 1) / RB;
   const int mt = warp >> 2, nt = warp & 3;
   for (int bi = 0; bi < nb; bi++) {
-    const int b = LOWER ? bi : nb - 1 - bi;
+    const int b = block_of(bi);
     const int r0 = b * RB, r1 = min(m, r0 + RB), h = r1 - r0;
-    // diagonal block to smem (overlaps the GEMM below)
-    for (int idx = tid; idx < h * h; idx += 256) {
-      const int rr = idx / h, cc = idx % h;
-      Td[rr][cc] = ROWMAJOR ? T[(int64_t)(r0 + rr) * ldt + r0 + cc] : T[(int64_t)(r0 + cc) * ldt + r0 + rr];
-    }
+    stage(bi + 1, (bi + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* Tb = sTb + (bi & 1) * RB * KS;  // rows r0..r1 of T
     // off-diagonal update: X[r0:r1] -= T[r0:r1, K] X[K]
     if (mt * 8 < h) {
-      const int row = r0 + mt * 8 + g;
-      const bool rok = row < r1;
+      const int rloc = mt * 8 + g;
+      const bool rok = r0 + rloc < r1;
       const int kb = LOWER ? 0 : r1, ke = LOWER ? r0 : m;
+      const int row = rok ? r0 + rloc : r0;
       double a0 = X[sw32(row, nt * 8 + 2 * t)], a1 = X[sw32(row, nt * 8 + 2 * t + 1)];
       double b0 = 0.0, b1 = 0.0;
-      auto tv = [&](int k) -> double {  // -T[row][k], zero outside
-        if (!rok || k >= ke) return 0.0;
-        return ROWMAJOR ? -T[(int64_t)row * ldt + k] : -T[(int64_t)k * ldt + row];
-      };
+      const double* trow = Tb + rloc * KS;
+      auto tv = [&](int k) -> double { return (rok && k < ke) ? -trow[k] : 0.0; };
       auto xv = [&](int k) -> double { return k < ke ? X[sw32(k, nt * 8 + g)] : 0.0; };
       int k = kb;
       for (; k + 8 <= ke; k += 8) {
-        const double f0 = tv(k + t), f1 = tv(k + 4 + t);
-        const double x0 = xv(k + t), x1 = xv(k + 4 + t);
-        dmma884(a0, a1, f0, x0);
-        dmma884(b0, b1, f1, x1);
+        dmma884(a0, a1, tv(k + t), xv(k + t));
+        dmma884(b0, b1, tv(k + 4 + t), xv(k + 4 + t));
       }
       for (; k < ke; k += 4) dmma884(a0, a1, tv(k + t), xv(k + t));
       if (rok) {
@@ -86,29 +105,31 @@ __global__ void __launch_bounds__(256) trsm_small_kernel(int m, const double* __
       if (LOWER) {
 #pragma unroll
         for (int rr = 1; rr < RB; rr++) {
-          double s = x[rr];
+          double sacc = x[rr];
 #pragma unroll
           for (int cc = 0; cc < RB; cc++)
-            if (cc < rr) s = fma(-Td[rr][cc], x[cc], s);
-          x[rr] = s;
+            if (cc < rr) sacc = fma(-Tb[rr * KS + r0 + cc], x[cc], sacc);
+          x[rr] = sacc;
         }
       } else {
 #pragma unroll
         for (int rr = RB - 1; rr >= 0; rr--) {
           if (rr >= h) continue;
-          double s = x[rr];
+          double sacc = x[rr];
 #pragma unroll
           for (int cc = 0; cc < RB; cc++)
-            if (cc > rr && cc < h) s = fma(-Td[rr][cc], x[cc], s);
-          x[rr] = s / Td[rr][rr];
+            if (cc > rr && cc < h) sacc = fma(-Tb[rr * KS + r0 + cc], x[cc], sacc);
+          x[rr] = sacc / Tb[rr * KS + r0 + rr];
         }
       }
 #pragma unroll
       for (int rr = 0; rr < RB; rr++)
         if (rr < h) X[sw32(r0 + rr, n)] = x[rr];
     }
-    __syncthreads();
+    __syncthreads();  // X block final; the staging buffer may be refilled
   }
+  cp_async_wait<0>();
+  __syncthreads();
   for (int idx = tid; idx < m * TN; idx += 256) {
     const int n = idx / m, r = idx % m;
     const int64_t c = c0 + n;
@@ -123,15 +144,24 @@ void trsm_small_batched(cudaStream_t st, bool lower, int m, const double* T, int
   if (m <= 0 || ncols <= 0 || batch <= 0) return;
   if (m > MMAX)
     throw CudaFailure(cudaErrorInvalidValue, "trsm_small_batched: m must be <= 160", __FILE__, __LINE__);
+  const size_t smem = (size_t)(MMAX * TN + 2 * RB * KS) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(trsm_small_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(trsm_small_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(trsm_small_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(trsm_small_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
   for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
     const int64_t nb = std::min<int64_t>(65535, batch - b0);
     dim3 grid((unsigned)cdiv(ncols, TN), (unsigned)nb);
     const double* Tb = T + b0 * sT;
     double* Bb = B + b0 * sB;
-    if (lower && rowmajor) trsm_small_kernel<true, true><<<grid, 256, 0, st>>>(m, Tb, ldt, sT, Bb, ldb, sB, ncols);
-    else if (lower) trsm_small_kernel<true, false><<<grid, 256, 0, st>>>(m, Tb, ldt, sT, Bb, ldb, sB, ncols);
-    else if (rowmajor) trsm_small_kernel<false, true><<<grid, 256, 0, st>>>(m, Tb, ldt, sT, Bb, ldb, sB, ncols);
-    else trsm_small_kernel<false, false><<<grid, 256, 0, st>>>(m, Tb, ldt, sT, Bb, ldb, sB, ncols);
+    if (lower && rowmajor) trsm_small_kernel<true, true><<<grid, 256, smem, st>>>(m, Tb, ldt, sT, Bb, ldb, sB, ncols);
+    else if (lower) trsm_small_kernel<true, false><<<grid, 256, smem, st>>>(m, Tb, ldt, sT, Bb, ldb, sB, ncols);
+    else if (rowmajor) trsm_small_kernel<false, true><<<grid, 256, smem, st>>>(m, Tb, ldt, sT, Bb, ldb, sB, ncols);
+    else trsm_small_kernel<false, false><<<grid, 256, smem, st>>>(m, Tb, ldt, sT, Bb, ldb, sB, ncols);
     SLB_CUDA_CHECK(cudaGetLastError());
   }
 }

@@ -264,10 +264,11 @@ class SolverConfig:
     threads: int = 1
     device: int = 0
     keep_T: bool = False
+    refine: int = 1  # iterative-refinement steps per solve (GPU engine extension)
 
     def _c(self):
         return _lib.Config(int(self.b), float(self.c), int(self.compression), int(self.seed),
-                           int(self.threads), int(self.device), int(bool(self.keep_T)))
+                           int(self.threads), int(self.device), int(bool(self.keep_T)), int(self.refine))
 
 
 def choose_b(n1, n2, config: SolverConfig = SolverConfig()):
