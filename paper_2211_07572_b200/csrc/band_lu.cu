@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   const int Wp = a.Wp, NW = Wp + 8;
   const int RS = ((Wp + 15) / 16) * 16 + 4;  // row stride = 4 mod 16 doubles
   double* win = smem;                        // NW * RS
-  int* perm = reinterpret_cast<int*>(win + NW * RS + 16);  // 2 Wp (after 16 doubles of panel scratch)
+  int* perm = reinterpret_cast<int*>(win + NW * RS + 16 + 8 * Wp);  // 2 Wp (after panel scratch + entering rows)
   __shared__ int s_sing;
   __shared__ int s_piv[8];
 
@@ -189,8 +189,16 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm[p] = p;
   __syncthreads();
 
+  double* ent = win + NW * RS + 16;  // 8 x Wp staging for the entering rows
   for (int kb = 0; kb < Wp; kb += 8) {
     const int kend = kb + 8;
+    // prefetch the 8 bottom rows entering after this block (overlaps (a)-(d))
+    for (int idx = tid; idx < 8 * Wp; idx += blockDim.x) {
+      const int q = idx / Wp, j = idx % Wp;
+      const int pe = kend + Wp + q;
+      if (pe < rows_total) cp_async8(ent + idx, NX + (int64_t)j * Wp + (pe - Wp), true);
+    }
+    cp_async_commit();
     // (a) panel factorization by warp 0 with the panel in registers: lane owns
     //     positions kb + lane + 32 i (i < RPL), 8 panel columns each.
     if (warp == 0) {
@@ -353,12 +361,13 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
     }
     __syncthreads();
     // (e) retire positions kb..kb+7; bottom rows kend..kend+7 enter at positions kend+Wp..
+    cp_async_wait<0>();
     for (int idx = tid; idx < 8 * Wp; idx += blockDim.x) {
       const int q = idx / Wp, j = idx % Wp;
       double* rr = rowp(kb + q);
       LU11[(int64_t)(kb + q) * Wp + j] = rr[j];
       const int pe = kend + Wp + q;
-      if (pe < rows_total) rr[j] = NX[(int64_t)j * Wp + (pe - Wp)];
+      if (pe < rows_total) rr[j] = ent[idx];
     }
     __syncthreads();
   }
@@ -375,17 +384,6 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
       const int i = idx / Wp, j = idx % Wp;
       L21[idx] = rowp(Wp + i)[j];
     }
-    const double* V = SV + (int64_t)Wp * Wp;
-    auto Rval = [&](int p, int c) -> double {
-      if (p < Wp) return c < Wp ? V[(int64_t)c * Wp + p] : 0.0;
-      return NX[(int64_t)(Wp + c) * Wp + (p - Wp)];  // [D | Usup] = NX columns Wp..3Wp-1
-    };
-    double* r2 = a.sv_out + s * a.sSV;
-    for (int idx = tid; idx < 2 * Wp * Wp; idx += blockDim.x) {
-      const int c = idx / Wp, i = idx % Wp;
-      U1213[idx] = Rval(perm[i], c);
-      r2[idx] = Rval(perm[Wp + i], c);
-    }
   } else {
     for (int idx = tid; idx < 3 * Wp * Wp; idx += blockDim.x) L21[idx] = 0.0;  // L21 and U1213
   }
@@ -395,7 +393,26 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   }
 }
 
-// Conversion helpers (per strip, all levels batched): X = [I | U1213] and
+// R = perm_l [V_l 0 ; D_{l+1} Usup_{l+1}]: R1 -> U1213 slot, R2 -> sv_out.
+__global__ void gather_r_kernel(LevelArgs a) {
+  const int s = blockIdx.y, Wp = a.Wp;
+  const double* V = a.sv_in + s * a.sSV + (int64_t)Wp * Wp;
+  const double* NX = a.nx + s * a.sNX;
+  const int32_t* perm = a.perm + s * a.sP;
+  double* U1213 = a.slot + s * a.sF + 2LL * Wp * Wp;
+  double* r2 = a.sv_out + s * a.sSV;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * Wp * Wp; idx += gridDim.x * blockDim.x) {
+    const int c = idx / Wp, i = idx % Wp;
+    auto Rval = [&](int p) -> double {
+      if (p < Wp) return c < Wp ? V[(int64_t)c * Wp + p] : 0.0;
+      return NX[(int64_t)(Wp + c) * Wp + (p - Wp)];
+    };
+    U1213[idx] = Rval(perm[i]);
+    r2[idx] = Rval(perm[Wp + i]);
+  }
+}
+
+// Conversion helpers (per strip, batched over levels): X = [I | U1213], and
 // the final packing of [Ainv | H] and Fbot into DMMA fragment order.
 __global__ void convert_init_kernel(int Wp, const double* slots, int64_t lvl, double* X, int64_t sX) {
   const int64_t l = blockIdx.y;
@@ -462,7 +479,7 @@ void init_sv(cudaStream_t st, int nstrips, int Wp, const double* nx0, int64_t sN
 void level_lu(cudaStream_t st, const LevelArgs& a) {
   const int Wp = a.Wp;
   const int RS = ((Wp + 15) / 16) * 16 + 4;
-  const size_t smem = (size_t)((Wp + 8) * RS + 16) * sizeof(double) + 2 * Wp * sizeof(int);
+  const size_t smem = (size_t)((Wp + 8) * RS + 16 + 8 * Wp) * sizeof(double) + 2 * Wp * sizeof(int);
   static size_t attr = 0;
   if (smem > attr) {
     SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -473,16 +490,21 @@ void level_lu(cudaStream_t st, const LevelArgs& a) {
 }
 
 // LU form -> GEMM form for levels [0, nl) of one strip (slots at stride lvl):
-//   Linv = L11^{-1};  Fbot = -L21 Linv;  [Ainv | H] = U11^{-1} [Linv | U1213];  pack.
-void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* X, double* Fb) {
-  const int64_t sX = 3LL * Wp * Wp, sFb = (int64_t)Wp * Wp;
+//   X = [I | U1213];  X[:, :Wp] = L11^{-1} (lower TRSM);  Fbot = -L21 L11^{-1} (GEMM);
+//   X = U11^{-1} X = [Ainv | H] (upper TRSM);  pack [Ainv ; Fbot] and H.
+// work: 4 Wp^2 doubles per level.  Runs on a low-priority stream behind the
+// chain (one launch group per chunk of levels).
+void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* work) {
+  const int64_t w2 = (int64_t)Wp * Wp, sX = 3 * w2;
+  double* X = work;
+  double* Fb = work + nl * sX;
   convert_init_kernel<<<dim3((unsigned)cdiv(3 * Wp * Wp, 256), (unsigned)nl), 256, 0, st>>>(Wp, slots, lvl, X, sX);
   SLB_CUDA_CHECK(cudaGetLastError());
   trsm_small_batched(st, true, Wp, slots, Wp, lvl, X, Wp, sX, Wp, nl);
-  dgemm_batched(st, Wp, Wp, Wp, -1.0, slots + (int64_t)Wp * Wp, Wp, lvl, X, Wp, sX, 0.0, Fb, Wp, sFb, nl, true);
+  dgemm_batched(st, Wp, Wp, Wp, -1.0, slots + w2, Wp, lvl, X, Wp, sX, 0.0, Fb, Wp, w2, nl, true);
   trsm_small_batched(st, false, Wp, slots, Wp, lvl, X, Wp, sX, 3 * Wp, nl);
   convert_pack_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(4LL * Wp * Wp, 256), 64), (unsigned)nl), 256, 0, st>>>(
-      Wp, X, sX, Fb, sFb, slots, lvl);
+      Wp, X, sX, Fb, w2, slots, lvl);
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 

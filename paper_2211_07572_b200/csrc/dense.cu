@@ -24,7 +24,11 @@ constexpr int PNB = 32;          // panel width
 constexpr int PTHREADS = 256;    // rows per CTA of the panel cluster (<= 16 CTAs)
 
 // Factor rows [j, n) x cols [j, j + nb) of A in place.  Thread (rank, tid)
-// owns panel row i = rank * 512 + tid.  ipiv[j + k] = global pivot row.
+// owns panel row i = rank * PTHREADS + tid in registers.  Per column one
+// cluster barrier: every CTA publishes its best candidate (value, row index,
+// row data) and, if it owns it, row k, into parity-double-buffered shared
+// memory; after the barrier every CTA reads the candidates through DSMEM and
+// applies the same swap and rank-1 update.  ipiv[j + k] = global pivot row.
 __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_t lda, int64_t n,
                                                                int64_t j, int nb, int32_t* ipiv,
                                                                DevStatus* status, int block_index) {
@@ -37,12 +41,12 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
   const bool own = i < m;
   __shared__ double s_wv[PTHREADS / 32];
   __shared__ int s_wi[PTHREADS / 32];
-  __shared__ double s_cv;      // CTA candidate |value|
-  __shared__ int s_ci;         // CTA candidate row
-  __shared__ double s_rowP[PNB];
-  __shared__ double s_rowK[PNB];
-  __shared__ double s_prow[PNB];
-  __shared__ double s_krow[PNB];
+  __shared__ double s_cv[2];
+  __shared__ int s_ci[2];
+  __shared__ double s_crow[2][PNB];  // this CTA's candidate row
+  __shared__ double s_krow[2][PNB];  // row k (owner CTA only)
+  __shared__ double s_prow[PNB];     // local copies after the barrier
+  __shared__ double s_kloc[PNB];
   __shared__ int s_piv;
 
   double r[PNB];
@@ -50,7 +54,8 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
   for (int c = 0; c < PNB; c++) r[c] = (own && c < nb) ? A[(j + c) * lda + j + i] : 0.0;
 
   for (int k = 0; k < nb; k++) {
-    // (1) local argmax over rows i >= k (first max by row index)
+    const int pb = k & 1;
+    // (1) CTA-local argmax over rows i >= k (first max by row index)
     double v = -1.0;
     int vi = INT_MAX;
     if (own && i >= k) {
@@ -88,64 +93,69 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
         }
       }
       if (lane == 0) {
-        s_cv = v;
-        s_ci = vi;
+        s_cv[pb] = v;
+        s_ci[pb] = vi;
       }
     }
+    __syncthreads();
+    // (2) publish the candidate row and row k
+    if (own && i == s_ci[pb])
+#pragma unroll
+      for (int c = 0; c < PNB; c++) s_crow[pb][c] = r[c];
+    if (own && i == k)
+#pragma unroll
+      for (int c = 0; c < PNB; c++) s_krow[pb][c] = r[c];
     cluster.sync();
-    // (2) cluster-wide pivot (every CTA computes the same answer); candidates read in parallel
+    // (3) every CTA resolves the same pivot and copies both rows locally
     if (warp == 0) {
       double bv = -1.0;
-      int bi = INT_MAX;
+      int bi = INT_MAX, bc = 0;
       if (lane < ncta) {
-        bv = *cluster.map_shared_rank(&s_cv, lane);
-        bi = *cluster.map_shared_rank(&s_ci, lane);
+        bv = *cluster.map_shared_rank(&s_cv[pb], lane);
+        bi = *cluster.map_shared_rank(&s_ci[pb], lane);
+        bc = lane;
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
         if (ov > bv || (ov == bv && oi < bi)) {
           bv = ov;
           bi = oi;
+          bc = oc;
         }
       }
-      if (lane == 0) {
-        if (!(bv > 0.0)) {
-          bi = k;
-          if (rank == 0) {
-            atomicOr(&status->flags, ERR_SINGULAR);
-            atomicMin(&status->singular_block, block_index);
-          }
+      if (!(bv > 0.0)) {  // exactly singular column: no interchange
+        bi = k;
+        bc = k / PTHREADS;
+        if (lane == 0 && rank == 0) {
+          atomicOr(&status->flags, ERR_SINGULAR);
+          atomicMin(&status->singular_block, block_index);
         }
+      }
+      // pivot row: candidate row of CTA bc (or row k itself when no interchange)
+      const double* src = (bi == k) ? cluster.map_shared_rank(&s_krow[pb][0], k / PTHREADS)
+                                    : cluster.map_shared_rank(&s_crow[pb][0], bc);
+      s_prow[lane] = src[lane];
+      s_kloc[lane] = *cluster.map_shared_rank(&s_krow[pb][lane], k / PTHREADS);
+      if (lane == 0) {
         s_piv = bi;
         if (rank == 0) ipiv[j + k] = (int32_t)(j + bi);
       }
     }
     __syncthreads();
     const int p = s_piv;
-    // (3) owners publish rows p and k
-    if (own && i == p)
-#pragma unroll
-      for (int c = 0; c < PNB; c++) s_rowP[c] = r[c];
-    if (own && i == k)
-#pragma unroll
-      for (int c = 0; c < PNB; c++) s_rowK[c] = r[c];
-    cluster.sync();
-    // (4) local copies of both rows (parallel DSMEM reads), then swap
-    if (tid < PNB) s_prow[tid] = *cluster.map_shared_rank(&s_rowP[tid], p / PTHREADS);
-    else if (tid < 2 * PNB) s_krow[tid - PNB] = *cluster.map_shared_rank(&s_rowK[tid - PNB], k / PTHREADS);
-    __syncthreads();
     if (p != k) {
       if (own && i == k) {
 #pragma unroll
         for (int c = 0; c < PNB; c++) r[c] = s_prow[c];
       } else if (own && i == p) {
 #pragma unroll
-        for (int c = 0; c < PNB; c++) r[c] = s_krow[c];
+        for (int c = 0; c < PNB; c++) r[c] = s_kloc[c];
       }
     }
-    // (5) scale + rank-1 update of rows below k
+    // (4) scale + rank-1 update of rows below k
     if (own && i > k) {
       const double pv = s_prow[k];
       const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
@@ -167,20 +177,41 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
       if (c < nb) A[(j + c) * lda + j + i] = r[c];
 }
 
-// Row swaps ipiv[k1..k2) applied (in order) to columns [c0, c1).
-__global__ void laswp_kernel(double* A, int64_t lda, int64_t c0, int64_t c1, const int32_t* ipiv,
-                             int64_t k1, int64_t k2) {
-  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= c1) return;
-  double* col = A + c * lda;
-  for (int64_t k = k1; k < k2; k++) {
-    const int64_t p = ipiv[k];
-    if (p != k) {
-      const double t = col[k];
-      col[k] = col[p];
-      col[p] = t;
+// Row interchanges ipiv[k1..k2) (LAPACK order) as one permutation of rows
+// [k1, n): idx[r - k1] = source row of row r.  One CTA, swaps replayed in
+// shared memory by one thread (n - k1 <= 8192).
+__global__ void swap_perm_kernel(const int32_t* ipiv, int64_t n, int64_t k1, int64_t k2, int32_t* idx) {
+  extern __shared__ int32_t sidx[];
+  const int64_t m = n - k1;
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) sidx[r] = (int32_t)(k1 + r);
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int64_t k = k1; k < k2; k++) {
+      const int64_t p = ipiv[k];
+      if (p != k) {
+        const int32_t t = sidx[k - k1];
+        sidx[k - k1] = sidx[p - k1];
+        sidx[p - k1] = t;
+      }
     }
-  }
+  __syncthreads();
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) idx[r] = sidx[r];
+}
+// tmp[c][r] = A[c][idx[r]] for rows [k1, n) of columns [c0, c1)
+__global__ void gather_rows_kernel(const double* A, int64_t lda, int64_t c0, int64_t c1, int64_t k1, int64_t m,
+                                   const int32_t* idx, double* tmp) {
+  const int64_t c = c0 + blockIdx.y;
+  const double* col = A + c * lda;
+  double* t = tmp + (int64_t)blockIdx.y * m;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x)
+    t[r] = col[idx[r]];
+}
+__global__ void scatter_rows_kernel(double* A, int64_t lda, int64_t c0, int64_t k1, int64_t m, const double* tmp) {
+  const int64_t c = c0 + blockIdx.y;
+  double* col = A + c * lda + k1;
+  const double* t = tmp + (int64_t)blockIdx.y * m;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x)
+    col[r] = t[r];
 }
 
 __global__ void finite_kernel(const double* a, int64_t count, DevStatus* status) {
@@ -222,10 +253,44 @@ void panel(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t j, int nb
   SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel_getrf_kernel, A, lda, n, j, nb, ipiv, status, block_index));
 }
 
-void laswp(cudaStream_t st, double* A, int64_t lda, int64_t c0, int64_t c1, const int32_t* ipiv,
-           int64_t k1, int64_t k2) {
+// Scratch for laswp (grown on demand, per device; stage two is stream ordered).
+struct SwapScratch {
+  int32_t* idx = nullptr;
+  double* tmp = nullptr;
+  size_t idx_n = 0, tmp_n = 0;
+};
+SwapScratch& swap_scratch() {
+  static SwapScratch s;
+  return s;
+}
+
+// Apply ipiv[k1..k2) to columns [c0, c1) of the n-row matrix A: replay the
+// interchanges once as a row permutation, then a coalesced permuted copy.
+void laswp(cudaStream_t st, double* A, int64_t lda, int64_t c0, int64_t c1, const int32_t* ipiv, int64_t k1,
+           int64_t k2, int64_t n) {
   if (c1 <= c0 || k2 <= k1) return;
-  laswp_kernel<<<(unsigned)cdiv(c1 - c0, 128), 128, 0, st>>>(A, lda, c0, c1, ipiv, k1, k2);
+  const int64_t m = n - k1, nc = c1 - c0;
+  SwapScratch& S = swap_scratch();
+  if (S.idx_n < (size_t)m) {
+    SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (S.idx) cudaFree(S.idx);
+    SLB_CUDA_CHECK(cudaMalloc(&S.idx, m * sizeof(int32_t)));
+    S.idx_n = m;
+  }
+  if (S.tmp_n < (size_t)(m * nc)) {
+    SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (S.tmp) cudaFree(S.tmp);
+    SLB_CUDA_CHECK(cudaMalloc(&S.tmp, m * nc * sizeof(double)));
+    S.tmp_n = m * nc;
+  }
+  swap_perm_kernel<<<1, 1024, m * sizeof(int32_t), st>>>(ipiv, n, k1, k2, S.idx);
+  SLB_CUDA_CHECK(cudaGetLastError());
+  for (int64_t cb = 0; cb < nc; cb += 65535) {
+    const int64_t ncb = std::min<int64_t>(65535, nc - cb);
+    dim3 grid((unsigned)std::min<int64_t>(cdiv(m, 256), 16), (unsigned)ncb);
+    gather_rows_kernel<<<grid, 256, 0, st>>>(A, lda, c0 + cb, c0 + cb + ncb, k1, m, S.idx, S.tmp + cb * m);
+    scatter_rows_kernel<<<grid, 256, 0, st>>>(A, lda, c0 + cb, k1, m, S.tmp + cb * m);
+  }
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -264,12 +329,12 @@ void getrf_rec(cudaStream_t st, double* A, int64_t n, int64_t c0, int64_t c1, in
   int64_t h = round_up(w / 2, PNB);
   if (h >= w) h = w - PNB;
   getrf_rec(st, A, n, c0, c0 + h, ipiv, status, block_index);
-  laswp(st, A, n, c0 + h, c1, ipiv, c0, c0 + h);
+  laswp(st, A, n, c0 + h, c1, ipiv, c0, c0 + h, n);
   trsm(st, true, A + c0 * n + c0, n, h, A + (c0 + h) * n + c0, n, w - h);
   dgemm_batched(st, n - c0 - h, w - h, h, -1.0, A + c0 * n + c0 + h, n, 0, A + (c0 + h) * n + c0, n, 0, 1.0,
                 A + (c0 + h) * n + c0 + h, n, 0, 1);
   getrf_rec(st, A, n, c0 + h, c1, ipiv, status, block_index);
-  laswp(st, A, n, c0, c0 + h, ipiv, c0 + h, c1);
+  laswp(st, A, n, c0, c0 + h, ipiv, c0 + h, c1, n);
 }
 
 }  // namespace
@@ -281,7 +346,7 @@ void dgetrf(cudaStream_t st, int64_t n, double* a, int32_t* ipiv, double* /*work
 
 void dgetrs(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const int32_t* ipiv, double* b,
             int64_t ldb, double* /*work*/) {
-  laswp(st, b, ldb, 0, nrhs, ipiv, 0, n);
+  laswp(st, b, ldb, 0, nrhs, ipiv, 0, n, n);
   trsm(st, true, lu, n, n, b, ldb, nrhs);
   trsm(st, false, lu, n, n, b, ldb, nrhs);
 }
@@ -302,28 +367,51 @@ void check_finite(cudaStream_t st, const double* a, int64_t count, DevStatus* st
 namespace {
 constexpr int GV_ROWS = 64;   // rows per CTA (lane -> 2 rows)
 constexpr int GV_SPLIT = 8;   // K splits
-__global__ void gemv_partial_kernel(int64_t m, int64_t n, int64_t nrhs, const double* A, int64_t lda,
-                                    const double* x, int64_t ldx, double* part) {
+__global__ void __launch_bounds__(256) gemv_partial_kernel(int64_t m, int64_t n, int64_t nrhs, const double* A,
+                                                           int64_t lda, const double* x, int64_t ldx, double* part) {
+  // CTA: 64 rows (lane -> 2 consecutive rows as one 16-byte load), 8 warps split the K range,
+  // each warp keeps 4 columns in flight.
   const int64_t r0 = (int64_t)blockIdx.x * GV_ROWS;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t kc = cdiv(n, GV_SPLIT);
   const int64_t k0 = blockIdx.y * kc, k1 = min(n, k0 + kc);
   __shared__ double red[8][GV_ROWS];
+  const int64_t ra = r0 + 2 * lane;
+  const bool full = ra + 1 < m && ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   for (int64_t c = 0; c < nrhs; c++) {
-    double a0 = 0.0, a1 = 0.0;
-    const int64_t ra = r0 + 2 * lane, rb = ra + 1;
-    for (int64_t k = k0 + warp; k < k1; k += nw) {
-      const double xv = x[c * ldx + k];
-      const double* col = A + k * lda;
-      if (ra < m) a0 = fma(col[ra], xv, a0);
-      if (rb < m) a1 = fma(col[rb], xv, a1);
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    const double* xc = x + c * ldx;
+    int64_t k = k0 + warp;
+    for (; k + 24 < k1; k += 32) {  // 4 columns per iteration (stride 8 warps)
+      double2 v[4];
+      double xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const double* col = A + (k + 8 * u) * lda;
+        xv[u] = xc[k + 8 * u];
+        if (full) v[u] = *reinterpret_cast<const double2*>(col + ra);
+        else v[u] = make_double2(ra < m ? col[ra] : 0.0, ra + 1 < m ? col[ra + 1] : 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u += 2) {
+        a0 = fma(v[u].x, xv[u], a0);
+        a1 = fma(v[u].y, xv[u], a1);
+        b0 = fma(v[u + 1].x, xv[u + 1], b0);
+        b1 = fma(v[u + 1].y, xv[u + 1], b1);
+      }
     }
-    red[warp][2 * lane] = a0;
-    red[warp][2 * lane + 1] = a1;
+    for (; k < k1; k += 8) {
+      const double* col = A + k * lda;
+      const double xv = xc[k];
+      if (ra < m) a0 = fma(col[ra], xv, a0);
+      if (ra + 1 < m) a1 = fma(col[ra + 1], xv, a1);
+    }
+    red[warp][2 * lane] = a0 + b0;
+    red[warp][2 * lane + 1] = a1 + b1;
     __syncthreads();
     if (threadIdx.x < GV_ROWS) {
       double s = 0.0;
-      for (int w = 0; w < nw; w++) s += red[w][threadIdx.x];
+      for (int w = 0; w < 8; w++) s += red[w][threadIdx.x];
       const int64_t r = r0 + threadIdx.x;
       if (r < m) part[((int64_t)blockIdx.y * nrhs + c) * m + r] = s;
     }

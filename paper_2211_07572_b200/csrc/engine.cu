@@ -344,10 +344,32 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   extract_levels(st, A, F->strips.p, S, n2, Wp, 0, LCH, nx.p, sNX, F->status.p);
   init_sv(st, S, Wp, nx.p, sNX, svb[0], sSV);
   g_launches += 2;
+  // LU-form -> GEMM-form conversion runs behind the chain on a low-priority
+  // stream, one chunk of CCH levels at a time (idle SMs during the chain).
+  const int64_t CCH = std::min<int64_t>(n2, 256);
+  cudaStream_t cst;
+  {
+    int lo = 0, hi = 0;
+    SLB_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SLB_CUDA_CHECK(cudaStreamCreateWithPriority(&cst, cudaStreamNonBlocking, lo));
+  }
+  DBuf<double> cwork;
+  cwork.alloc(dev, (size_t)CCH * 4 * Wp * Wp * S);
+  cudaEvent_t chunk_ev;
+  SLB_CUDA_CHECK(cudaEventCreateWithFlags(&chunk_ev, cudaEventDisableTiming));
+  auto convert_chunk = [&](int64_t c0, int64_t c1) {
+    SLB_CUDA_CHECK(cudaEventRecord(chunk_ev, st));
+    SLB_CUDA_CHECK(cudaStreamWaitEvent(cst, chunk_ev, 0));
+    for (int s = 0; s < S; s++) {
+      convert_levels(cst, Wp, F->fac.p + s * F->sF + c0 * lvl, lvl, c1 - c0, cwork.p + (size_t)s * CCH * 4 * Wp * Wp);
+      g_launches += 5;
+    }
+  };
   int cur = 0;
   for (int64_t l = 0; l < n2; l++) {
     const int64_t nxt = l + 1;
     const bool has_next = nxt < n2;
+    if (l > 0 && l % CCH == 0) convert_chunk(l - CCH, l);
     if (has_next && nxt % LCH == 0) {
       extract_levels(st, A, F->strips.p, S, n2, Wp, nxt, std::min(LCH, n2 - nxt), nx.p, sNX, F->status.p);
       g_launches++;
@@ -372,27 +394,18 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     level_lu(st, la);
     g_launches++;
     if (has_next) {
-      double* LU11 = la.slot;
-      double* L21 = la.slot + (size_t)Wp * Wp;
-      double* U1213 = la.slot + (size_t)2 * Wp * Wp;
-      trsm_small_batched(st, true, Wp, LU11, Wp, F->sF, U1213, Wp, F->sF, 2 * Wp, S);
-      dgemm_batched(st, Wp, 2 * Wp, Wp, -1.0, L21, Wp, F->sF, U1213, Wp, F->sF, 1.0, svb[1 - cur], Wp, sSV, S, true);
-      g_launches += 2;
+      level_update(st, la);
+      g_launches++;
     }
     cur = 1 - cur;
   }
+  convert_chunk(((n2 - 1) / CCH) * CCH, n2);
+  SLB_CUDA_CHECK(cudaEventRecord(chunk_ev, cst));
+  SLB_CUDA_CHECK(cudaStreamWaitEvent(st, chunk_ev, 0));
+  SLB_CUDA_CHECK(cudaEventDestroy(chunk_ev));
+  SLB_CUDA_CHECK(cudaStreamDestroy(cst));
   nx.release();
   sv.release();
-  // LU form -> GEMM-form sweep operators, all levels in parallel (per strip)
-  {
-    DBuf<double> X, Fb;
-    X.alloc(dev, (size_t)n2 * 3 * Wp * Wp);
-    Fb.alloc(dev, (size_t)n2 * Wp * Wp);
-    for (int s = 0; s < S; s++) {
-      convert_levels(st, Wp, F->fac.p + s * F->sF, lvl, n2, X.p, Fb.p);
-      g_launches += 5;
-    }
-  }
   SLB_CUDA_CHECK(cudaEventRecord(ec, st));
   {
     DevStatus hs;

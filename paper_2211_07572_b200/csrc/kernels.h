@@ -82,7 +82,9 @@ struct LevelArgs {
   int32_t level;
 };
 void level_lu(cudaStream_t st, const LevelArgs& a);
-void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* X, double* Fb);
+// U1213 = L11^{-1} R1 and [S|V]_{l+1} = R2 - L21 U1213 in one launch (trsm.cu).
+void level_update(cudaStream_t st, const LevelArgs& a);
+void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* work);
 
 // ---- schur.cu --------------------------------------------------------------------
 struct SchurArgs {

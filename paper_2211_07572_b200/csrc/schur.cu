@@ -26,11 +26,11 @@ namespace slb {
 namespace {
 
 constexpr int THREADS = 512;
-constexpr int STAGES = 3;
 
 // Compile-time layout of a sweep kernel with C right-hand-side columns.
 template <int C>
 struct Lay {
+  static constexpr int STAGES = C >= 32 ? 3 : 8;      // cp.async ring depth (deep for bandwidth-bound solves)
   static constexpr int NT = C / 8;                    // n8 tiles
   static constexpr int FWN = NT >= 2 ? 2 : 1;         // forward n groups (per half)
   static constexpr int FWM = 8 / FWN;                 // forward m groups (per half)
@@ -54,6 +54,7 @@ struct TaskGeom {
 template <int C, int MTMAX>
 __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
   using L = Lay<C>;
+  constexpr int STAGES = L::STAGES;
   extern __shared__ double sm[];
   const int Wp = a.Wp;
   const int64_t n2 = a.n2;
@@ -62,6 +63,13 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
   double* stg = sm + 2 * Wp * C;         // STAGES slots of 16*Wp doubles
   int* sperm = reinterpret_cast<int*>(stg + STAGES * 16 * Wp);
   __shared__ int s_task;
+  __shared__ __align__(8) uint64_t full_bar[L::STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[L::STAGES];
+  // Ring state persists across tasks: slot = global slice counter % STAGES.
+  // The producer (thread 0) fills slot s for slice q after all warps released
+  // slice q - STAGES from it; consumers wait on full_bar[s] with parity
+  // (q / STAGES) & 1 and release with one arrive per warp.
+  uint64_t g_prod = 0, g_cons = 0;  // global slice counters (producer: thread 0 only)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -73,6 +81,14 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
   const int64_t lvl_stride = 4LL * Wp * Wp;
   const int kf = Wp / 8, kb = Wp / 4;           // slices per level (fwd, bwd)
   double* ybase = a.ybuf + (int64_t)blockIdx.x * a.sY;
+  if (tid == 0) {
+    for (int i = 0; i < STAGES; i++) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], THREADS / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
 
   for (;;) {
     if (tid == 0) s_task = atomicAdd(a.task_counter, 1);
@@ -116,7 +132,8 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     // The producer walks it with its own cursor.
     int64_t p_lvl = T.l0, p_j = 0;
     bool p_fwd = true, p_done = false;
-    auto issue = [&](int stage) {
+    auto issue = [&]() {
+      if (tid != 0) return;
       if (!p_done) {
         const double* src;
         int len;
@@ -140,14 +157,26 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
             if (--p_lvl < T.lstop) p_done = true;
           }
         }
-        double* dst = stg + stage * fslice;
-        for (int c = tid; c < len / 2; c += THREADS) cp_async16(dst + 2 * c, src + 2 * c, true);
+        const int sl = (int)(g_prod % STAGES);
+        if (g_prod >= (uint64_t)STAGES) mbar_wait(&empty_bar[sl], (uint32_t)(((g_prod / STAGES) - 1) & 1));
+        mbar_arrive_expect_tx(&full_bar[sl], (uint32_t)(len * sizeof(double)));
+        bulk_g2s(stg + sl * fslice, src, (uint32_t)(len * sizeof(double)), &full_bar[sl]);
+        g_prod++;
       }
-      cp_async_commit();
+    };
+    // consumer side: wait for the current slice, release it after use
+    auto acquire = [&]() -> const double* {
+      const int sl = (int)(g_cons % STAGES);
+      mbar_wait(&full_bar[sl], (uint32_t)((g_cons / STAGES) & 1));
+      return stg + sl * fslice;
+    };
+    auto release = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[(int)(g_cons % STAGES)]);
+      g_cons++;
     };
 
-    int64_t slice = 0;
-    for (int i = 0; i < STAGES - 1; i++) issue(i);
+    for (int i = 0; i < STAGES - 1; i++) issue();
 
     // ---------------- forward sweep ----------------
     for (int idx = tid; idx < Wp * C; idx += THREADS) zb[idx] = 0.0;
@@ -197,11 +226,9 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
           }
         }
       __syncthreads();
-      for (int j = 0; j < kf; j++, slice++) {
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        issue((int)((slice + STAGES - 1) % STAGES));
-        const double* A = stg + (slice % STAGES) * fslice;
+      for (int j = 0; j < kf; j++) {
+        issue();
+        const double* A = acquire();
 #pragma unroll
         for (int kk = 0; kk < 2; kk++) {
           const int k = j * 8 + kk * 4 + t;  // B row
@@ -219,6 +246,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
             }
           }
         }
+        release();
       }
       // epilogue: y_l -> HBM slab (canonical tile order), z_{l+1} -> smem
       double* ylev = ybase + (l - T.l0) * (int64_t)Wp * C;
@@ -268,11 +296,9 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
       }
       const double* xp = sm + p_buf * Wp * C;        // x_{l+1}
       const double* xq = sm + (1 - p_buf) * Wp * C;  // x_{l+2}
-      for (int j = 0; j < kbl; j++, slice++) {
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        issue((int)((slice + STAGES - 1) % STAGES));
-        const double* A = stg + (slice % STAGES) * fslice;
+      for (int j = 0; j < kbl; j++) {
+        issue();
+        const double* A = acquire();
         const double* xs = (j * 8 < Wp) ? xp : xq;
         const int kbase = (j * 8 < Wp) ? j * 8 : j * 8 - Wp;
 #pragma unroll
@@ -292,6 +318,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
             }
           }
         }
+        release();
       }
       __syncthreads();  // everyone done reading x_{l+2}
       double* xo = sm + (1 - p_buf) * Wp * C;  // x_l overwrites x_{l+2}
@@ -331,7 +358,6 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
       }
       p_buf = 1 - p_buf;
     }
-    cp_async_wait<0>();
     __syncthreads();
   }
 }
@@ -340,7 +366,7 @@ template <int C>
 void launch_sweep(cudaStream_t st, const SchurArgs& a, int nslots) {
   using L = Lay<C>;
   const int Wp = a.Wp;
-  const size_t smem = (size_t)(2 * Wp * C + STAGES * 16 * Wp) * sizeof(double) + 2 * Wp * sizeof(int);
+  const size_t smem = (size_t)(2 * Wp * C + L::STAGES * 16 * Wp) * sizeof(double) + 2 * Wp * sizeof(int);
   const int mth = Wp / 8;
   const int mt = std::max((mth + L::FWM - 1) / L::FWM, (mth + L::BWM - 1) / L::BWM);
   auto go = [&](auto kern) {

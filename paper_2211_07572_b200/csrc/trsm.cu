@@ -167,3 +167,150 @@ void trsm_small_batched(cudaStream_t st, bool lower, int m, const double* T, int
 }
 
 }  // namespace slb
+
+// ---------------------------------------------------------------------------
+// Fused per-level update of the band-LU chain (one launch per level):
+//   R = perm_l [V_l 0 ; D_{l+1} Usup_{l+1}],  U1213 = L11^{-1} R1,
+//   [S | V]_{l+1} = R2 - L21 U1213.
+// grid (2Wp / 32 column tiles, strips), 256 threads; the 32-column tile of
+// U1213 stays in shared memory between the TRSM and the GEMM, L11/L21 rows
+// are staged through a cp.async double buffer.
+namespace slb {
+namespace {
+__global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
+  extern __shared__ double sm[];
+  const int Wp = a.Wp, s = blockIdx.y;
+  double* X = sm;                 // MMAX * TN   (U1213 tile, swizzled)
+  double* sTb = sm + MMAX * TN;   // 2 x RB x KS (staged rows of L11 / L21)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int c0 = blockIdx.x * TN;
+  const double* V = a.sv_in + s * a.sSV + (int64_t)Wp * Wp;
+  const double* NX = a.nx + s * a.sNX;
+  const int32_t* perm = a.perm + s * a.sP;
+  double* slot = a.slot + s * a.sF;
+  const double* LU11 = slot;
+  const double* L21 = slot + (int64_t)Wp * Wp;
+  double* U1213 = slot + 2LL * Wp * Wp;
+  double* svo = a.sv_out + s * a.sSV;
+  auto Rval = [&](int p, int c) -> double {
+    if (p < Wp) return c < Wp ? V[(int64_t)c * Wp + p] : 0.0;
+    return NX[(int64_t)(Wp + c) * Wp + (p - Wp)];
+  };
+  const int m = Wp;
+  const int nb = (m + RB - 1) / RB;
+  auto stage_rows = [&](const double* T, int r0, int buf) {  // rows r0..r0+16 of a row-major Wp x Wp
+    const int h = min(m, r0 + RB) - r0;
+    double* dst = sTb + buf * RB * KS;
+    for (int idx = tid; idx < h * m; idx += 256) {
+      const int rr = idx / m, c = idx % m;
+      cp_async8(dst + rr * KS + c, T + (int64_t)(r0 + rr) * m + c, true);
+    }
+  };
+  // ---- R1 tile -> X (gathered through perm)
+  stage_rows(LU11, 0, 0);
+  cp_async_commit();
+  const int ncol = min(TN, 2 * Wp - c0);
+  for (int idx = tid; idx < m * TN; idx += 256) {
+    const int n = idx / m, r = idx % m;
+    X[sw32(r, n)] = n < ncol ? Rval(perm[r], c0 + n) : 0.0;
+  }
+  const int mt = warp >> 2, nt = warp & 3;
+  // ---- TRSM: X = L11^{-1} X (unit lower)
+  for (int b = 0; b < nb; b++) {
+    const int r0 = b * RB, r1 = min(m, r0 + RB), h = r1 - r0;
+    if (b + 1 < nb) stage_rows(LU11, (b + 1) * RB, (b + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* Tb = sTb + (b & 1) * RB * KS;
+    if (mt * 8 < h) {
+      const int rloc = mt * 8 + g;
+      const bool rok = r0 + rloc < r1;
+      const int row = rok ? r0 + rloc : r0;
+      double a0 = X[sw32(row, nt * 8 + 2 * t)], a1 = X[sw32(row, nt * 8 + 2 * t + 1)];
+      double b0 = 0.0, b1 = 0.0;
+      const double* trow = Tb + rloc * KS;
+      auto tv = [&](int k) -> double { return (rok && k < r0) ? -trow[k] : 0.0; };
+      auto xv = [&](int k) -> double { return k < r0 ? X[sw32(k, nt * 8 + g)] : 0.0; };
+      int k = 0;
+      for (; k + 8 <= r0; k += 8) {
+        dmma884(a0, a1, tv(k + t), xv(k + t));
+        dmma884(b0, b1, tv(k + 4 + t), xv(k + 4 + t));
+      }
+      for (; k < r0; k += 4) dmma884(a0, a1, tv(k + t), xv(k + t));
+      if (rok) {
+        X[sw32(row, nt * 8 + 2 * t)] = a0 + b0;
+        X[sw32(row, nt * 8 + 2 * t + 1)] = a1 + b1;
+      }
+    }
+    __syncthreads();
+    if (tid < TN) {
+      const int n = tid;
+      double x[RB];
+#pragma unroll
+      for (int rr = 0; rr < RB; rr++) x[rr] = rr < h ? X[sw32(r0 + rr, n)] : 0.0;
+#pragma unroll
+      for (int rr = 1; rr < RB; rr++) {
+        double sacc = x[rr];
+#pragma unroll
+        for (int cc = 0; cc < RB; cc++)
+          if (cc < rr) sacc = fma(-Tb[rr * KS + r0 + cc], x[cc], sacc);
+        x[rr] = sacc;
+      }
+#pragma unroll
+      for (int rr = 0; rr < RB; rr++)
+        if (rr < h) X[sw32(r0 + rr, n)] = x[rr];
+    }
+    __syncthreads();
+  }
+  // ---- U1213 tile out
+  for (int idx = tid; idx < m * ncol; idx += 256) {
+    const int n = idx / m, r = idx % m;
+    U1213[(int64_t)(c0 + n) * Wp + r] = X[sw32(r, n)];
+  }
+  // ---- GEMM: out = R2 - L21 X, row blocks of 16 of L21 staged like L11
+  stage_rows(L21, 0, 0);
+  cp_async_commit();
+  for (int b = 0; b < nb; b++) {
+    const int r0 = b * RB, r1 = min(m, r0 + RB), h = r1 - r0;
+    if (b + 1 < nb) stage_rows(L21, (b + 1) * RB, (b + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* Tb = sTb + (b & 1) * RB * KS;
+    if (mt * 8 < h) {
+      const int rloc = mt * 8 + g;
+      const bool rok = r0 + rloc < r1;
+      const int row = rok ? r0 + rloc : r0;
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+      const double* trow = Tb + rloc * KS;
+      auto tv = [&](int k) -> double { return rok ? -trow[k] : 0.0; };
+      auto xv = [&](int k) -> double { return X[sw32(k, nt * 8 + g)]; };
+      int k = 0;
+      for (; k + 8 <= m; k += 8) {
+        dmma884(a0, a1, tv(k + t), xv(k + t));
+        dmma884(b0, b1, tv(k + 4 + t), xv(k + 4 + t));
+      }
+      for (; k < m; k += 4) dmma884(a0, a1, tv(k + t), xv(k + t));
+      const int col = c0 + nt * 8 + 2 * t;
+      if (rok && col < 2 * Wp) svo[(int64_t)col * Wp + row] = Rval(perm[Wp + row], col) + a0 + b0;
+      if (rok && col + 1 < 2 * Wp) svo[(int64_t)(col + 1) * Wp + row] = Rval(perm[Wp + row], col + 1) + a1 + b1;
+    }
+    __syncthreads();
+  }
+}
+}  // namespace
+
+void level_update(cudaStream_t st, const LevelArgs& a) {
+  const size_t smem = (size_t)(MMAX * TN + 2 * RB * KS) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(level_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)cdiv(2 * a.Wp, TN), (unsigned)a.nstrips);
+  level_update_kernel<<<grid, 256, smem, st>>>(a);
+  SLB_CUDA_CHECK(cudaGetLastError());
+}
+}  // namespace slb
