@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   const int Wp = a.Wp, NW = Wp + 8;
   const int RS = ((Wp + 15) / 16) * 16 + 4;  // row stride = 4 mod 16 doubles
   double* win = smem;                        // NW * RS
-  int* perm = reinterpret_cast<int*>(win + NW * RS + 16 + 8 * Wp);  // 2 Wp (after panel scratch + entering rows)
+  int* perm = reinterpret_cast<int*>(win + NW * RS + 32 + 8 * Wp);  // 2 Wp (after panel scratch + entering rows)
   __shared__ int s_sing;
   __shared__ int s_piv[8];
 
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm[p] = p;
   __syncthreads();
 
-  double* ent = win + NW * RS + 16;  // 8 x Wp staging for the entering rows
+  double* ent = win + NW * RS + 32;  // 8 x Wp staging for the entering rows
   for (int kb = 0; kb < Wp; kb += 8) {
     const int kend = kb + 8;
     // prefetch the 8 bottom rows entering after this block (overlaps (a)-(d))
@@ -199,92 +199,96 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
       if (pe < rows_total) cp_async8(ent + idx, NX + (int64_t)j * Wp + (pe - Wp), true);
     }
     cp_async_commit();
-    // (a) panel factorization by warp 0 with the panel in registers: lane owns
-    //     positions kb + lane + 32 i (i < RPL), 8 panel columns each.
-    if (warp == 0) {
-      constexpr int RPL = 6;  // rows per lane (Wp + 8 <= 192)
+    // (a) panel factorization by warps 0-3 (128 threads) with the panel in
+    //     registers: thread p owns the rows initially at positions
+    //     kb + p + 128 i (i < 2), 8 panel columns each.  Interchanges only
+    //     update each row's position register (pos); the data move happens
+    //     once, when the panel is written back.  Two named barriers per column.
+    if (warp < 4) {
+      constexpr int RPL = 2;
+      const int pt = tid;  // 0..127
       const int rlast = min(kb + 7 + Wp, rows_total - 1);
       double v[RPL][8];
+      int pos[RPL];
 #pragma unroll
       for (int i = 0; i < RPL; i++) {
-        const int pos = kb + lane + 32 * i;
-        if (pos <= rlast) {
-          const double* row = rowp(pos);
+        pos[i] = kb + pt + 128 * i;
+        if (pos[i] <= rlast) {
+          const double* row = rowp(pos[i]);
 #pragma unroll
           for (int q = 0; q < 8; q++) v[i][q] = row[kb + q];
         } else {
+          pos[i] = 0x3fffffff;  // inactive
 #pragma unroll
           for (int q = 0; q < 8; q++) v[i][q] = 0.0;
         }
       }
+      double* pcand = win + NW * RS;  // scratch: [2][4] (value) + [2][4] (pos as double) + [2][8] (pivot row)
 #pragma unroll
       for (int q = 0; q < 8; q++) {
-        const int c = kb + q;
+        const int c = kb + q, par = q & 1;
         const int hi = min(c + Wp, rows_total - 1);
-        // argmax of |column c| over positions c..hi (first max)
         double best = -1.0;
         int bpos = 0x7fffffff;
 #pragma unroll
         for (int i = 0; i < RPL; i++) {
-          const int pos = kb + lane + 32 * i;
           const double av = fabs(v[i][q]);
-          if (pos >= c && pos <= hi && av > best) {
+          if (pos[i] >= c && pos[i] <= hi && av > best) {
             best = av;
-            bpos = pos;
+            bpos = pos[i];
           }
         }
         double mx = best;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        int r = (int)__reduce_min_sync(0xffffffffu, (unsigned)(best == mx ? bpos : 0x7fffffff));
-        if (!(mx > 0.0)) {
-          r = c;
-          if (lane == 0) s_sing = 1;
+        const int rw = (int)__reduce_min_sync(0xffffffffu, (unsigned)(best == mx ? bpos : 0x7fffffff));
+        if (lane == 0) {
+          pcand[par * 4 + warp] = mx;
+          pcand[8 + par * 4 + warp] = (double)rw;
         }
-        // swap rows c (lane q, i = 0) and r through shared scratch
-        const int lr = (r - kb) & 31, ir = (r - kb) >> 5;
-        double* sc = win + NW * RS;  // 16 doubles of scratch after the window
-        if (r != c) {
-          if (lane == lr) {
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        double gm = pcand[par * 4];
+        int r = (int)pcand[8 + par * 4];
 #pragma unroll
-            for (int i = 0; i < RPL; i++)
-              if (i == ir)
-#pragma unroll
-                for (int qq = 0; qq < 8; qq++) sc[qq] = v[i][qq];
+        for (int w2 = 1; w2 < 4; w2++) {
+          const double cv = pcand[par * 4 + w2];
+          const int cr = (int)pcand[8 + par * 4 + w2];
+          if (cv > gm || (cv == gm && cr < r)) {
+            gm = cv;
+            r = cr;
           }
-          if (lane == q) {
+        }
+        if (!(gm > 0.0)) {
+          r = c;
+          if (pt == 0) s_sing = 1;
+        }
+        // the winner publishes its row; positions c and r exchange
 #pragma unroll
-            for (int qq = 0; qq < 8; qq++) sc[8 + qq] = v[0][qq];
-          }
-          __syncwarp();
-          if (lane == q) {
+        for (int i = 0; i < RPL; i++)
+          if (pos[i] == r)
 #pragma unroll
-            for (int qq = 0; qq < 8; qq++) v[0][qq] = sc[qq];
-          }
-          if (lane == lr) {
+            for (int qq = 0; qq < 8; qq++) pcand[16 + par * 8 + qq] = v[i][qq];
 #pragma unroll
-            for (int i = 0; i < RPL; i++)
-              if (i == ir)
-#pragma unroll
-                for (int qq = 0; qq < 8; qq++) v[i][qq] = sc[8 + qq];
-          }
-          if (lane == 0) {
+        for (int i = 0; i < RPL; i++) {
+          if (pos[i] == r) pos[i] = c;
+          else if (pos[i] == c) pos[i] = r;
+        }
+        if (pt == 0) {
+          if (r != c) {
             const int tp = perm[c];
             perm[c] = perm[r];
             perm[r] = tp;
           }
-          __syncwarp();
+          s_piv[q] = r;
         }
-        if (lane == 0) s_piv[q] = r;
-        // pivot row broadcast (lane q, i = 0 holds row c after the swap)
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
         double pr[8];
 #pragma unroll
-        for (int qq = 0; qq < 8; qq++) pr[qq] = __shfl_sync(0xffffffffu, v[0][qq], q);
-        const double inv = pr[q] != 0.0 ? 1.0 / pr[q] : 0.0;
+        for (int qq = 0; qq < 8; qq++) pr[qq] = pcand[16 + par * 8 + qq];
+        const double inv = pr[q] != 0.0 ? __drcp_rn(pr[q]) : 0.0;
 #pragma unroll
         for (int i = 0; i < RPL; i++) {
-          const int pos = kb + lane + 32 * i;
-          if (pos > c && pos <= hi) {
+          if (pos[i] > c && pos[i] <= hi) {
             const double m = v[i][q] * inv;
             v[i][q] = m;
 #pragma unroll
@@ -294,9 +298,8 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
       }
 #pragma unroll
       for (int i = 0; i < RPL; i++) {
-        const int pos = kb + lane + 32 * i;
-        if (pos <= rlast) {
-          double* row = rowp(pos);
+        if (pos[i] <= rlast) {
+          double* row = rowp(pos[i]);
 #pragma unroll
           for (int q = 0; q < 8; q++) row[kb + q] = v[i][q];
         }
@@ -335,27 +338,30 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
       for (int q = 1; q < 8; q++) rowp(kb + q)[j] = u[q];
     }
     __syncthreads();
-    // (d) trailing update on the DMMA pipe: rows kend..kb+7+Wp, cols kend..Wp-1
+    // (d) trailing update on the DMMA pipe: rows kend..kb+7+Wp, cols kend..Wp-1.
+    //     A warp owns m tiles (8 rows) and sweeps the n tiles; its A fragments
+    //     (the 8 multipliers of each row) are loaded once.
     {
       const int rlast = min(kb + 7 + Wp, rows_total - 1);
       const int mt_n = (rlast - kend + 1 + 7) / 8;
       const int nt_n = (Wp - kend) / 8;
-      const double* u0 = rowp(kb + t);       // B fragments: U[kb + t][col], U[kb + 4 + t][col]
+      const double* u0 = rowp(kb + t);
       const double* u1 = rowp(kb + 4 + t);
-      for (int tile = warp; tile < mt_n * nt_n; tile += nwarps) {
-        const int mi = tile / nt_n, ni = tile % nt_n;
-        const int pos = kend + mi * 8 + g;
-        const bool ok = pos <= rlast;
-        double* row = rowp(ok ? pos : kend);
-        const int c0 = kend + ni * 8;
+      for (int mi = warp; mi < mt_n; mi += nwarps) {
+        const int p = kend + mi * 8 + g;
+        const bool ok = p <= rlast;
+        double* row = rowp(ok ? p : kend);
         const double a0 = ok ? -row[kb + t] : 0.0, a1 = ok ? -row[kb + 4 + t] : 0.0;
-        const double b0 = u0[c0 + g], b1 = u1[c0 + g];
-        double d0 = ok ? row[c0 + 2 * t] : 0.0, d1 = ok ? row[c0 + 2 * t + 1] : 0.0;
-        dmma884(d0, d1, a0, b0);
-        dmma884(d0, d1, a1, b1);
-        if (ok) {
-          row[c0 + 2 * t] = d0;
-          row[c0 + 2 * t + 1] = d1;
+        for (int ni = 0; ni < nt_n; ni++) {
+          const int c0 = kend + ni * 8;
+          const double b0 = u0[c0 + g], b1 = u1[c0 + g];
+          double d0 = row[c0 + 2 * t], d1 = row[c0 + 2 * t + 1];
+          dmma884(d0, d1, a0, b0);
+          dmma884(d0, d1, a1, b1);
+          if (ok) {
+            row[c0 + 2 * t] = d0;
+            row[c0 + 2 * t + 1] = d1;
+          }
         }
       }
     }
@@ -479,7 +485,7 @@ void init_sv(cudaStream_t st, int nstrips, int Wp, const double* nx0, int64_t sN
 void level_lu(cudaStream_t st, const LevelArgs& a) {
   const int Wp = a.Wp;
   const int RS = ((Wp + 15) / 16) * 16 + 4;
-  const size_t smem = (size_t)((Wp + 8) * RS + 16 + 8 * Wp) * sizeof(double) + 2 * Wp * sizeof(int);
+  const size_t smem = (size_t)((Wp + 8) * RS + 32 + 8 * Wp) * sizeof(double) + 2 * Wp * sizeof(int);
   static size_t attr = 0;
   if (smem > attr) {
     SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
