@@ -21,7 +21,7 @@ namespace slb {
 namespace {
 
 constexpr int PNB = 32;          // panel width
-constexpr int PTHREADS = 256;    // rows per CTA of the panel cluster (<= 16 CTAs)
+constexpr int PTHREADS = 256;    // rows per CTA of the panel cluster (<= 16 CTAs: n <= 4096)
 
 // Factor rows [j, n) x cols [j, j + nb) of A in place.  Thread (rank, tid)
 // owns panel row i = rank * PTHREADS + tid in registers.  Per column one
@@ -137,8 +137,10 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
       // pivot row: candidate row of CTA bc (or row k itself when no interchange)
       const double* src = (bi == k) ? cluster.map_shared_rank(&s_krow[pb][0], k / PTHREADS)
                                     : cluster.map_shared_rank(&s_crow[pb][0], bc);
-      s_prow[lane] = src[lane];
-      s_kloc[lane] = *cluster.map_shared_rank(&s_krow[pb][lane], k / PTHREADS);
+      if (lane < PNB) {
+        s_prow[lane] = src[lane];
+        s_kloc[lane] = *cluster.map_shared_rank(&s_krow[pb][lane], k / PTHREADS);
+      }
       if (lane == 0) {
         s_piv = bi;
         if (rank == 0) ipiv[j + k] = (int32_t)(j + bi);

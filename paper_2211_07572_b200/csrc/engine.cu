@@ -976,6 +976,9 @@ int slablu_gpu_debug_dense_bench(int64_t n, int device, double* out) {
     for (auto& e0 : ev) cudaEventDestroy(e0);
     cudaStreamDestroy(st);
     return 0;
+  } catch (const CudaFailure& f) {
+    fprintf(stderr, "debug_dense_bench: %s at %s:%d (%s)\n", cudaGetErrorString(f.err), f.file, f.line, f.expr);
+    return 1;
   } catch (...) {
     return 1;
   }
