@@ -1,0 +1,263 @@
+// slablu_b200.hpp — C++ mirror of the reference solver API on top of the C ABI
+// (include/slablu_gpu.h, libslablu_gpu.so).  Header-only.
+//
+// Names, argument meaning and error behaviour follow the reference library
+// (/root/reference/proj/include/slablu/):
+//   Error, ConfigError, SingularMatrixError        common.hpp:32-60
+//   ProblemSpec, assemble_fd5, SparseSystem        problem.hpp:40-132
+//   kappa_from_ppw, canned problems                problem.hpp:153-157, 210-261
+//   SolverConfig, CompressionChoice, choose_b      driver.hpp:37-66
+//   GridStrip, SlabPartition, partition            partition.hpp:27-91
+//   Factorization, factorize, solve                driver.hpp:72-179
+//
+// Matrices are column major std::vector<double> (the reference uses
+// Eigen::MatrixXd, also column major; INTEGRATION.md shows the Eigen shim).
+#ifndef SLABLU_B200_HPP
+#define SLABLU_B200_HPP
+
+#include <cmath>
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "slablu_gpu.h"
+
+namespace slablu_b200 {
+
+// ---- errors (common.hpp:32-60) --------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& what) : std::runtime_error(what) {}
+};
+class ConfigError : public Error {
+ public:
+  explicit ConfigError(const std::string& what) : Error(what) {}
+};
+class SingularMatrixError : public Error {
+ public:
+  SingularMatrixError(const std::string& what, std::ptrdiff_t index)
+      : Error(what + " (index " + std::to_string(index) + ")"), index(index) {}
+  std::ptrdiff_t index;
+};
+
+namespace detail {
+inline void check(const slablu_gpu_status& s) {
+  if (s.code == SLABLU_OK) return;
+  const std::string msg(s.msg);
+  if (s.code == SLABLU_ERR_CONFIG) throw ConfigError(msg);
+  if (s.code == SLABLU_ERR_SINGULAR) throw SingularMatrixError(msg, static_cast<std::ptrdiff_t>(s.index));
+  throw Error(msg);
+}
+}  // namespace detail
+
+// ---- problems (problem.hpp) --------------------------------------------------
+using ScalarField = std::function<double(double, double)>;
+
+struct ProblemSpec {
+  int64_t n1 = 0;
+  int64_t n2 = 0;
+  double h = 0.0;
+  double kappa = 0.0;
+  ScalarField coefficient_field = [](double, double) { return 1.0; };
+  ScalarField dirichlet_data = [](double, double) { return 0.0; };
+  ScalarField body_load = [](double, double) { return 0.0; };
+};
+
+struct SparseSystem {
+  std::vector<int32_t> row_ptr, col_idx;  // Eigen RowMajor compressed form
+  std::vector<double> values;
+  std::vector<double> rhs;
+  int64_t n1 = 0, n2 = 0;
+  double h = 0.0;
+  int64_t dim() const { return n1 * n2; }
+  int64_t node_index(int64_t i, int64_t j) const { return i * n2 + j; }
+};
+
+inline SparseSystem assemble_fd5(const ProblemSpec& spec) {
+  SparseSystem s;
+  s.n1 = spec.n1;
+  s.n2 = spec.n2;
+  s.h = spec.h;
+  const int64_t n = spec.n1 * spec.n2;
+  if (n <= 0 || spec.n2 < 2 || spec.n1 < spec.n2) throw ConfigError("assemble_fd5: grid must satisfy n1 >= n2 >= 2");
+  s.row_ptr.assign(n + 1, 0);
+  s.col_idx.assign(5 * n, 0);
+  s.values.assign(5 * n, 0.0);
+  s.rhs.assign(n, 0.0);
+  struct Fields {
+    const ProblemSpec* p;
+  } f{&spec};
+  auto coef = [](double x, double y, void* u) { return static_cast<Fields*>(u)->p->coefficient_field(x, y); };
+  auto dir = [](double x, double y, void* u) { return static_cast<Fields*>(u)->p->dirichlet_data(x, y); };
+  auto load = [](double x, double y, void* u) { return static_cast<Fields*>(u)->p->body_load(x, y); };
+  int64_t nnz = 0;
+  detail::check(slablu_gpu_assemble_fd5(spec.n1, spec.n2, spec.h, spec.kappa, coef, dir, load, &f, s.row_ptr.data(),
+                                        s.col_idx.data(), s.values.data(), s.rhs.data(), &nnz));
+  s.col_idx.resize(nnz);
+  s.values.resize(nnz);
+  return s;
+}
+
+inline double kappa_from_ppw(double ppw, int64_t n2) {
+  if (!(ppw > 0.0)) throw ConfigError("kappa_from_ppw: ppw must be positive");
+  if (n2 < 2) throw ConfigError("kappa_from_ppw: n2 must be at least 2");
+  return slablu_gpu_kappa_from_ppw(ppw, n2);
+}
+inline double bessel_j0(double t) { return slablu_gpu_bessel_j0(t); }
+
+inline ProblemSpec poisson_log_problem(int64_t n1, int64_t n2) {
+  ProblemSpec s;
+  s.n1 = n1;
+  s.n2 = n2;
+  s.h = 1.0 / double(n2 + 1);
+  s.dirichlet_data = [](double x, double y) { return std::log(std::hypot(x + 0.1, y - 0.5)); };
+  return s;
+}
+inline ProblemSpec helmholtz_problem(int64_t n1, int64_t n2, double kappa) {
+  ProblemSpec s;
+  s.n1 = n1;
+  s.n2 = n2;
+  s.h = 1.0 / double(n2 + 1);
+  s.kappa = kappa;
+  s.dirichlet_data = [kappa](double x, double y) { return bessel_j0(kappa * std::hypot(x + 0.1, y - 0.5)); };
+  return s;
+}
+inline ProblemSpec helmholtz_bump_problem(int64_t n1, int64_t n2, double kappa) {
+  ProblemSpec s = helmholtz_problem(n1, n2, kappa);
+  s.coefficient_field = [n1, n2](double x, double y) {
+    const double h = 1.0 / double(n2 + 1);
+    const double cx = 0.5 * double(n1 + 1) * h, cy = 0.5;
+    const double d2 = (x - cx) * (x - cx) + (y - cy) * (y - cy);
+    return 1.0 - 0.9 * std::exp(-64.0 * d2);
+  };
+  return s;
+}
+
+// ---- configuration and geometry (driver.hpp:37-66, partition.hpp) ------------
+enum class CompressionChoice { automatic = 0, dense = 1, hbs = 2 };
+
+struct SolverConfig {
+  int64_t b = 0;
+  double c = 0.6;
+  CompressionChoice compression = CompressionChoice::automatic;
+  double hbs_tol = 1e-11;
+  double hbs_trunc_rel = 1e-13;
+  int64_t hbs_leaf_size = 64;
+  uint64_t seed = 0;
+  int threads = 1;
+  // engine extensions
+  int device = 0;
+  bool keep_T = false;
+  int refine = 1;
+  slablu_gpu_config c_config() const {
+    slablu_gpu_config g{};
+    g.b = b;
+    g.c = c;
+    g.compression = static_cast<int>(compression);
+    g.seed = seed;
+    g.threads = threads;
+    g.device = device;
+    g.keep_T = keep_T ? 1 : 0;
+    g.refine = refine;
+    return g;
+  }
+};
+
+inline int64_t choose_b(int64_t n1, int64_t n2, const SolverConfig& config) {
+  int64_t out = 0;
+  detail::check(slablu_gpu_choose_b(n1, n2, config.b, config.c, &out));
+  return out;
+}
+
+struct GridStrip {
+  int64_t first_col = 0;
+  int64_t width = 0;
+};
+struct SlabPartition {
+  int64_t n1 = 0, n2 = 0, b = 0;
+  std::vector<GridStrip> interfaces, interiors;
+  int64_t interface_count() const { return static_cast<int64_t>(interfaces.size()); }
+  int64_t interior_count() const { return static_cast<int64_t>(interiors.size()); }
+  int64_t dim() const { return n1 * n2; }
+  int64_t interface_offset(int64_t j) const { return interfaces[j].first_col * n2; }
+  int64_t interior_offset(int64_t i) const { return interiors[i].first_col * n2; }
+  int64_t interior_size(int64_t i) const { return interiors[i].width * n2; }
+  int64_t left_interior(int64_t j) const { return j; }
+  int64_t right_interior(int64_t j) const { return j + 1 < interior_count() ? j + 1 : -1; }
+};
+
+inline SlabPartition partition(int64_t n1, int64_t n2, int64_t b) {
+  const int64_t cap = n1 + 2 > 4 ? n1 + 2 : 4;
+  std::vector<int64_t> ints(2 * cap), ifcs(2 * cap);
+  int64_t ni = 0, nf = 0;
+  detail::check(slablu_gpu_partition(n1, n2, b, &ni, ints.data(), &nf, ifcs.data(), cap));
+  SlabPartition p;
+  p.n1 = n1;
+  p.n2 = n2;
+  p.b = b;
+  for (int64_t k = 0; k < ni; k++) p.interiors.push_back({ints[2 * k], ints[2 * k + 1]});
+  for (int64_t k = 0; k < nf; k++) p.interfaces.push_back({ifcs[2 * k], ifcs[2 * k + 1]});
+  return p;
+}
+
+// ---- factorize / solve (driver.hpp:72-179) -----------------------------------
+class Factorization {
+ public:
+  int64_t n1 = 0, n2 = 0, b = 0;
+  SolverConfig config{};
+  double t_stage1 = 0.0, t_stage2 = 0.0;  // seconds (device time)
+  std::size_t storage_stage1 = 0, storage_stage2 = 0;
+  int64_t hbs_max_rank = 0;
+
+  bool single_slab() const { return stats_.single_slab != 0; }
+  std::size_t storage_scalars() const { return storage_stage1 + storage_stage2; }
+  const slablu_gpu_stats_t& stats() const { return stats_; }
+  const slablu_gpu_fact* handle() const { return h_.get(); }
+
+ private:
+  struct Deleter {
+    void operator()(slablu_gpu_fact* f) const { slablu_gpu_destroy(f); }
+  };
+  std::shared_ptr<slablu_gpu_fact> h_;
+  slablu_gpu_stats_t stats_{};
+  friend Factorization factorize(const SparseSystem&, SolverConfig);
+};
+
+inline Factorization factorize(const SparseSystem& system, SolverConfig config) {
+  if (system.dim() == 0) throw ConfigError("factorize: empty system");
+  const slablu_gpu_config c = config.c_config();
+  slablu_gpu_fact* raw = nullptr;
+  detail::check(slablu_gpu_factorize(system.n1, system.n2, system.row_ptr.data(), system.col_idx.data(),
+                                     system.values.data(), &c, &raw));
+  Factorization f;
+  f.h_ = std::shared_ptr<slablu_gpu_fact>(raw, Factorization::Deleter{});
+  detail::check(slablu_gpu_stats(raw, &f.stats_));
+  f.n1 = system.n1;
+  f.n2 = system.n2;
+  f.b = f.stats_.b;
+  config.b = f.b;
+  config.compression = CompressionChoice::dense;
+  f.config = config;
+  f.t_stage1 = f.stats_.t_stage1;
+  f.t_stage2 = f.stats_.t_stage2;
+  f.storage_stage1 = static_cast<std::size_t>(f.stats_.storage_stage1);
+  f.storage_stage2 = static_cast<std::size_t>(f.stats_.storage_stage2);
+  return f;
+}
+
+// u (N x nrhs, column major) = A^{-1} f (N x nrhs, column major)
+inline std::vector<double> solve(const Factorization& fact, const std::vector<double>& f, int64_t nrhs = 1) {
+  const int64_t n = fact.n1 * fact.n2;
+  if (nrhs < 0 || static_cast<int64_t>(f.size()) != n * nrhs)
+    throw Error("solve: rhs length must equal the grid size");
+  std::vector<double> u(f.size());
+  detail::check(slablu_gpu_solve(fact.handle(), f.data(), n, nrhs, u.data(), n));
+  return u;
+}
+
+}  // namespace slablu_b200
+
+#endif  // SLABLU_B200_HPP
