@@ -603,10 +603,15 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   dtasks.alloc(dev, tasks.size());
   counter.alloc(dev, 1);
   SLB_CUDA_CHECK(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  const int nslots = std::min(sm_count(dev), ntasks);
+  const bool clustered = CH == 8;  // cluster sweeps for small nrhs (solve.cu)
+  const int nslots = clustered ? ntasks : std::min(sm_count(dev), ntasks);
   const int64_t sY = n2 * F->Wp * CH;
   DBuf<double> ybuf;
   ybuf.alloc(dev, (size_t)nslots * sY);
+  auto run_sweep = [&](const SchurArgs& args) {
+    if (clustered) strip_solve(st, args, ntasks);
+    else sweep(st, args, nslots);
+  };
   SchurArgs sa{};
   sa.chunk = CH;
   sa.u13 = F->u13.p;
@@ -636,7 +641,7 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     sa.mode = SWEEP_RECOVER;
     sa.u_ifc = nullptr;
     sa.out = up;
-    sweep(st, sa, nslots);
+    run_sweep(sa);
     g_launches++;
   } else {
     DBuf<double> red, uifc, contrib, tmp, part;
@@ -651,7 +656,7 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     SLB_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
     sa.mode = SWEEP_REDUCE;
     sa.out = contrib.p;
-    sweep(st, sa, nslots);
+    run_sweep(sa);
     SLB_CUDA_CHECK(cudaEventRecord(s1, st));
     combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, S, F->strips.p, contrib.p);
     g_launches += 3;
@@ -676,7 +681,7 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     sa.mode = SWEEP_RECOVER;
     sa.u_ifc = uifc.p;
     sa.out = up;
-    sweep(st, sa, nslots);
+    run_sweep(sa);
     SLB_CUDA_CHECK(cudaEventRecord(s3, st));
     scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc.p, K, nrhs, F->ifc_off.p, n2, up, N);
     g_launches += 2;

@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
   double* tb = sm + Wp * C;              // forward: t_top  | backward: x buffer 1
   double* stg = sm + 2 * Wp * C;         // STAGES slots of 16*Wp doubles
   int* sperm = reinterpret_cast<int*>(stg + STAGES * 16 * Wp);
+  uint8_t* su13 = reinterpret_cast<uint8_t*>(sperm + 2 * Wp);  // n2 flags of the current strip
   __shared__ int s_task;
   __shared__ __align__(8) uint64_t full_bar[L::STAGES];
   __shared__ __align__(8) uint64_t empty_bar[L::STAGES];
@@ -69,7 +70,9 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
   // The producer (thread 0) fills slot s for slice q after all warps released
   // slice q - STAGES from it; consumers wait on full_bar[s] with parity
   // (q / STAGES) & 1 and release with one arrive per warp.
-  uint64_t g_prod = 0, g_cons = 0;  // global slice counters (producer: thread 0 only)
+  // ring positions + phases (producer state lives in thread 0 only)
+  int p_slot = 0, c_slot = 0;
+  uint32_t p_round = 0, c_phase = 0;  // p_round: completed passes over the ring (producer)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -107,7 +110,11 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     const StripDesc sd = a.strips[T.s];
     const double* fac = a.fac + T.s * a.sF;
     const int32_t* permg = a.perm + T.s * a.sP;
-    const uint8_t* u13 = a.u13 + T.s * n2;
+    {
+      const uint8_t* u13g = a.u13 + T.s * n2;
+      for (int64_t i = tid; i < n2; i += THREADS) su13[i] = u13g[i];
+      __syncthreads();
+    }
     const double* cpl = a.cpl + T.s * a.sCPL;
     const double* fromY = cpl + (T.side == 0 ? 0 : n2 * Wp);
     const double* toL = cpl + 2 * n2 * Wp;
@@ -129,51 +136,62 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
 
     // Slice stream: forward levels l0..n2-1 (kf slices each), then backward
     // levels n2-1..lstop (kb slices, or kb/2 when U13 = 0 on that level).
-    // The producer walks it with its own cursor.
-    int64_t p_lvl = T.l0, p_j = 0;
+    // The producer (thread 0) walks it with an incremental cursor; the U13
+    // flags of the strip sit in shared memory (loaded at task start).
+    const double* p_src = fac + (int64_t)T.l0 * lvl_stride;
+    int p_len = fslice, p_left = kf;
+    int64_t p_lvl = T.l0;
     bool p_fwd = true, p_done = false;
     auto issue = [&]() {
-      if (tid != 0) return;
-      if (!p_done) {
-        const double* src;
-        int len;
-        if (p_fwd) {
-          src = fac + p_lvl * lvl_stride + p_j * fslice;
-          len = fslice;
-          if (++p_j == kf) {
-            p_j = 0;
-            if (++p_lvl == n2) {
-              p_fwd = false;
-              p_lvl = n2 - 1;
-              if (p_lvl < T.lstop) p_done = true;
-            }
+      if (tid != 0 || p_done) return;
+      const double* src = p_src;
+      const int len = p_len;
+      if (--p_left > 0) {
+        p_src += p_len;
+      } else if (p_fwd) {
+        if (++p_lvl == n2) {
+          p_fwd = false;
+          p_lvl = n2 - 1;
+          if (p_lvl < T.lstop) {
+            p_done = true;
+          } else {
+            p_src = fac + p_lvl * lvl_stride + 2LL * Wp * Wp;
+            p_len = bslice;
+            p_left = su13[p_lvl] ? kb : kb / 2;
           }
         } else {
-          src = fac + p_lvl * lvl_stride + 2LL * Wp * Wp + p_j * bslice;
-          len = bslice;
-          const int kbl = u13[p_lvl] ? kb : kb / 2;
-          if (++p_j == kbl) {
-            p_j = 0;
-            if (--p_lvl < T.lstop) p_done = true;
-          }
+          p_src += p_len + (lvl_stride - (int64_t)kf * fslice);
+          p_left = kf;
         }
-        const int sl = (int)(g_prod % STAGES);
-        if (g_prod >= (uint64_t)STAGES) mbar_wait(&empty_bar[sl], (uint32_t)(((g_prod / STAGES) - 1) & 1));
-        mbar_arrive_expect_tx(&full_bar[sl], (uint32_t)(len * sizeof(double)));
-        bulk_g2s(stg + sl * fslice, src, (uint32_t)(len * sizeof(double)), &full_bar[sl]);
-        g_prod++;
+      } else {
+        if (--p_lvl < T.lstop) {
+          p_done = true;
+        } else {
+          p_src = fac + p_lvl * lvl_stride + 2LL * Wp * Wp;
+          p_left = su13[p_lvl] ? kb : kb / 2;
+        }
+      }
+      const int sl = p_slot;
+      if (p_round > 0) mbar_wait(&empty_bar[sl], (p_round - 1) & 1u);
+      mbar_arrive_expect_tx(&full_bar[sl], (uint32_t)(len * sizeof(double)));
+      bulk_g2s(stg + sl * fslice, src, (uint32_t)(len * sizeof(double)), &full_bar[sl]);
+      if (++p_slot == STAGES) {
+        p_slot = 0;
+        p_round++;
       }
     };
     // consumer side: wait for the current slice, release it after use
     auto acquire = [&]() -> const double* {
-      const int sl = (int)(g_cons % STAGES);
-      mbar_wait(&full_bar[sl], (uint32_t)((g_cons / STAGES) & 1));
-      return stg + sl * fslice;
+      mbar_wait(&full_bar[c_slot], c_phase);
+      return stg + c_slot * fslice;
     };
     auto release = [&]() {
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[(int)(g_cons % STAGES)]);
-      g_cons++;
+      if (lane == 0) mbar_arrive(&empty_bar[c_slot]);
+      if (++c_slot == STAGES) {
+        c_slot = 0;
+        c_phase ^= 1u;
+      }
     };
 
     for (int i = 0; i < STAGES - 1; i++) issue();
@@ -278,7 +296,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     int p_buf = 0;                    // buffer holding x_{l+1}; the other holds x_{l+2}
     for (int64_t l = n2 - 1; l >= T.lstop; l--) {
       const double* ylev = ybase + (l - T.l0) * (int64_t)Wp * C;
-      const int kbl = u13[l] ? kb : kb / 2;  // U13 = 0: x_{l+2} does not enter
+      const int kbl = su13[l] ? kb : kb / 2;  // U13 = 0: x_{l+2} does not enter
       double acc[MTMAX][L::BNT][2];
 #pragma unroll
       for (int mi = 0; mi < MTMAX; mi++) {
@@ -366,7 +384,7 @@ template <int C>
 void launch_sweep(cudaStream_t st, const SchurArgs& a, int nslots) {
   using L = Lay<C>;
   const int Wp = a.Wp;
-  const size_t smem = (size_t)(2 * Wp * C + L::STAGES * 16 * Wp) * sizeof(double) + 2 * Wp * sizeof(int);
+  const size_t smem = (size_t)(2 * Wp * C + L::STAGES * 16 * Wp) * sizeof(double) + 2 * Wp * sizeof(int) + a.n2;
   const int mth = Wp / 8;
   const int mt = std::max((mth + L::FWM - 1) / L::FWM, (mth + L::BWM - 1) / L::BWM);
   auto go = [&](auto kern) {
