@@ -603,14 +603,18 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   dtasks.alloc(dev, tasks.size());
   counter.alloc(dev, 1);
   SLB_CUDA_CHECK(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  const bool clustered = CH == 8;  // cluster sweeps for small nrhs (solve.cu)
+  const bool clustered = CH == 8 && strip_solve_fits(F->Wp, n2);  // cluster sweeps for small nrhs (solve.cu)
   const int nslots = clustered ? ntasks : std::min(sm_count(dev), ntasks);
   const int64_t sY = n2 * F->Wp * CH;
   DBuf<double> ybuf;
   ybuf.alloc(dev, (size_t)nslots * sY);
   auto run_sweep = [&](const SchurArgs& args) {
-    if (clustered) strip_solve(st, args, ntasks);
-    else sweep(st, args, nslots);
+    if (clustered) {
+      strip_solve(st, args, ntasks);  // rhs pack + cluster sweep
+      g_launches++;
+    } else {
+      sweep(st, args, nslots);
+    }
   };
   SchurArgs sa{};
   sa.chunk = CH;

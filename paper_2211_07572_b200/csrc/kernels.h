@@ -120,7 +120,8 @@ constexpr int kSweepChunk = 64;
 void sweep(cudaStream_t st, const SchurArgs& a, int nslots);
 // Solve-phase slab sweeps (8 RHS columns per task) on clusters of 4 CTAs (solve.cu);
 // ybuf holds ntasks slabs of n2 * Wp * 8 doubles.
-void strip_solve(cudaStream_t st, const SchurArgs& a, int ntasks);
+bool strip_solve_fits(int Wp, int64_t n2);
+void strip_solve(cudaStream_t st, const SchurArgs& a, int ntasks);  // launches 2 kernels
 
 // T block assembly from per-strip G buffers (reference order: direct, left strip, right strip).
 void assemble_T(cudaStream_t st, int64_t n2, int nifc, int nstrips, const StripDesc* strips,

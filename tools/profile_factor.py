@@ -34,5 +34,8 @@ for r in range(a.reps):
         for k in range(2):  # second call is warm
             u = S.solve(f, sysm.rhs)
             st = f.refresh_stats()
-            print(f"  solve[{k}]: {st.t_solve_last*1e3:.2f} ms (strip sweeps {st.t_solve_strips*1e3:.2f} ms)", flush=True)
+            import numpy as np
+            r = np.linalg.norm(sysm.matvec(u).ravel() - sysm.rhs.ravel()) / np.linalg.norm(sysm.rhs)
+            print(f"  solve[{k}]: {st.t_solve_last*1e3:.2f} ms (strip sweeps {st.t_solve_strips*1e3:.2f} ms) "
+                  f"relres={r:.2e}", flush=True)
     f.close()
