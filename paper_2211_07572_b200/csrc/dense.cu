@@ -10,6 +10,7 @@
 // bulk work is DMMA GEMM (gemm.cu) with large K from the recursion.
 // trsm: recursive, 64-row leaves solved per right-hand-side column.
 #include <climits>
+#include <cstdlib>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -25,29 +26,48 @@ constexpr int PTHREADS = 256;    // rows per CTA of the panel cluster (<= 16 CTA
 
 // Factor rows [j, n) x cols [j, j + nb) of A in place.  Thread (rank, tid)
 // owns panel row i = rank * PTHREADS + tid in registers.  Per column one
-// cluster barrier: every CTA publishes its best candidate (value, row index,
+// cluster barrier (relaxed arrive after a CTA fence: the exchange is shared-memory only): every CTA publishes its best candidate (value, row index,
 // row data) and, if it owns it, row k, into parity-double-buffered shared
 // memory; after the barrier every CTA reads the candidates through DSMEM and
 // applies the same swap and rank-1 update.  ipiv[j + k] = global pivot row.
-__global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_t lda, int64_t n,
-                                                               int64_t j, int nb, int32_t* ipiv,
-                                                               DevStatus* status, int block_index) {
+template <bool RELAXED>
+__device__ __forceinline__ void panel_cluster_barrier() {
+  if (RELAXED) {
+    // shared-memory exchange only: perform this CTA's shared stores, then a relaxed arrive
+    __threadfence_block();
+    asm volatile("barrier.cluster.arrive.relaxed;\n" ::: "memory");
+  } else {
+    asm volatile("barrier.cluster.arrive.release;\n" ::: "memory");
+  }
+  asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void better(double& v, int& vi, double ov, int oi) {
+  if (ov > v || (ov == v && oi < vi)) {
+    v = ov;
+    vi = oi;
+  }
+}
+
+template <bool RELAXED>
+__global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_t lda, int64_t n, int64_t j, int nb,
+                                                               int32_t* ipiv, DevStatus* status, int block_index) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int ncta = (int)cluster.num_blocks();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = PTHREADS / 32;
   const int64_t m = n - j;
   const int64_t i = (int64_t)rank * PTHREADS + tid;
   const bool own = i < m;
-  __shared__ double s_wv[PTHREADS / 32];
-  __shared__ int s_wi[PTHREADS / 32];
+  __shared__ double s_wv[NW];
+  __shared__ int s_wi[NW];
   __shared__ double s_cv[2];
   __shared__ int s_ci[2];
   __shared__ double s_crow[2][PNB];  // this CTA's candidate row
   __shared__ double s_krow[2][PNB];  // row k (owner CTA only)
-  __shared__ double s_prow[PNB];     // local copies after the barrier
-  __shared__ double s_kloc[PNB];
-  __shared__ int s_piv;
+  __shared__ double s_prow[NW][PNB];  // per-warp copies of the pivot row
+  __shared__ double s_kloc[NW][PNB];  // per-warp copies of row k
 
   double r[PNB];
 #pragma unroll
@@ -55,7 +75,8 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
 
   for (int k = 0; k < nb; k++) {
     const int pb = k & 1;
-    // (1) CTA-local argmax over rows i >= k (first max by row index)
+    // (1) CTA argmax over rows i >= k (first max by row index); every warp reduces the
+    //     per-warp winners redundantly, so one CTA barrier suffices
     double v = -1.0;
     int vi = INT_MAX;
     if (own && i >= k) {
@@ -67,99 +88,79 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
       vi = (int)i;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
-      if (ov > v || (ov == v && oi < vi)) {
-        v = ov;
-        vi = oi;
-      }
-    }
+    for (int o = 16; o > 0; o >>= 1) better(v, vi, __shfl_xor_sync(0xffffffffu, v, o), __shfl_xor_sync(0xffffffffu, vi, o));
     if (lane == 0) {
       s_wv[warp] = v;
       s_wi[warp] = vi;
     }
     __syncthreads();
-    if (warp == 0) {
-      v = lane < PTHREADS / 32 ? s_wv[lane] : -1.0;
-      vi = lane < PTHREADS / 32 ? s_wi[lane] : INT_MAX;
+    v = lane < NW ? s_wv[lane] : -1.0;
+    vi = lane < NW ? s_wi[lane] : INT_MAX;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
-        if (ov > v || (ov == v && oi < vi)) {
-          v = ov;
-          vi = oi;
-        }
-      }
-      if (lane == 0) {
-        s_cv[pb] = v;
-        s_ci[pb] = vi;
-      }
+    for (int o = NW / 2; o > 0; o >>= 1) better(v, vi, __shfl_xor_sync(0xffffffffu, v, o), __shfl_xor_sync(0xffffffffu, vi, o));
+    v = __shfl_sync(0xffffffffu, v, 0);
+    vi = __shfl_sync(0xffffffffu, vi, 0);
+    // (2) publish the CTA candidate and row k
+    if (tid == 0) {
+      s_cv[pb] = v;
+      s_ci[pb] = vi;
     }
-    __syncthreads();
-    // (2) publish the candidate row and row k
-    if (own && i == s_ci[pb])
+    if (own && i == vi)
 #pragma unroll
       for (int c = 0; c < PNB; c++) s_crow[pb][c] = r[c];
     if (own && i == k)
 #pragma unroll
       for (int c = 0; c < PNB; c++) s_krow[pb][c] = r[c];
-    cluster.sync();
-    // (3) every CTA resolves the same pivot and copies both rows locally
-    if (warp == 0) {
-      double bv = -1.0;
-      int bi = INT_MAX, bc = 0;
-      if (lane < ncta) {
-        bv = *cluster.map_shared_rank(&s_cv[pb], lane);
-        bi = *cluster.map_shared_rank(&s_ci[pb], lane);
-        bc = lane;
-      }
+    panel_cluster_barrier<RELAXED>();
+    // (3) every warp resolves the same pivot and copies both rows into its own slot
+    double bv = -1.0;
+    int bi = INT_MAX, bc = 0;
+    if (lane < ncta) {
+      bv = *cluster.map_shared_rank(&s_cv[pb], lane);
+      bi = *cluster.map_shared_rank(&s_ci[pb], lane);
+      bc = lane;
+    }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-        if (ov > bv || (ov == bv && oi < bi)) {
-          bv = ov;
-          bi = oi;
-          bc = oc;
-        }
-      }
-      if (!(bv > 0.0)) {  // exactly singular column: no interchange
-        bi = k;
-        bc = k / PTHREADS;
-        if (lane == 0 && rank == 0) {
-          atomicOr(&status->flags, ERR_SINGULAR);
-          atomicMin(&status->singular_block, block_index);
-        }
-      }
-      // pivot row: candidate row of CTA bc (or row k itself when no interchange)
-      const double* src = (bi == k) ? cluster.map_shared_rank(&s_krow[pb][0], k / PTHREADS)
-                                    : cluster.map_shared_rank(&s_crow[pb][0], bc);
-      if (lane < PNB) {
-        s_prow[lane] = src[lane];
-        s_kloc[lane] = *cluster.map_shared_rank(&s_krow[pb][lane], k / PTHREADS);
-      }
-      if (lane == 0) {
-        s_piv = bi;
-        if (rank == 0) ipiv[j + k] = (int32_t)(j + bi);
+    for (int o = 8; o > 0; o >>= 1) {  // ncta <= 16
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+        bc = oc;
       }
     }
-    __syncthreads();
-    const int p = s_piv;
+    bv = __shfl_sync(0xffffffffu, bv, 0);
+    bi = __shfl_sync(0xffffffffu, bi, 0);
+    bc = __shfl_sync(0xffffffffu, bc, 0);
+    if (!(bv > 0.0)) {  // exactly singular column: no interchange
+      bi = k;
+      bc = k / PTHREADS;
+      if (tid == 0 && rank == 0) {
+        atomicOr(&status->flags, ERR_SINGULAR);
+        atomicMin(&status->singular_block, block_index);
+      }
+    }
+    const double* src = (bi == k) ? cluster.map_shared_rank(&s_krow[pb][0], k / PTHREADS)
+                                  : cluster.map_shared_rank(&s_crow[pb][0], bc);
+    s_prow[warp][lane] = src[lane];  // PNB == 32 == warp size
+    s_kloc[warp][lane] = *cluster.map_shared_rank(&s_krow[pb][lane], k / PTHREADS);
+    if (tid == 0 && rank == 0) ipiv[j + k] = (int32_t)(j + bi);
+    __syncwarp();
+    const int p = bi;
     if (p != k) {
       if (own && i == k) {
 #pragma unroll
-        for (int c = 0; c < PNB; c++) r[c] = s_prow[c];
+        for (int c = 0; c < PNB; c++) r[c] = s_prow[warp][c];
       } else if (own && i == p) {
 #pragma unroll
-        for (int c = 0; c < PNB; c++) r[c] = s_kloc[c];
+        for (int c = 0; c < PNB; c++) r[c] = s_kloc[warp][c];
       }
     }
     // (4) scale + rank-1 update of rows below k
     if (own && i > k) {
-      const double pv = s_prow[k];
+      const double pv = s_prow[warp][k];
       const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
       double l = 0.0;
 #pragma unroll
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
 #pragma unroll
       for (int c = 0; c < PNB; c++) {
         if (c == k) r[c] = l;
-        else if (c > k) r[c] = fma(-l, s_prow[c], r[c]);
+        else if (c > k) r[c] = fma(-l, s_prow[warp][c], r[c]);
       }
     }
   }
@@ -236,10 +237,15 @@ void panel(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t j, int nb
   const int ncta = (int)cdiv(m, PTHREADS);
   if (ncta > 16)
     throw CudaFailure(cudaErrorInvalidValue, "dgetrf: block dimension > 4096 unsupported", __FILE__, __LINE__);
-  static bool attr = false;
-  if (!attr) {
-    SLB_CUDA_CHECK(cudaFuncSetAttribute(panel_getrf_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
+  static const bool relaxed = [] {
+    const char* e = getenv("SLB_PANEL_BARRIER");
+    return !(e && e[0] == 'r' && e[1] == 'e' && e[2] == 'l' && e[3] == 'e');  // "release": full-scope barrier
+  }();
+  auto kern = relaxed ? panel_getrf_kernel<true> : panel_getrf_kernel<false>;
+  static bool attr[2] = {false, false};
+  if (!attr[relaxed]) {
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr[relaxed] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ncta);
@@ -252,7 +258,7 @@ void panel(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t j, int nb
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel_getrf_kernel, A, lda, n, j, nb, ipiv, status, block_index));
+  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, A, lda, n, j, nb, ipiv, status, block_index));
 }
 
 // Scratch for laswp (grown on demand, per device; stage two is stream ordered).
