@@ -13,6 +13,8 @@
  *   slablu_gpu_T_block         <- ReducedSystem blocks    (stage_one.hpp:303-338, staged parity)
  *   slablu_gpu_reduce_rhs      <- reduce_rhs              (stage_one.hpp:415-433, staged parity)
  *   slablu_gpu_destroy         <- ~Factorization
+ *   slablu_gpu_shard_*         <- (no reference counterpart: the multi-GPU split of
+ *                                 factorize/solve designed in SURVEY.md §8(e))
  *
  * Conventions (mirroring the reference):
  *   - matrices are column major; the operator is the reference's CSR
@@ -140,6 +142,42 @@ slablu_gpu_status slablu_gpu_T_block(const slablu_gpu_fact* fact, int which, int
 slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* fact, const double* f, int64_t nrhs,
                                         double* out);
 void slablu_gpu_destroy(slablu_gpu_fact* fact);
+
+/* ---- multi-GPU: strip-sharded factorization and solve ----------------------
+ * One process per GPU.  Rank r of G owns the contiguous global strips
+ * [s_begin, s_end) (s_begin = r*S/G) and the interfaces [j_begin, j_end) whose
+ * right strip it owns (the last rank also owns a trailing interface).  Stage
+ * one (band LU, Schur blocks) is local.  Stage two and the interface solves
+ * are pipelined over the ranks with ONE message per rank boundary and phase;
+ * the caller moves it (ncclSend/ncclRecv over NVLink between processes, or a
+ * device copy between logical shards on one GPU):
+ *   factorize : shard_factorize_device, then shard_sweep(in from r-1, out to r+1),
+ *               messages n2 x n2 (ld n2)
+ *   solve     : shard_solve_forward(in from r-1, out to r+1), then
+ *               shard_solve_backward(in from r+1, out to r-1), messages n2 x nrhs (ld n2)
+ * NULL message pointers on the ends (rank 0 has no "from r-1" etc.).  All
+ * buffers are device memory of the shard's device.  A sharded factorization
+ * is not usable with slablu_gpu_solve; the sharded solve keeps per-solve state
+ * in the factorization (one solve at a time) and does no refinement. */
+typedef struct {
+  int rank, nranks;
+  int64_t s_begin, s_end;     /* local strips (global indices) */
+  int64_t j_begin, j_end;     /* owned interfaces */
+  int64_t n_strips, n_interfaces;  /* global counts */
+} slablu_gpu_shard_t;
+slablu_gpu_status slablu_gpu_shard_plan(int64_t n1, int64_t n2, int64_t b, int rank, int nranks,
+                                        slablu_gpu_shard_t* out);
+slablu_gpu_status slablu_gpu_shard_factorize_device(int64_t n1, int64_t n2, int64_t nnz,
+                                                    const int32_t* d_row_ptr, const int32_t* d_col_idx,
+                                                    const double* d_val, const slablu_gpu_config* config,
+                                                    int rank, int nranks, slablu_gpu_fact** out);
+slablu_gpu_status slablu_gpu_shard_sweep(slablu_gpu_fact* fact, const double* d_in, double* d_out);
+/* d_f: n x nrhs (ld ldf >= n) device; kept (copied) until the backward phase. */
+slablu_gpu_status slablu_gpu_shard_solve_forward(slablu_gpu_fact* fact, const double* d_f, int64_t ldf,
+                                                 int64_t nrhs, const double* d_in, double* d_out);
+/* d_u: n x nrhs with ldu == n; receives the shard's unknowns, other entries untouched. */
+slablu_gpu_status slablu_gpu_shard_solve_backward(slablu_gpu_fact* fact, const double* d_in, double* d_out,
+                                                  double* d_u, int64_t ldu);
 
 /* Device count visible to the engine (0 when CUDA is unusable). */
 int slablu_gpu_device_count(void);

@@ -34,6 +34,11 @@ class Stats(ctypes.Structure):
                 ("t_solve_strips", D)]
 
 
+class ShardT(ctypes.Structure):
+    _fields_ = [("rank", I), ("nranks", I), ("s_begin", I64), ("s_end", I64), ("j_begin", I64),
+                ("j_end", I64), ("n_strips", I64), ("n_interfaces", I64)]
+
+
 FIELD_FN = ctypes.CFUNCTYPE(D, D, D, P)
 
 # exported symbols of include/slablu_gpu.h (checked by tests/test_abi.py)
@@ -43,7 +48,8 @@ EXPORTS = [
     "slablu_gpu_choose_b", "slablu_gpu_partition", "slablu_gpu_factorize",
     "slablu_gpu_factorize_device", "slablu_gpu_solve", "slablu_gpu_solve_device",
     "slablu_gpu_stats", "slablu_gpu_T_block", "slablu_gpu_reduce_rhs", "slablu_gpu_destroy",
-    "slablu_gpu_device_count",
+    "slablu_gpu_device_count", "slablu_gpu_shard_plan", "slablu_gpu_shard_factorize_device",
+    "slablu_gpu_shard_sweep", "slablu_gpu_shard_solve_forward", "slablu_gpu_shard_solve_backward",
 ]
 
 _lib = None
@@ -77,6 +83,16 @@ def lib():
     L.slablu_gpu_partition.argtypes = [I64, I64, I64, P, P, P, P, I64]
     L.slablu_gpu_factorize.restype = St
     L.slablu_gpu_factorize.argtypes = [I64, I64, P, P, P, P, P]
+    L.slablu_gpu_shard_plan.restype = St
+    L.slablu_gpu_shard_plan.argtypes = [I64, I64, I64, I, I, P]
+    L.slablu_gpu_shard_factorize_device.restype = St
+    L.slablu_gpu_shard_factorize_device.argtypes = [I64, I64, I64, P, P, P, P, I, I, P]
+    L.slablu_gpu_shard_sweep.restype = St
+    L.slablu_gpu_shard_sweep.argtypes = [P, P, P]
+    L.slablu_gpu_shard_solve_forward.restype = St
+    L.slablu_gpu_shard_solve_forward.argtypes = [P, P, I64, I64, P, P]
+    L.slablu_gpu_shard_solve_backward.restype = St
+    L.slablu_gpu_shard_solve_backward.argtypes = [P, P, P, P, I64]
     L.slablu_gpu_factorize_device.restype = St
     L.slablu_gpu_factorize_device.argtypes = [I64, I64, I64, P, P, P, P, P]
     L.slablu_gpu_solve.restype = St

@@ -114,30 +114,41 @@ struct DBuf {
 };
 
 // ---------------------------------------------------------------------------
+// f on the interfaces j in [jlo, jhi) (zero elsewhere: a shard owns only those)
 __global__ void gather_ifc_kernel(const double* f, int64_t ldf, int64_t nrhs, int nifc, const int64_t* off,
-                                  int64_t n2, double* out, int64_t K) {
+                                  int64_t n2, double* out, int64_t K, int jlo, int jhi) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= K * nrhs) return;
   const int64_t c = idx / K, r = idx % K, j = r / n2, q = r % n2;
-  out[idx] = f[c * ldf + off[j] + q];
+  out[idx] = (j >= jlo && j < jhi) ? f[c * ldf + off[j] + q] : 0.0;
 }
 __global__ void scatter_ifc_kernel(const double* u_ifc, int64_t K, int64_t nrhs, const int64_t* off, int64_t n2,
-                                   double* u, int64_t ldu) {
+                                   double* u, int64_t ldu, int jlo, int jhi) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= K * nrhs) return;
   const int64_t c = idx / K, r = idx % K, j = r / n2, q = r % n2;
-  u[c * ldu + off[j] + q] = u_ifc[idx];
+  if (j >= jlo && j < jhi) u[c * ldu + off[j] + q] = u_ifc[idx];
 }
-// red_j = (f_j - contrib[strip j][R]) - contrib[strip j+1][L]  (stage_one.hpp:423-432 order)
+// red_j = (f_j - contrib[strip j][R]) - contrib[strip j+1][L]  (stage_one.hpp:423-432 order);
+// strips are the shard's, global strip g at local index g - sbase
 __global__ void combine_reduce_kernel(double* red, int64_t K, int64_t nrhs, int64_t n2, int nstrips,
-                                      const StripDesc* strips, const double* contrib) {
+                                      const StripDesc* strips, const double* contrib, int sbase) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= K * nrhs) return;
   const int64_t c = idx / K, r = idx % K, j = r / n2, q = r % n2;
   double v = red[idx];
-  if (j < nstrips && strips[j].right == j) v -= contrib[((int64_t)(j * 2 + 1) * nrhs + c) * n2 + q];
-  if (j + 1 < nstrips && strips[j + 1].left == j) v -= contrib[((int64_t)((j + 1) * 2 + 0) * nrhs + c) * n2 + q];
+  const int64_t a = j - sbase, b = j + 1 - sbase;  // local strips left / right of interface j
+  if (a >= 0 && a < nstrips && strips[a].right == j) v -= contrib[((int64_t)(a * 2 + 1) * nrhs + c) * n2 + q];
+  if (b >= 0 && b < nstrips && strips[b].left == j) v -= contrib[((int64_t)(b * 2 + 0) * nrhs + c) * n2 + q];
   red[idx] = v;
+}
+// y[:, c] += x[:, c] for an n x nrhs block (lds, ldd)
+__global__ void add2d_kernel(const double* x, int64_t ldx, double* y, int64_t ldy, int64_t rows, int64_t cols) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < rows * cols;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx % rows, c = idx / rows;
+    y[c * ldy + r] += x[c * ldx + r];
+  }
 }
 // r = f - A u (CSR, one thread per row and column), then u stays; used for refinement.
 __global__ void residual_kernel(const int32_t* rp, const int32_t* ci, const double* v, int64_t n, int64_t nrhs,
@@ -160,6 +171,13 @@ __global__ void copy2d_kernel(const double* src, int64_t lds, double* dst, int64
     const int64_t r = idx % rows, c = idx / rows;
     dst[c * ldd + r] = src[c * lds + r];
   }
+}
+
+void add2d(cudaStream_t st, const double* x, int64_t ldx, double* y, int64_t ldy, int64_t rows, int64_t cols) {
+  if (rows <= 0 || cols <= 0) return;
+  add2d_kernel<<<(unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 8192), 256, 0, st>>>(x, ldx, y, ldy, rows, cols);
+  SLB_CUDA_CHECK(cudaGetLastError());
+  g_launches++;
 }
 
 void copy2d(cudaStream_t st, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols) {
@@ -188,6 +206,13 @@ struct slablu_gpu_fact {
   int64_t n1 = 0, n2 = 0, N = 0, b = 0;
   bool single = false;
   int S = 0, K = 0, Wp = 0;
+  // multi-GPU shard (nranks > 1): global strips [s0, s1) are local (F->S of them, local index
+  // s - s0), interfaces [j0, j1) are owned; K and every interface-indexed array stay global
+  int rank = 0, nranks = 1, Sg = 0, s0 = 0, s1 = 0, j0 = 0, j1 = 0;
+  bool swept = false;
+  // shard solve state between the forward and backward phases
+  DBuf<double> sh_f, sh_red, sh_uifc;
+  int64_t sh_nrhs = 0;
   std::vector<StripDesc> strips_h;
   std::vector<int64_t> ifc_off_h;
   std::vector<int32_t> sym_h;
@@ -238,8 +263,18 @@ void throw_status(const DevStatus& st) {
 int64_t cfg_device(const slablu_gpu_config* c) { return c ? c->device : 0; }
 
 // Factorize with the CSR already on the device.
+// Contiguous strip split for rank r of G and the interfaces it owns (those whose right strip
+// is local; the last rank also owns a trailing interface).  Shared by the engine and
+// slablu_gpu_shard_plan so that hosts and engine agree.
+void shard_ranges(int Sg, int K, int rank, int nranks, int* s0, int* s1, int* j0, int* j1) {
+  *s0 = (int)((int64_t)rank * Sg / nranks);
+  *s1 = (int)((int64_t)(rank + 1) * Sg / nranks);
+  *j0 = rank == 0 ? 0 : *s0 - 1;
+  *j1 = rank == nranks - 1 ? K : *s1 - 1;
+}
+
 slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32_t* rp, const int32_t* ci,
-                                const double* v, const slablu_gpu_config* cfg) {
+                                const double* v, const slablu_gpu_config* cfg, int rank = 0, int nranks = 1) {
   if (n1 * n2 == 0) throw HostError(SLABLU_ERR_CONFIG, "factorize: empty system");
   slablu_gpu_config c{};
   c.c = 0.6;
@@ -269,8 +304,19 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     ints = p.interiors;
     ifcs = p.interfaces;
   }
-  F->S = (int)ints.size();
+  F->Sg = (int)ints.size();
   F->K = (int)ifcs.size();
+  F->rank = rank;
+  F->nranks = nranks;
+  if (nranks > 1) {
+    if (F->single) throw HostError(SLABLU_ERR_CONFIG, "shard: the degenerate single-slab path does not shard");
+    if (F->Sg < nranks)
+      throw HostError(SLABLU_ERR_CONFIG, "shard: " + std::to_string(F->Sg) + " strips cannot cover " +
+                                             std::to_string(nranks) + " ranks");
+  }
+  shard_ranges(F->Sg, F->K, rank, nranks, &F->s0, &F->s1, &F->j0, &F->j1);
+  ints = std::vector<GridStrip>(ints.begin() + F->s0, ints.begin() + F->s1);
+  F->S = (int)ints.size();
   int64_t wmax = 0;
   for (auto& s : ints) wmax = std::max(wmax, s.width);
   F->Wp = (int)round_up(wmax, 8);
@@ -281,8 +327,9 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     StripDesc d;
     d.col0 = (int32_t)ints[s].first_col;
     d.w = (int32_t)ints[s].width;
-    d.left = s > 0 ? s - 1 : -1;
-    d.right = s < K ? s : -1;
+    const int gs = F->s0 + s;  // global strip index
+    d.left = gs > 0 ? gs - 1 : -1;
+    d.right = gs < K ? gs : -1;
     d.left_off = d.left >= 0 ? ifcs[d.left].first_col * n2 : -1;
     d.right_off = d.right >= 0 ? ifcs[d.right].first_col * n2 : -1;
     F->strips_h.push_back(d);
@@ -489,8 +536,17 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     ybuf.release();
     // ---- T assembly --------------------------------------------------------------------
     F->T.alloc(dev, (size_t)(3 * K - 2) * n2 * n2);
+    TRanges tr;
+    tr.sbase = F->s0;
+    tr.nstrips_global = F->Sg;
+    tr.dlo = std::max(0, F->s0 - 1);  // diag blocks touching a local strip
+    tr.dhi = std::min(K, F->s1);
+    tr.olo = F->j0;  // owned: direct operator terms
+    tr.ohi = F->j1;
+    tr.ulo = std::max(0, F->s0 - 1);  // super/sub j come from strip j+1
+    tr.uhi = std::min(K - 1, F->s1 - 1);
     assemble_T(st, n2, K, S, F->strips.p, F->sym.p, gbuf.p, sG, F->Tdiag(), F->Tsup(), F->Tsub(), A,
-               F->ifc_off.p, F->status.p);
+               F->ifc_off.p, F->status.p, tr);
     g_launches += 2;
     check_finite(st, F->T.p, (int64_t)(3 * K - 2) * n2 * n2, F->status.p);
     g_launches++;
@@ -508,7 +564,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     X.alloc(dev, bs);
     I.alloc(dev, bs);
     ipiv.alloc(dev, n2);
-    for (int j = 0; j < K; j++) {
+    for (int j = 0; j < (nranks > 1 ? 0 : K); j++) {  // sharded: slablu_gpu_shard_sweep
       double* Sj = F->Tdiag() + j * bs;
       if (j > 0) {
         dgemm_batched(st, n2, n2, n2, 1.0, F->Tdiag() + (j - 1) * bs, n2, 0, F->Tsup() + (j - 1) * bs, n2, 0, 0.0,
@@ -656,13 +712,13 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     part.alloc(dev, (size_t)8 * n2 * nrhs);
     const unsigned gb = (unsigned)cdiv(K * nrhs, 256);
     // reduce_rhs (stage_one.hpp:415-433)
-    gather_ifc_kernel<<<gb, 256, 0, st>>>(fp, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K);
+    gather_ifc_kernel<<<gb, 256, 0, st>>>(fp, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K, 0, F->K);
     SLB_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
     sa.mode = SWEEP_REDUCE;
     sa.out = contrib.p;
     run_sweep(sa);
     SLB_CUDA_CHECK(cudaEventRecord(s1, st));
-    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, S, F->strips.p, contrib.p);
+    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, S, F->strips.p, contrib.p, 0);
     g_launches += 3;
     // sweep solve (stage_two.hpp:170-188) with S_j^{-1}
     const int64_t bs = n2 * n2;
@@ -687,7 +743,7 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     sa.out = up;
     run_sweep(sa);
     SLB_CUDA_CHECK(cudaEventRecord(s3, st));
-    scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc.p, K, nrhs, F->ifc_off.p, n2, up, N);
+    scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc.p, K, nrhs, F->ifc_off.p, n2, up, N, 0, F->K);
     g_launches += 2;
     SLB_CUDA_CHECK(cudaGetLastError());
     SLB_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -708,7 +764,243 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
 // solve with F->refine steps of iterative refinement against the original
 // operator: u += A~^{-1} (f - A u).  Restores componentwise backward stability
 // lost to the explicit level/Schur inverses.
+// Slab sweeps of the solve for the factorization's (local) strips: reduce (contributions
+// to_X A_ii^{-1} f_i) or recover (A_ii^{-1}(f_i - couplings u)), as in solve_once.
+struct StripSweeper {
+  const slablu_gpu_fact* F;
+  cudaStream_t st;
+  int CH = 8, ntasks = 0, nslots = 0;
+  bool clustered = false;
+  DBuf<int32_t> dtasks, counter;
+  DBuf<double> ybuf;
+  SchurArgs sa{};
+  StripSweeper(const slablu_gpu_fact* F_, const double* fp, int64_t nrhs) : F(F_), st(F_->stream) {
+    const int dev = F->device;
+    const int64_t n2 = F->n2;
+    CH = nrhs <= 8 ? 8 : kSweepChunk;
+    const int64_t nch = cdiv(nrhs, CH);
+    std::vector<int32_t> tasks;
+    for (int s = 0; s < F->S; s++)
+      for (int64_t cch = 0; cch < nch; cch++) {
+        tasks.push_back(s);
+        tasks.push_back(0);
+        tasks.push_back((int32_t)(cch * CH));
+      }
+    ntasks = (int)(tasks.size() / 3);
+    dtasks.alloc(dev, tasks.size());
+    counter.alloc(dev, 1);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    clustered = CH == 8 && strip_solve_fits(F->Wp, n2);
+    nslots = clustered ? ntasks : std::min(sm_count(dev), ntasks);
+    const int64_t sY = n2 * F->Wp * CH;
+    ybuf.alloc(dev, (size_t)nslots * sY);
+    sa.chunk = CH;
+    sa.u13 = F->u13.p;
+    sa.Wp = F->Wp;
+    sa.n2 = n2;
+    sa.nstrips = F->S;
+    sa.strips = F->strips.p;
+    sa.fac = F->fac.p;
+    sa.sF = F->sF;
+    sa.perm = F->perm.p;
+    sa.sP = F->sP;
+    sa.cpl = F->cpl.p;
+    sa.sCPL = F->sCPL;
+    sa.sym = F->sym.p;
+    sa.ybuf = ybuf.p;
+    sa.sY = sY;
+    sa.task_counter = counter.p;
+    sa.ntasks = ntasks;
+    sa.tasks = dtasks.p;
+    sa.N = F->N;
+    sa.K = (int64_t)F->K * n2;
+    sa.nrhs = nrhs;
+    sa.f = fp;
+  }
+  void run(SweepMode mode, const double* u_ifc, double* out) {
+    SLB_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
+    sa.mode = mode;
+    sa.u_ifc = u_ifc;
+    sa.out = out;
+    if (clustered) {
+      strip_solve(st, sa, ntasks);  // rhs pack + cluster sweep
+      g_launches += 2;
+    } else {
+      sweep(st, sa, nslots);
+      g_launches++;
+    }
+  }
+};
+
+void require_shard(const slablu_gpu_fact* F, const char* who) {
+  if (F->nranks <= 1) throw HostError(SLABLU_ERR_CONFIG, std::string(who) + ": not a sharded factorization");
+}
+
+// Stage two of a shard (stage_two.hpp:131-150 restricted to the owned interfaces [j0, j1)):
+// T_{j0 j0} += M_in (rank r-1's strip term and its sweep correction); S_j as usual;
+// M_out = (strip s1-1's term on interface j1) - sub_{j1-1} S_{j1-1}^{-1} super_{j1-1}.
+void shard_sweep_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
+  require_shard(F, "shard_sweep");
+  if (F->rank > 0 && !d_in) throw HostError(SLABLU_ERR_CONFIG, "shard_sweep: rank > 0 needs the message of rank - 1");
+  if (F->rank < F->nranks - 1 && !d_out)
+    throw HostError(SLABLU_ERR_CONFIG, "shard_sweep: rank < nranks - 1 needs an output message buffer");
+  SLB_CUDA_CHECK(cudaSetDevice(F->device));
+  cudaStream_t st = F->stream;
+  const int dev = F->device;
+  const int64_t n2 = F->n2, bs = n2 * n2;
+  const int j0 = F->j0, j1 = F->j1;
+  const int64_t l0 = g_launches.load();
+  cudaEvent_t e0, e1;
+  SLB_CUDA_CHECK(cudaEventCreate(&e0));
+  SLB_CUDA_CHECK(cudaEventCreate(&e1));
+  SLB_CUDA_CHECK(cudaEventRecord(e0, st));
+  if (F->rank > 0) add2d(st, d_in, n2, F->Tdiag() + j0 * bs, n2, n2, n2);
+  DBuf<double> X, I;
+  DBuf<int32_t> ipiv;
+  X.alloc(dev, bs);
+  I.alloc(dev, bs);
+  ipiv.alloc(dev, n2);
+  for (int j = j0; j < j1; j++) {
+    double* Sj = F->Tdiag() + j * bs;
+    if (j > j0) {
+      dgemm_batched(st, n2, n2, n2, 1.0, F->Tdiag() + (j - 1) * bs, n2, 0, F->Tsup() + (j - 1) * bs, n2, 0, 0.0, X.p,
+                    n2, 0, 1);
+      dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X.p, n2, 0, 1.0, Sj, n2, 0, 1);
+      g_launches += 2;
+    }
+    dgetrf(st, n2, Sj, ipiv.p, nullptr, F->status.p, j);
+    dset_identity(st, I.p, n2);
+    dgetrs(st, n2, n2, Sj, ipiv.p, I.p, n2, nullptr);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(Sj, I.p, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    g_launches += 4;
+  }
+  if (F->rank < F->nranks - 1) {
+    SLB_CUDA_CHECK(cudaMemcpyAsync(d_out, F->Tdiag() + j1 * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (j1 > j0) {
+      dgemm_batched(st, n2, n2, n2, 1.0, F->Tdiag() + (j1 - 1) * bs, n2, 0, F->Tsup() + (j1 - 1) * bs, n2, 0, 0.0,
+                    X.p, n2, 0, 1);
+      dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j1 - 1) * bs, n2, 0, X.p, n2, 0, 1.0, d_out, n2, 0, 1);
+      g_launches += 2;
+    }
+  }
+  SLB_CUDA_CHECK(cudaEventRecord(e1, st));
+  SLB_CUDA_CHECK(cudaEventSynchronize(e1));
+  {
+    DevStatus hs;
+    SLB_CUDA_CHECK(cudaMemcpy(&hs, F->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost));
+    if (hs.flags & ERR_SINGULAR)
+      throw HostError(SLABLU_ERR_SINGULAR, "sweep_build: singular Schur complement block", hs.singular_block);
+  }
+  float ms = 0;
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  F->t2 = ms * 1e-3;
+  F->launches_factor += g_launches.load() - l0;
+  F->swept = true;
+}
+
+// Solve, forward half (shard): reduce_rhs on the local strips (stage_one.hpp:415-433) and the
+// forward block sweep over the owned interfaces (stage_two.hpp:170-180).  Messages are
+// n2 x nrhs (ld n2): d_in = strip s0-1's reduction term on interface j0 minus sub u from rank-1.
+void shard_solve_fwd_impl(slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, const double* d_in,
+                          double* d_out) {
+  require_shard(F, "shard_solve_forward");
+  if (!F->swept) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_forward: call slablu_gpu_shard_sweep first");
+  if (F->rank > 0 && !d_in) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_forward: rank > 0 needs the message of rank - 1");
+  if (F->rank < F->nranks - 1 && !d_out)
+    throw HostError(SLABLU_ERR_CONFIG, "shard_solve_forward: rank < nranks - 1 needs an output message buffer");
+  SLB_CUDA_CHECK(cudaSetDevice(F->device));
+  cudaStream_t st = F->stream;
+  const int dev = F->device;
+  const int64_t n2 = F->n2, N = F->N, Kn = (int64_t)F->K * n2, bs = n2 * n2;
+  const int j0 = F->j0, j1 = F->j1;
+  F->sh_nrhs = nrhs;
+  F->sh_f.alloc(dev, (size_t)N * nrhs);
+  copy2d(st, d_f, ldf, F->sh_f.p, N, N, nrhs);
+  F->sh_red.alloc(dev, (size_t)std::max<int64_t>(Kn, 1) * nrhs);
+  F->sh_uifc.alloc(dev, (size_t)std::max<int64_t>(Kn, 1) * nrhs);
+  SLB_CUDA_CHECK(cudaMemsetAsync(F->sh_uifc.p, 0, F->sh_uifc.bytes(), st));
+  DBuf<double> contrib, part;
+  contrib.alloc(dev, (size_t)F->S * 2 * nrhs * n2);
+  part.alloc(dev, (size_t)8 * n2 * nrhs);
+  const unsigned gb = (unsigned)cdiv(Kn * nrhs, 256);
+  gather_ifc_kernel<<<gb, 256, 0, st>>>(F->sh_f.p, N, nrhs, F->K, F->ifc_off.p, n2, F->sh_red.p, Kn, j0, j1);
+  StripSweeper sw(F, F->sh_f.p, nrhs);
+  sw.run(SWEEP_REDUCE, nullptr, contrib.p);
+  combine_reduce_kernel<<<gb, 256, 0, st>>>(F->sh_red.p, Kn, nrhs, n2, F->S, F->strips.p, contrib.p, F->s0);
+  g_launches += 2;
+  double* red = F->sh_red.p;
+  double* uifc = F->sh_uifc.p;
+  if (F->rank > 0) add2d(st, d_in, n2, red + j0 * n2, Kn, n2, nrhs);
+  for (int j = j0; j < j1; j++) {
+    double* rj = red + j * n2;
+    if (j > j0) {
+      dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j - 1) * bs, n2, uifc + (j - 1) * n2, Kn, 1.0, rj, Kn,
+                        part.p);
+      g_launches += 2;
+    }
+    dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tdiag() + j * bs, n2, rj, Kn, 0.0, uifc + j * n2, Kn, part.p);
+    g_launches += 2;
+  }
+  if (F->rank < F->nranks - 1) {
+    copy2d(st, red + j1 * n2, Kn, d_out, n2, n2, nrhs);
+    if (j1 > j0) {
+      dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j1 - 1) * bs, n2, uifc + (j1 - 1) * n2, Kn, 1.0, d_out,
+                        n2, part.p);
+      g_launches += 2;
+    }
+  }
+  SLB_CUDA_CHECK(cudaGetLastError());
+  SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
+// Solve, backward half (shard): backward block sweep (stage_two.hpp:181-187) with u_{j1} from
+// rank+1, recover_interiors on the local strips (stage_one.hpp:438-462).  d_u (ld N) receives the
+// shard's unknowns (local strips and owned interfaces); every other entry is left untouched.
+void shard_solve_bwd_impl(slablu_gpu_fact* F, const double* d_in, double* d_out, double* d_u, int64_t ldu) {
+  require_shard(F, "shard_solve_backward");
+  if (F->sh_nrhs <= 0 || !F->sh_red.p)
+    throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: call slablu_gpu_shard_solve_forward first");
+  if (ldu != F->N) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: ldu must equal n1*n2");
+  if (F->rank < F->nranks - 1 && !d_in)
+    throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: rank < nranks - 1 needs u of interface j_end");
+  if (F->rank > 0 && !d_out) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: rank > 0 needs an output buffer");
+  SLB_CUDA_CHECK(cudaSetDevice(F->device));
+  cudaStream_t st = F->stream;
+  const int dev = F->device;
+  const int64_t n2 = F->n2, N = F->N, Kn = (int64_t)F->K * n2, bs = n2 * n2, nrhs = F->sh_nrhs;
+  const int j0 = F->j0, j1 = F->j1;
+  double* uifc = F->sh_uifc.p;
+  DBuf<double> tmp, part;
+  tmp.alloc(dev, (size_t)n2 * nrhs);
+  part.alloc(dev, (size_t)8 * n2 * nrhs);
+  if (F->rank < F->nranks - 1) copy2d(st, d_in, n2, uifc + j1 * n2, Kn, n2, nrhs);
+  for (int j = j1 - 1; j >= j0; j--) {
+    if (j + 1 >= F->K) continue;
+    dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tsup() + j * bs, n2, uifc + (j + 1) * n2, Kn, 0.0, tmp.p, n2, part.p);
+    dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tdiag() + j * bs, n2, tmp.p, n2, 1.0, uifc + j * n2, Kn, part.p);
+    g_launches += 4;
+  }
+  if (F->rank > 0) copy2d(st, uifc + j0 * n2, Kn, d_out, n2, n2, nrhs);
+  StripSweeper sw(F, F->sh_f.p, nrhs);
+  sw.run(SWEEP_RECOVER, uifc, d_u);
+  const unsigned gb = (unsigned)cdiv(Kn * nrhs, 256);
+  if (Kn > 0) {
+    scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc, Kn, nrhs, F->ifc_off.p, n2, d_u, N, j0, j1);
+    g_launches++;
+  }
+  SLB_CUDA_CHECK(cudaGetLastError());
+  SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+  F->sh_f.release();
+  F->sh_red.release();
+  F->sh_uifc.release();
+  F->sh_nrhs = 0;
+}
+
 void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu) {
+  if (F->nranks > 1)
+    throw HostError(SLABLU_ERR_CONFIG, "solve: sharded factorization, use slablu_gpu_shard_solve_forward/backward");
   std::lock_guard<std::mutex> guard(F->solve_mu);
   cudaStream_t st = F->stream;
   const int dev = F->device;
@@ -824,6 +1116,60 @@ slablu_gpu_status slablu_gpu_factorize_device(int64_t n1, int64_t n2, int64_t nn
   })
 }
 
+slablu_gpu_status slablu_gpu_shard_plan(int64_t n1, int64_t n2, int64_t b, int rank, int nranks,
+                                        slablu_gpu_shard_t* out) {
+  ABI_TRY({
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw HostError(SLABLU_ERR_CONFIG, "shard_plan: bad rank/nranks");
+    if (b > n1 - 2 || n1 < 3) throw HostError(SLABLU_ERR_CONFIG, "shard_plan: the single-slab path does not shard");
+    Partition p = partition(n1, n2, b);
+    const int Sg = (int)p.interiors.size(), K = (int)p.interfaces.size();
+    if (Sg < nranks) throw HostError(SLABLU_ERR_CONFIG, "shard_plan: fewer strips than ranks");
+    int s0, s1, j0, j1;
+    shard_ranges(Sg, K, rank, nranks, &s0, &s1, &j0, &j1);
+    *out = slablu_gpu_shard_t{rank, nranks, s0, s1, j0, j1, Sg, K};
+  })
+}
+
+slablu_gpu_status slablu_gpu_shard_factorize_device(int64_t n1, int64_t n2, int64_t nnz, const int32_t* d_row_ptr,
+                                                    const int32_t* d_col_idx, const double* d_val,
+                                                    const slablu_gpu_config* config, int rank, int nranks,
+                                                    slablu_gpu_fact** out) {
+  ABI_TRY({
+    require_device();
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw HostError(SLABLU_ERR_CONFIG, "shard_factorize: bad rank/nranks");
+    slablu_gpu_config c{};
+    c.c = 0.6;
+    if (config) c = *config;
+    c.refine = 0;  // refinement needs the global residual; the sharded solve is direct
+    *out = factorize_impl(n1, n2, nnz, d_row_ptr, d_col_idx, d_val, &c, rank, nranks);
+  })
+}
+
+slablu_gpu_status slablu_gpu_shard_sweep(slablu_gpu_fact* fact, const double* d_in, double* d_out) {
+  ABI_TRY({
+    if (!fact) throw HostError(SLABLU_ERR_GENERIC, "shard_sweep: null factorization");
+    shard_sweep_impl(fact, d_in, d_out);
+  })
+}
+
+slablu_gpu_status slablu_gpu_shard_solve_forward(slablu_gpu_fact* fact, const double* d_f, int64_t ldf, int64_t nrhs,
+                                                 const double* d_in, double* d_out) {
+  ABI_TRY({
+    if (!fact) throw HostError(SLABLU_ERR_GENERIC, "shard_solve_forward: null factorization");
+    if (nrhs < 1 || ldf < fact->N) throw HostError(SLABLU_ERR_GENERIC, "shard_solve_forward: bad rhs shape");
+    shard_solve_fwd_impl(fact, d_f, ldf, nrhs, d_in, d_out);
+  })
+}
+
+slablu_gpu_status slablu_gpu_shard_solve_backward(slablu_gpu_fact* fact, const double* d_in, double* d_out,
+                                                  double* d_u, int64_t ldu) {
+  ABI_TRY({
+    if (!fact) throw HostError(SLABLU_ERR_GENERIC, "shard_solve_backward: null factorization");
+    shard_solve_bwd_impl(fact, d_in, d_out, d_u, ldu);
+  })
+}
+
 slablu_gpu_status slablu_gpu_solve(const slablu_gpu_fact* fact, const double* f, int64_t ldf, int64_t nrhs,
                                    double* u, int64_t ldu) {
   ABI_TRY({
@@ -931,9 +1277,9 @@ slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* F, const double* 
     sa.ybuf = ybuf.p; sa.sY = sY; sa.task_counter = counter.p; sa.ntasks = ntasks; sa.tasks = dtasks.p;
     sa.N = N; sa.K = K; sa.nrhs = nrhs; sa.f = df.p; sa.mode = SWEEP_REDUCE; sa.out = contrib.p;
     const unsigned gb = (unsigned)cdiv(K * nrhs, 256);
-    gather_ifc_kernel<<<gb, 256, 0, st>>>(df.p, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K);
+    gather_ifc_kernel<<<gb, 256, 0, st>>>(df.p, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K, 0, F->K);
     sweep(st, sa, nslots);
-    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, F->S, F->strips.p, contrib.p);
+    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, F->S, F->strips.p, contrib.p, 0);
     SLB_CUDA_CHECK(cudaGetLastError());
     SLB_CUDA_CHECK(cudaStreamSynchronize(st));
     SLB_CUDA_CHECK(cudaMemcpy(out, red.p, K * nrhs * sizeof(double), cudaMemcpyDeviceToHost));

@@ -124,9 +124,16 @@ bool strip_solve_fits(int Wp, int64_t n2);
 void strip_solve(cudaStream_t st, const SchurArgs& a, int ntasks);  // launches 2 kernels
 
 // T block assembly from per-strip G buffers (reference order: direct, left strip, right strip).
+// Interface-block ranges of a (possibly sharded) factorization: local strips are the global
+// strips [sbase, sbase + nstrips); diag blocks [dlo, dhi) receive local strip terms, owned
+// interfaces [olo, ohi) also their direct operator terms, super/sub [ulo, uhi) come from local strips.
+struct TRanges {
+  int sbase = 0, nstrips_global = 0;
+  int dlo = 0, dhi = 0, olo = 0, ohi = 0, ulo = 0, uhi = 0;
+};
 void assemble_T(cudaStream_t st, int64_t n2, int nifc, int nstrips, const StripDesc* strips,
                 const int32_t* sym, const double* gbuf, int64_t sG, double* Tdiag, double* Tsup,
-                double* Tsub, CsrDev A, const int64_t* ifc_off, DevStatus* status);
+                double* Tsub, CsrDev A, const int64_t* ifc_off, DevStatus* status, const TRanges& tr);
 
 // ---- dense.cu (stage two) -------------------------------------------------------
 // In-place LU with partial pivoting of an n x n column-major matrix (ld = n).

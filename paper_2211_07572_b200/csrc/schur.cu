@@ -419,10 +419,11 @@ __device__ __forceinline__ double cval(const double* gb, int64_t n2, int sym, in
   return gb[((int64_t)(X * 2 + Y) * n2 + p) * n2 + q];
 }
 
-// grid (ceil(n2/32), ceil(n2/32), nblocks) with blocks ordered diag j (k), super j (k-1), sub j (k-1)
+// grid (ceil(n2/32), ceil(n2/32), nblocks) with blocks ordered diag j (k), super j (k-1), sub j (k-1);
+// blocks outside the shard's ranges are skipped, strip terms from non-local strips are left out
 __global__ void assemble_T_kernel(int64_t n2, int nifc, int nstrips, const int32_t* sym,
                                   const double* gbuf, int64_t sG, double* Tdiag, double* Tsup,
-                                  double* Tsub) {
+                                  double* Tsub, TRanges tr) {
   __shared__ double tile[32][33];
   const int b = blockIdx.z;
   int kind, j;
@@ -436,6 +437,7 @@ __global__ void assemble_T_kernel(int64_t n2, int nifc, int nstrips, const int32
     kind = 2;
     j = b - (2 * nifc - 1);
   }
+  if (kind == 0 ? (j < tr.dlo || j >= tr.dhi) : (j < tr.ulo || j >= tr.uhi)) return;
   double* T = (kind == 0 ? Tdiag : kind == 1 ? Tsup : Tsub) + (int64_t)j * n2 * n2;
   const int64_t p0 = (int64_t)blockIdx.x * 32, q0 = (int64_t)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
@@ -445,7 +447,7 @@ __global__ void assemble_T_kernel(int64_t n2, int nifc, int nstrips, const int32
   int ns = 0, st_[2], X_[2], Y_[2];
   if (kind == 0) {
     st_[ns] = j; X_[ns] = 1; Y_[ns] = 1; ns++;
-    if (j + 1 < nstrips) { st_[ns] = j + 1; X_[ns] = 0; Y_[ns] = 0; ns++; }
+    if (j + 1 < tr.nstrips_global) { st_[ns] = j + 1; X_[ns] = 0; Y_[ns] = 0; ns++; }
   } else if (kind == 1) {
     st_[ns] = j + 1; X_[ns] = 0; Y_[ns] = 1; ns++;
   } else {
@@ -459,8 +461,10 @@ __global__ void assemble_T_kernel(int64_t n2, int nifc, int nstrips, const int32
     val[r] = (p < n2 && q < n2) ? T[q * n2 + p] : 0.0;
   }
   for (int e = 0; e < ns; e++) {
-    const double* gb = gbuf + st_[e] * sG;
-    const int sy = sym[st_[e]];
+    const int ls = st_[e] - tr.sbase;  // local strip
+    if (ls < 0 || ls >= nstrips) continue;
+    const double* gb = gbuf + ls * sG;
+    const int sy = sym[ls];
     // coalesced path: load the 32x32 tile with q fastest (row-major gbuf) then transpose
     __syncthreads();
 #pragma unroll
@@ -479,12 +483,12 @@ __global__ void assemble_T_kernel(int64_t n2, int nifc, int nstrips, const int32
   }
 }
 
-// Direct interface blocks from the CSR: grid = nifc, each block scans the
+// Direct interface blocks from the CSR: grid = owned interfaces, each block scans the
 // interface's rows and scatters into the zeroed T blocks.
 __global__ void direct_T_kernel(CsrDev A, int64_t n2, int nifc, const int64_t* ifc_off,
                                 const StripDesc* strips, int nstrips, double* Tdiag, double* Tsup,
-                                double* Tsub, DevStatus* status) {
-  const int j = blockIdx.x;
+                                double* Tsub, DevStatus* status, TRanges tr) {
+  const int j = tr.olo + blockIdx.x;
   const int64_t off = ifc_off[j];
   for (int64_t p = threadIdx.x; p < n2; p += blockDim.x) {
     const int64_t r = off + p;
@@ -494,16 +498,25 @@ __global__ void direct_T_kernel(CsrDev A, int64_t n2, int nifc, const int64_t* i
       if (c >= off && c < off + n2) {
         Tdiag[(int64_t)j * n2 * n2 + (c - off) * n2 + p] = v;
       } else if (j + 1 < nifc && c >= ifc_off[j + 1] && c < ifc_off[j + 1] + n2) {
-        Tsup[(int64_t)j * n2 * n2 + (c - ifc_off[j + 1]) * n2 + p] = v;
+        if (j >= tr.ulo && j < tr.uhi) Tsup[(int64_t)j * n2 * n2 + (c - ifc_off[j + 1]) * n2 + p] = v;
+        else atomicOr(&status->flags, ERR_IFC_STRUCTURE);  // interface-interface coupling across shards
       } else if (j > 0 && c >= ifc_off[j - 1] && c < ifc_off[j - 1] + n2) {
-        Tsub[(int64_t)(j - 1) * n2 * n2 + (c - ifc_off[j - 1]) * n2 + p] = v;
+        if (j - 1 >= tr.ulo && j - 1 < tr.uhi) Tsub[(int64_t)(j - 1) * n2 * n2 + (c - ifc_off[j - 1]) * n2 + p] = v;
+        else atomicOr(&status->flags, ERR_IFC_STRUCTURE);
       } else {
-        // must belong to the strip left (j) or right (j+1) of the interface
-        bool ok = false;
-        for (int s = j; s <= j + 1 && s < nstrips; s++) {
-          const int64_t b0 = (int64_t)strips[s].col0 * n2, b1 = b0 + (int64_t)strips[s].w * n2;
+        // must belong to the strip left (j) or right (j+1) of the interface (a non-local strip
+        // cannot be checked here; its own shard checks it)
+        bool ok = false, unverifiable = false;
+        for (int s = j; s <= j + 1 && s < tr.nstrips_global; s++) {
+          const int ls = s - tr.sbase;
+          if (ls < 0 || ls >= nstrips) {
+            unverifiable = true;
+            continue;
+          }
+          const int64_t b0 = (int64_t)strips[ls].col0 * n2, b1 = b0 + (int64_t)strips[ls].w * n2;
           if (c >= b0 && c < b1) ok = true;
         }
+        ok = ok || unverifiable;
         if (!ok) atomicOr(&status->flags, ERR_IFC_STRUCTURE);
       }
     }
@@ -514,18 +527,21 @@ __global__ void direct_T_kernel(CsrDev A, int64_t n2, int nifc, const int64_t* i
 
 void assemble_T(cudaStream_t st, int64_t n2, int nifc, int nstrips, const StripDesc* strips,
                 const int32_t* sym, const double* gbuf, int64_t sG, double* Tdiag, double* Tsup,
-                double* Tsub, CsrDev A, const int64_t* ifc_off, DevStatus* status) {
+                double* Tsub, CsrDev A, const int64_t* ifc_off, DevStatus* status, const TRanges& tr) {
   const int64_t bsz = n2 * n2 * sizeof(double);
   SLB_CUDA_CHECK(cudaMemsetAsync(Tdiag, 0, bsz * nifc, st));
   if (nifc > 1) {
     SLB_CUDA_CHECK(cudaMemsetAsync(Tsup, 0, bsz * (nifc - 1), st));
     SLB_CUDA_CHECK(cudaMemsetAsync(Tsub, 0, bsz * (nifc - 1), st));
   }
-  direct_T_kernel<<<nifc, 256, 0, st>>>(A, n2, nifc, ifc_off, strips, nstrips, Tdiag, Tsup, Tsub, status);
-  SLB_CUDA_CHECK(cudaGetLastError());
+  if (tr.ohi > tr.olo) {
+    direct_T_kernel<<<tr.ohi - tr.olo, 256, 0, st>>>(A, n2, nifc, ifc_off, strips, nstrips, Tdiag, Tsup, Tsub,
+                                                     status, tr);
+    SLB_CUDA_CHECK(cudaGetLastError());
+  }
   const int nblocks = 3 * nifc - 2;
   dim3 grid((unsigned)cdiv(n2, 32), (unsigned)cdiv(n2, 32), (unsigned)nblocks);
-  assemble_T_kernel<<<grid, dim3(32, 8), 0, st>>>(n2, nifc, nstrips, sym, gbuf, sG, Tdiag, Tsup, Tsub);
+  assemble_T_kernel<<<grid, dim3(32, 8), 0, st>>>(n2, nifc, nstrips, sym, gbuf, sG, Tdiag, Tsup, Tsub, tr);
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -1,0 +1,200 @@
+"""Multi-GPU SlabLU: strip-sharded factorization and solve.
+
+The reference has no multi-GPU path; this is the engine's.  Stage one of
+SlabLU is independent per strip, so rank r of G owns the contiguous global
+strips [s_begin, s_end) and runs their band LU and Schur sweeps alone.  The
+block-tridiagonal stage two (stage_two.hpp:131-188) is a recurrence over the
+interfaces, so it is pipelined over the ranks: rank r owns the interfaces whose
+right strip it holds and exchanges ONE message with each neighbour per phase:
+
+  factorize  r-1 -> r : M = (strip s_begin-1's Schur term on interface j_begin)
+                            - sub S^{-1} super of r-1's last interface        (n2 x n2)
+  solve fwd  r-1 -> r : strip s_begin-1's reduce_rhs term - sub u             (n2 x nrhs)
+  solve bwd  r+1 -> r : u of interface j_end                                  (n2 x nrhs)
+
+Messages are device tensors moved with torch.distributed send/recv (NCCL over
+NVLink between processes), or plain device copies between logical shards of
+one process (``factorize_logical`` / ``solve_logical``), which is how the
+single-GPU tests exercise the engine's shard code.  Any backend with the
+``Shard`` method set can be driven by the same orchestration, which is how the
+CPU tests (gloo, world_size 2) check the protocol.
+"""
+import ctypes
+from dataclasses import dataclass
+
+from . import _lib
+from ._lib import lib
+from .slablu import SolverConfig, _check
+
+
+def shard_ranges(n_strips, n_interfaces, rank, nranks):
+    """(s_begin, s_end, j_begin, j_end): mirror of the engine's shard_ranges (engine.cu)."""
+    s0 = rank * n_strips // nranks
+    s1 = (rank + 1) * n_strips // nranks
+    j0 = 0 if rank == 0 else s0 - 1
+    j1 = n_interfaces if rank == nranks - 1 else s1 - 1
+    return s0, s1, j0, j1
+
+
+@dataclass
+class ShardPlan:
+    rank: int
+    nranks: int
+    s_begin: int
+    s_end: int
+    j_begin: int
+    j_end: int
+    n_strips: int
+    n_interfaces: int
+
+
+def shard_plan(n1, n2, b, rank, nranks) -> ShardPlan:
+    out = _lib.ShardT()
+    _check(lib().slablu_gpu_shard_plan(int(n1), int(n2), int(b), int(rank), int(nranks), ctypes.byref(out)))
+    return ShardPlan(out.rank, out.nranks, out.s_begin, out.s_end, out.j_begin, out.j_end, out.n_strips,
+                     out.n_interfaces)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+class Shard:
+    """One rank's shard of the factorization on its GPU (C-ABI handle).
+
+    row_ptr/col_idx/values: the full operator's CSR as CUDA tensors of the
+    shard's device (every rank reads only its strips and interfaces)."""
+
+    def __init__(self, n1, n2, row_ptr, col_idx, values, config: SolverConfig, rank, nranks):
+        import torch
+        self.torch = torch
+        self.n1, self.n2, self.N = int(n1), int(n2), int(n1) * int(n2)
+        self.rank, self.nranks = int(rank), int(nranks)
+        self.device = row_ptr.device
+        h = ctypes.c_void_p()
+        cfg = config._c()
+        _check(lib().slablu_gpu_shard_factorize_device(self.n1, self.n2, int(values.numel()), row_ptr.data_ptr(),
+                                                        col_idx.data_ptr(), values.data_ptr(), ctypes.byref(cfg),
+                                                        self.rank, self.nranks, ctypes.byref(h)))
+        self._h = h
+        st = _lib.Stats()
+        _check(lib().slablu_gpu_stats(self._h, ctypes.byref(st)))
+        self.b = int(st.b)
+        self.plan = shard_plan(self.n1, self.n2, self.b, self.rank, self.nranks)
+        self.stats = st
+
+    def new_message(self, cols):
+        """An n2 x cols column-major message buffer (torch shape (cols, n2))."""
+        return self.torch.empty((cols, self.n2), dtype=self.torch.float64, device=self.device)
+
+    def sweep(self, m_in, m_out):
+        _check(lib().slablu_gpu_shard_sweep(self._h, _ptr(m_in), _ptr(m_out)))
+
+    def solve_forward(self, f, m_in, m_out):
+        """f: (nrhs, N) CUDA tensor (column-major N x nrhs)."""
+        nrhs = f.shape[0] if f.dim() == 2 else 1
+        _check(lib().slablu_gpu_shard_solve_forward(self._h, f.data_ptr(), self.N, nrhs, _ptr(m_in), _ptr(m_out)))
+
+    def solve_backward(self, m_in, m_out, u):
+        """u: (nrhs, N) CUDA tensor; receives this shard's unknowns (others untouched)."""
+        _check(lib().slablu_gpu_shard_solve_backward(self._h, _ptr(m_in), _ptr(m_out), u.data_ptr(), self.N))
+
+    def refresh_stats(self):
+        st = _lib.Stats()
+        _check(lib().slablu_gpu_stats(self._h, ctypes.byref(st)))
+        self.stats = st
+        return st
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().slablu_gpu_destroy(self._h)
+            self._h = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class TorchExchange:
+    """Neighbour messages over torch.distributed (NCCL for CUDA tensors, gloo for CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+
+    def send_next(self, t):
+        self.dist.send(t, self.rank + 1, group=self.group)
+
+    def send_prev(self, t):
+        self.dist.send(t, self.rank - 1, group=self.group)
+
+    def recv_prev(self, t):
+        self.dist.recv(t, self.rank - 1, group=self.group)
+
+    def recv_next(self, t):
+        self.dist.recv(t, self.rank + 1, group=self.group)
+
+
+def factorize_dist(shard, ex):
+    """Stage two of a sharded factorization across processes (call after stage one)."""
+    last = shard.rank == shard.nranks - 1
+    m_in = None
+    if shard.rank > 0:
+        m_in = shard.new_message(shard.n2)
+        ex.recv_prev(m_in)
+    m_out = None if last else shard.new_message(shard.n2)
+    shard.sweep(m_in, m_out)
+    if not last:
+        ex.send_next(m_out)
+
+
+def solve_dist(shard, f, u, ex):
+    """u (nrhs, N), zero-initialised by the caller, receives this rank's unknowns."""
+    nrhs = f.shape[0] if f.dim() == 2 else 1
+    last = shard.rank == shard.nranks - 1
+    m_in = None
+    if shard.rank > 0:
+        m_in = shard.new_message(nrhs)
+        ex.recv_prev(m_in)
+    m_out = None if last else shard.new_message(nrhs)
+    shard.solve_forward(f, m_in, m_out)
+    if not last:
+        ex.send_next(m_out)
+    b_in = None
+    if not last:
+        b_in = shard.new_message(nrhs)
+        ex.recv_next(b_in)
+    b_out = shard.new_message(nrhs) if shard.rank > 0 else None
+    shard.solve_backward(b_in, b_out, u)
+    if shard.rank > 0:
+        ex.send_prev(b_out)
+    return u
+
+
+def factorize_logical(shards):
+    """Stage two for G shards held by one process (messages are device copies)."""
+    m = None
+    for r, sh in enumerate(shards):
+        out = sh.new_message(sh.n2) if r < len(shards) - 1 else None
+        sh.sweep(m, out)
+        m = out
+
+
+def solve_logical(shards, f, u_parts):
+    """Pipelined solve over logical shards; u_parts[r] (zeroed) receives shard r's unknowns."""
+    nrhs = f.shape[0] if f.dim() == 2 else 1
+    m = None
+    for r, sh in enumerate(shards):
+        out = sh.new_message(nrhs) if r < len(shards) - 1 else None
+        sh.solve_forward(f, m, out)
+        m = out
+    m = None
+    for r in range(len(shards) - 1, -1, -1):
+        sh = shards[r]
+        out = sh.new_message(nrhs) if r > 0 else None
+        sh.solve_backward(m, out, u_parts[r])
+        m = out
+    return u_parts
