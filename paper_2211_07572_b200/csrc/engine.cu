@@ -209,7 +209,7 @@ struct slablu_gpu_fact {
   // multi-GPU shard (nranks > 1): global strips [s0, s1) are local (F->S of them, local index
   // s - s0), interfaces [j0, j1) are owned; K and every interface-indexed array stay global
   int rank = 0, nranks = 1, Sg = 0, s0 = 0, s1 = 0, j0 = 0, j1 = 0;
-  bool swept = false;
+  bool sharded = false, swept = false;
   // shard solve state between the forward and backward phases
   DBuf<double> sh_f, sh_red, sh_uifc;
   int64_t sh_nrhs = 0;
@@ -274,7 +274,8 @@ void shard_ranges(int Sg, int K, int rank, int nranks, int* s0, int* s1, int* j0
 }
 
 slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32_t* rp, const int32_t* ci,
-                                const double* v, const slablu_gpu_config* cfg, int rank = 0, int nranks = 1) {
+                                const double* v, const slablu_gpu_config* cfg, int rank = 0, int nranks = 1,
+                                bool sharded = false) {
   if (n1 * n2 == 0) throw HostError(SLABLU_ERR_CONFIG, "factorize: empty system");
   slablu_gpu_config c{};
   c.c = 0.6;
@@ -308,7 +309,8 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   F->K = (int)ifcs.size();
   F->rank = rank;
   F->nranks = nranks;
-  if (nranks > 1) {
+  F->sharded = sharded;
+  if (sharded) {
     if (F->single) throw HostError(SLABLU_ERR_CONFIG, "shard: the degenerate single-slab path does not shard");
     if (F->Sg < nranks)
       throw HostError(SLABLU_ERR_CONFIG, "shard: " + std::to_string(F->Sg) + " strips cannot cover " +
@@ -564,7 +566,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     X.alloc(dev, bs);
     I.alloc(dev, bs);
     ipiv.alloc(dev, n2);
-    for (int j = 0; j < (nranks > 1 ? 0 : K); j++) {  // sharded: slablu_gpu_shard_sweep
+    for (int j = 0; j < (sharded ? 0 : K); j++) {  // sharded: slablu_gpu_shard_sweep
       double* Sj = F->Tdiag() + j * bs;
       if (j > 0) {
         dgemm_batched(st, n2, n2, n2, 1.0, F->Tdiag() + (j - 1) * bs, n2, 0, F->Tsup() + (j - 1) * bs, n2, 0, 0.0,
@@ -833,7 +835,7 @@ struct StripSweeper {
 };
 
 void require_shard(const slablu_gpu_fact* F, const char* who) {
-  if (F->nranks <= 1) throw HostError(SLABLU_ERR_CONFIG, std::string(who) + ": not a sharded factorization");
+  if (!F->sharded) throw HostError(SLABLU_ERR_CONFIG, std::string(who) + ": not a sharded factorization");
 }
 
 // Stage two of a shard (stage_two.hpp:131-150 restricted to the owned interfaces [j0, j1)):
@@ -999,7 +1001,7 @@ void shard_solve_bwd_impl(slablu_gpu_fact* F, const double* d_in, double* d_out,
 }
 
 void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu) {
-  if (F->nranks > 1)
+  if (F->sharded)
     throw HostError(SLABLU_ERR_CONFIG, "solve: sharded factorization, use slablu_gpu_shard_solve_forward/backward");
   std::lock_guard<std::mutex> guard(F->solve_mu);
   cudaStream_t st = F->stream;
@@ -1142,7 +1144,7 @@ slablu_gpu_status slablu_gpu_shard_factorize_device(int64_t n1, int64_t n2, int6
     c.c = 0.6;
     if (config) c = *config;
     c.refine = 0;  // refinement needs the global residual; the sharded solve is direct
-    *out = factorize_impl(n1, n2, nnz, d_row_ptr, d_col_idx, d_val, &c, rank, nranks);
+    *out = factorize_impl(n1, n2, nnz, d_row_ptr, d_col_idx, d_val, &c, rank, nranks, true);
   })
 }
 

@@ -27,6 +27,7 @@ def _shards(sysm, n1, n2, b, G):
     (1, 64, 40, 7, 30.0, 3, 2),
     (2, 120, 60, 9, 40.0, 4, 1),
     (1, 64, 40, 7, 30.0, 8, 3),     # one strip per rank
+    (1, 64, 40, 7, 30.0, 1, 1),     # one shard = the whole problem through the shard entry points
 ])
 def test_logical_shards_match_oracle(kind, n1, n2, b, kappa, G, nrhs):
     spec = (S.poisson_log_problem(n1, n2) if kind == 0 else
