@@ -27,6 +27,9 @@
  *     its device memory; solves are const and may be issued repeatedly.
  *   - there is no CPU fallback: without a usable CUDA device every compute
  *     entry point returns SLABLU_ERR_CUDA.
+ *   - device-pointer entry points run on the factorization's own stream: the
+ *     caller's writes to their inputs must be complete before the call, and
+ *     outputs are complete when the call returns.
  */
 #ifndef SLABLU_GPU_H
 #define SLABLU_GPU_H
@@ -178,6 +181,10 @@ slablu_gpu_status slablu_gpu_shard_solve_forward(slablu_gpu_fact* fact, const do
 /* d_u: n x nrhs with ldu == n; receives the shard's unknowns, other entries untouched. */
 slablu_gpu_status slablu_gpu_shard_solve_backward(slablu_gpu_fact* fact, const double* d_in, double* d_out,
                                                   double* d_u, int64_t ldu);
+/* r = f - A u over all n rows with the operator kept by a factorization made with
+ * config.refine > 0 (device buffers, ld n); the host-driven refinement of the sharded solve. */
+slablu_gpu_status slablu_gpu_residual(const slablu_gpu_fact* fact, const double* d_f, int64_t ldf, int64_t nrhs,
+                                      const double* d_u, int64_t ldu, double* d_r);
 
 /* Device count visible to the engine (0 when CUDA is unusable). */
 int slablu_gpu_device_count(void);

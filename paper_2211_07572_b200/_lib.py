@@ -50,6 +50,7 @@ EXPORTS = [
     "slablu_gpu_stats", "slablu_gpu_T_block", "slablu_gpu_reduce_rhs", "slablu_gpu_destroy",
     "slablu_gpu_device_count", "slablu_gpu_shard_plan", "slablu_gpu_shard_factorize_device",
     "slablu_gpu_shard_sweep", "slablu_gpu_shard_solve_forward", "slablu_gpu_shard_solve_backward",
+    "slablu_gpu_residual",
 ]
 
 _lib = None
@@ -87,6 +88,8 @@ def lib():
     L.slablu_gpu_shard_plan.argtypes = [I64, I64, I64, I, I, P]
     L.slablu_gpu_shard_factorize_device.restype = St
     L.slablu_gpu_shard_factorize_device.argtypes = [I64, I64, I64, P, P, P, P, I, I, P]
+    L.slablu_gpu_residual.restype = St
+    L.slablu_gpu_residual.argtypes = [P, P, I64, I64, P, I64, P]
     L.slablu_gpu_shard_sweep.restype = St
     L.slablu_gpu_shard_sweep.argtypes = [P, P, P]
     L.slablu_gpu_shard_solve_forward.restype = St

@@ -1143,8 +1143,24 @@ slablu_gpu_status slablu_gpu_shard_factorize_device(int64_t n1, int64_t n2, int6
     slablu_gpu_config c{};
     c.c = 0.6;
     if (config) c = *config;
-    c.refine = 0;  // refinement needs the global residual; the sharded solve is direct
+    // refine > 0 keeps a copy of the CSR for slablu_gpu_residual (host-driven refinement)
     *out = factorize_impl(n1, n2, nnz, d_row_ptr, d_col_idx, d_val, &c, rank, nranks, true);
+  })
+}
+
+slablu_gpu_status slablu_gpu_residual(const slablu_gpu_fact* fact, const double* d_f, int64_t ldf, int64_t nrhs,
+                                     const double* d_u, int64_t ldu, double* d_r) {
+  ABI_TRY({
+    if (!fact) throw HostError(SLABLU_ERR_GENERIC, "residual: null factorization");
+    if (!fact->a_rp.p) throw HostError(SLABLU_ERR_CONFIG, "residual: factorize with config.refine > 0 to keep the operator");
+    if (ldf != fact->N || ldu != fact->N || nrhs < 1) throw HostError(SLABLU_ERR_GENERIC, "residual: ld must equal n1*n2");
+    SLB_CUDA_CHECK(cudaSetDevice(fact->device));
+    const int64_t N = fact->N;
+    residual_kernel<<<(unsigned)cdiv(N * nrhs, 256), 256, 0, fact->stream>>>(fact->a_rp.p, fact->a_ci.p, fact->a_v.p, N,
+                                                                         nrhs, d_f, d_u, d_r);
+    SLB_CUDA_CHECK(cudaGetLastError());
+    SLB_CUDA_CHECK(cudaStreamSynchronize(fact->stream));
+    g_launches++;
   })
 }
 

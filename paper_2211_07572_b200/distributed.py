@@ -99,6 +99,11 @@ class Shard:
         """u: (nrhs, N) CUDA tensor; receives this shard's unknowns (others untouched)."""
         _check(lib().slablu_gpu_shard_solve_backward(self._h, _ptr(m_in), _ptr(m_out), u.data_ptr(), self.N))
 
+    def residual(self, f, u, r):
+        """r = f - A u (all rows; f, u, r: (nrhs, N) CUDA tensors)."""
+        nrhs = f.shape[0] if f.dim() == 2 else 1
+        _check(lib().slablu_gpu_residual(self._h, f.data_ptr(), self.N, nrhs, u.data_ptr(), self.N, r.data_ptr()))
+
     def refresh_stats(self):
         st = _lib.Stats()
         _check(lib().slablu_gpu_stats(self._h, ctypes.byref(st)))
@@ -174,6 +179,24 @@ def solve_dist(shard, f, u, ex):
     return u
 
 
+def solve_dist_refined(shard, f, ex, refine=1, group=None):
+    """Full solution on every rank: pipelined solve, all-reduce of the disjoint pieces, then
+    ``refine`` steps of iterative refinement (every rank forms the whole residual r = f - A u)."""
+    import torch
+    import torch.distributed as dist
+    u = torch.zeros_like(f)
+    solve_dist(shard, f, u, ex)
+    dist.all_reduce(u, group=group)
+    for _ in range(refine):
+        r = torch.empty_like(f)
+        shard.residual(f, u, r)
+        du = torch.zeros_like(f)
+        solve_dist(shard, r, du, ex)
+        dist.all_reduce(du, group=group)
+        u += du
+    return u
+
+
 def factorize_logical(shards):
     """Stage two for G shards held by one process (messages are device copies)."""
     m = None
@@ -181,6 +204,17 @@ def factorize_logical(shards):
         out = sh.new_message(sh.n2) if r < len(shards) - 1 else None
         sh.sweep(m, out)
         m = out
+
+
+def solve_logical_refined(shards, f, refine=1):
+    """solve_logical + iterative refinement; returns the full solution."""
+    import torch
+    u = sum(solve_logical(shards, f, [torch.zeros_like(f) for _ in shards]))
+    for _ in range(refine):
+        r = torch.empty_like(f)
+        shards[0].residual(f, u, r)
+        u = u + sum(solve_logical(shards, r, [torch.zeros_like(f) for _ in shards]))
+    return u
 
 
 def solve_logical(shards, f, u_parts):

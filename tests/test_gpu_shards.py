@@ -55,6 +55,25 @@ def test_logical_shards_match_oracle(kind, n1, n2, b, kappa, G, nrhs):
         sh.close()
 
 
+def test_logical_shards_refined_backward_error():
+    n1, n2, b, kappa, G = 200, 120, 15, 80.0, 3
+    sysm = S.assemble_fd5(S.helmholtz_bump_problem(n1, n2, kappa))
+    shards, dev = _shards(sysm, n1, n2, b, G)
+    D.factorize_logical(shards)
+    ft = torch.from_numpy(sysm.rhs).to(dev).reshape(1, -1)
+    u0 = D.solve_logical_refined(shards, ft, refine=0).cpu().numpy().ravel()
+    u1 = D.solve_logical_refined(shards, ft, refine=1).cpu().numpy().ravel()
+    rows = np.repeat(np.arange(sysm.dim()), np.diff(sysm.row_ptr))
+    a_inf = np.bincount(rows, weights=np.abs(sysm.values)).max()
+
+    def berr(u):
+        return np.linalg.norm(sysm.matvec(u) - sysm.rhs) / (a_inf * np.linalg.norm(u) + np.linalg.norm(sysm.rhs))
+    assert berr(u1) < 1e-15
+    assert berr(u1) <= berr(u0)
+    for sh in shards:
+        sh.close()
+
+
 def test_sharded_factorization_refuses_plain_solve():
     sysm = S.assemble_fd5(S.poisson_log_problem(40, 10))
     shards, dev = _shards(sysm, 40, 10, 3, 2)
