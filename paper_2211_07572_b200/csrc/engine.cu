@@ -18,6 +18,7 @@
 #include <climits>
 #include <cstring>
 #include <map>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -406,6 +407,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   cwork.alloc(dev, (size_t)CCH * 4 * Wp * Wp * S);
   cudaEvent_t chunk_ev;
   SLB_CUDA_CHECK(cudaEventCreateWithFlags(&chunk_ev, cudaEventDisableTiming));
+  static const bool defer_conv = getenv("SLB_CONV_DEFER") != nullptr;  // measurement: no overlap
   auto convert_chunk = [&](int64_t c0, int64_t c1) {
     SLB_CUDA_CHECK(cudaEventRecord(chunk_ev, st));
     SLB_CUDA_CHECK(cudaStreamWaitEvent(cst, chunk_ev, 0));
@@ -418,7 +420,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   for (int64_t l = 0; l < n2; l++) {
     const int64_t nxt = l + 1;
     const bool has_next = nxt < n2;
-    if (l > 0 && l % CCH == 0) convert_chunk(l - CCH, l);
+    if (l > 0 && l % CCH == 0 && !defer_conv) convert_chunk(l - CCH, l);
     if (has_next && nxt % LCH == 0) {
       extract_levels(st, A, F->strips.p, S, n2, Wp, nxt, std::min(LCH, n2 - nxt), nx.p, sNX, F->status.p);
       g_launches++;
@@ -448,6 +450,12 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     }
     cur = 1 - cur;
   }
+  cudaEvent_t chain_end = nullptr;
+  if (defer_conv) {
+    SLB_CUDA_CHECK(cudaEventCreate(&chain_end));
+    SLB_CUDA_CHECK(cudaEventRecord(chain_end, st));
+    for (int64_t c0 = 0; c0 + CCH < n2; c0 += CCH) convert_chunk(c0, c0 + CCH);
+  }
   convert_chunk(((n2 - 1) / CCH) * CCH, n2);
   SLB_CUDA_CHECK(cudaEventRecord(chunk_ev, cst));
   SLB_CUDA_CHECK(cudaStreamWaitEvent(st, chunk_ev, 0));
@@ -456,6 +464,14 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   nx.release();
   sv.release();
   SLB_CUDA_CHECK(cudaEventRecord(ec, st));
+  if (chain_end) {
+    SLB_CUDA_CHECK(cudaEventSynchronize(ec));
+    float a = 0, b2 = 0;
+    SLB_CUDA_CHECK(cudaEventElapsedTime(&a, e0, chain_end));
+    SLB_CUDA_CHECK(cudaEventElapsedTime(&b2, chain_end, ec));
+    fprintf(stderr, "[slablu] chain alone %.1f ms, conversion after it %.1f ms\n", a, b2);
+    cudaEventDestroy(chain_end);
+  }
   {
     DevStatus hs;
     SLB_CUDA_CHECK(cudaMemcpyAsync(&hs, F->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));

@@ -25,6 +25,71 @@ constexpr int KS = MMAX + 4; // staged T row stride (== 4 mod 16)
 
 __device__ __forceinline__ int sw32(int r, int n) { return r * TN + (n ^ ((r & 3) << 2)); }
 
+// Inverses of the nb diagonal RB x RB blocks of T (unit lower or upper non-unit), identity
+// padded past m, into Dv[b][i][k] (row-major).  Thread (b, c) forms column c by substitution,
+// once per CTA, so the per-block diagonal step becomes a small DMMA product instead of a
+// 16-step serial solve by one warp while the others wait at the barrier.
+template <bool LOWER, bool ROWMAJOR>
+__device__ __forceinline__ void diag_inverses(const double* T, int64_t ldt, int m, int nb, double* Dv, int tid,
+                                              int nthreads) {
+  for (int idx = tid; idx < nb * RB * RB; idx += nthreads) {
+    const int b = idx / (RB * RB), i = (idx / RB) % RB, k = idx % RB;
+    const int r0 = b * RB, h = min(m, r0 + RB) - r0;
+    Dv[idx] = (i < h && k < h) ? T[ROWMAJOR ? (int64_t)(r0 + i) * ldt + r0 + k : (int64_t)(r0 + k) * ldt + r0 + i]
+                               : (i == k ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  double x[RB];
+  const bool mine = tid < nb * RB;
+  if (mine) {
+    const int c = tid % RB;
+    const double* D = Dv + (tid / RB) * RB * RB;
+    if (LOWER) {
+#pragma unroll
+      for (int i = 0; i < RB; i++) {
+        double sacc = i == c ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < RB; k++)
+          if (k < i) sacc = fma(-D[i * RB + k], x[k], sacc);
+        x[i] = sacc;
+      }
+    } else {
+#pragma unroll
+      for (int i = RB - 1; i >= 0; i--) {
+        double sacc = i == c ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < RB; k++)
+          if (k > i) sacc = fma(-D[i * RB + k], x[k], sacc);
+        x[i] = sacc / D[i * RB + i];
+      }
+    }
+  }
+  __syncthreads();
+  if (mine) {
+    const int c = tid % RB;
+    double* D = Dv + (tid / RB) * RB * RB;
+#pragma unroll
+    for (int i = 0; i < RB; i++) D[i * RB + c] = x[i];
+  }
+  __syncthreads();
+}
+
+// X[r0:r0+16, 0:32] = Dinv_b X[r0:r0+16, 0:32] in place; 8 warps, warp (mt, nt) one 8x8 tile.
+__device__ __forceinline__ void apply_diag_inverse(const double* Di, double* X, int r0, int r1, int warp, int g,
+                                                   int t) {
+  const int mt = warp >> 2, nt = warp & 3;
+  double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < RB / 4; kk++)
+    dmma884(d0, d1, Di[(mt * 8 + g) * RB + kk * 4 + t], X[sw32(r0 + kk * 4 + t, nt * 8 + g)]);
+  __syncthreads();
+  const int row = r0 + mt * 8 + g;
+  if (row < r1) {
+    X[sw32(row, nt * 8 + 2 * t)] = d0;
+    X[sw32(row, nt * 8 + 2 * t + 1)] = d1;
+  }
+}
+
 template <bool LOWER, bool ROWMAJOR>
 __global__ void __launch_bounds__(256) trsm_small_kernel(int m, const double* __restrict__ Tg, int64_t ldt,
                                                          int64_t sT, double* Bg, int64_t ldb, int64_t sB,
@@ -32,6 +97,7 @@ __global__ void __launch_bounds__(256) trsm_small_kernel(int m, const double* __
   extern __shared__ double sm[];
   double* X = sm;                       // MMAX * TN
   double* sTb = sm + MMAX * TN;         // 2 x RB x KS
+  double* Dv = sTb + 2 * RB * KS;       // (MMAX / RB) x RB x RB diagonal-block inverses
   const int64_t item = blockIdx.y;
   const double* T = Tg + item * sT;
   double* B = Bg + item * sB;
@@ -64,6 +130,8 @@ __global__ void __launch_bounds__(256) trsm_small_kernel(int m, const double* __
     const int64_t c = c0 + n;
     X[sw32(r, n)] = c < ncols ? B[c * ldb + r] : 0.0;
   }
+  for (int idx = m * TN + tid; idx < nb * RB * TN; idx += 256) X[idx] = 0.0;  // padding rows of the last block
+  diag_inverses<LOWER, ROWMAJOR>(T, ldt, m, nb, Dv, tid, 256);
   const int mt = warp >> 2, nt = warp & 3;
   for (int bi = 0; bi < nb; bi++) {
     const int b = block_of(bi);
@@ -96,36 +164,8 @@ __global__ void __launch_bounds__(256) trsm_small_kernel(int m, const double* __
       }
     }
     __syncthreads();
-    // diagonal solve, one thread per column
-    if (tid < TN) {
-      const int n = tid;
-      double x[RB];
-#pragma unroll
-      for (int rr = 0; rr < RB; rr++) x[rr] = rr < h ? X[sw32(r0 + rr, n)] : 0.0;
-      if (LOWER) {
-#pragma unroll
-        for (int rr = 1; rr < RB; rr++) {
-          double sacc = x[rr];
-#pragma unroll
-          for (int cc = 0; cc < RB; cc++)
-            if (cc < rr) sacc = fma(-Tb[rr * KS + r0 + cc], x[cc], sacc);
-          x[rr] = sacc;
-        }
-      } else {
-#pragma unroll
-        for (int rr = RB - 1; rr >= 0; rr--) {
-          if (rr >= h) continue;
-          double sacc = x[rr];
-#pragma unroll
-          for (int cc = 0; cc < RB; cc++)
-            if (cc > rr && cc < h) sacc = fma(-Tb[rr * KS + r0 + cc], x[cc], sacc);
-          x[rr] = sacc / Tb[rr * KS + r0 + rr];
-        }
-      }
-#pragma unroll
-      for (int rr = 0; rr < RB; rr++)
-        if (rr < h) X[sw32(r0 + rr, n)] = x[rr];
-    }
+    // diagonal block: X_b = D_b^{-1} X_b (precomputed inverse, DMMA)
+    apply_diag_inverse(Dv + b * RB * RB, X, r0, r1, warp, g, t);
     __syncthreads();  // X block final; the staging buffer may be refilled
   }
   cp_async_wait<0>();
@@ -144,7 +184,7 @@ void trsm_small_batched(cudaStream_t st, bool lower, int m, const double* T, int
   if (m <= 0 || ncols <= 0 || batch <= 0) return;
   if (m > MMAX)
     throw CudaFailure(cudaErrorInvalidValue, "trsm_small_batched: m must be <= 160", __FILE__, __LINE__);
-  const size_t smem = (size_t)(MMAX * TN + 2 * RB * KS) * sizeof(double);
+  const size_t smem = (size_t)(MMAX * TN + 2 * RB * KS + MMAX * RB) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     SLB_CUDA_CHECK(cudaFuncSetAttribute(trsm_small_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -182,6 +222,7 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
   const int Wp = a.Wp, s = blockIdx.y;
   double* X = sm;                 // MMAX * TN   (U1213 tile, swizzled)
   double* sTb = sm + MMAX * TN;   // 2 x RB x KS (staged rows of L11 / L21)
+  double* Dv = sTb + 2 * RB * KS; // inverses of L11's 16 x 16 diagonal blocks
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int c0 = blockIdx.x * TN;
@@ -215,6 +256,8 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
     const int n = idx / m, r = idx % m;
     X[sw32(r, n)] = n < ncol ? Rval(perm[r], c0 + n) : 0.0;
   }
+  for (int idx = m * TN + tid; idx < nb * RB * TN; idx += 256) X[idx] = 0.0;
+  diag_inverses<true, true>(LU11, Wp, m, nb, Dv, tid, 256);
   const int mt = warp >> 2, nt = warp & 3;
   // ---- TRSM: X = L11^{-1} X (unit lower)
   for (int b = 0; b < nb; b++) {
@@ -245,23 +288,7 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
       }
     }
     __syncthreads();
-    if (tid < TN) {
-      const int n = tid;
-      double x[RB];
-#pragma unroll
-      for (int rr = 0; rr < RB; rr++) x[rr] = rr < h ? X[sw32(r0 + rr, n)] : 0.0;
-#pragma unroll
-      for (int rr = 1; rr < RB; rr++) {
-        double sacc = x[rr];
-#pragma unroll
-        for (int cc = 0; cc < RB; cc++)
-          if (cc < rr) sacc = fma(-Tb[rr * KS + r0 + cc], x[cc], sacc);
-        x[rr] = sacc;
-      }
-#pragma unroll
-      for (int rr = 0; rr < RB; rr++)
-        if (rr < h) X[sw32(r0 + rr, n)] = x[rr];
-    }
+    apply_diag_inverse(Dv + b * RB * RB, X, r0, r1, warp, g, t);
     __syncthreads();
   }
   // ---- U1213 tile out
@@ -303,7 +330,7 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
 }  // namespace
 
 void level_update(cudaStream_t st, const LevelArgs& a) {
-  const size_t smem = (size_t)(MMAX * TN + 2 * RB * KS) * sizeof(double);
+  const size_t smem = (size_t)(MMAX * TN + 2 * RB * KS + MMAX * RB) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     SLB_CUDA_CHECK(cudaFuncSetAttribute(level_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
