@@ -148,8 +148,10 @@ void dgemm_batched(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alph
     dscale_batched(st, M, N, beta, C, ldc, sC, batch);
     return;
   }
-  // small tiles when the big-tile grid would not fill the GPU twice
-  const bool small = cdiv(M, 128) * cdiv(N, 128) * batch < 296;
+  // small tiles when the big-tile grid would not fill the GPU twice, or when big tiles would
+  // mostly compute padding (e.g. the 152 x 152 level blocks of the conversion)
+  const double pad_big = (double)round_up(M, 128) * round_up(N, 128), pad_small = (double)round_up(M, 64) * round_up(N, 64);
+  const bool small = cdiv(M, 128) * cdiv(N, 128) * batch < 296 || pad_big > 1.3 * pad_small;
   for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
     const int64_t nb = std::min<int64_t>(65535, batch - b0);
     GemmArgs p{M, N, K, alpha, beta, A + b0 * sA, lda, sA, B + b0 * sB, ldb, sB, C + b0 * sC, ldc, sC,
