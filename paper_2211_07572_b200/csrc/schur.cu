@@ -61,8 +61,8 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
   double* zb = sm;                       // forward: z      | backward: x buffer 0
   double* tb = sm + Wp * C;              // forward: t_top  | backward: x buffer 1
   double* stg = sm + 2 * Wp * C;         // STAGES slots of 16*Wp doubles
-  int* sperm = reinterpret_cast<int*>(stg + STAGES * 16 * Wp);
-  uint8_t* su13 = reinterpret_cast<uint8_t*>(sperm + 2 * Wp);  // n2 flags of the current strip
+  int* spermb = reinterpret_cast<int*>(stg + STAGES * 16 * Wp);  // [2][2 Wp] pivot orders (level l, l+1)
+  uint8_t* su13 = reinterpret_cast<uint8_t*>(spermb + 4 * Wp);  // n2 flags of the current strip
   __shared__ int s_task;
   __shared__ __align__(8) uint64_t full_bar[L::STAGES];
   __shared__ __align__(8) uint64_t empty_bar[L::STAGES];
@@ -212,21 +212,39 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     const int half = warp >> 3;            // 0: Ainv rows (y), 1: Fbot rows (z')
     const int fwm = (warp & 7) / L::FWN;   // m group
     const int fwn = (warp & 7) % L::FWN;   // n group
+    // pivot order of the first level now; each level prefetches the next one (cp.async)
+    for (int i = tid; i < 2 * Wp; i += THREADS) spermb[i] = permg[T.l0 * 2 * Wp + i];
+    int pcur = 0;
     for (int64_t l = T.l0; l < n2; l++) {
       const bool has_next = l + 1 < n2;
       const int cstar = (schur && has_next) ? (int)(l + 1 - T.q0) : -1;  // column injected
       const bool inj = cstar >= 0 && cstar < ncols;
       const double* fvec = inj ? fromY + (l + 1) * Wp : nullptr;
-      for (int i = tid; i < 2 * Wp; i += THREADS) sperm[i] = permg[l * 2 * Wp + i];
-      __syncthreads();
+      cp_async_wait<0>();
+      __syncthreads();  // sperm (this level) and z_l complete
+      const int* sperm = spermb + pcur * 2 * Wp;
+      if (has_next && tid < Wp / 2)  // 2 Wp int32 = Wp / 2 16-byte pieces
+        cp_async16(spermb + (pcur ^ 1) * 2 * Wp + 4 * tid, permg + (l + 1) * 2 * Wp + 4 * tid, true);
+      cp_async_commit();
+      pcur ^= 1;
       auto vval = [&](int src, int n) -> double {
         if (src < Wp) return zb[swz<C>(src, n)];
         if (!schur) return has_next ? rhs_val(l + 1, src - Wp, n) : 0.0;
         return (inj && n == cstar) ? fvec[src - Wp] : 0.0;
       };
-      for (int idx = tid; idx < Wp * C; idx += THREADS) {
-        const int r = idx / C, n = idx % C;
-        tb[swz<C>(r, n)] = vval(sperm[r], n);
+      // t_top = rows perm[0..Wp) of [z_l ; b_{l+1}]: one row per warp step, two columns per lane
+      for (int r = warp; r < Wp; r += THREADS / 32) {
+        const int src = sperm[r];
+        if (2 * lane < C) {
+          double2 v;
+          if (src < Wp) {
+            v = *reinterpret_cast<const double2*>(&zb[swz<C>(src, 2 * lane)]);
+          } else {
+            v.x = vval(src, 2 * lane);
+            v.y = vval(src, 2 * lane + 1);
+          }
+          *reinterpret_cast<double2*>(&tb[swz<C>(r, 2 * lane)]) = v;
+        }
       }
       double acc[MTMAX][L::FNT][2];
 #pragma unroll
@@ -384,7 +402,7 @@ template <int C>
 void launch_sweep(cudaStream_t st, const SchurArgs& a, int nslots) {
   using L = Lay<C>;
   const int Wp = a.Wp;
-  const size_t smem = (size_t)(2 * Wp * C + L::STAGES * 16 * Wp) * sizeof(double) + 2 * Wp * sizeof(int) + a.n2;
+  const size_t smem = (size_t)(2 * Wp * C + L::STAGES * 16 * Wp) * sizeof(double) + 4 * Wp * sizeof(int) + a.n2;
   const int mth = Wp / 8;
   const int mt = std::max((mth + L::FWM - 1) / L::FWM, (mth + L::BWM - 1) / L::BWM);
   auto go = [&](auto kern) {
