@@ -42,6 +42,15 @@ __device__ __forceinline__ void panel_cluster_barrier() {
   asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory");
 }
 
+// r[k] for a runtime k without local memory or branches (selects over the unrolled row)
+template <int N>
+__device__ __forceinline__ double pick(const double (&r)[N], int k) {
+  double x = 0.0;
+#pragma unroll
+  for (int c = 0; c < N; c++) x = c == k ? r[c] : x;
+  return x;
+}
+
 __device__ __forceinline__ void better(double& v, int& vi, double ov, int oi) {
   if (ov > v || (ov == v && oi < vi)) {
     v = ov;
@@ -73,6 +82,12 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
 #pragma unroll
   for (int c = 0; c < PNB; c++) r[c] = (own && c < nb) ? A[(j + c) * lda + j + i] : 0.0;
 
+#ifdef SLB_PANEL_PROF
+  long long P0 = clock64(), ph[5] = {0, 0, 0, 0, 0};
+#define PP(k_) { const long long q_ = clock64(); ph[k_] += q_ - P0; P0 = q_; }
+#else
+#define PP(k_)
+#endif
   for (int k = 0; k < nb; k++) {
     const int pb = k & 1;
     // (1) CTA argmax over rows i >= k (first max by row index); every warp reduces the
@@ -80,11 +95,7 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
     double v = -1.0;
     int vi = INT_MAX;
     if (own && i >= k) {
-      double x = 0.0;
-#pragma unroll
-      for (int c = 0; c < PNB; c++)
-        if (c == k) x = r[c];
-      v = fabs(x);
+      v = fabs(pick(r, k));
       vi = (int)i;
     }
 #pragma unroll
@@ -100,6 +111,7 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
     for (int o = NW / 2; o > 0; o >>= 1) better(v, vi, __shfl_xor_sync(0xffffffffu, v, o), __shfl_xor_sync(0xffffffffu, vi, o));
     v = __shfl_sync(0xffffffffu, v, 0);
     vi = __shfl_sync(0xffffffffu, vi, 0);
+    PP(0)
     // (2) publish the CTA candidate and row k
     if (tid == 0) {
       s_cv[pb] = v;
@@ -112,6 +124,7 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
 #pragma unroll
       for (int c = 0; c < PNB; c++) s_krow[pb][c] = r[c];
     panel_cluster_barrier<RELAXED>();
+    PP(1)
     // (3) every warp resolves the same pivot and copies both rows into its own slot
     double bv = -1.0;
     int bi = INT_MAX, bc = 0;
@@ -148,31 +161,34 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
     s_kloc[warp][lane] = *cluster.map_shared_rank(&s_krow[pb][lane], k / PTHREADS);
     if (tid == 0 && rank == 0) ipiv[j + k] = (int32_t)(j + bi);
     __syncwarp();
+    PP(2)
     const int p = bi;
+    const double* prow = s_prow[warp];
     if (p != k) {
-      if (own && i == k) {
+      const double* src_row = (own && i == k) ? prow : s_kloc[warp];
+      if (own && (i == k || i == p)) {
 #pragma unroll
-        for (int c = 0; c < PNB; c++) r[c] = s_prow[warp][c];
-      } else if (own && i == p) {
-#pragma unroll
-        for (int c = 0; c < PNB; c++) r[c] = s_kloc[warp][c];
+        for (int c = 0; c < PNB; c++) r[c] = src_row[c];
       }
     }
-    // (4) scale + rank-1 update of rows below k
+    // (4) scale + rank-1 update of rows below k, branch-free over the register row
     if (own && i > k) {
-      const double pv = s_prow[warp][k];
+      const double pv = prow[k];
       const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
-      double l = 0.0;
-#pragma unroll
-      for (int c = 0; c < PNB; c++)
-        if (c == k) l = r[c] * inv;
+      const double l = pick(r, k) * inv;
 #pragma unroll
       for (int c = 0; c < PNB; c++) {
-        if (c == k) r[c] = l;
-        else if (c > k) r[c] = fma(-l, s_prow[warp][c], r[c]);
+        const double nv = fma(-l, prow[c], r[c]);
+        r[c] = c > k ? nv : (c == k ? l : r[c]);
       }
     }
+    PP(3)
   }
+#ifdef SLB_PANEL_PROF
+  if (tid == 0 && (rank == 0 || rank == ncta - 1) && j == 0)
+    printf("PANEL rank %d m=%lld: argmax %lld publish+barrier %lld resolve %lld update %lld (cycles)\n", rank,
+           (long long)m, ph[0], ph[1], ph[2], ph[3]);
+#endif
   cluster.sync();
   if (own)
 #pragma unroll
