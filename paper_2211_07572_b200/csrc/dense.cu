@@ -129,8 +129,8 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
     double bv = -1.0;
     int bi = INT_MAX, bc = 0;
     if (lane < ncta) {
-      bv = *cluster.map_shared_rank(&s_cv[pb], lane);
-      bi = *cluster.map_shared_rank(&s_ci[pb], lane);
+      bv = dsmem_ld_f64(dsmem_map(&s_cv[pb], lane));
+      bi = dsmem_ld_s32(dsmem_map(&s_ci[pb], lane));
       bc = lane;
     }
 #pragma unroll
@@ -155,10 +155,11 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
         atomicMin(&status->singular_block, block_index);
       }
     }
-    const double* src = (bi == k) ? cluster.map_shared_rank(&s_krow[pb][0], k / PTHREADS)
-                                  : cluster.map_shared_rank(&s_crow[pb][0], bc);
-    s_prow[warp][lane] = src[lane];  // PNB == 32 == warp size
-    s_kloc[warp][lane] = *cluster.map_shared_rank(&s_krow[pb][lane], k / PTHREADS);
+    const uint32_t krow = dsmem_map(&s_krow[pb][lane], k / PTHREADS);  // PNB == 32 == warp size
+    const uint32_t prow_addr = (bi == k) ? krow : dsmem_map(&s_crow[pb][lane], bc);
+    const double pval = dsmem_ld_f64(prow_addr), kval = dsmem_ld_f64(krow);
+    s_prow[warp][lane] = pval;
+    s_kloc[warp][lane] = kval;
     if (tid == 0 && rank == 0) ipiv[j + k] = (int32_t)(j + bi);
     __syncwarp();
     PP(2)
