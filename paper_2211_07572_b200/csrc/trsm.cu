@@ -243,22 +243,30 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
   auto stage_rows = [&](const double* T, int r0, int buf) {  // rows r0..r0+16 of a row-major Wp x Wp
     const int h = min(m, r0 + RB) - r0;
     double* dst = sTb + buf * RB * KS;
-    for (int idx = tid; idx < h * m; idx += 256) {
-      const int rr = idx / m, c = idx % m;
-      cp_async8(dst + rr * KS + c, T + (int64_t)(r0 + rr) * m + c, true);
+    const int m2 = m / 2;  // Wp is a multiple of 8: rows are whole 16-byte pieces
+    for (int idx = tid; idx < h * m2; idx += 256) {
+      const int rr = idx / m2, c = 2 * (idx % m2);
+      cp_async16(dst + rr * KS + c, T + (int64_t)(r0 + rr) * m + c, true);
     }
   };
   // ---- R1 tile -> X (gathered through perm)
+#ifdef SLB_UPD_PROF
+  long long P0 = clock64(), ph[6] = {0, 0, 0, 0, 0, 0};
+#define UP(k_) { const long long q_ = clock64(); ph[k_] += q_ - P0; P0 = q_; }
+#else
+#define UP(k_)
+#endif
   stage_rows(LU11, 0, 0);
   cp_async_commit();
   const int ncol = min(TN, 2 * Wp - c0);
+  const int mt = warp >> 2, nt = warp & 3;
   for (int idx = tid; idx < m * TN; idx += 256) {
     const int n = idx / m, r = idx % m;
     X[sw32(r, n)] = n < ncol ? Rval(perm[r], c0 + n) : 0.0;
   }
   for (int idx = m * TN + tid; idx < nb * RB * TN; idx += 256) X[idx] = 0.0;
   diag_inverses<true, true>(LU11, Wp, m, nb, Dv, tid, 256);
-  const int mt = warp >> 2, nt = warp & 3;
+  UP(0)
   // ---- TRSM: X = L11^{-1} X (unit lower)
   for (int b = 0; b < nb; b++) {
     const int r0 = b * RB, r1 = min(m, r0 + RB), h = r1 - r0;
@@ -266,6 +274,7 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
+    UP(1)
     const double* Tb = sTb + (b & 1) * RB * KS;
     if (mt * 8 < h) {
       const int rloc = mt * 8 + g;
@@ -291,6 +300,7 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
     apply_diag_inverse(Dv + b * RB * RB, X, r0, r1, warp, g, t);
     __syncthreads();
   }
+  UP(2)
   // ---- U1213 tile out
   for (int idx = tid; idx < m * ncol; idx += 256) {
     const int n = idx / m, r = idx % m;
@@ -305,6 +315,7 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
+    UP(3)
     const double* Tb = sTb + (b & 1) * RB * KS;
     if (mt * 8 < h) {
       const int rloc = mt * 8 + g;
@@ -325,7 +336,13 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
       if (rok && col + 1 < 2 * Wp) svo[(int64_t)(col + 1) * Wp + row] = Rval(perm[Wp + row], col + 1) + a1 + b1;
     }
     __syncthreads();
+    UP(4)
   }
+#ifdef SLB_UPD_PROF
+  if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && (a.level % 1000) == 1)
+    printf("UPD l=%d: gather %lld trsm-wait %lld trsm-compute %lld gemm-wait %lld gemm-compute %lld (cycles)\n", a.level,
+           ph[0], ph[1], ph[2], ph[3], ph[4]);
+#endif
 }
 }  // namespace
 
