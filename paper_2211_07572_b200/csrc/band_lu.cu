@@ -464,7 +464,7 @@ void extract_levels(cudaStream_t st, CsrDev A, const StripDesc* strips, int nstr
                     int Wp, int64_t L0, int64_t nl, double* nx, int64_t sNX, DevStatus* status) {
   if (nl <= 0) return;
   extract_levels_kernel<<<dim3((unsigned)nl, (unsigned)nstrips), 128, 0, st>>>(A, strips, n2, Wp, L0,
-                                                                            nx, sNX, status);
+                                                                            nx, sNX, status); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -472,13 +472,13 @@ void extract_couplings(cudaStream_t st, CsrDev A, const StripDesc* strips, int n
                        int Wp, double* cpl, int64_t sCPL, int32_t* sym, DevStatus* status) {
   dim3 block(32, 8);
   dim3 grid((unsigned)cdiv(n2, 8), (unsigned)nstrips);
-  extract_couplings_kernel<<<grid, block, 0, st>>>(A, strips, n2, Wp, cpl, sCPL, sym, status);
+  extract_couplings_kernel<<<grid, block, 0, st>>>(A, strips, n2, Wp, cpl, sCPL, sym, status); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
 void init_sv(cudaStream_t st, int nstrips, int Wp, const double* nx0, int64_t sNX, double* sv,
              int64_t sSV) {
-  init_sv_kernel<<<nstrips, 256, 0, st>>>(Wp, nx0, sNX, sv, sSV);
+  init_sv_kernel<<<nstrips, 256, 0, st>>>(Wp, nx0, sNX, sv, sSV); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -491,7 +491,7 @@ void level_lu(cudaStream_t st, const LevelArgs& a) {
     SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  level_lu_kernel<<<a.nstrips, 512, smem, st>>>(a);
+  level_lu_kernel<<<a.nstrips, 512, smem, st>>>(a); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -504,13 +504,13 @@ void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t
   const int64_t w2 = (int64_t)Wp * Wp, sX = 3 * w2;
   double* X = work;
   double* Fb = work + nl * sX;
-  convert_init_kernel<<<dim3((unsigned)cdiv(3 * Wp * Wp, 256), (unsigned)nl), 256, 0, st>>>(Wp, slots, lvl, X, sX);
+  convert_init_kernel<<<dim3((unsigned)cdiv(3 * Wp * Wp, 256), (unsigned)nl), 256, 0, st>>>(Wp, slots, lvl, X, sX); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
   trsm_small_batched(st, true, Wp, slots, Wp, lvl, X, Wp, sX, Wp, nl);
   dgemm_batched(st, Wp, Wp, Wp, -1.0, slots + w2, Wp, lvl, X, Wp, sX, 0.0, Fb, Wp, w2, nl, true);
   trsm_small_batched(st, false, Wp, slots, Wp, lvl, X, Wp, sX, 3 * Wp, nl);
   convert_pack_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(4LL * Wp * Wp, 256), 64), (unsigned)nl), 256, 0, st>>>(
-      Wp, X, sX, Fb, w2, slots, lvl);
+      Wp, X, sX, Fb, w2, slots, lvl); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 

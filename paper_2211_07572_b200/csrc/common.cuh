@@ -5,6 +5,7 @@
 // written for that pipe: m8n8k4 fragments, cp.async staging, padded shared
 // tiles (row stride == 4 mod 16 doubles so a fragment load is 2 wavefronts).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -59,6 +60,10 @@ __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return cdiv(
 }  // namespace slb
 
 namespace slb {
+// Kernels launched by the engine (every launch site calls count_launch(); reported as
+// gpu_launches / solve_launches).
+extern std::atomic<long long> g_kernel_count;
+inline void count_launch() { g_kernel_count.fetch_add(1, std::memory_order_relaxed); }
 // ---- mbarrier + TMA bulk copy (cp.async.bulk) helpers ----------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));

@@ -234,6 +234,28 @@ __global__ void scatter_rows_kernel(double* A, int64_t lda, int64_t c0, int64_t 
     col[r] = t[r];
 }
 
+// The panel's interchanges ipiv[j, j+nb) applied, in order, to every column outside the panel
+// (LAPACK dlaswp on both sides at once): one thread per column, rows swapped in registers-free
+// place.  Applying them when the panel finishes is equivalent to the recursion's deferred laswp
+// calls (row interchanges commute with the updates of columns not yet touched).
+__global__ void panel_swaps_kernel(double* A, int64_t lda, int64_t n, int64_t j, int nb, const int32_t* ipiv) {
+  __shared__ int32_t sp[PNB];
+  if (threadIdx.x < nb) sp[threadIdx.x] = ipiv[j + threadIdx.x];
+  __syncthreads();
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= j) c += nb;  // skip the panel's own columns
+  if (c >= n) return;
+  double* col = A + c * lda;
+  for (int q = 0; q < nb; q++) {
+    const int64_t r = j + q, p = sp[q];
+    if (p != r) {
+      const double t = col[r];
+      col[r] = col[p];
+      col[p] = t;
+    }
+  }
+}
+
 __global__ void finite_kernel(const double* a, int64_t count, DevStatus* status) {
   bool bad = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
@@ -275,7 +297,7 @@ void panel(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t j, int nb
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, A, lda, n, j, nb, ipiv, status, block_index));
+  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, A, lda, n, j, nb, ipiv, status, block_index)); count_launch();
 }
 
 // Scratch for laswp (grown on demand, per device; stage two is stream ordered).
@@ -308,13 +330,13 @@ void laswp(cudaStream_t st, double* A, int64_t lda, int64_t c0, int64_t c1, cons
     SLB_CUDA_CHECK(cudaMalloc(&S.tmp, m * nc * sizeof(double)));
     S.tmp_n = m * nc;
   }
-  swap_perm_kernel<<<1, 1024, m * sizeof(int32_t), st>>>(ipiv, n, k1, k2, S.idx);
+  swap_perm_kernel<<<1, 1024, m * sizeof(int32_t), st>>>(ipiv, n, k1, k2, S.idx); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
   for (int64_t cb = 0; cb < nc; cb += 65535) {
     const int64_t ncb = std::min<int64_t>(65535, nc - cb);
     dim3 grid((unsigned)std::min<int64_t>(cdiv(m, 256), 16), (unsigned)ncb);
-    gather_rows_kernel<<<grid, 256, 0, st>>>(A, lda, c0 + cb, c0 + cb + ncb, k1, m, S.idx, S.tmp + cb * m);
-    scatter_rows_kernel<<<grid, 256, 0, st>>>(A, lda, c0 + cb, k1, m, S.tmp + cb * m);
+    gather_rows_kernel<<<grid, 256, 0, st>>>(A, lda, c0 + cb, c0 + cb + ncb, k1, m, S.idx, S.tmp + cb * m); count_launch();
+    scatter_rows_kernel<<<grid, 256, 0, st>>>(A, lda, c0 + cb, k1, m, S.tmp + cb * m); count_launch();
   }
   SLB_CUDA_CHECK(cudaGetLastError());
 }
@@ -349,17 +371,19 @@ void getrf_rec(cudaStream_t st, double* A, int64_t n, int64_t c0, int64_t c1, in
   const int64_t w = c1 - c0;
   if (w <= PNB) {
     panel(st, A, n, n, c0, (int)w, ipiv, status, block_index);
+    if (n - w > 0) {  // interchanges on every other column now, so the recursion needs no laswp
+      panel_swaps_kernel<<<(unsigned)cdiv(n - w, 128), 128, 0, st>>>(A, n, n, c0, (int)w, ipiv); count_launch();
+      SLB_CUDA_CHECK(cudaGetLastError());
+    }
     return;
   }
   int64_t h = round_up(w / 2, PNB);
   if (h >= w) h = w - PNB;
   getrf_rec(st, A, n, c0, c0 + h, ipiv, status, block_index);
-  laswp(st, A, n, c0 + h, c1, ipiv, c0, c0 + h, n);
   trsm(st, true, A + c0 * n + c0, n, h, A + (c0 + h) * n + c0, n, w - h);
   dgemm_batched(st, n - c0 - h, w - h, h, -1.0, A + c0 * n + c0 + h, n, 0, A + (c0 + h) * n + c0, n, 0, 1.0,
                 A + (c0 + h) * n + c0 + h, n, 0, 1);
   getrf_rec(st, A, n, c0 + h, c1, ipiv, status, block_index);
-  laswp(st, A, n, c0, c0 + h, ipiv, c0 + h, c1, n);
 }
 
 }  // namespace
@@ -377,13 +401,13 @@ void dgetrs(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const in
 }
 
 void dset_identity(cudaStream_t st, double* a, int64_t n) {
-  identity_kernel<<<(unsigned)std::min<int64_t>(cdiv(n * n, 256), 8192), 256, 0, st>>>(a, n);
+  identity_kernel<<<(unsigned)std::min<int64_t>(cdiv(n * n, 256), 8192), 256, 0, st>>>(a, n); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
 void check_finite(cudaStream_t st, const double* a, int64_t count, DevStatus* status) {
   if (count <= 0) return;
-  finite_kernel<<<(unsigned)std::min<int64_t>(cdiv(count, 256), 4096), 256, 0, st>>>(a, count, status);
+  finite_kernel<<<(unsigned)std::min<int64_t>(cdiv(count, 256), 4096), 256, 0, st>>>(a, count, status); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -463,9 +487,9 @@ void dgemv_batched_rhs(cudaStream_t st, int64_t m, int64_t n, int64_t nrhs, doub
     return;
   }
   dim3 grid((unsigned)cdiv(m, GV_ROWS), GV_SPLIT);
-  gemv_partial_kernel<<<grid, 256, 0, st>>>(m, n, nrhs, A, lda, x, ldx, part);
+  gemv_partial_kernel<<<grid, 256, 0, st>>>(m, n, nrhs, A, lda, x, ldx, part); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
-  gemv_reduce_kernel<<<(unsigned)cdiv(m * nrhs, 256), 256, 0, st>>>(m, nrhs, alpha, part, beta, y, ldy);
+  gemv_reduce_kernel<<<(unsigned)cdiv(m * nrhs, 256), 256, 0, st>>>(m, nrhs, alpha, part, beta, y, ldy); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 

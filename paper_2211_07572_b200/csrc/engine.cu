@@ -27,8 +27,9 @@
 #include "kernels.h"
 
 namespace slb {
+std::atomic<long long> g_kernel_count{0};
 
-std::atomic<int64_t> g_launches{0};
+
 
 namespace {
 
@@ -176,16 +177,14 @@ __global__ void copy2d_kernel(const double* src, int64_t lds, double* dst, int64
 
 void add2d(cudaStream_t st, const double* x, int64_t ldx, double* y, int64_t ldy, int64_t rows, int64_t cols) {
   if (rows <= 0 || cols <= 0) return;
-  add2d_kernel<<<(unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 8192), 256, 0, st>>>(x, ldx, y, ldy, rows, cols);
+  add2d_kernel<<<(unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 8192), 256, 0, st>>>(x, ldx, y, ldy, rows, cols); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
-  g_launches++;
 }
 
 void copy2d(cudaStream_t st, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols) {
   if (rows <= 0 || cols <= 0) return;
-  copy2d_kernel<<<(unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 8192), 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
+  copy2d_kernel<<<(unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 8192), 256, 0, st>>>(src, lds, dst, ldd, rows, cols); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
-  g_launches++;
 }
 
 int sm_count(int dev) {
@@ -283,7 +282,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   if (cfg) c = *cfg;
   if (c.compression == 2)
     throw HostError(SLABLU_ERR_UNSUPPORTED, "factorize: hbs compression is not implemented by the GPU engine");
-  const int64_t launches0 = g_launches.load();
+  const int64_t launches0 = slb::g_kernel_count.load();
   auto F = std::make_unique<slablu_gpu_fact>();
   F->device = c.device;
   SLB_CUDA_CHECK(cudaSetDevice(c.device));
@@ -382,7 +381,6 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     SLB_CUDA_CHECK(cudaMemcpyAsync(F->sym.p, ones.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   }
   extract_couplings(st, A, F->strips.p, S, n2, Wp, F->cpl.p, F->sCPL, F->sym.p, F->status.p);
-  g_launches++;
 
   const int64_t LCH = std::min<int64_t>(n2, 64);
   const int64_t sNX = LCH * 3 * Wp * Wp;
@@ -393,7 +391,6 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   double* svb[2] = {sv.p, sv.p + (size_t)S * sSV};
   extract_levels(st, A, F->strips.p, S, n2, Wp, 0, LCH, nx.p, sNX, F->status.p);
   init_sv(st, S, Wp, nx.p, sNX, svb[0], sSV);
-  g_launches += 2;
   // LU-form -> GEMM-form conversion runs behind the chain on a low-priority
   // stream, one chunk of CCH levels at a time (idle SMs during the chain).
   const int64_t CCH = std::min<int64_t>(n2, 256);
@@ -413,7 +410,6 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     SLB_CUDA_CHECK(cudaStreamWaitEvent(cst, chunk_ev, 0));
     for (int s = 0; s < S; s++) {
       convert_levels(cst, Wp, F->fac.p + s * F->sF + c0 * lvl, lvl, c1 - c0, cwork.p + (size_t)s * CCH * 4 * Wp * Wp);
-      g_launches += 5;
     }
   };
   int cur = 0;
@@ -423,7 +419,6 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     if (l > 0 && l % CCH == 0 && !defer_conv) convert_chunk(l - CCH, l);
     if (has_next && nxt % LCH == 0) {
       extract_levels(st, A, F->strips.p, S, n2, Wp, nxt, std::min(LCH, n2 - nxt), nx.p, sNX, F->status.p);
-      g_launches++;
     }
     LevelArgs la;
     la.Wp = Wp;
@@ -443,10 +438,8 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     la.status = F->status.p;
     la.level = (int32_t)l;
     level_lu(st, la);
-    g_launches++;
     if (has_next) {
       level_update(st, la);
-      g_launches++;
     }
     cur = 1 - cur;
   }
@@ -549,7 +542,6 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     sa.tasks = dtasks.p;
     sa.mode = SWEEP_SCHUR;
     sweep(st, sa, nslots);
-    g_launches++;
     SLB_CUDA_CHECK(cudaEventRecord(es, st));
     ybuf.release();
     // ---- T assembly --------------------------------------------------------------------
@@ -565,9 +557,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     tr.uhi = std::min(K - 1, F->s1 - 1);
     assemble_T(st, n2, K, S, F->strips.p, F->sym.p, gbuf.p, sG, F->Tdiag(), F->Tsup(), F->Tsub(), A,
                F->ifc_off.p, F->status.p, tr);
-    g_launches += 2;
     check_finite(st, F->T.p, (int64_t)(3 * K - 2) * n2 * n2, F->status.p);
-    g_launches++;
     if (c.keep_T) {
       F->Tkeep.alloc(dev, F->T.n);
       SLB_CUDA_CHECK(cudaMemcpyAsync(F->Tkeep.p, F->T.p, F->T.bytes(), cudaMemcpyDeviceToDevice, st));
@@ -588,13 +578,11 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
         dgemm_batched(st, n2, n2, n2, 1.0, F->Tdiag() + (j - 1) * bs, n2, 0, F->Tsup() + (j - 1) * bs, n2, 0, 0.0,
                       X.p, n2, 0, 1);
         dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X.p, n2, 0, 1.0, Sj, n2, 0, 1);
-        g_launches += 2;
       }
       dgetrf(st, n2, Sj, ipiv.p, nullptr, F->status.p, j);
       dset_identity(st, I.p, n2);
       dgetrs(st, n2, n2, Sj, ipiv.p, I.p, n2, nullptr);
       SLB_CUDA_CHECK(cudaMemcpyAsync(Sj, I.p, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      g_launches += 4;
     }
   } else {
     SLB_CUDA_CHECK(cudaEventRecord(es, st));
@@ -632,12 +620,12 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     }
   }
   if (!F->single) F->storage2 = (int64_t)(K + 2 * (K - 1)) * n2 * n2;
-  F->launches_factor = g_launches.load() - launches0;
+  F->launches_factor = slb::g_kernel_count.load() - launches0;
   return F.release();
 }
 
 void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu) {
-  const int64_t launches0 = g_launches.load();
+  const int64_t launches0 = slb::g_kernel_count.load();
   SLB_CUDA_CHECK(cudaSetDevice(F->device));
   cudaStream_t st = F->stream;
   const int dev = F->device;
@@ -685,7 +673,6 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   auto run_sweep = [&](const SchurArgs& args) {
     if (clustered) {
       strip_solve(st, args, ntasks);  // rhs pack + cluster sweep
-      g_launches++;
     } else {
       sweep(st, args, nslots);
     }
@@ -720,7 +707,6 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     sa.u_ifc = nullptr;
     sa.out = up;
     run_sweep(sa);
-    g_launches++;
   } else {
     DBuf<double> red, uifc, contrib, tmp, part;
     red.alloc(dev, (size_t)K * nrhs);
@@ -730,14 +716,13 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     part.alloc(dev, (size_t)8 * n2 * nrhs);
     const unsigned gb = (unsigned)cdiv(K * nrhs, 256);
     // reduce_rhs (stage_one.hpp:415-433)
-    gather_ifc_kernel<<<gb, 256, 0, st>>>(fp, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K, 0, F->K);
+    gather_ifc_kernel<<<gb, 256, 0, st>>>(fp, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K, 0, F->K); count_launch();
     SLB_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
     sa.mode = SWEEP_REDUCE;
     sa.out = contrib.p;
     run_sweep(sa);
     SLB_CUDA_CHECK(cudaEventRecord(s1, st));
-    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, S, F->strips.p, contrib.p, 0);
-    g_launches += 3;
+    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, S, F->strips.p, contrib.p, 0); count_launch();
     // sweep solve (stage_two.hpp:170-188) with S_j^{-1}
     const int64_t bs = n2 * n2;
     for (int j = 0; j < F->K; j++) {
@@ -745,13 +730,11 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
       if (j > 0) dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j - 1) * bs, n2, uifc.p + (j - 1) * n2, K,
                                    1.0, rj, K, part.p);
       dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tdiag() + j * bs, n2, rj, K, 0.0, uifc.p + j * n2, K, part.p);
-      g_launches += j > 0 ? 4 : 2;
     }
     for (int j = F->K - 2; j >= 0; j--) {
       dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tsup() + j * bs, n2, uifc.p + (j + 1) * n2, K, 0.0, tmp.p, n2,
                         part.p);
       dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tdiag() + j * bs, n2, tmp.p, n2, 1.0, uifc.p + j * n2, K, part.p);
-      g_launches += 4;
     }
     // recover_interiors (stage_one.hpp:438-462)
     SLB_CUDA_CHECK(cudaEventRecord(s2, st));
@@ -761,8 +744,7 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     sa.out = up;
     run_sweep(sa);
     SLB_CUDA_CHECK(cudaEventRecord(s3, st));
-    scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc.p, K, nrhs, F->ifc_off.p, n2, up, N, 0, F->K);
-    g_launches += 2;
+    scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc.p, K, nrhs, F->ifc_off.p, n2, up, N, 0, F->K); count_launch();
     SLB_CUDA_CHECK(cudaGetLastError());
     SLB_CUDA_CHECK(cudaStreamSynchronize(st));
   }
@@ -776,7 +758,7 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   F->t_solve = a * 1e-3;
   F->t_solve_strips = F->single ? a * 1e-3 : (b + c) * 1e-3;
   for (cudaEvent_t ev : {s0, s1, s2, s3, s4}) cudaEventDestroy(ev);
-  F->launches_solve = g_launches.load() - launches0;
+  F->launches_solve = slb::g_kernel_count.load() - launches0;
 }
 
 // solve with F->refine steps of iterative refinement against the original
@@ -842,10 +824,8 @@ struct StripSweeper {
     sa.out = out;
     if (clustered) {
       strip_solve(st, sa, ntasks);  // rhs pack + cluster sweep
-      g_launches += 2;
     } else {
       sweep(st, sa, nslots);
-      g_launches++;
     }
   }
 };
@@ -867,7 +847,7 @@ void shard_sweep_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
   const int dev = F->device;
   const int64_t n2 = F->n2, bs = n2 * n2;
   const int j0 = F->j0, j1 = F->j1;
-  const int64_t l0 = g_launches.load();
+  const int64_t l0 = slb::g_kernel_count.load();
   cudaEvent_t e0, e1;
   SLB_CUDA_CHECK(cudaEventCreate(&e0));
   SLB_CUDA_CHECK(cudaEventCreate(&e1));
@@ -884,13 +864,11 @@ void shard_sweep_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
       dgemm_batched(st, n2, n2, n2, 1.0, F->Tdiag() + (j - 1) * bs, n2, 0, F->Tsup() + (j - 1) * bs, n2, 0, 0.0, X.p,
                     n2, 0, 1);
       dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X.p, n2, 0, 1.0, Sj, n2, 0, 1);
-      g_launches += 2;
     }
     dgetrf(st, n2, Sj, ipiv.p, nullptr, F->status.p, j);
     dset_identity(st, I.p, n2);
     dgetrs(st, n2, n2, Sj, ipiv.p, I.p, n2, nullptr);
     SLB_CUDA_CHECK(cudaMemcpyAsync(Sj, I.p, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    g_launches += 4;
   }
   if (F->rank < F->nranks - 1) {
     SLB_CUDA_CHECK(cudaMemcpyAsync(d_out, F->Tdiag() + j1 * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -898,7 +876,6 @@ void shard_sweep_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
       dgemm_batched(st, n2, n2, n2, 1.0, F->Tdiag() + (j1 - 1) * bs, n2, 0, F->Tsup() + (j1 - 1) * bs, n2, 0, 0.0,
                     X.p, n2, 0, 1);
       dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j1 - 1) * bs, n2, 0, X.p, n2, 0, 1.0, d_out, n2, 0, 1);
-      g_launches += 2;
     }
   }
   SLB_CUDA_CHECK(cudaEventRecord(e1, st));
@@ -914,7 +891,7 @@ void shard_sweep_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   F->t2 = ms * 1e-3;
-  F->launches_factor += g_launches.load() - l0;
+  F->launches_factor += slb::g_kernel_count.load() - l0;
   F->swept = true;
 }
 
@@ -943,11 +920,10 @@ void shard_solve_fwd_impl(slablu_gpu_fact* F, const double* d_f, int64_t ldf, in
   contrib.alloc(dev, (size_t)F->S * 2 * nrhs * n2);
   part.alloc(dev, (size_t)8 * n2 * nrhs);
   const unsigned gb = (unsigned)cdiv(Kn * nrhs, 256);
-  gather_ifc_kernel<<<gb, 256, 0, st>>>(F->sh_f.p, N, nrhs, F->K, F->ifc_off.p, n2, F->sh_red.p, Kn, j0, j1);
+  gather_ifc_kernel<<<gb, 256, 0, st>>>(F->sh_f.p, N, nrhs, F->K, F->ifc_off.p, n2, F->sh_red.p, Kn, j0, j1); count_launch();
   StripSweeper sw(F, F->sh_f.p, nrhs);
   sw.run(SWEEP_REDUCE, nullptr, contrib.p);
-  combine_reduce_kernel<<<gb, 256, 0, st>>>(F->sh_red.p, Kn, nrhs, n2, F->S, F->strips.p, contrib.p, F->s0);
-  g_launches += 2;
+  combine_reduce_kernel<<<gb, 256, 0, st>>>(F->sh_red.p, Kn, nrhs, n2, F->S, F->strips.p, contrib.p, F->s0); count_launch();
   double* red = F->sh_red.p;
   double* uifc = F->sh_uifc.p;
   if (F->rank > 0) add2d(st, d_in, n2, red + j0 * n2, Kn, n2, nrhs);
@@ -956,17 +932,14 @@ void shard_solve_fwd_impl(slablu_gpu_fact* F, const double* d_f, int64_t ldf, in
     if (j > j0) {
       dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j - 1) * bs, n2, uifc + (j - 1) * n2, Kn, 1.0, rj, Kn,
                         part.p);
-      g_launches += 2;
     }
     dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tdiag() + j * bs, n2, rj, Kn, 0.0, uifc + j * n2, Kn, part.p);
-    g_launches += 2;
   }
   if (F->rank < F->nranks - 1) {
     copy2d(st, red + j1 * n2, Kn, d_out, n2, n2, nrhs);
     if (j1 > j0) {
       dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j1 - 1) * bs, n2, uifc + (j1 - 1) * n2, Kn, 1.0, d_out,
                         n2, part.p);
-      g_launches += 2;
     }
   }
   SLB_CUDA_CHECK(cudaGetLastError());
@@ -998,15 +971,13 @@ void shard_solve_bwd_impl(slablu_gpu_fact* F, const double* d_in, double* d_out,
     if (j + 1 >= F->K) continue;
     dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tsup() + j * bs, n2, uifc + (j + 1) * n2, Kn, 0.0, tmp.p, n2, part.p);
     dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tdiag() + j * bs, n2, tmp.p, n2, 1.0, uifc + j * n2, Kn, part.p);
-    g_launches += 4;
   }
   if (F->rank > 0) copy2d(st, uifc + j0 * n2, Kn, d_out, n2, n2, nrhs);
   StripSweeper sw(F, F->sh_f.p, nrhs);
   sw.run(SWEEP_RECOVER, uifc, d_u);
   const unsigned gb = (unsigned)cdiv(Kn * nrhs, 256);
   if (Kn > 0) {
-    scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc, Kn, nrhs, F->ifc_off.p, n2, d_u, N, j0, j1);
-    g_launches++;
+    scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc, Kn, nrhs, F->ifc_off.p, n2, d_u, N, j0, j1); count_launch();
   }
   SLB_CUDA_CHECK(cudaGetLastError());
   SLB_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -1027,7 +998,7 @@ void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   SLB_CUDA_CHECK(cudaEventCreate(&e0));
   SLB_CUDA_CHECK(cudaEventCreate(&e1));
   SLB_CUDA_CHECK(cudaEventRecord(e0, st));
-  const int64_t l0 = g_launches.load();
+  const int64_t l0 = slb::g_kernel_count.load();
   if (F->refine == 0 || !F->a_rp.p) {
     solve_once(F, d_f, ldf, nrhs, d_u, ldu);
   } else {
@@ -1041,13 +1012,12 @@ void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     double t_strips = F->t_solve_strips;
     const unsigned gb = (unsigned)cdiv(N * nrhs, 256);
     for (int it = 0; it < F->refine; it++) {
-      residual_kernel<<<gb, 256, 0, st>>>(F->a_rp.p, F->a_ci.p, F->a_v.p, N, nrhs, f.p, u.p, r.p);
+      residual_kernel<<<gb, 256, 0, st>>>(F->a_rp.p, F->a_ci.p, F->a_v.p, N, nrhs, f.p, u.p, r.p); count_launch();
       SLB_CUDA_CHECK(cudaGetLastError());
       solve_once(F, r.p, N, nrhs, du.p, N);
       t_strips += F->t_solve_strips;
-      axpy_kernel<<<gb, 256, 0, st>>>(N * nrhs, du.p, u.p);
+      axpy_kernel<<<gb, 256, 0, st>>>(N * nrhs, du.p, u.p); count_launch();
       SLB_CUDA_CHECK(cudaGetLastError());
-      g_launches += 2;
     }
     copy2d(st, u.p, N, d_u, ldu, N, nrhs);
     F->t_solve_strips = t_strips;
@@ -1057,7 +1027,7 @@ void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   float ms = 0;
   SLB_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
   F->t_solve = ms * 1e-3;
-  F->launches_solve = g_launches.load() - l0;
+  F->launches_solve = slb::g_kernel_count.load() - l0;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
 }
@@ -1173,10 +1143,9 @@ slablu_gpu_status slablu_gpu_residual(const slablu_gpu_fact* fact, const double*
     SLB_CUDA_CHECK(cudaSetDevice(fact->device));
     const int64_t N = fact->N;
     residual_kernel<<<(unsigned)cdiv(N * nrhs, 256), 256, 0, fact->stream>>>(fact->a_rp.p, fact->a_ci.p, fact->a_v.p, N,
-                                                                         nrhs, d_f, d_u, d_r);
+                                                                         nrhs, d_f, d_u, d_r); count_launch();
     SLB_CUDA_CHECK(cudaGetLastError());
     SLB_CUDA_CHECK(cudaStreamSynchronize(fact->stream));
-    g_launches++;
   })
 }
 
@@ -1311,9 +1280,9 @@ slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* F, const double* 
     sa.ybuf = ybuf.p; sa.sY = sY; sa.task_counter = counter.p; sa.ntasks = ntasks; sa.tasks = dtasks.p;
     sa.N = N; sa.K = K; sa.nrhs = nrhs; sa.f = df.p; sa.mode = SWEEP_REDUCE; sa.out = contrib.p;
     const unsigned gb = (unsigned)cdiv(K * nrhs, 256);
-    gather_ifc_kernel<<<gb, 256, 0, st>>>(df.p, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K, 0, F->K);
+    gather_ifc_kernel<<<gb, 256, 0, st>>>(df.p, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K, 0, F->K); count_launch();
     sweep(st, sa, nslots);
-    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, F->S, F->strips.p, contrib.p, 0);
+    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, F->S, F->strips.p, contrib.p, 0); count_launch();
     SLB_CUDA_CHECK(cudaGetLastError());
     SLB_CUDA_CHECK(cudaStreamSynchronize(st));
     SLB_CUDA_CHECK(cudaMemcpy(out, red.p, K * nrhs * sizeof(double), cudaMemcpyDeviceToHost));

@@ -158,10 +158,10 @@ void dgemm_batched(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alph
                transA ? 1 : 0};
     if (small) {
       dim3 grid((unsigned)cdiv(M, 64), (unsigned)cdiv(N, 64), (unsigned)nb);
-      dgemm_kernel<64, 64, 2, 2><<<grid, 128, smem_small, st>>>(p);
+      dgemm_kernel<64, 64, 2, 2><<<grid, 128, smem_small, st>>>(p); count_launch();
     } else {
       dim3 grid((unsigned)cdiv(M, 128), (unsigned)cdiv(N, 128), (unsigned)nb);
-      dgemm_kernel<128, 128, 2, 4><<<grid, 256, smem_big, st>>>(p);
+      dgemm_kernel<128, 128, 2, 4><<<grid, 256, smem_big, st>>>(p); count_launch();
     }
     SLB_CUDA_CHECK(cudaGetLastError());
   }
@@ -182,7 +182,7 @@ void dscale_batched(cudaStream_t st, int64_t M, int64_t N, double beta, double* 
                     int64_t sC, int64_t batch) {
   if (M <= 0 || N <= 0 || batch <= 0 || beta == 1.0) return;
   const int64_t blocks = std::min<int64_t>(cdiv(M * N, 256), 4096);
-  dscale_kernel<<<dim3((unsigned)blocks, 1, (unsigned)batch), 256, 0, st>>>(M, N, beta, C, ldc, sC);
+  dscale_kernel<<<dim3((unsigned)blocks, 1, (unsigned)batch), 256, 0, st>>>(M, N, beta, C, ldc, sC); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 

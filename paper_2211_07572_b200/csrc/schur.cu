@@ -407,7 +407,7 @@ void launch_sweep(cudaStream_t st, const SchurArgs& a, int nslots) {
   const int mt = std::max((mth + L::FWM - 1) / L::FWM, (mth + L::BWM - 1) / L::BWM);
   auto go = [&](auto kern) {
     SLB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<nslots, THREADS, smem, st>>>(a);
+    kern<<<nslots, THREADS, smem, st>>>(a); count_launch();
   };
   if (mt <= 1) go(sweep_kernel<C, 1>);
   else if (mt <= 2) go(sweep_kernel<C, 2>);
@@ -554,12 +554,12 @@ void assemble_T(cudaStream_t st, int64_t n2, int nifc, int nstrips, const StripD
   }
   if (tr.ohi > tr.olo) {
     direct_T_kernel<<<tr.ohi - tr.olo, 256, 0, st>>>(A, n2, nifc, ifc_off, strips, nstrips, Tdiag, Tsup, Tsub,
-                                                     status, tr);
+                                                     status, tr); count_launch();
     SLB_CUDA_CHECK(cudaGetLastError());
   }
   const int nblocks = 3 * nifc - 2;
   dim3 grid((unsigned)cdiv(n2, 32), (unsigned)cdiv(n2, 32), (unsigned)nblocks);
-  assemble_T_kernel<<<grid, dim3(32, 8), 0, st>>>(n2, nifc, nstrips, sym, gbuf, sG, Tdiag, Tsup, Tsub, tr);
+  assemble_T_kernel<<<grid, dim3(32, 8), 0, st>>>(n2, nifc, nstrips, sym, gbuf, sG, Tdiag, Tsup, Tsub, tr); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -499,7 +499,7 @@ void strip_solve(cudaStream_t st, const SchurArgs& a, int ntasks) {
   const int Wp = a.Wp;
   if (!strip_solve_fits(Wp, a.n2))
     throw CudaFailure(cudaErrorInvalidValue, "strip_solve: slab too wide for the cluster split", __FILE__, __LINE__);
-  rhs_pack_kernel<<<dim3((unsigned)ntasks, (unsigned)cdiv(a.n2, 32)), 256, 0, st>>>(a);
+  rhs_pack_kernel<<<dim3((unsigned)ntasks, (unsigned)cdiv(a.n2, 32)), 256, 0, st>>>(a); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
   const size_t smem = (size_t)solve_lay(Wp, a.n2).bytes;
   static const bool relaxed = [] {
@@ -524,7 +524,7 @@ void strip_solve(cudaStream_t st, const SchurArgs& a, int ntasks) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
+  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a)); count_launch();
 }
 
 }  // namespace slb

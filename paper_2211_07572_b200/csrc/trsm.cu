@@ -202,6 +202,7 @@ void trsm_small_batched(cudaStream_t st, bool lower, int m, const double* T, int
     else if (lower) trsm_small_kernel<true, false><<<grid, 256, smem, st>>>(m, Tb, ldt, sT, Bb, ldb, sB, ncols);
     else if (rowmajor) trsm_small_kernel<false, true><<<grid, 256, smem, st>>>(m, Tb, ldt, sT, Bb, ldb, sB, ncols);
     else trsm_small_kernel<false, false><<<grid, 256, smem, st>>>(m, Tb, ldt, sT, Bb, ldb, sB, ncols);
+    count_launch();
     SLB_CUDA_CHECK(cudaGetLastError());
   }
 }
@@ -354,7 +355,7 @@ void level_update(cudaStream_t st, const LevelArgs& a) {
     attr = true;
   }
   dim3 grid((unsigned)cdiv(2 * a.Wp, TN), (unsigned)a.nstrips);
-  level_update_kernel<<<grid, 256, smem, st>>>(a);
+  level_update_kernel<<<grid, 256, smem, st>>>(a); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 }  // namespace slb
