@@ -474,6 +474,18 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
       if (F->single) throw HostError(SLABLU_ERR_SINGULAR, "BandedLU: exactly singular pivot", hs.singular_strip);
       throw HostError(SLABLU_ERR_SINGULAR, "factor_one_interior: singular slab interior", hs.singular_strip);
     }
+    if (getenv("SLB_U13_STATS")) {
+      std::vector<uint8_t> h((size_t)S * n2);
+      SLB_CUDA_CHECK(cudaMemcpy(h.data(), F->u13.p, h.size(), cudaMemcpyDeviceToHost));
+      int64_t ones = 0, pairs = 0;
+      for (int s = 0; s < S; s++)
+        for (int64_t l = 0; l < n2; l++) {
+          ones += h[s * n2 + l];
+          pairs += (h[s * n2 + l] || (l > 0 && h[s * n2 + l - 1])) ? 1 : 0;
+        }
+      fprintf(stderr, "[slablu] U13 != 0 on %lld of %lld levels; level or its predecessor: %lld\n", (long long)ones,
+              (long long)(S * n2), (long long)pairs);
+    }
     F->sym_h.resize(S);
     SLB_CUDA_CHECK(cudaMemcpy(F->sym_h.data(), F->sym.p, S * sizeof(int32_t), cudaMemcpyDeviceToHost));
   }
