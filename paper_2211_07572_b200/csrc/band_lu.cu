@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   __syncthreads();
 
   double* ent = win + NW * RS + 32;  // 8 x Wp staging for the entering rows
+#ifdef SLB_PANEL8_PROF
+  long long pq[5] = {0, 0, 0, 0, 0};
+#endif
   for (int kb = 0; kb < Wp; kb += 8) {
     const int kend = kb + 8;
     // prefetch the 8 bottom rows entering after this block (overlaps (a)-(d))
@@ -224,29 +227,43 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
         }
       }
       double* pcand = win + NW * RS;  // scratch: [2][4] (value) + [2][4] (pos as double) + [2][8] (pivot row)
+#ifdef SLB_PANEL8_PROF
+      long long Q0 = clock64();
+#define QP(k_) { const long long q_ = clock64(); pq[k_] += q_ - Q0; Q0 = q_; }
+#else
+#define QP(k_)
+#endif
 #pragma unroll
       for (int q = 0; q < 8; q++) {
         const int c = kb + q, par = q & 1;
         const int hi = min(c + Wp, rows_total - 1);
-        double best = -1.0;
+        double best = 0.0;
         int bpos = 0x7fffffff;
 #pragma unroll
         for (int i = 0; i < RPL; i++) {
           const double av = fabs(v[i][q]);
-          if (pos[i] >= c && pos[i] <= hi && av > best) {
+          if (pos[i] >= c && pos[i] <= hi && (av > best || (av == best && pos[i] < bpos))) {
             best = av;
             bpos = pos[i];
           }
         }
-        double mx = best;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        const int rw = (int)__reduce_min_sync(0xffffffffu, (unsigned)(best == mx ? bpos : 0x7fffffff));
+        // warp arg-max with hardware reductions: non-negative doubles order like their bit
+        // patterns, so max(hi word), then max(lo word) among those lanes, then the smallest
+        // position among exact maxima (dgbtrf's first-max rule)
+        const unsigned long long key = (unsigned long long)__double_as_longlong(best);
+        const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, khi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
+        const bool ismax = khi == mhi && klo == mlo;
+        const int rw = (int)__reduce_min_sync(0xffffffffu, ismax ? (unsigned)bpos : 0x7fffffffu);
+        const double mx = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+        QP(0)
         if (lane == 0) {
           pcand[par * 4 + warp] = mx;
           pcand[8 + par * 4 + warp] = (double)rw;
         }
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        QP(1)
         double gm = pcand[par * 4];
         int r = (int)pcand[8 + par * 4];
 #pragma unroll
@@ -273,15 +290,10 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
           if (pos[i] == r) pos[i] = c;
           else if (pos[i] == c) pos[i] = r;
         }
-        if (pt == 0) {
-          if (r != c) {
-            const int tp = perm[c];
-            perm[c] = perm[r];
-            perm[r] = tp;
-          }
-          s_piv[q] = r;
-        }
+        if (pt == 0) s_piv[q] = r;  // perm is updated after the panel (off the critical path)
+        QP(2)
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        QP(3)
         double pr[8];
 #pragma unroll
         for (int qq = 0; qq < 8; qq++) pr[qq] = pcand[16 + par * 8 + qq];
@@ -295,6 +307,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
             for (int qq = q + 1; qq < 8; qq++) v[i][qq] = fma(-m, pr[qq], v[i][qq]);
           }
         }
+        QP(4)
       }
 #pragma unroll
       for (int i = 0; i < RPL; i++) {
@@ -304,6 +317,15 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
           for (int q = 0; q < 8; q++) row[kb + q] = v[i][q];
         }
       }
+      if (pt == 0)
+        for (int q = 0; q < 8; q++) {
+          const int c = kb + q, r = s_piv[q];
+          if (r != c) {
+            const int tp = perm[c];
+            perm[c] = perm[r];
+            perm[r] = tp;
+          }
+        }
     }
     __syncthreads();
     // (b) the panel's row swaps on all other columns, in pivot order
@@ -378,6 +400,11 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
     __syncthreads();
   }
 
+#ifdef SLB_PANEL8_PROF
+  if (tid == 0 && s == 0 && (a.level % 1000) == 1)
+    printf("PANEL8 l=%d: argmax %lld bar1 %lld resolve %lld bar2 %lld update %lld (cycles, %d columns)\n", a.level,
+           pq[0], pq[1], pq[2], pq[3], pq[4], Wp);
+#endif
   int32_t* perm_out = a.perm + s * a.sP;
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm_out[p] = perm[p];
   {
