@@ -156,6 +156,7 @@ __global__ void init_sv_kernel(int Wp, const double* nx0, int64_t sNX, double* s
 // and sv_out <- R2 = bottom rows.  The chain then forms
 //   U1213 = L11^{-1} R1 (trsm_small_batched) and [S|V]_{l+1} = R2 - L21 U1213 (GEMM).
 // grid = nstrips, block = 512.
+template <int PW>  // warps factoring the 8-column panel (1 or 4; 4 is used)
 __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   extern __shared__ double smem[];
   const int Wp = a.Wp, NW = Wp + 8;
@@ -207,15 +208,16 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
     //     kb + p + 128 i (i < 2), 8 panel columns each.  Interchanges only
     //     update each row's position register (pos); the data move happens
     //     once, when the panel is written back.  Two named barriers per column.
-    if (warp < 4) {
-      constexpr int RPL = 2;
-      const int pt = tid;  // 0..127
+    if (warp < PW) {
+      constexpr int NT = PW * 32;                  // panel threads
+      constexpr int RPL = PW == 1 ? 5 : 2;         // rows per thread (Wp + 8 <= NT * RPL)
+      const int pt = tid;
       const int rlast = min(kb + 7 + Wp, rows_total - 1);
       double v[RPL][8];
       int pos[RPL];
 #pragma unroll
       for (int i = 0; i < RPL; i++) {
-        pos[i] = kb + pt + 128 * i;
+        pos[i] = kb + pt + NT * i;
         if (pos[i] <= rlast) {
           const double* row = rowp(pos[i]);
 #pragma unroll
@@ -233,6 +235,10 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
 #else
 #define QP(k_)
 #endif
+      auto panel_sync = [&]() {
+        if (PW == 1) __syncwarp();
+        else asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
+      };
 #pragma unroll
       for (int q = 0; q < 8; q++) {
         const int c = kb + q, par = q & 1;
@@ -258,23 +264,27 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
         const int rw = (int)__reduce_min_sync(0xffffffffu, ismax ? (unsigned)bpos : 0x7fffffffu);
         const double mx = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
         QP(0)
-        if (lane == 0) {
-          pcand[par * 4 + warp] = mx;
-          pcand[8 + par * 4 + warp] = (double)rw;
-        }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
-        QP(1)
-        double gm = pcand[par * 4];
-        int r = (int)pcand[8 + par * 4];
+        double gm = mx;
+        int r = rw;
+        if (PW > 1) {  // combine the warps' candidates through shared memory
+          if (lane == 0) {
+            pcand[par * 4 + warp] = mx;
+            pcand[8 + par * 4 + warp] = (double)rw;
+          }
+          panel_sync();
+          gm = pcand[par * 4];
+          r = (int)pcand[8 + par * 4];
 #pragma unroll
-        for (int w2 = 1; w2 < 4; w2++) {
-          const double cv = pcand[par * 4 + w2];
-          const int cr = (int)pcand[8 + par * 4 + w2];
-          if (cv > gm || (cv == gm && cr < r)) {
-            gm = cv;
-            r = cr;
+          for (int w2 = 1; w2 < PW; w2++) {
+            const double cv = pcand[par * 4 + w2];
+            const int cr = (int)pcand[8 + par * 4 + w2];
+            if (cv > gm || (cv == gm && cr < r)) {
+              gm = cv;
+              r = cr;
+            }
           }
         }
+        QP(1)
         if (!(gm > 0.0)) {
           r = c;
           if (pt == 0) s_sing = 1;
@@ -292,7 +302,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
         }
         if (pt == 0) s_piv[q] = r;  // perm is updated after the panel (off the critical path)
         QP(2)
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        panel_sync();
         QP(3)
         double pr[8];
 #pragma unroll
@@ -515,10 +525,11 @@ void level_lu(cudaStream_t st, const LevelArgs& a) {
   const size_t smem = (size_t)((Wp + 8) * RS + 32 + 8 * Wp) * sizeof(double) + 2 * Wp * sizeof(int);
   static size_t attr = 0;
   if (smem > attr) {
-    SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  level_lu_kernel<<<a.nstrips, 512, smem, st>>>(a); count_launch();
+  // 4 panel warps: measured faster than one warp with 5 rows per lane (register pressure)
+  level_lu_kernel<4><<<a.nstrips, 512, smem, st>>>(a); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
