@@ -384,7 +384,33 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
         const bool ok = p <= rlast;
         double* row = rowp(ok ? p : kend);
         const double a0 = ok ? -row[kb + t] : 0.0, a1 = ok ? -row[kb + 4 + t] : 0.0;
-        for (int ni = 0; ni < nt_n; ni++) {
+        // four n tiles per step: their loads issue together, the DMMA chains interleave
+        int ni = 0;
+        for (; ni + 4 <= nt_n; ni += 4) {
+          double b0[4], b1[4], d0[4], d1[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int c0 = kend + (ni + u) * 8;
+            b0[u] = u0[c0 + g];
+            b1[u] = u1[c0 + g];
+            d0[u] = row[c0 + 2 * t];
+            d1[u] = row[c0 + 2 * t + 1];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            dmma884(d0[u], d1[u], a0, b0[u]);
+            dmma884(d0[u], d1[u], a1, b1[u]);
+          }
+          if (ok) {
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              const int c0 = kend + (ni + u) * 8;
+              row[c0 + 2 * t] = d0[u];
+              row[c0 + 2 * t + 1] = d1[u];
+            }
+          }
+        }
+        for (; ni < nt_n; ni++) {
           const int c0 = kend + ni * 8;
           const double b0 = u0[c0 + g], b1 = u1[c0 + g];
           double d0 = row[c0 + 2 * t], d1 = row[c0 + 2 * t + 1];
