@@ -286,7 +286,13 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   auto F = std::make_unique<slablu_gpu_fact>();
   F->device = c.device;
   SLB_CUDA_CHECK(cudaSetDevice(c.device));
-  SLB_CUDA_CHECK(cudaStreamCreateWithFlags(&F->stream, cudaStreamNonBlocking));
+  {
+    // the level chain is latency-bound: its stream gets the greatest priority so that its CTAs
+    // are scheduled ahead of the conversion kernels running beside it (which use the least)
+    int least = 0, greatest = 0;
+    SLB_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    SLB_CUDA_CHECK(cudaStreamCreateWithPriority(&F->stream, cudaStreamNonBlocking, greatest));
+  }
   cudaStream_t st = F->stream;
   F->n1 = n1;
   F->n2 = n2;
