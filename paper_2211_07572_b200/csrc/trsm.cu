@@ -74,6 +74,32 @@ __device__ __forceinline__ void diag_inverses(const double* T, int64_t ldt, int 
   __syncthreads();
 }
 
+// d -= T[row, kb:ke) . X[kb:ke, tile cols] for one 8x8 tile (row = this lane's row of T staged
+// in trow, X swizzled); four independent DMMA chains, operands of four k4 steps loaded together.
+// (ke - kb) must be a multiple of 4.
+__device__ __forceinline__ void sub_row_block(const double* trow, const double* X, int col8, int kb, int ke, bool rok,
+                                              int t, int g, double& d0, double& d1) {
+  double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  int k = kb;
+  for (; k + 16 <= ke; k += 16) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      av[u] = rok ? -trow[k + 4 * u + t] : 0.0;
+      bv[u] = X[sw32(k + 4 * u + t, col8 + g)];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) dmma884(c[u][0], c[u][1], av[u], bv[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < 3; u++) {  // remainder: at most three k4 steps (static register indices)
+    if (k < ke) dmma884(c[u][0], c[u][1], rok ? -trow[k + t] : 0.0, X[sw32(k + t, col8 + g)]);
+    k += 4;
+  }
+  d0 += (c[0][0] + c[1][0]) + (c[2][0] + c[3][0]);
+  d1 += (c[0][1] + c[1][1]) + (c[2][1] + c[3][1]);
+}
+
 // X[r0:r0+16, 0:32] = Dinv_b X[r0:r0+16, 0:32] in place; 8 warps, warp (mt, nt) one 8x8 tile.
 __device__ __forceinline__ void apply_diag_inverse(const double* Di, double* X, int r0, int r1, int warp, int g,
                                                    int t) {
@@ -224,6 +250,7 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
   double* X = sm;                 // MMAX * TN   (U1213 tile, swizzled)
   double* sTb = sm + MMAX * TN;   // 2 x RB x KS (staged rows of L11 / L21)
   double* Dv = sTb + 2 * RB * KS; // inverses of L11's 16 x 16 diagonal blocks
+  int* sperm = reinterpret_cast<int*>(Dv + MMAX * RB);  // this level's pivot order (2 Wp)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int c0 = blockIdx.x * TN;
@@ -261,9 +288,11 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
   cp_async_commit();
   const int ncol = min(TN, 2 * Wp - c0);
   const int mt = warp >> 2, nt = warp & 3;
+  for (int i = tid; i < 2 * Wp; i += 256) sperm[i] = perm[i];
+  __syncthreads();
   for (int idx = tid; idx < m * TN; idx += 256) {
     const int n = idx / m, r = idx % m;
-    X[sw32(r, n)] = n < ncol ? Rval(perm[r], c0 + n) : 0.0;
+    X[sw32(r, n)] = n < ncol ? Rval(sperm[r], c0 + n) : 0.0;
   }
   for (int idx = m * TN + tid; idx < nb * RB * TN; idx += 256) X[idx] = 0.0;
   diag_inverses<true, true>(LU11, Wp, m, nb, Dv, tid, 256);
@@ -282,19 +311,10 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
       const bool rok = r0 + rloc < r1;
       const int row = rok ? r0 + rloc : r0;
       double a0 = X[sw32(row, nt * 8 + 2 * t)], a1 = X[sw32(row, nt * 8 + 2 * t + 1)];
-      double b0 = 0.0, b1 = 0.0;
-      const double* trow = Tb + rloc * KS;
-      auto tv = [&](int k) -> double { return (rok && k < r0) ? -trow[k] : 0.0; };
-      auto xv = [&](int k) -> double { return k < r0 ? X[sw32(k, nt * 8 + g)] : 0.0; };
-      int k = 0;
-      for (; k + 8 <= r0; k += 8) {
-        dmma884(a0, a1, tv(k + t), xv(k + t));
-        dmma884(b0, b1, tv(k + 4 + t), xv(k + 4 + t));
-      }
-      for (; k < r0; k += 4) dmma884(a0, a1, tv(k + t), xv(k + t));
+      sub_row_block(Tb + rloc * KS, X, nt * 8, 0, r0, rok, t, g, a0, a1);
       if (rok) {
-        X[sw32(row, nt * 8 + 2 * t)] = a0 + b0;
-        X[sw32(row, nt * 8 + 2 * t + 1)] = a1 + b1;
+        X[sw32(row, nt * 8 + 2 * t)] = a0;
+        X[sw32(row, nt * 8 + 2 * t + 1)] = a1;
       }
     }
     __syncthreads();
@@ -310,6 +330,13 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
   // ---- GEMM: out = R2 - L21 X, row blocks of 16 of L21 staged like L11
   stage_rows(L21, 0, 0);
   cp_async_commit();
+  // R2 values of this thread's outputs, one block ahead (their latency hides behind a block)
+  const int colq = c0 + nt * 8 + 2 * t;
+  auto r2 = [&](int b, int dc) -> double {
+    const int row = b * RB + mt * 8 + g;
+    return (b < nb && row < m && colq + dc < 2 * Wp) ? Rval(sperm[Wp + row], colq + dc) : 0.0;
+  };
+  double rn0 = r2(0, 0), rn1 = r2(0, 1);
   for (int b = 0; b < nb; b++) {
     const int r0 = b * RB, r1 = min(m, r0 + RB), h = r1 - r0;
     if (b + 1 < nb) stage_rows(L21, (b + 1) * RB, (b + 1) & 1);
@@ -322,19 +349,14 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
       const int rloc = mt * 8 + g;
       const bool rok = r0 + rloc < r1;
       const int row = rok ? r0 + rloc : r0;
-      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-      const double* trow = Tb + rloc * KS;
-      auto tv = [&](int k) -> double { return rok ? -trow[k] : 0.0; };
-      auto xv = [&](int k) -> double { return X[sw32(k, nt * 8 + g)]; };
-      int k = 0;
-      for (; k + 8 <= m; k += 8) {
-        dmma884(a0, a1, tv(k + t), xv(k + t));
-        dmma884(b0, b1, tv(k + 4 + t), xv(k + 4 + t));
-      }
-      for (; k < m; k += 4) dmma884(a0, a1, tv(k + t), xv(k + t));
-      const int col = c0 + nt * 8 + 2 * t;
-      if (rok && col < 2 * Wp) svo[(int64_t)col * Wp + row] = Rval(perm[Wp + row], col) + a0 + b0;
-      if (rok && col + 1 < 2 * Wp) svo[(int64_t)(col + 1) * Wp + row] = Rval(perm[Wp + row], col + 1) + a1 + b1;
+      const int col = colq;
+      const double r0v = rn0, r1v = rn1;
+      rn0 = r2(b + 1, 0);
+      rn1 = r2(b + 1, 1);
+      double a0 = 0.0, a1 = 0.0;
+      sub_row_block(Tb + rloc * KS, X, nt * 8, 0, m, rok, t, g, a0, a1);
+      if (rok && col < 2 * Wp) svo[(int64_t)col * Wp + row] = r0v + a0;
+      if (rok && col + 1 < 2 * Wp) svo[(int64_t)(col + 1) * Wp + row] = r1v + a1;
     }
     __syncthreads();
     UP(4)
@@ -348,7 +370,7 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
 }  // namespace
 
 void level_update(cudaStream_t st, const LevelArgs& a) {
-  const size_t smem = (size_t)(MMAX * TN + 2 * RB * KS + MMAX * RB) * sizeof(double);
+  const size_t smem = (size_t)(MMAX * TN + 2 * RB * KS + MMAX * RB) * sizeof(double) + 2 * MMAX * sizeof(int);
   static bool attr = false;
   if (!attr) {
     SLB_CUDA_CHECK(cudaFuncSetAttribute(level_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
