@@ -191,6 +191,12 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   __syncthreads();
 
   double* ent = win + NW * RS + 32;  // 8 x Wp staging for the entering rows
+#ifdef SLB_LU_PROF
+  long long L0 = clock64(), lp[6] = {0, 0, 0, 0, 0, 0};
+#define LP(k_) { const long long q_ = clock64(); lp[k_] += q_ - L0; L0 = q_; }
+#else
+#define LP(k_)
+#endif
 #ifdef SLB_PANEL8_PROF
   long long pq[5] = {0, 0, 0, 0, 0};
 #endif
@@ -327,17 +333,19 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
           for (int q = 0; q < 8; q++) row[kb + q] = v[i][q];
         }
       }
-      if (pt == 0)
-        for (int q = 0; q < 8; q++) {
-          const int c = kb + q, r = s_piv[q];
-          if (r != c) {
-            const int tp = perm[c];
-            perm[c] = perm[r];
-            perm[r] = tp;
-          }
-        }
     }
     __syncthreads();
+    LP(0)
+    // pivot-order bookkeeping for the panel (one thread, beside the swaps)
+    if (tid == blockDim.x - 1)
+      for (int q = 0; q < 8; q++) {
+        const int c = kb + q, r = s_piv[q];
+        if (r != c) {
+          const int tp = perm[c];
+          perm[c] = perm[r];
+          perm[r] = tp;
+        }
+      }
     // (b) the panel's row swaps on all other columns, in pivot order
     for (int jj = tid; jj < Wp - 8; jj += blockDim.x) {
       const int col = jj < kb ? jj : jj + 8;
@@ -354,6 +362,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
       }
     }
     __syncthreads();
+    LP(1)
     // (c) U block: pivot rows kb..kb+7 on the trailing columns, U = L_bb^{-1} A
     for (int j = kend + tid; j < Wp; j += blockDim.x) {
       double u[8];
@@ -370,6 +379,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
       for (int q = 1; q < 8; q++) rowp(kb + q)[j] = u[q];
     }
     __syncthreads();
+    LP(2)
     // (d) trailing update on the DMMA pipe: rows kend..kb+7+Wp, cols kend..Wp-1.
     //     A warp owns m tiles (8 rows) and sweeps the n tiles; its A fragments
     //     (the 8 multipliers of each row) are loaded once.
@@ -424,6 +434,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
       }
     }
     __syncthreads();
+    LP(3)
     // (e) retire positions kb..kb+7; bottom rows kend..kend+7 enter at positions kend+Wp..
     cp_async_wait<0>();
     for (int idx = tid; idx < 8 * Wp; idx += blockDim.x) {
@@ -434,7 +445,13 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
       if (pe < rows_total) rr[j] = ent[idx];
     }
     __syncthreads();
+    LP(4)
   }
+#ifdef SLB_LU_PROF
+  if (tid == 0 && s == 0 && (a.level % 1000) == 1)
+    printf("LEVEL_LU l=%d: panel %lld swap %lld ublock %lld trailing %lld retire %lld (cycles)\n", a.level, lp[0], lp[1],
+           lp[2], lp[3], lp[4]);
+#endif
 
 #ifdef SLB_PANEL8_PROF
   if (tid == 0 && s == 0 && (a.level % 1000) == 1)
