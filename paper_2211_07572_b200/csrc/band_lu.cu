@@ -33,7 +33,8 @@ __device__ __forceinline__ void raise(DevStatus* st, int32_t bit) { atomicOr(&st
 // Level blocks [Lsub | D | Usup] of one strip level from the CSR.
 // grid (nl, nstrips), block 128.
 __global__ void extract_levels_kernel(CsrDev A, const StripDesc* strips, int64_t n2, int Wp,
-                                      int64_t L0, double* nx, int64_t sNX, DevStatus* status) {
+                                      int64_t L0, double* nx, int64_t sNX, DevStatus* status, double* dsub,
+                                      uint8_t* lnd) {
   const int s = blockIdx.y;
   const int64_t L = L0 + blockIdx.x;
   const StripDesc sd = strips[s];
@@ -58,6 +59,10 @@ __global__ void extract_levels_kernel(CsrDev A, const StripDesc* strips, int64_t
         }
         // dy in {-1, 0, 1}: Lsub, D, Usup
         out[((dy + 1) * Wp + cx) * Wp + ix] = v;
+        if (dy == -1) {
+          if (cx == ix) dsub[((int64_t)s * n2 + L - 1) * Wp + ix] = v;
+          else if (v != 0.0) lnd[(int64_t)s * n2 + L] = 1;
+        }
       } else if (sd.left >= 0 && c >= sd.left_off && c < sd.left_off + n2) {
         if (c - sd.left_off != L) raise(status, ERR_COUPLING_LEVEL);
       } else if (sd.right >= 0 && c >= sd.right_off && c < sd.right_off + n2) {
@@ -463,7 +468,8 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   {
     // U13 != 0 iff a row of level l+1 was pivoted into the top half
     const int up = __syncthreads_or(tid < Wp && perm[tid] >= Wp);
-    if (tid == 0) a.u13[s * a.sU13] = (uint8_t)(up ? 1 : 0);
+    const int nd = a.has_next ? a.lnd[s * a.sU13] : 0;
+    if (tid == 0) a.u13[s * a.sU13] = (uint8_t)((up ? 1 : 0) | (nd ? 2 : 0));
   }
   if (a.has_next) {
     for (int idx = tid; idx < Wp * Wp; idx += blockDim.x) {
@@ -541,10 +547,11 @@ __global__ void convert_pack_kernel(int Wp, const double* X, int64_t sX, const d
 }  // namespace
 
 void extract_levels(cudaStream_t st, CsrDev A, const StripDesc* strips, int nstrips, int64_t n2,
-                    int Wp, int64_t L0, int64_t nl, double* nx, int64_t sNX, DevStatus* status) {
+                    int Wp, int64_t L0, int64_t nl, double* nx, int64_t sNX, DevStatus* status, double* dsub,
+                    uint8_t* lnd) {
   if (nl <= 0) return;
   extract_levels_kernel<<<dim3((unsigned)nl, (unsigned)nstrips), 128, 0, st>>>(A, strips, n2, Wp, L0,
-                                                                            nx, sNX, status); count_launch();
+                                                                            nx, sNX, status, dsub, lnd); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -223,6 +223,8 @@ struct slablu_gpu_fact {
   DBuf<double> cpl;
   DBuf<int32_t> sym;
   DBuf<uint8_t> u13;
+  DBuf<uint8_t> lnd;    // Lsub off-diagonal flags per (strip, level)
+  DBuf<double> dsub;    // diag(Lsub_{l+1}) per (strip, level)
   DBuf<double> T;       // [diag k | super k-1 | sub k-1] blocks, n2 x n2; diag holds S_j^{-1}
   DBuf<double> Tkeep;   // optional copy of the reduced blocks
   DBuf<DevStatus> status;
@@ -382,6 +384,10 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   F->cpl.alloc(dev, (size_t)S * F->sCPL);
   F->sym.alloc(dev, S);
   F->u13.alloc(dev, (size_t)S * n2);
+  F->lnd.alloc(dev, (size_t)S * n2);
+  F->dsub.alloc(dev, (size_t)S * n2 * Wp);
+  SLB_CUDA_CHECK(cudaMemsetAsync(F->lnd.p, 0, F->lnd.bytes(), st));
+  SLB_CUDA_CHECK(cudaMemsetAsync(F->dsub.p, 0, F->dsub.bytes(), st));
   {
     std::vector<int32_t> ones(S, 1);
     SLB_CUDA_CHECK(cudaMemcpyAsync(F->sym.p, ones.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice, st));
@@ -395,7 +401,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   sv.alloc(dev, (size_t)2 * S * 2 * Wp * Wp);
   const int64_t sSV = 2LL * Wp * Wp;
   double* svb[2] = {sv.p, sv.p + (size_t)S * sSV};
-  extract_levels(st, A, F->strips.p, S, n2, Wp, 0, LCH, nx.p, sNX, F->status.p);
+  extract_levels(st, A, F->strips.p, S, n2, Wp, 0, LCH, nx.p, sNX, F->status.p, F->dsub.p, F->lnd.p);
   init_sv(st, S, Wp, nx.p, sNX, svb[0], sSV);
   // LU-form -> GEMM-form conversion runs behind the chain on a low-priority
   // stream, one chunk of CCH levels at a time (idle SMs during the chain).
@@ -424,7 +430,8 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     const bool has_next = nxt < n2;
     if (l > 0 && l % CCH == 0 && !defer_conv) convert_chunk(l - CCH, l);
     if (has_next && nxt % LCH == 0) {
-      extract_levels(st, A, F->strips.p, S, n2, Wp, nxt, std::min(LCH, n2 - nxt), nx.p, sNX, F->status.p);
+      extract_levels(st, A, F->strips.p, S, n2, Wp, nxt, std::min(LCH, n2 - nxt), nx.p, sNX, F->status.p,
+                     F->dsub.p, F->lnd.p);
     }
     LevelArgs la;
     la.Wp = Wp;
@@ -441,6 +448,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     la.sP = F->sP;
     la.u13 = F->u13.p + l;
     la.sU13 = n2;
+    la.lnd = F->lnd.p + (has_next ? l + 1 : l);
     la.status = F->status.p;
     la.level = (int32_t)l;
     level_lu(st, la);
@@ -486,10 +494,10 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
       int64_t ones = 0, pairs = 0;
       for (int s = 0; s < S; s++)
         for (int64_t l = 0; l < n2; l++) {
-          ones += h[s * n2 + l];
-          pairs += (h[s * n2 + l] || (l > 0 && h[s * n2 + l - 1])) ? 1 : 0;
+          ones += h[s * n2 + l] & 1;
+          pairs += h[s * n2 + l] != 0 ? 1 : 0;
         }
-      fprintf(stderr, "[slablu] U13 != 0 on %lld of %lld levels; level or its predecessor: %lld\n", (long long)ones,
+      fprintf(stderr, "[slablu] U13 != 0 on %lld of %lld levels; full forward operator needed on %lld\n", (long long)ones,
               (long long)(S * n2), (long long)pairs);
     }
     F->sym_h.resize(S);
@@ -550,6 +558,8 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     sa.sCPL = F->sCPL;
     sa.sym = F->sym.p;
     sa.u13 = F->u13.p;
+    sa.dsub = F->dsub.p;
+    sa.fsc = getenv("SLB_FSC") ? 1 : 0;  // forward shortcut: measured neutral at cfg3, off by default
     sa.chunk = kSweepChunk;
     sa.gbuf = gbuf.p;
     sa.sG = sG;
@@ -698,6 +708,8 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   SchurArgs sa{};
   sa.chunk = CH;
   sa.u13 = F->u13.p;
+    sa.dsub = F->dsub.p;
+    sa.fsc = getenv("SLB_FSC") ? 1 : 0;  // forward shortcut: measured neutral at cfg3, off by default
   sa.Wp = F->Wp;
   sa.n2 = n2;
   sa.nstrips = S;
@@ -814,6 +826,8 @@ struct StripSweeper {
     ybuf.alloc(dev, (size_t)nslots * sY);
     sa.chunk = CH;
     sa.u13 = F->u13.p;
+    sa.dsub = F->dsub.p;
+    sa.fsc = getenv("SLB_FSC") ? 1 : 0;  // forward shortcut: measured neutral at cfg3, off by default
     sa.Wp = F->Wp;
     sa.n2 = n2;
     sa.nstrips = F->S;
@@ -1293,6 +1307,8 @@ slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* F, const double* 
     ybuf.alloc(dev, (size_t)nslots * sY);
     SchurArgs sa{};
     sa.chunk = kSweepChunk; sa.u13 = F->u13.p;
+    sa.dsub = F->dsub.p;
+    sa.fsc = getenv("SLB_FSC") ? 1 : 0;  // forward shortcut: measured neutral at cfg3, off by default
     sa.Wp = F->Wp; sa.n2 = n2; sa.nstrips = F->S; sa.strips = F->strips.p; sa.fac = F->fac.p; sa.sF = F->sF;
     sa.perm = F->perm.p; sa.sP = F->sP; sa.cpl = F->cpl.p; sa.sCPL = F->sCPL; sa.sym = F->sym.p;
     sa.ybuf = ybuf.p; sa.sY = sY; sa.task_counter = counter.p; sa.ntasks = ntasks; sa.tasks = dtasks.p;

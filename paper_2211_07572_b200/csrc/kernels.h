@@ -54,8 +54,11 @@ struct CsrDev {
 
 // Extract per-level dense blocks [Lsub | D | Usup] (Wp x 3Wp, ld Wp) for levels
 // [L0, L0+nl) of every strip into nx (stride per strip sNX, per level 3*Wp*Wp).
+// Also records, per (strip, level L), the diagonal of Lsub_L into dsub[s][L-1][i] and whether
+// Lsub_L has an off-diagonal entry into lnd[s][L] (the forward sweep shortcut needs diagonal Lsub).
 void extract_levels(cudaStream_t st, CsrDev A, const StripDesc* strips, int nstrips, int64_t n2,
-                    int Wp, int64_t L0, int64_t nl, double* nx, int64_t sNX, DevStatus* status);
+                    int Wp, int64_t L0, int64_t nl, double* nx, int64_t sNX, DevStatus* status, double* dsub,
+                    uint8_t* lnd);
 // Per-level coupling vectors fromL/fromR/toL/toR (n2 x Wp each per strip).
 void extract_couplings(cudaStream_t st, CsrDev A, const StripDesc* strips, int nstrips, int64_t n2,
                        int Wp, double* cpl, int64_t sCPL, int32_t* sym_flags, DevStatus* status);
@@ -76,8 +79,10 @@ struct LevelArgs {
   int64_t sF;            // per-strip stride of factor storage
   int32_t* perm;         // 2Wp      (factor storage, level l)
   int64_t sP;
-  uint8_t* u13;          // flag for this level (per strip stride n2)
+  uint8_t* u13;          // flags of this level (per strip stride n2): bit 0 U13 != 0 (a level-l+1
+                         // row pivoted up), bit 1 Lsub_{l+1} not diagonal; 0 = Fbot t = -dsub * y
   int64_t sU13;
+  const uint8_t* lnd;    // Lsub_{l+1} off-diagonal flag (per strip stride n2), level l+1
   DevStatus* status;
   int32_t level;
 };
@@ -99,7 +104,9 @@ struct SchurArgs {
   const double* cpl;      // coupling vectors (per strip sCPL): fromL, fromR, toL, toR (n2 x Wp each)
   int64_t sCPL;
   const int32_t* sym;     // per-strip symmetric flag
-  const uint8_t* u13;     // per (strip, level): 1 if a next-level row was pivoted up (U13 != 0)
+  const uint8_t* u13;     // per (strip, level) flags: bit 0 U13 != 0, bit 1 Lsub_{l+1} not diagonal
+  const double* dsub;     // per (strip, level) diag(Lsub_{l+1}) (Wp), per strip stride n2 * Wp
+  int fsc;                // forward shortcut enabled (levels with flags == 0)
   double* gbuf;           // per strip 4 * n2 * n2 (row-major [X][Y][p][q])
   int64_t sG;
   double* ybuf;           // per CTA slot: n2 * Wp * C

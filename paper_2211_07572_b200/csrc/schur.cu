@@ -30,7 +30,10 @@ constexpr int THREADS = 512;
 // Compile-time layout of a sweep kernel with C right-hand-side columns.
 template <int C>
 struct Lay {
-  static constexpr int STAGES = C >= 32 ? 3 : 8;      // cp.async ring depth (deep for bandwidth-bound solves)
+  // operand ring: SK k4 steps per slice, STAGES slices (measured at cfg3: k8 slices x 3 beat
+  // k4 slices x 6 by 17%, the per-slice synchronisation outweighs the deeper prefetch)
+  static constexpr int SK = 2;
+  static constexpr int STAGES = C >= 32 ? 3 : 8;
   static constexpr int NT = C / 8;                    // n8 tiles
   static constexpr int FWN = NT >= 2 ? 2 : 1;         // forward n groups (per half)
   static constexpr int FWM = 8 / FWN;                 // forward m groups (per half)
@@ -61,8 +64,9 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
   double* zb = sm;                       // forward: z      | backward: x buffer 0
   double* tb = sm + Wp * C;              // forward: t_top  | backward: x buffer 1
   double* stg = sm + 2 * Wp * C;         // STAGES slots of 16*Wp doubles
-  int* spermb = reinterpret_cast<int*>(stg + STAGES * 16 * Wp);  // [2][2 Wp] pivot orders (level l, l+1)
-  uint8_t* su13 = reinterpret_cast<uint8_t*>(spermb + 4 * Wp);  // n2 flags of the current strip
+  int* spermb = reinterpret_cast<int*>(stg + STAGES * 8 * L::SK * Wp);  // [2][2 Wp] pivot orders (level l, l+1)
+  double* sdsub = reinterpret_cast<double*>(spermb + 4 * Wp);    // [2][Wp] diag(Lsub_{l+1}) (level l, l+1)
+  uint8_t* su13 = reinterpret_cast<uint8_t*>(sdsub + 2 * Wp);    // n2 level flags of the current strip
   __shared__ int s_task;
   __shared__ __align__(8) uint64_t full_bar[L::STAGES];
   __shared__ __align__(8) uint64_t empty_bar[L::STAGES];
@@ -78,11 +82,13 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
   const int g = lane >> 2, t = lane & 3;
   const int MTH = Wp / 8;                       // m8 tiles per Wp rows
   const int FMT = (MTH + L::FWM - 1) / L::FWM;  // forward m tiles per warp
+  const int FMT2 = (MTH + 2 * L::FWM - 1) / (2 * L::FWM);  // ... when all warps take Ainv rows
   const int BMT = (MTH + L::BWM - 1) / L::BWM;  // backward m tiles per warp
-  const int fslice = 16 * Wp;                   // doubles per forward k8 slice
-  const int bslice = 8 * Wp;                    // doubles per backward k8 slice
+  constexpr int SK = L::SK;
+  const int fslice = 8 * SK * Wp;               // doubles per forward slice (SK k4 steps of [Ainv ; Fbot])
+  const int bslice = 4 * SK * Wp;               // doubles per backward slice (SK k4 steps of H)
   const int64_t lvl_stride = 4LL * Wp * Wp;
-  const int kf = Wp / 8, kb = Wp / 4;           // slices per level (fwd, bwd)
+  const int kf = Wp / (4 * SK), kb = Wp / (2 * SK);  // slices per level (fwd, bwd)
   double* ybase = a.ybuf + (int64_t)blockIdx.x * a.sY;
   if (tid == 0) {
     for (int i = 0; i < STAGES; i++) {
@@ -146,6 +152,8 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
       if (tid != 0 || p_done) return;
       const double* src = p_src;
       const int len = p_len;
+      // shortcut level (flags == 0): only the Ainv half of each k4 block of [Ainv ; Fbot]
+      const bool split = a.fsc && p_fwd && su13[p_lvl] == 0;
       if (--p_left > 0) {
         p_src += p_len;
       } else if (p_fwd) {
@@ -157,7 +165,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
           } else {
             p_src = fac + p_lvl * lvl_stride + 2LL * Wp * Wp;
             p_len = bslice;
-            p_left = su13[p_lvl] ? kb : kb / 2;
+            p_left = (su13[p_lvl] & 1) ? kb : kb / 2;
           }
         } else {
           p_src += p_len + (lvl_stride - (int64_t)kf * fslice);
@@ -168,13 +176,20 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
           p_done = true;
         } else {
           p_src = fac + p_lvl * lvl_stride + 2LL * Wp * Wp;
-          p_left = su13[p_lvl] ? kb : kb / 2;
+          p_left = (su13[p_lvl] & 1) ? kb : kb / 2;
         }
       }
       const int sl = p_slot;
       if (p_round > 0) mbar_wait(&empty_bar[sl], (p_round - 1) & 1u);
-      mbar_arrive_expect_tx(&full_bar[sl], (uint32_t)(len * sizeof(double)));
-      bulk_g2s(stg + sl * fslice, src, (uint32_t)(len * sizeof(double)), &full_bar[sl]);
+      if (split) {
+        const uint32_t hb = (uint32_t)(4 * Wp * sizeof(double));  // MTH m8 tiles of one k4 step
+        mbar_arrive_expect_tx(&full_bar[sl], SK * hb);
+#pragma unroll
+        for (int kk = 0; kk < SK; kk++) bulk_g2s(stg + sl * fslice + kk * 4 * Wp, src + kk * 8 * Wp, hb, &full_bar[sl]);
+      } else {
+        mbar_arrive_expect_tx(&full_bar[sl], (uint32_t)(len * sizeof(double)));
+        bulk_g2s(stg + sl * fslice, src, (uint32_t)(len * sizeof(double)), &full_bar[sl]);
+      }
       if (++p_slot == STAGES) {
         p_slot = 0;
         p_round++;
@@ -213,20 +228,39 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     const int fwm = (warp & 7) / L::FWN;   // m group
     const int fwn = (warp & 7) % L::FWN;   // n group
     // pivot order of the first level now; each level prefetches the next one (cp.async)
+    const double* dsubg = a.dsub + (int64_t)T.s * n2 * Wp;
     for (int i = tid; i < 2 * Wp; i += THREADS) spermb[i] = permg[T.l0 * 2 * Wp + i];
+    for (int i = tid; i < Wp; i += THREADS) sdsub[i] = dsubg[T.l0 * Wp + i];
     int pcur = 0;
+#ifdef SLB_SCHUR_PROF
+    long long S0 = clock64(), sp[6] = {0, 0, 0, 0, 0, 0};
+#define SP(k_) { const long long q_ = clock64(); sp[k_] += q_ - S0; S0 = q_; }
+#else
+#define SP(k_)
+#endif
     for (int64_t l = T.l0; l < n2; l++) {
       const bool has_next = l + 1 < n2;
       const int cstar = (schur && has_next) ? (int)(l + 1 - T.q0) : -1;  // column injected
       const bool inj = cstar >= 0 && cstar < ncols;
       const double* fvec = inj ? fromY + (l + 1) * Wp : nullptr;
+      SP(4)
       cp_async_wait<0>();
       __syncthreads();  // sperm (this level) and z_l complete
+      SP(0)
       const int* sperm = spermb + pcur * 2 * Wp;
+      const double* dsl = sdsub + pcur * Wp;
       if (has_next && tid < Wp / 2)  // 2 Wp int32 = Wp / 2 16-byte pieces
         cp_async16(spermb + (pcur ^ 1) * 2 * Wp + 4 * tid, permg + (l + 1) * 2 * Wp + 4 * tid, true);
+      else if (has_next && tid >= 256 && tid < 256 + Wp / 2)  // Wp doubles = Wp / 2 pieces
+        cp_async16(sdsub + (pcur ^ 1) * Wp + 2 * (tid - 256), dsubg + (l + 1) * Wp + 2 * (tid - 256), true);
       cp_async_commit();
       pcur ^= 1;
+      // shortcut level: no level-(l+1) row pivoted up and Lsub_{l+1} diagonal, so
+      // Fbot t_top = -diag(Lsub_{l+1}) y_l: stream Ainv only, all warps on its rows
+      const bool sc = a.fsc && su13[l] == 0;
+      const int hf = sc ? 0 : half;
+      const int fm = sc ? warp / L::FWN : fwm;
+      const int fmt = sc ? FMT2 : FMT;
       auto vval = [&](int src, int n) -> double {
         if (src < Wp) return zb[swz<C>(src, n)];
         if (!schur) return has_next ? rhs_val(l + 1, src - Wp, n) : 0.0;
@@ -252,8 +286,8 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
 #pragma unroll
         for (int nj = 0; nj < L::FNT; nj++) {
           acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
-          const int mt = fwm * FMT + mi;
-          if (half == 1 && mi < FMT && mt < MTH) {
+          const int mt = fm * fmt + mi;
+          if (hf == 1 && mi < fmt && mt < MTH) {
             const int row = mt * 8 + g;
             const int col = (fwn * L::FNT + nj) * 8 + 2 * t;
             const int src = sperm[Wp + row];
@@ -261,21 +295,23 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
             acc[mi][nj][1] = vval(src, col + 1);
           }
         }
+      SP(1)
       __syncthreads();
+      SP(2)
       for (int j = 0; j < kf; j++) {
         issue();
         const double* A = acquire();
 #pragma unroll
-        for (int kk = 0; kk < 2; kk++) {
-          const int k = j * 8 + kk * 4 + t;  // B row
+        for (int kk = 0; kk < SK; kk++) {
+          const int k = j * 4 * SK + kk * 4 + t;  // B row
           double bf[L::FNT];
 #pragma unroll
           for (int nj = 0; nj < L::FNT; nj++) bf[nj] = tb[swz<C>(k, (fwn * L::FNT + nj) * 8 + g)];
-          const double* Ak = A + kk * (2 * MTH) * 32 + half * MTH * 32 + lane;
+          const double* Ak = A + kk * (sc ? MTH : 2 * MTH) * 32 + hf * MTH * 32 + lane;
 #pragma unroll
           for (int mi = 0; mi < MTMAX; mi++) {
-            const int mt = fwm * FMT + mi;
-            if (mi < FMT && mt < MTH) {
+            const int mt = fm * fmt + mi;
+            if (mi < fmt && mt < MTH) {
               const double af = Ak[mt * 32];
 #pragma unroll
               for (int nj = 0; nj < L::FNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
@@ -284,16 +320,17 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
         }
         release();
       }
+      SP(3)
       // epilogue: y_l -> HBM slab (canonical tile order), z_{l+1} -> smem
       double* ylev = ybase + (l - T.l0) * (int64_t)Wp * C;
 #pragma unroll
       for (int mi = 0; mi < MTMAX; mi++) {
-        const int mt = fwm * FMT + mi;
-        if (mi >= FMT || mt >= MTH) continue;
+        const int mt = fm * fmt + mi;
+        if (mi >= fmt || mt >= MTH) continue;
 #pragma unroll
         for (int nj = 0; nj < L::FNT; nj++) {
           const int nt = fwn * L::FNT + nj;
-          if (half == 0) {
+          if (hf == 0) {
             double2* dst = reinterpret_cast<double2*>(ylev + ((int64_t)(mt * L::NT + nt) * 32 + lane) * 2);
             *dst = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
           } else {
@@ -303,8 +340,43 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
           }
         }
       }
+      if (sc) {
+        // z_{l+1}[i] = t_bot[i] - d_i y_l[i]: read every t_bot value (old z_l rows) first,
+        // then overwrite z in place after the barrier
+#pragma unroll
+        for (int mi = 0; mi < MTMAX; mi++) {
+          const int mt = fm * fmt + mi;
+          if (mi >= fmt || mt >= MTH) continue;
+          const int row = mt * 8 + g;
+          const int src = sperm[Wp + row];
+          const double dd = dsl[row];
+#pragma unroll
+          for (int nj = 0; nj < L::FNT; nj++) {
+            const int col = (fwn * L::FNT + nj) * 8 + 2 * t;
+            acc[mi][nj][0] = fma(-dd, acc[mi][nj][0], vval(src, col));
+            acc[mi][nj][1] = fma(-dd, acc[mi][nj][1], vval(src, col + 1));
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int mi = 0; mi < MTMAX; mi++) {
+          const int mt = fm * fmt + mi;
+          if (mi >= fmt || mt >= MTH) continue;
+#pragma unroll
+          for (int nj = 0; nj < L::FNT; nj++) {
+            const int row = mt * 8 + g, col = (fwn * L::FNT + nj) * 8 + 2 * t;
+            zb[swz<C>(row, col)] = acc[mi][nj][0];
+            zb[swz<C>(row, col + 1)] = acc[mi][nj][1];
+          }
+        }
+      }
     }
 
+#ifdef SLB_SCHUR_PROF
+    if (tid == 0 && blockIdx.x == 0)
+      printf("SCHUR task %d levels %lld: topsync %lld build %lld presync %lld kloop %lld epi %lld (cycles)\n", task,
+             (long long)(n2 - T.l0), sp[0], sp[1], sp[2], sp[3], sp[4]);
+#endif
     // ---------------- backward sweep ----------------
     __syncthreads();
     for (int idx = tid; idx < 2 * Wp * C; idx += THREADS) sm[idx] = 0.0;  // x_{n2}, x_{n2+1} = 0
@@ -314,7 +386,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     int p_buf = 0;                    // buffer holding x_{l+1}; the other holds x_{l+2}
     for (int64_t l = n2 - 1; l >= T.lstop; l--) {
       const double* ylev = ybase + (l - T.l0) * (int64_t)Wp * C;
-      const int kbl = su13[l] ? kb : kb / 2;  // U13 = 0: x_{l+2} does not enter
+      const int kbl = (su13[l] & 1) ? kb : kb / 2;  // U13 = 0: x_{l+2} does not enter
       double acc[MTMAX][L::BNT][2];
 #pragma unroll
       for (int mi = 0; mi < MTMAX; mi++) {
@@ -335,10 +407,11 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
       for (int j = 0; j < kbl; j++) {
         issue();
         const double* A = acquire();
-        const double* xs = (j * 8 < Wp) ? xp : xq;
-        const int kbase = (j * 8 < Wp) ? j * 8 : j * 8 - Wp;
+        const int kj = j * 4 * SK;
+        const double* xs = (kj < Wp) ? xp : xq;
+        const int kbase = (kj < Wp) ? kj : kj - Wp;
 #pragma unroll
-        for (int kk = 0; kk < 2; kk++) {
+        for (int kk = 0; kk < SK; kk++) {
           const int k = kbase + kk * 4 + t;
           double bf[L::BNT];
 #pragma unroll
@@ -402,7 +475,8 @@ template <int C>
 void launch_sweep(cudaStream_t st, const SchurArgs& a, int nslots) {
   using L = Lay<C>;
   const int Wp = a.Wp;
-  const size_t smem = (size_t)(2 * Wp * C + L::STAGES * 16 * Wp) * sizeof(double) + 4 * Wp * sizeof(int) + a.n2;
+  const size_t smem =
+      (size_t)(2 * Wp * C + L::STAGES * 8 * L::SK * Wp + 2 * Wp) * sizeof(double) + 4 * Wp * sizeof(int) + a.n2;
   const int mth = Wp / 8;
   const int mt = std::max((mth + L::FWM - 1) / L::FWM, (mth + L::BWM - 1) / L::BWM);
   auto go = [&](auto kern) {

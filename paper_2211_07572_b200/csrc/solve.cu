@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
         ls = 0;
         lph ^= 1u;
       }
-      const int nsl = fwd ? kf : (su13[l] ? kb : kb / 2);
+      const int nsl = fwd ? kf : ((su13[l] & 1) ? kb : kb / 2);
       const double* base = fac + l * lvl + (fwd ? 0 : 2LL * Wp * Wp);
       for (int j = 0; j < nsl; j++) {
         QS()
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
   consumer_bar();
   int i1 = 1, i2 = 2, i0 = 0;  // x_{l+1} in xb[i1], x_{l+2} in xb[i2], x_l written into xb[i0]
   for (int64_t l = n2 - 1; l >= 0; l--) {
-    const int kbl = su13[l] ? kb : kb / 2;
+    const int kbl = (su13[l] & 1) ? kb : kb / 2;
     const double* x1 = xb + i1 * WC;
     const double* x2 = xb + i2 * WC;
     double* x0 = xb + i0 * WC;
