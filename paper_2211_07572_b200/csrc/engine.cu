@@ -559,7 +559,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     sa.sym = F->sym.p;
     sa.u13 = F->u13.p;
     sa.dsub = F->dsub.p;
-    sa.fsc = getenv("SLB_FSC") ? 1 : 0;  // forward shortcut: measured neutral at cfg3, off by default
+    sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
     sa.chunk = kSweepChunk;
     sa.gbuf = gbuf.p;
     sa.sG = sG;
@@ -709,7 +709,7 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   sa.chunk = CH;
   sa.u13 = F->u13.p;
     sa.dsub = F->dsub.p;
-    sa.fsc = getenv("SLB_FSC") ? 1 : 0;  // forward shortcut: measured neutral at cfg3, off by default
+    sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
   sa.Wp = F->Wp;
   sa.n2 = n2;
   sa.nstrips = S;
@@ -827,7 +827,7 @@ struct StripSweeper {
     sa.chunk = CH;
     sa.u13 = F->u13.p;
     sa.dsub = F->dsub.p;
-    sa.fsc = getenv("SLB_FSC") ? 1 : 0;  // forward shortcut: measured neutral at cfg3, off by default
+    sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
     sa.Wp = F->Wp;
     sa.n2 = n2;
     sa.nstrips = F->S;
@@ -1308,7 +1308,7 @@ slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* F, const double* 
     SchurArgs sa{};
     sa.chunk = kSweepChunk; sa.u13 = F->u13.p;
     sa.dsub = F->dsub.p;
-    sa.fsc = getenv("SLB_FSC") ? 1 : 0;  // forward shortcut: measured neutral at cfg3, off by default
+    sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
     sa.Wp = F->Wp; sa.n2 = n2; sa.nstrips = F->S; sa.strips = F->strips.p; sa.fac = F->fac.p; sa.sF = F->sF;
     sa.perm = F->perm.p; sa.sP = F->sP; sa.cpl = F->cpl.p; sa.sCPL = F->sCPL; sa.sym = F->sym.p;
     sa.ybuf = ybuf.p; sa.sY = sY; sa.task_counter = counter.p; sa.ntasks = ntasks; sa.tasks = dtasks.p;

@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     for (int i = tid; i < Wp; i += THREADS) sdsub[i] = dsubg[T.l0 * Wp + i];
     int pcur = 0;
 #ifdef SLB_SCHUR_PROF
-    long long S0 = clock64(), sp[6] = {0, 0, 0, 0, 0, 0};
+    long long S0 = clock64(), sp[6] = {0, 0, 0, 0, 0, 0}, wacq = 0, nsc = 0;
 #define SP(k_) { const long long q_ = clock64(); sp[k_] += q_ - S0; S0 = q_; }
 #else
 #define SP(k_)
@@ -258,6 +258,9 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
       // shortcut level: no level-(l+1) row pivoted up and Lsub_{l+1} diagonal, so
       // Fbot t_top = -diag(Lsub_{l+1}) y_l: stream Ainv only, all warps on its rows
       const bool sc = a.fsc && su13[l] == 0;
+#ifdef SLB_SCHUR_PROF
+      nsc += sc ? 1 : 0;
+#endif
       const int hf = sc ? 0 : half;
       const int fm = sc ? warp / L::FWN : fwm;
       const int fmt = sc ? FMT2 : FMT;
@@ -299,8 +302,18 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
       __syncthreads();
       SP(2)
       for (int j = 0; j < kf; j++) {
+#ifdef SLB_SCHUR_PROF
+        long long W0 = clock64();
+        issue();
+        long long W1 = clock64();
+        const double* A = acquire();
+        long long W2 = clock64();
+        sp[5] += W1 - W0;
+        wacq += W2 - W1;
+#else
         issue();
         const double* A = acquire();
+#endif
 #pragma unroll
         for (int kk = 0; kk < SK; kk++) {
           const int k = j * 4 * SK + kk * 4 + t;  // B row
@@ -311,11 +324,11 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
 #pragma unroll
           for (int mi = 0; mi < MTMAX; mi++) {
             const int mt = fm * fmt + mi;
-            if (mi < fmt && mt < MTH) {
-              const double af = Ak[mt * 32];
+            // warp-uniform exit, not a predicate: predicated-off DMMAs still occupy the pipe
+            if (mi >= fmt || mt >= MTH) break;
+            const double af = Ak[mt * 32];
 #pragma unroll
-              for (int nj = 0; nj < L::FNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
-            }
+            for (int nj = 0; nj < L::FNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
           }
         }
         release();
@@ -373,9 +386,9 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     }
 
 #ifdef SLB_SCHUR_PROF
-    if (tid == 0 && blockIdx.x == 0)
-      printf("SCHUR task %d levels %lld: topsync %lld build %lld presync %lld kloop %lld epi %lld (cycles)\n", task,
-             (long long)(n2 - T.l0), sp[0], sp[1], sp[2], sp[3], sp[4]);
+    if ((tid == 0 || tid == 160) && blockIdx.x == 0)
+      printf("SCHUR tid %d task %d levels %lld: topsync %lld build %lld presync %lld kloop %lld (issue %lld acquire-wait %lld) epi %lld shortcut-levels %lld\n",
+             tid, task, (long long)(n2 - T.l0), sp[0], sp[1], sp[2], sp[3], sp[5], wacq, sp[4], nsc);
 #endif
     // ---------------- backward sweep ----------------
     __syncthreads();
@@ -420,11 +433,10 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
 #pragma unroll
           for (int mi = 0; mi < MTMAX; mi++) {
             const int mt = bwm * BMT + mi;
-            if (mi < BMT && mt < MTH) {
-              const double af = Ak[mt * 32];
+            if (mi >= BMT || mt >= MTH) break;  // warp-uniform exit (see the forward loop)
+            const double af = Ak[mt * 32];
 #pragma unroll
-              for (int nj = 0; nj < L::BNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
-            }
+            for (int nj = 0; nj < L::BNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
           }
         }
         release();
