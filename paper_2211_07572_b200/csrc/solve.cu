@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
   const SolveLay Ly = solve_lay(Wp, n2);
   const int WC = Ly.WC;
   const int MTH = Wp / 8, MTF = 2 * MTH;
-  const int bm0 = mtile0_of(MTH, rank), bmn = mtiles_of(MTH, rank);
+  const int bm0 = mtile0_of(MTH, rank), bmn = mtiles_of(MTH, rank);  // backward: rows of H
+  const int fm0 = mtile0_of(MTF, rank), fmn = mtiles_of(MTF, rank);  // forward: contiguous [Ainv ; Fbot] tiles
   double* z = sm + Ly.z;  // [2][Wp x C] z_l parity buffers (own rows valid after level 0)
   double* tt = sm + Ly.tt;
   double* xb = sm + Ly.xb;  // [3][Wp x C] x_l, x_{l+1}, x_{l+2}
@@ -158,9 +159,9 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
   double* ybase = a.ybuf + (int64_t)task * a.sY;  // b_l (packed) in, y_l out: n2 x (Wp x C)
 
   for (int64_t i = tid; i < n2; i += THREADS) su13[i] = a.u13[s * n2 + i];
-  if (tid < MTH) {
+  if (tid < MTH) {  // owner of z row tile b = owner of forward tile MTH + b
     int r = 0;
-    while (r + 1 < G && mtile0_of(MTH, r + 1) <= tid) r++;
+    while (r + 1 < G && mtile0_of(MTF, r + 1) <= MTH + tid) r++;
     owner[tid] = r;
   }
   if (tid == 0) {
@@ -239,15 +240,13 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
         if (lane == 0) {
           double* dst = stg + slot * Ly.slot_d;
           const uint32_t tb = (uint32_t)bmn * 32 * 8;
-          if (fwd) {
-            mbar_arrive_expect_tx(&full_bar[slot], 4 * tb);
-            if (tb) {
+          if (fwd) {  // one contiguous run of fmn tiles per k4 step
+            const uint32_t fb = (uint32_t)fmn * 32 * 8;
+            mbar_arrive_expect_tx(&full_bar[slot], 2 * fb);
+            if (fb) {
 #pragma unroll
-              for (int kk = 0; kk < 2; kk++) {
-                const double* src = base + ((int64_t)(2 * j + kk) * MTF + bm0) * 32;
-                bulk_g2s(dst + kk * 2 * bmn * 32, src, tb, &full_bar[slot]);
-                bulk_g2s(dst + kk * 2 * bmn * 32 + bmn * 32, src + MTH * 32, tb, &full_bar[slot]);
-              }
+              for (int kk = 0; kk < 2; kk++)
+                bulk_g2s(dst + kk * fmn * 32, base + ((int64_t)(2 * j + kk) * MTF + fm0) * 32, fb, &full_bar[slot]);
             }
           } else {
             mbar_arrive_expect_tx(&full_bar[slot], 2 * tb);
@@ -317,16 +316,17 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
         if (idx < WC) tt[idx] = v[k];
       }
     }
-    // warp w owns local tiles w, w+8 of this CTA's 2*bmn tiles (top rows bm0.., then bottom rows)
+    // warp w owns local tiles w, w+8 of this CTA's fmn forward tiles fm0.. (global tile < MTH:
+    // a row of y_l, else a row of z_{l+1})
     double acc[2][2];
     int lts[2];
 #pragma unroll
     for (int u = 0; u < 2; u++) {
       const int lt = warp + 8 * u;
-      lts[u] = lt < 2 * bmn ? lt : -1;
+      lts[u] = lt < fmn ? lt : -1;
       acc[u][0] = acc[u][1] = 0.0;
-      if (lts[u] >= bmn) {  // bottom half: z_{l+1} = t_bot + Fbot t_top
-        const int src = sperm[Wp + (bm0 + lt - bmn) * 8 + g];
+      if (lts[u] >= 0 && fm0 + lt >= MTH) {  // bottom half: z_{l+1} = t_bot + Fbot t_top
+        const int src = sperm[Wp + (fm0 + lt - MTH) * 8 + g];
         acc[u][0] = vval(src, 2 * t);
         acc[u][1] = vval(src, 2 * t + 1);
       }
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
         const double bf = tt[(j * 8 + kk * 4 + t) * C + g];
 #pragma unroll
         for (int u = 0; u < 2; u++)
-          if (lts[u] >= 0) dmma884(acc[u][0], acc[u][1], A[kk * 2 * bmn * 32 + lts[u] * 32 + lane], bf);
+          if (lts[u] >= 0) dmma884(acc[u][0], acc[u][1], A[kk * fmn * 32 + lts[u] * 32 + lane], bf);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[slot]);
@@ -362,12 +362,13 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
 #pragma unroll
     for (int u = 0; u < 2; u++) {
       if (lts[u] < 0) continue;
-      if (lts[u] < bmn) {
-        const int row = (bm0 + lts[u]) * 8 + g;
+      const int mt = fm0 + lts[u];
+      if (mt < MTH) {
+        const int row = mt * 8 + g;
         ylev[row * C + 2 * t] = acc[u][0];
         ylev[row * C + 2 * t + 1] = acc[u][1];
       } else {
-        const int row = (bm0 + lts[u] - bmn) * 8 + g;
+        const int row = (mt - MTH) * 8 + g;
         zn[row * C + 2 * t] = acc[u][0];
         zn[row * C + 2 * t + 1] = acc[u][1];
       }
