@@ -197,13 +197,8 @@ def run_ours(args):
     import torch
     import paper_2211_07572_b200 as S
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank, world = 0, 1  # N > 1 runs run_ours_sharded
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     kind, n1, n2, b, ppw, desc = CONFIGS[args.config]
     spec, kappa = problem(args.config)
@@ -226,14 +221,18 @@ def run_ours(args):
 
     def barrier():
         torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
 
     for w in range(args.warmup):
         f = S.factorize_device(n1, n2, d_rp, d_ci, d_v, cfgS)
         log(f"[bench] warmup {w}: T_factor {f.t_stage1 + f.t_stage2:.3f}s (chain {f.stats.t_chain:.3f}, "
             f"schur {f.stats.t_schur:.3f}, asm {f.stats.t_assemble:.3f}, stage2 {f.t_stage2:.3f})")
         f.close()
+    # working set vs the 126 MB L2: the factor operators alone are 32 Wp^2 n2 bytes per strip
+    widths, _ = geometry(n1, n2, b)
+    wp = -(-max(widths) // 8) * 8
+    factor_bytes = len(widths) * 32 * wp * wp * n2
+    flush = factor_bytes < 4 * 126e6
+    l2buf = torch.empty(64 << 20, dtype=torch.float64, device=dev) if flush else None  # 512 MB
     clocks = ClockSampler()
     clocks.start()
     barrier()
@@ -243,6 +242,9 @@ def run_ours(args):
     for s in range(args.steps):
         if fact is not None:
             fact.close()
+        if l2buf is not None:  # evict the previous step's data (not timed: engine events)
+            l2buf.fill_(float(s))
+            torch.cuda.synchronize()
         fact = S.factorize_device(n1, n2, d_rp, d_ci, d_v, cfgS)
         t_fac.append(fact.t_stage1 + fact.t_stage2)
         t_schur.append(fact.stats.t_schur)
@@ -285,12 +287,7 @@ def run_ours(args):
     h2d = sysm.row_ptr.nbytes + sysm.col_idx.nbytes + sysm.values.nbytes + sysm.rhs.nbytes
     d2h = N * 8
     T = float(np.mean(t_fac))
-    if dist is not None:
-        tt = torch.tensor([T, float(np.mean(t_e2e))], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        T, te = float(tt[0]), float(tt[1])
-    else:
-        te = float(np.mean(t_e2e))
+    te = float(np.mean(t_e2e))
     band, schur, sweep = algorithmic_flops(n1, n2, b)
     T_schur = float(np.mean(t_schur))
     cpu = None
@@ -308,7 +305,9 @@ def run_ours(args):
         "ms_per_step": T * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (deterministic canned problem, inputs resident in HBM; factors > L2 so no flush needed)",
         "config": {"workload": desc, "n1": n1, "n2": n2, "b": b, "kappa": kappa, "N": N,
-                   "parallelism": "replicas" if world > 1 else "single-gpu", "l2": "inputs+factors >> 126 MB L2"},
+                   "parallelism": "single-gpu",
+                   "l2": (f"L2 flushed between steps (512 MB write); factor operators {factor_bytes / 1e6:.0f} MB"
+                          if flush else f"no flush needed: factor operators {factor_bytes / 1e9:.1f} GB >> 126 MB L2")},
         "T_factor_s": T, "T_stage1_s": T - float(np.mean(t_st2)), "T_stage2_s": float(np.mean(t_st2)),
         "phases_s": {"chain": float(np.mean(t_chain)), "schur": T_schur},
         "solve_ms_per_rhs": t_solve1 * 1e3, "solve_ms_per_rhs_batched": t_solveB / nrhs * 1e3, "solve_batch": nrhs,

@@ -226,3 +226,17 @@ def test_ten_ppw_helmholtz_vs_oracle(n, b):
     print(f"10ppw n={n}: diff vs oracle {d:.3e}, backward error gpu {eta_g:.3e} oracle {eta_o:.3e}")
     assert eta_g < 1e-14 and eta_g < 10 * eta_o + 1e-16
     assert d < 1e-8
+
+
+def test_forward_shortcut_matches_full_operator(monkeypatch):
+    """Levels without cross-level pivoting use Fbot t = -diag(Lsub) y (schur.cu); the full
+    [Ainv ; Fbot] operator must give the same T blocks and solution."""
+    n1, n2, b, kappa = 96, 64, 11, 50.0
+    sys_g = S.assemble_fd5(S.helmholtz_bump_problem(n1, n2, kappa))
+    fa = S.factorize(sys_g, S.SolverConfig(b=b, keep_T=True))
+    monkeypatch.setenv("SLB_NO_FSC", "1")
+    fb = S.factorize(sys_g, S.SolverConfig(b=b, keep_T=True))
+    for j in range(fa.stats.interfaces):
+        assert relerr(fa.T_block("diag", j), fb.T_block("diag", j)) < 1e-12
+    ua, ub = S.solve(fa, sys_g.rhs), S.solve(fb, sys_g.rhs)
+    assert relerr(ua, ub) < 1e-12
