@@ -467,9 +467,10 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm_out[p] = perm[p];
   {
     // U13 != 0 iff a row of level l+1 was pivoted into the top half
-    const int up = __syncthreads_or(tid < Wp && perm[tid] >= Wp);
+    // bits: 0 U13 != 0, 1 Lsub_{l+1} not diagonal, 2..5 rows of level l+1 pivoted up (15 = more)
+    const int nup = __syncthreads_count(tid < Wp && perm[tid] >= Wp);
     const int nd = a.has_next ? a.lnd[s * a.sU13] : 0;
-    if (tid == 0) a.u13[s * a.sU13] = (uint8_t)((up ? 1 : 0) | (nd ? 2 : 0));
+    if (tid == 0) a.u13[s * a.sU13] = (uint8_t)((nup ? 1 : 0) | (nd ? 2 : 0) | (min(nup, 15) << 2));
   }
   if (a.has_next) {
     for (int idx = tid; idx < Wp * Wp; idx += blockDim.x) {
@@ -588,7 +589,32 @@ void level_lu(cudaStream_t st, const LevelArgs& a) {
 //   X = U11^{-1} X = [Ainv | H] (upper TRSM);  pack [Ainv ; Fbot] and H.
 // work: 4 Wp^2 doubles per level.  Runs on a low-priority stream behind the
 // chain (one launch group per chunk of levels).
-void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* work) {
+// Rows of Fbot at the bottom positions i that hold a row pivoted down from level l (perm[Wp+i] < Wp):
+// the only rows where Fbot t_top differs from -diag(Lsub_{l+1}) y_l.  Up to 8 per level, in
+// position order, into exc[level][e][k] (row-major) and excpos[level][e] (-1 unused).
+__global__ void convert_exc_kernel(int Wp, const int32_t* perm, const double* Fb, int64_t w2, double* exc,
+                                   int32_t* excpos) {
+  const int64_t l = blockIdx.x;
+  const int32_t* p = perm + l * 2 * Wp;
+  __shared__ int pos[8];
+  __shared__ int cnt;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int i = 0; i < Wp && c < 8; i++)
+      if (p[Wp + i] < Wp) pos[c++] = i;
+    cnt = c;
+    for (int e = 0; e < 8; e++) excpos[l * 8 + e] = e < c ? pos[e] : -1;
+  }
+  __syncthreads();
+  const double* f = Fb + l * w2;
+  for (int idx = threadIdx.x; idx < cnt * Wp; idx += blockDim.x) {
+    const int e = idx / Wp, k = idx % Wp;
+    exc[(l * 8 + e) * Wp + k] = f[(int64_t)k * Wp + pos[e]];
+  }
+}
+
+void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* work,
+                    const int32_t* perm, double* exc, int32_t* excpos) {
   const int64_t w2 = (int64_t)Wp * Wp, sX = 3 * w2;
   double* X = work;
   double* Fb = work + nl * sX;
@@ -599,6 +625,7 @@ void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t
   trsm_small_batched(st, false, Wp, slots, Wp, lvl, X, Wp, sX, 3 * Wp, nl);
   convert_pack_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(4LL * Wp * Wp, 256), 64), (unsigned)nl), 256, 0, st>>>(
       Wp, X, sX, Fb, w2, slots, lvl); count_launch();
+  convert_exc_kernel<<<(unsigned)nl, 256, 0, st>>>(Wp, perm, Fb, w2, exc, excpos); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 

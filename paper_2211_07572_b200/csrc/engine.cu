@@ -225,6 +225,8 @@ struct slablu_gpu_fact {
   DBuf<uint8_t> u13;
   DBuf<uint8_t> lnd;    // Lsub off-diagonal flags per (strip, level)
   DBuf<double> dsub;    // diag(Lsub_{l+1}) per (strip, level)
+  DBuf<double> exc;     // exceptional Fbot rows per (strip, level): 8 x Wp
+  DBuf<int32_t> excpos; // their positions: 8 per (strip, level)
   DBuf<double> T;       // [diag k | super k-1 | sub k-1] blocks, n2 x n2; diag holds S_j^{-1}
   DBuf<double> Tkeep;   // optional copy of the reduced blocks
   DBuf<DevStatus> status;
@@ -386,6 +388,8 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   F->u13.alloc(dev, (size_t)S * n2);
   F->lnd.alloc(dev, (size_t)S * n2);
   F->dsub.alloc(dev, (size_t)S * n2 * Wp);
+  F->exc.alloc(dev, (size_t)S * n2 * 8 * Wp);
+  F->excpos.alloc(dev, (size_t)S * n2 * 8);
   SLB_CUDA_CHECK(cudaMemsetAsync(F->lnd.p, 0, F->lnd.bytes(), st));
   SLB_CUDA_CHECK(cudaMemsetAsync(F->dsub.p, 0, F->dsub.bytes(), st));
   {
@@ -421,7 +425,9 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     SLB_CUDA_CHECK(cudaEventRecord(chunk_ev, st));
     SLB_CUDA_CHECK(cudaStreamWaitEvent(cst, chunk_ev, 0));
     for (int s = 0; s < S; s++) {
-      convert_levels(cst, Wp, F->fac.p + s * F->sF + c0 * lvl, lvl, c1 - c0, cwork.p + (size_t)s * CCH * 4 * Wp * Wp);
+      convert_levels(cst, Wp, F->fac.p + s * F->sF + c0 * lvl, lvl, c1 - c0, cwork.p + (size_t)s * CCH * 4 * Wp * Wp,
+                     F->perm.p + s * F->sP + c0 * 2 * Wp, F->exc.p + ((size_t)s * n2 + c0) * 8 * Wp,
+                     F->excpos.p + ((size_t)s * n2 + c0) * 8);
     }
   };
   int cur = 0;
@@ -491,12 +497,16 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     if (getenv("SLB_U13_STATS")) {
       std::vector<uint8_t> h((size_t)S * n2);
       SLB_CUDA_CHECK(cudaMemcpy(h.data(), F->u13.p, h.size(), cudaMemcpyDeviceToHost));
-      int64_t ones = 0, pairs = 0;
+      int64_t ones = 0, pairs = 0, hist[16] = {0};
       for (int s = 0; s < S; s++)
         for (int64_t l = 0; l < n2; l++) {
           ones += h[s * n2 + l] & 1;
-          pairs += h[s * n2 + l] != 0 ? 1 : 0;
+          pairs += (h[s * n2 + l] & 3) != 0 ? 1 : 0;
+          hist[h[s * n2 + l] >> 2]++;
         }
+      fprintf(stderr, "[slablu] rows pivoted up per level:");
+      for (int i = 0; i < 16; i++) fprintf(stderr, " %d:%lld", i, (long long)hist[i]);
+      fprintf(stderr, "\n");
       fprintf(stderr, "[slablu] U13 != 0 on %lld of %lld levels; full forward operator needed on %lld\n", (long long)ones,
               (long long)(S * n2), (long long)pairs);
     }
@@ -560,6 +570,8 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     sa.u13 = F->u13.p;
     sa.dsub = F->dsub.p;
     sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
+    sa.exc = F->exc.p;
+    sa.excpos = F->excpos.p;
     sa.chunk = kSweepChunk;
     sa.gbuf = gbuf.p;
     sa.sG = sG;
@@ -710,6 +722,8 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   sa.u13 = F->u13.p;
     sa.dsub = F->dsub.p;
     sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
+    sa.exc = F->exc.p;
+    sa.excpos = F->excpos.p;
   sa.Wp = F->Wp;
   sa.n2 = n2;
   sa.nstrips = S;
@@ -828,6 +842,8 @@ struct StripSweeper {
     sa.u13 = F->u13.p;
     sa.dsub = F->dsub.p;
     sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
+    sa.exc = F->exc.p;
+    sa.excpos = F->excpos.p;
     sa.Wp = F->Wp;
     sa.n2 = n2;
     sa.nstrips = F->S;
@@ -1309,6 +1325,8 @@ slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* F, const double* 
     sa.chunk = kSweepChunk; sa.u13 = F->u13.p;
     sa.dsub = F->dsub.p;
     sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
+    sa.exc = F->exc.p;
+    sa.excpos = F->excpos.p;
     sa.Wp = F->Wp; sa.n2 = n2; sa.nstrips = F->S; sa.strips = F->strips.p; sa.fac = F->fac.p; sa.sF = F->sF;
     sa.perm = F->perm.p; sa.sP = F->sP; sa.cpl = F->cpl.p; sa.sCPL = F->sCPL; sa.sym = F->sym.p;
     sa.ybuf = ybuf.p; sa.sY = sY; sa.task_counter = counter.p; sa.ntasks = ntasks; sa.tasks = dtasks.p;

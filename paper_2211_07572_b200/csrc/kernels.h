@@ -89,7 +89,9 @@ struct LevelArgs {
 void level_lu(cudaStream_t st, const LevelArgs& a);
 // U1213 = L11^{-1} R1 and [S|V]_{l+1} = R2 - L21 U1213 in one launch (trsm.cu).
 void level_update(cudaStream_t st, const LevelArgs& a);
-void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* work);
+// perm: the chunk's first level (2 Wp per level); exc/excpos: that level's exceptional Fbot rows
+void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* work,
+                    const int32_t* perm, double* exc, int32_t* excpos);
 
 // ---- schur.cu --------------------------------------------------------------------
 struct SchurArgs {
@@ -106,7 +108,9 @@ struct SchurArgs {
   const int32_t* sym;     // per-strip symmetric flag
   const uint8_t* u13;     // per (strip, level) flags: bit 0 U13 != 0, bit 1 Lsub_{l+1} not diagonal
   const double* dsub;     // per (strip, level) diag(Lsub_{l+1}) (Wp), per strip stride n2 * Wp
-  int fsc;                // forward shortcut enabled (levels with flags == 0)
+  int fsc;                // forward shortcut enabled (Lsub diagonal, <= 8 rows pivoted up)
+  const double* exc;      // per (strip, level) up to 8 exceptional Fbot rows (8 x Wp), strip stride n2*8*Wp
+  const int32_t* excpos;  // their bottom positions (8 per level, -1 unused), strip stride n2*8
   double* gbuf;           // per strip 4 * n2 * n2 (row-major [X][Y][p][q])
   int64_t sG;
   double* ybuf;           // per CTA slot: n2 * Wp * C

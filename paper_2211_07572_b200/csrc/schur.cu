@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
       const double* src = p_src;
       const int len = p_len;
       // shortcut level (flags == 0): only the Ainv half of each k4 block of [Ainv ; Fbot]
-      const bool split = a.fsc && p_fwd && su13[p_lvl] == 0;
+      const bool split = a.fsc && p_fwd && (su13[p_lvl] & 2) == 0 && (su13[p_lvl] >> 2) <= 8;
       if (--p_left > 0) {
         p_src += p_len;
       } else if (p_fwd) {
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
       pcur ^= 1;
       // shortcut level: no level-(l+1) row pivoted up and Lsub_{l+1} diagonal, so
       // Fbot t_top = -diag(Lsub_{l+1}) y_l: stream Ainv only, all warps on its rows
-      const bool sc = a.fsc && su13[l] == 0;
+      const bool sc = a.fsc && (su13[l] & 2) == 0 && (su13[l] >> 2) <= 8;
 #ifdef SLB_SCHUR_PROF
       nsc += sc ? 1 : 0;
 #endif
@@ -354,8 +354,14 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
         }
       }
       if (sc) {
-        // z_{l+1}[i] = t_bot[i] - d_i y_l[i]: read every t_bot value (old z_l rows) first,
-        // then overwrite z in place after the barrier
+        // z_{l+1}[i] = t_bot[i] - d_i y_l[i], except at the (few) bottom positions holding a row
+        // pivoted down from level l, where z_{l+1}[i] = t_bot[i] + Fbot[i,:] t_top.  Every t_bot
+        // value (old z_l rows) is read first; z is overwritten in place after the barrier.
+        const int ncx = su13[l] >> 2;
+        const int ex = tid / C, en = tid % C;
+        const int64_t li = (int64_t)T.s * n2 + l;
+        const int expos = ex < ncx ? a.excpos[li * 8 + ex] : 0;
+        double exv = ex < ncx ? vval(sperm[Wp + expos], en) : 0.0;  // t_bot at the exceptional row
 #pragma unroll
         for (int mi = 0; mi < MTMAX; mi++) {
           const int mt = fm * fmt + mi;
@@ -381,6 +387,21 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
             zb[swz<C>(row, col)] = acc[mi][nj][0];
             zb[swz<C>(row, col + 1)] = acc[mi][nj][1];
           }
+        }
+        if (ncx > 0) {
+          if (ex < ncx) {  // + Fbot[i,:] t_top (t_top is intact until the next level's build)
+            const double* er = a.exc + (li * 8 + ex) * Wp;
+            double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+            for (int k = 0; k < Wp; k += 4) {
+              q0 = fma(er[k], tb[swz<C>(k, en)], q0);
+              q1 = fma(er[k + 1], tb[swz<C>(k + 1, en)], q1);
+              q2 = fma(er[k + 2], tb[swz<C>(k + 2, en)], q2);
+              q3 = fma(er[k + 3], tb[swz<C>(k + 3, en)], q3);
+            }
+            exv += (q0 + q1) + (q2 + q3);
+          }
+          __syncthreads();  // the generic rows above also wrote these positions
+          if (ex < ncx) zb[swz<C>(expos, en)] = exv;
         }
       }
     }
