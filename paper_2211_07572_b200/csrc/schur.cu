@@ -38,6 +38,9 @@ struct Lay {
   static constexpr int FWN = NT >= 2 ? 2 : 1;         // forward n groups (per half)
   static constexpr int FWM = 8 / FWN;                 // forward m groups (per half)
   static constexpr int FNT = NT / FWN;                // forward n tiles per warp
+  static constexpr int SWN = NT >= 4 ? 4 : NT;        // shortcut forward (Ainv rows only): n groups
+  static constexpr int SWM = 16 / SWN;                // ... m groups
+  static constexpr int SNT = NT / SWN;                // ... n tiles per warp
   static constexpr int BWN = NT >= 4 ? 4 : NT;        // backward n groups
   static constexpr int BWM = 16 / BWN;                // backward m groups
   static constexpr int BNT = NT / BWN;                // backward n tiles per warp
@@ -82,7 +85,6 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
   const int g = lane >> 2, t = lane & 3;
   const int MTH = Wp / 8;                       // m8 tiles per Wp rows
   const int FMT = (MTH + L::FWM - 1) / L::FWM;  // forward m tiles per warp
-  const int FMT2 = (MTH + 2 * L::FWM - 1) / (2 * L::FWM);  // ... when all warps take Ainv rows
   const int BMT = (MTH + L::BWM - 1) / L::BWM;  // backward m tiles per warp
   constexpr int SK = L::SK;
   const int fslice = 8 * SK * Wp;               // doubles per forward slice (SK k4 steps of [Ainv ; Fbot])
@@ -261,9 +263,12 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
 #ifdef SLB_SCHUR_PROF
       nsc += sc ? 1 : 0;
 #endif
+      // shortcut: all 16 warps on the MTH rows of Ainv, as SWM m groups x SWN n groups
       const int hf = sc ? 0 : half;
-      const int fm = sc ? warp / L::FWN : fwm;
-      const int fmt = sc ? FMT2 : FMT;
+      const int fm = sc ? warp / L::SWN : fwm;
+      const int fmt = sc ? (MTH + L::SWM - 1) / L::SWM : FMT;
+      const int fnb = sc ? (warp % L::SWN) * L::SNT : fwn * L::FNT;  // first n tile of this warp
+      const int fnn = sc ? L::SNT : L::FNT;                          // n tiles of this warp
       auto vval = [&](int src, int n) -> double {
         if (src < Wp) return zb[swz<C>(src, n)];
         if (!schur) return has_next ? rhs_val(l + 1, src - Wp, n) : 0.0;
@@ -314,21 +319,40 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
         issue();
         const double* A = acquire();
 #endif
+        if (sc) {  // Ainv rows only: SNT n tiles per warp
 #pragma unroll
-        for (int kk = 0; kk < SK; kk++) {
-          const int k = j * 4 * SK + kk * 4 + t;  // B row
-          double bf[L::FNT];
+          for (int kk = 0; kk < SK; kk++) {
+            const int k = j * 4 * SK + kk * 4 + t;  // B row
+            double bf[L::SNT];
 #pragma unroll
-          for (int nj = 0; nj < L::FNT; nj++) bf[nj] = tb[swz<C>(k, (fwn * L::FNT + nj) * 8 + g)];
-          const double* Ak = A + kk * (sc ? MTH : 2 * MTH) * 32 + hf * MTH * 32 + lane;
+            for (int nj = 0; nj < L::SNT; nj++) bf[nj] = tb[swz<C>(k, (fnb + nj) * 8 + g)];
+            const double* Ak = A + kk * MTH * 32 + lane;
 #pragma unroll
-          for (int mi = 0; mi < MTMAX; mi++) {
-            const int mt = fm * fmt + mi;
-            // warp-uniform exit, not a predicate: predicated-off DMMAs still occupy the pipe
-            if (mi >= fmt || mt >= MTH) break;
-            const double af = Ak[mt * 32];
+            for (int mi = 0; mi < MTMAX; mi++) {
+              const int mt = fm * fmt + mi;
+              if (mi >= fmt || mt >= MTH) break;  // warp-uniform exit (see below)
+              const double af = Ak[mt * 32];
 #pragma unroll
-            for (int nj = 0; nj < L::FNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
+              for (int nj = 0; nj < L::SNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < SK; kk++) {
+            const int k = j * 4 * SK + kk * 4 + t;  // B row
+            double bf[L::FNT];
+#pragma unroll
+            for (int nj = 0; nj < L::FNT; nj++) bf[nj] = tb[swz<C>(k, (fwn * L::FNT + nj) * 8 + g)];
+            const double* Ak = A + kk * (2 * MTH) * 32 + hf * MTH * 32 + lane;
+#pragma unroll
+            for (int mi = 0; mi < MTMAX; mi++) {
+              const int mt = fm * fmt + mi;
+              // warp-uniform exit, not a predicate: predicated-off DMMAs still occupy the pipe
+              if (mi >= fmt || mt >= MTH) break;
+              const double af = Ak[mt * 32];
+#pragma unroll
+              for (int nj = 0; nj < L::FNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
+            }
           }
         }
         release();
@@ -342,7 +366,8 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
         if (mi >= fmt || mt >= MTH) continue;
 #pragma unroll
         for (int nj = 0; nj < L::FNT; nj++) {
-          const int nt = fwn * L::FNT + nj;
+          if (nj >= fnn) break;
+          const int nt = fnb + nj;
           if (hf == 0) {
             double2* dst = reinterpret_cast<double2*>(ylev + ((int64_t)(mt * L::NT + nt) * 32 + lane) * 2);
             *dst = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
@@ -371,7 +396,8 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
           const double dd = dsl[row];
 #pragma unroll
           for (int nj = 0; nj < L::FNT; nj++) {
-            const int col = (fwn * L::FNT + nj) * 8 + 2 * t;
+            if (nj >= fnn) break;
+            const int col = (fnb + nj) * 8 + 2 * t;
             acc[mi][nj][0] = fma(-dd, acc[mi][nj][0], vval(src, col));
             acc[mi][nj][1] = fma(-dd, acc[mi][nj][1], vval(src, col + 1));
           }
@@ -383,7 +409,8 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
           if (mi >= fmt || mt >= MTH) continue;
 #pragma unroll
           for (int nj = 0; nj < L::FNT; nj++) {
-            const int row = mt * 8 + g, col = (fwn * L::FNT + nj) * 8 + 2 * t;
+            if (nj >= fnn) break;
+            const int row = mt * 8 + g, col = (fnb + nj) * 8 + 2 * t;
             zb[swz<C>(row, col)] = acc[mi][nj][0];
             zb[swz<C>(row, col + 1)] = acc[mi][nj][1];
           }
