@@ -394,14 +394,19 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
       const int nt_n = (Wp - kend) / 8;
       const double* u0 = rowp(kb + t);
       const double* u1 = rowp(kb + 4 + t);
-      for (int mi = warp; mi < mt_n; mi += nwarps) {
+      // units = (m tile, half of the n tiles): 2 mt_n units over the warps (whole rows per warp
+      // left a few warps with twice the work)
+      const int nh = (nt_n + 1) / 2;
+      for (int unit = warp; unit < 2 * mt_n; unit += nwarps) {
+        const int mi = unit >> 1;
+        const int nbeg = (unit & 1) * nh, nend = min(nt_n, nbeg + nh);
         const int p = kend + mi * 8 + g;
         const bool ok = p <= rlast;
         double* row = rowp(ok ? p : kend);
         const double a0 = ok ? -row[kb + t] : 0.0, a1 = ok ? -row[kb + 4 + t] : 0.0;
         // four n tiles per step: their loads issue together, the DMMA chains interleave
-        int ni = 0;
-        for (; ni + 4 <= nt_n; ni += 4) {
+        int ni = nbeg;
+        for (; ni + 4 <= nend; ni += 4) {
           double b0[4], b1[4], d0[4], d1[4];
 #pragma unroll
           for (int u = 0; u < 4; u++) {
@@ -425,7 +430,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
             }
           }
         }
-        for (; ni < nt_n; ni++) {
+        for (; ni < nend; ni++) {
           const int c0 = kend + ni * 8;
           const double b0 = u0[c0 + g], b1 = u1[c0 + g];
           double d0 = row[c0 + 2 * t], d1 = row[c0 + 2 * t + 1];
