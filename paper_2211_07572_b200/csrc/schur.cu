@@ -382,11 +382,15 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
         // z_{l+1}[i] = t_bot[i] - d_i y_l[i], except at the (few) bottom positions holding a row
         // pivoted down from level l, where z_{l+1}[i] = t_bot[i] + Fbot[i,:] t_top.  Every t_bot
         // value (old z_l rows) is read first; z is overwritten in place after the barrier.
-        const int ncx = su13[l] >> 2;
-        const int ex = tid / C, en = tid % C;
+        const int ncx = (su13[l] >> 2) & 15;
         const int64_t li = (int64_t)T.s * n2 + l;
-        const int expos = ex < ncx ? a.excpos[li * 8 + ex] : 0;
-        double exv = ex < ncx ? vval(sperm[Wp + expos], en) : 0.0;  // t_bot at the exceptional row
+        const int kn = tid >> 3, kp = tid & 7;  // exceptional rows: column kn, k-part kp of 8
+        double exv[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) {  // t_bot at the exceptional positions (old z rows)
+          exv[e] = 0.0;
+          if (e < ncx && kp == 0 && kn < C) exv[e] = vval(sperm[Wp + a.excpos[li * 8 + e]], kn);
+        }
 #pragma unroll
         for (int mi = 0; mi < MTMAX; mi++) {
           const int mt = fm * fmt + mi;
@@ -416,19 +420,29 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
           }
         }
         if (ncx > 0) {
-          if (ex < ncx) {  // + Fbot[i,:] t_top (t_top is intact until the next level's build)
-            const double* er = a.exc + (li * 8 + ex) * Wp;
-            double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
-            for (int k = 0; k < Wp; k += 4) {
-              q0 = fma(er[k], tb[swz<C>(k, en)], q0);
-              q1 = fma(er[k + 1], tb[swz<C>(k + 1, en)], q1);
-              q2 = fma(er[k + 2], tb[swz<C>(k + 2, en)], q2);
-              q3 = fma(er[k + 3], tb[swz<C>(k + 3, en)], q3);
+          // + Fbot[i,:] t_top (t_top is intact until the next level's build): every thread takes
+          // an eighth of the k range of one column, the parts meet through three shuffles
+#pragma unroll
+          for (int e = 0; e < 8; e++) {
+            if (e >= ncx) break;
+            double q = 0.0;
+            if (kn < C) {
+              const double* er = a.exc + (li * 8 + e) * Wp;
+              for (int k = kp; k < Wp; k += 8) q = fma(er[k], tb[swz<C>(k, kn)], q);
             }
-            exv += (q0 + q1) + (q2 + q3);
+            q += __shfl_xor_sync(0xffffffffu, q, 1);
+            q += __shfl_xor_sync(0xffffffffu, q, 2);
+            q += __shfl_xor_sync(0xffffffffu, q, 4);
+            exv[e] += q;
           }
           __syncthreads();  // the generic rows above also wrote these positions
-          if (ex < ncx) zb[swz<C>(expos, en)] = exv;
+          if (kp == 0 && kn < C) {
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+              if (e >= ncx) break;
+              zb[swz<C>(a.excpos[li * 8 + e], kn)] = exv[e];
+            }
+          }
         }
       }
     }
