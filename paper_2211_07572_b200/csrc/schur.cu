@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     for (int i = tid; i < Wp; i += THREADS) sdsub[i] = dsubg[T.l0 * Wp + i];
     int pcur = 0;
 #ifdef SLB_SCHUR_PROF
-    long long S0 = clock64(), sp[6] = {0, 0, 0, 0, 0, 0}, wacq = 0, nsc = 0;
+    long long S0 = clock64(), sp[6] = {0, 0, 0, 0, 0, 0}, wacq = 0, nsc = 0, ep[3] = {0, 0, 0};
 #define SP(k_) { const long long q_ = clock64(); sp[k_] += q_ - S0; S0 = q_; }
 #else
 #define SP(k_)
@@ -378,6 +378,9 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
           }
         }
       }
+#ifdef SLB_SCHUR_PROF
+      { const long long q_ = clock64(); ep[0] += q_ - S0; S0 = q_; }
+#endif
       if (sc) {
         // z_{l+1}[i] = t_bot[i] - d_i y_l[i], except at the (few) bottom positions holding a row
         // pivoted down from level l, where z_{l+1}[i] = t_bot[i] + Fbot[i,:] t_top.  Every t_bot
@@ -395,18 +398,25 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
         for (int mi = 0; mi < MTMAX; mi++) {
           const int mt = fm * fmt + mi;
           if (mi >= fmt || mt >= MTH) continue;
+          // unswapped bottom position i keeps level-(l+1) row i: t_bot[i] = b_{l+1}[i] (the
+          // exceptional positions are rewritten below)
           const int row = mt * 8 + g;
-          const int src = sperm[Wp + row];
           const double dd = dsl[row];
 #pragma unroll
           for (int nj = 0; nj < L::FNT; nj++) {
             if (nj >= fnn) break;
             const int col = (fnb + nj) * 8 + 2 * t;
-            acc[mi][nj][0] = fma(-dd, acc[mi][nj][0], vval(src, col));
-            acc[mi][nj][1] = fma(-dd, acc[mi][nj][1], vval(src, col + 1));
+            acc[mi][nj][0] = fma(-dd, acc[mi][nj][0], vval(Wp + row, col));
+            acc[mi][nj][1] = fma(-dd, acc[mi][nj][1], vval(Wp + row, col + 1));
           }
         }
+#ifdef SLB_SCHUR_PROF
+        { const long long q_ = clock64(); ep[1] += q_ - S0; S0 = q_; }
+#endif
         __syncthreads();
+#ifdef SLB_SCHUR_PROF
+        { const long long q_ = clock64(); ep[2] += q_ - S0; S0 = q_; }
+#endif
 #pragma unroll
         for (int mi = 0; mi < MTMAX; mi++) {
           const int mt = fm * fmt + mi;
@@ -449,8 +459,8 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
 
 #ifdef SLB_SCHUR_PROF
     if ((tid == 0 || tid == 160) && blockIdx.x == 0)
-      printf("SCHUR tid %d task %d levels %lld: topsync %lld build %lld presync %lld kloop %lld (issue %lld acquire-wait %lld) epi %lld shortcut-levels %lld\n",
-             tid, task, (long long)(n2 - T.l0), sp[0], sp[1], sp[2], sp[3], sp[5], wacq, sp[4], nsc);
+      printf("SCHUR tid %d task %d levels %lld: topsync %lld build %lld presync %lld kloop %lld (issue %lld acquire-wait %lld) epi %lld [ystore %lld zcomp %lld bar1 %lld] shortcut-levels %lld\n",
+             tid, task, (long long)(n2 - T.l0), sp[0], sp[1], sp[2], sp[3], sp[5], wacq, sp[4], ep[0], ep[1], ep[2], nsc);
 #endif
     // ---------------- backward sweep ----------------
     __syncthreads();
