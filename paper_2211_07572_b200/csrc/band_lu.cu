@@ -62,6 +62,8 @@ __global__ void extract_levels_kernel(CsrDev A, const StripDesc* strips, int64_t
         if (dy == -1) {
           if (cx == ix) dsub[((int64_t)s * n2 + L - 1) * Wp + ix] = v;
           else if (v != 0.0) lnd[(int64_t)s * n2 + L] = 1;
+        } else if (dy == 1 && cx != ix && v != 0.0) {
+          lnd[((int64_t)gridDim.y + s) * n2 + L] = 1;  // second plane: Usup_L not diagonal
         }
       } else if (sd.left >= 0 && c >= sd.left_off && c < sd.left_off + n2) {
         if (c - sd.left_off != L) raise(status, ERR_COUPLING_LEVEL);
@@ -475,7 +477,11 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
     // bits: 0 U13 != 0, 1 Lsub_{l+1} not diagonal, 2..5 rows of level l+1 pivoted up (15 = more)
     const int nup = __syncthreads_count(tid < Wp && perm[tid] >= Wp);
     const int nd = a.has_next ? a.lnd[s * a.sU13] : 0;
-    if (tid == 0) a.u13[s * a.sU13] = (uint8_t)((nup ? 1 : 0) | (nd ? 2 : 0) | (min(nup, 15) << 2));
+    const int ud = a.has_next ? a.lnd[(a.nstrips + s) * a.sU13] : 0;
+    // bit 6: Usup_{l+1} not diagonal (the x_{l+2} half of H is then not confined to the
+    // columns of the rows pivoted up)
+    if (tid == 0)
+      a.u13[s * a.sU13] = (uint8_t)((nup ? 1 : 0) | (nd ? 2 : 0) | (min(nup, 15) << 2) | (ud ? 64 : 0));
   }
   if (a.has_next) {
     for (int idx = tid; idx < Wp * Wp; idx += blockDim.x) {
@@ -618,8 +624,32 @@ __global__ void convert_exc_kernel(int Wp, const int32_t* perm, const double* Fb
   }
 }
 
+// The x_{l+2} half of H (columns 2Wp.. of [Ainv | H]) is nonzero only in the columns r of the
+// level-(l+1) rows pivoted up (Usup diagonal): up to 8 such columns per level into hcol[level][e][i]
+// with hidx[level][e] = r (-1 unused), in top-position order.
+__global__ void convert_hcol_kernel(int Wp, const int32_t* perm, const double* X, int64_t sX, double* hcol,
+                                    int32_t* hidx) {
+  const int64_t l = blockIdx.x;
+  const int32_t* p = perm + l * 2 * Wp;
+  __shared__ int cols[8];
+  __shared__ int cnt;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int i = 0; i < Wp && c < 8; i++)
+      if (p[i] >= Wp) cols[c++] = p[i] - Wp;
+    cnt = c;
+    for (int e = 0; e < 8; e++) hidx[l * 8 + e] = e < c ? cols[e] : -1;
+  }
+  __syncthreads();
+  const double* x = X + l * sX;
+  for (int idx = threadIdx.x; idx < cnt * Wp; idx += blockDim.x) {
+    const int e = idx / Wp, i = idx % Wp;
+    hcol[(l * 8 + e) * Wp + i] = x[(int64_t)(2 * Wp + cols[e]) * Wp + i];
+  }
+}
+
 void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* work,
-                    const int32_t* perm, double* exc, int32_t* excpos) {
+                    const int32_t* perm, double* exc, int32_t* excpos, double* hcol, int32_t* hidx) {
   const int64_t w2 = (int64_t)Wp * Wp, sX = 3 * w2;
   double* X = work;
   double* Fb = work + nl * sX;
@@ -631,6 +661,7 @@ void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t
   convert_pack_kernel<<<dim3((unsigned)std::min<int64_t>(cdiv(4LL * Wp * Wp, 256), 64), (unsigned)nl), 256, 0, st>>>(
       Wp, X, sX, Fb, w2, slots, lvl); count_launch();
   convert_exc_kernel<<<(unsigned)nl, 256, 0, st>>>(Wp, perm, Fb, w2, exc, excpos); count_launch();
+  convert_hcol_kernel<<<(unsigned)nl, 256, 0, st>>>(Wp, perm, X, sX, hcol, hidx); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -227,6 +227,8 @@ struct slablu_gpu_fact {
   DBuf<double> dsub;    // diag(Lsub_{l+1}) per (strip, level)
   DBuf<double> exc;     // exceptional Fbot rows per (strip, level): 8 x Wp
   DBuf<int32_t> excpos; // their positions: 8 per (strip, level)
+  DBuf<double> hcol;    // x_{l+2} columns of H per (strip, level): 8 x Wp
+  DBuf<int32_t> hidx;   // their column indices
   DBuf<double> T;       // [diag k | super k-1 | sub k-1] blocks, n2 x n2; diag holds S_j^{-1}
   DBuf<double> Tkeep;   // optional copy of the reduced blocks
   DBuf<DevStatus> status;
@@ -386,10 +388,12 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   F->cpl.alloc(dev, (size_t)S * F->sCPL);
   F->sym.alloc(dev, S);
   F->u13.alloc(dev, (size_t)S * n2);
-  F->lnd.alloc(dev, (size_t)S * n2);
+  F->lnd.alloc(dev, (size_t)2 * S * n2);  // planes: Lsub / Usup not diagonal
   F->dsub.alloc(dev, (size_t)S * n2 * Wp);
   F->exc.alloc(dev, (size_t)S * n2 * 8 * Wp);
   F->excpos.alloc(dev, (size_t)S * n2 * 8);
+  F->hcol.alloc(dev, (size_t)S * n2 * 8 * Wp);
+  F->hidx.alloc(dev, (size_t)S * n2 * 8);
   SLB_CUDA_CHECK(cudaMemsetAsync(F->lnd.p, 0, F->lnd.bytes(), st));
   SLB_CUDA_CHECK(cudaMemsetAsync(F->dsub.p, 0, F->dsub.bytes(), st));
   {
@@ -427,7 +431,8 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     for (int s = 0; s < S; s++) {
       convert_levels(cst, Wp, F->fac.p + s * F->sF + c0 * lvl, lvl, c1 - c0, cwork.p + (size_t)s * CCH * 4 * Wp * Wp,
                      F->perm.p + s * F->sP + c0 * 2 * Wp, F->exc.p + ((size_t)s * n2 + c0) * 8 * Wp,
-                     F->excpos.p + ((size_t)s * n2 + c0) * 8);
+                     F->excpos.p + ((size_t)s * n2 + c0) * 8, F->hcol.p + ((size_t)s * n2 + c0) * 8 * Wp,
+                     F->hidx.p + ((size_t)s * n2 + c0) * 8);
     }
   };
   int cur = 0;
@@ -572,6 +577,9 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
     sa.exc = F->exc.p;
     sa.excpos = F->excpos.p;
+    sa.bsc = getenv("SLB_NO_BSC") ? 0 : 1;  // backward shortcut (SLB_NO_BSC=1 disables, for A/B runs)
+    sa.hcol = F->hcol.p;
+    sa.hidx = F->hidx.p;
     sa.chunk = kSweepChunk;
     sa.gbuf = gbuf.p;
     sa.sG = sG;
@@ -724,6 +732,9 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
     sa.exc = F->exc.p;
     sa.excpos = F->excpos.p;
+    sa.bsc = getenv("SLB_NO_BSC") ? 0 : 1;  // backward shortcut (SLB_NO_BSC=1 disables, for A/B runs)
+    sa.hcol = F->hcol.p;
+    sa.hidx = F->hidx.p;
   sa.Wp = F->Wp;
   sa.n2 = n2;
   sa.nstrips = S;
@@ -844,6 +855,9 @@ struct StripSweeper {
     sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
     sa.exc = F->exc.p;
     sa.excpos = F->excpos.p;
+    sa.bsc = getenv("SLB_NO_BSC") ? 0 : 1;  // backward shortcut (SLB_NO_BSC=1 disables, for A/B runs)
+    sa.hcol = F->hcol.p;
+    sa.hidx = F->hidx.p;
     sa.Wp = F->Wp;
     sa.n2 = n2;
     sa.nstrips = F->S;
@@ -1327,6 +1341,9 @@ slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* F, const double* 
     sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
     sa.exc = F->exc.p;
     sa.excpos = F->excpos.p;
+    sa.bsc = getenv("SLB_NO_BSC") ? 0 : 1;  // backward shortcut (SLB_NO_BSC=1 disables, for A/B runs)
+    sa.hcol = F->hcol.p;
+    sa.hidx = F->hidx.p;
     sa.Wp = F->Wp; sa.n2 = n2; sa.nstrips = F->S; sa.strips = F->strips.p; sa.fac = F->fac.p; sa.sF = F->sF;
     sa.perm = F->perm.p; sa.sP = F->sP; sa.cpl = F->cpl.p; sa.sCPL = F->sCPL; sa.sym = F->sym.p;
     sa.ybuf = ybuf.p; sa.sY = sY; sa.task_counter = counter.p; sa.ntasks = ntasks; sa.tasks = dtasks.p;

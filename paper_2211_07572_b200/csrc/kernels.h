@@ -91,7 +91,7 @@ void level_lu(cudaStream_t st, const LevelArgs& a);
 void level_update(cudaStream_t st, const LevelArgs& a);
 // perm: the chunk's first level (2 Wp per level); exc/excpos: that level's exceptional Fbot rows
 void convert_levels(cudaStream_t st, int Wp, double* slots, int64_t lvl, int64_t nl, double* work,
-                    const int32_t* perm, double* exc, int32_t* excpos);
+                    const int32_t* perm, double* exc, int32_t* excpos, double* hcol, int32_t* hidx);
 
 // ---- schur.cu --------------------------------------------------------------------
 struct SchurArgs {
@@ -111,6 +111,9 @@ struct SchurArgs {
   int fsc;                // forward shortcut enabled (Lsub diagonal, <= 8 rows pivoted up)
   const double* exc;      // per (strip, level) up to 8 exceptional Fbot rows (8 x Wp), strip stride n2*8*Wp
   const int32_t* excpos;  // their bottom positions (8 per level, -1 unused), strip stride n2*8
+  int bsc;                // backward shortcut: x_{l+2} half of H applied as <= 8 columns
+  const double* hcol;     // per (strip, level) those columns (8 x Wp), strip stride n2*8*Wp
+  const int32_t* hidx;    // their indices (8 per level, -1 unused), strip stride n2*8
   double* gbuf;           // per strip 4 * n2 * n2 (row-major [X][Y][p][q])
   int64_t sG;
   double* ybuf;           // per CTA slot: n2 * Wp * C

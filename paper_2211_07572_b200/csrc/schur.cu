@@ -150,6 +150,11 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     int p_len = fslice, p_left = kf;
     int64_t p_lvl = T.l0;
     bool p_fwd = true, p_done = false;
+    // backward level streams the full H (kb slices) only if U13 != 0 and its x_{l+2} half cannot
+    // be applied as the few columns of the rows pivoted up (Usup not diagonal or > 8 such rows)
+    auto bwd_full = [&](uint8_t f) -> bool {
+      return (f & 1) && !(a.bsc && !(f & 64) && ((f >> 2) & 15) <= 8);
+    };
     auto issue = [&]() {
       if (tid != 0 || p_done) return;
       const double* src = p_src;
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
           } else {
             p_src = fac + p_lvl * lvl_stride + 2LL * Wp * Wp;
             p_len = bslice;
-            p_left = (su13[p_lvl] & 1) ? kb : kb / 2;
+            p_left = bwd_full(su13[p_lvl]) ? kb : kb / 2;
           }
         } else {
           p_src += p_len + (lvl_stride - (int64_t)kf * fslice);
@@ -178,7 +183,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
           p_done = true;
         } else {
           p_src = fac + p_lvl * lvl_stride + 2LL * Wp * Wp;
-          p_left = (su13[p_lvl] & 1) ? kb : kb / 2;
+          p_left = bwd_full(su13[p_lvl]) ? kb : kb / 2;
         }
       }
       const int sl = p_slot;
@@ -471,7 +476,9 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     int p_buf = 0;                    // buffer holding x_{l+1}; the other holds x_{l+2}
     for (int64_t l = n2 - 1; l >= T.lstop; l--) {
       const double* ylev = ybase + (l - T.l0) * (int64_t)Wp * C;
-      const int kbl = (su13[l] & 1) ? kb : kb / 2;  // U13 = 0: x_{l+2} does not enter
+      const uint8_t fl = su13[l];
+      const int kbl = bwd_full(fl) ? kb : kb / 2;  // else x_{l+2} enters through <= 8 columns of H
+      const int nhc = ((fl & 1) && !bwd_full(fl)) ? ((fl >> 2) & 15) : 0;
       double acc[MTMAX][L::BNT][2];
 #pragma unroll
       for (int mi = 0; mi < MTMAX; mi++) {
@@ -512,6 +519,27 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
           }
         }
         release();
+      }
+      if (nhc > 0) {  // acc (= -x) += H[:, r] x_{l+2}[r, :] for the columns r of the rows pivoted up
+        const int64_t li = (int64_t)T.s * n2 + l;
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+          if (e >= nhc) break;
+          const int r = a.hidx[li * 8 + e];
+          const double* hc = a.hcol + (li * 8 + e) * Wp;
+#pragma unroll
+          for (int mi = 0; mi < MTMAX; mi++) {
+            const int mt = bwm * BMT + mi;
+            if (mi >= BMT || mt >= MTH) break;
+            const double hv = hc[mt * 8 + g];
+#pragma unroll
+            for (int nj = 0; nj < L::BNT; nj++) {
+              const int col = (bwn * L::BNT + nj) * 8 + 2 * t;
+              acc[mi][nj][0] = fma(hv, xq[swz<C>(r, col)], acc[mi][nj][0]);
+              acc[mi][nj][1] = fma(hv, xq[swz<C>(r, col + 1)], acc[mi][nj][1]);
+            }
+          }
+        }
       }
       __syncthreads();  // everyone done reading x_{l+2}
       double* xo = sm + (1 - p_buf) * Wp * C;  // x_l overwrites x_{l+2}

@@ -240,3 +240,21 @@ def test_forward_shortcut_matches_full_operator(monkeypatch):
         assert relerr(fa.T_block("diag", j), fb.T_block("diag", j)) < 1e-12
     ua, ub = S.solve(fa, sys_g.rhs), S.solve(fb, sys_g.rhs)
     assert relerr(ua, ub) < 1e-12
+
+
+def test_backward_columns_match_full_operator(monkeypatch):
+    """U13 != 0 levels stream only the x_{l+1} half of H and apply the x_{l+2} half through the
+    few columns of the rows pivoted up (Usup diagonal); the explicit H must give the same blocks."""
+    n1, n2, b, kappa = 96, 64, 11, 50.0
+    sys_g = S.assemble_fd5(S.helmholtz_bump_problem(n1, n2, kappa))
+    f = np.column_stack([sys_g.rhs] + [S.gaussian_matrix(sys_g.dim(), 1, 5 + c)[:, 0] for c in range(11)])
+    fa = S.factorize(sys_g, S.SolverConfig(b=b, keep_T=True))
+    ua = S.solve(fa, f)  # 12 RHS: the 64-column sweep kernel
+    monkeypatch.setenv("SLB_NO_BSC", "1")
+    fb = S.factorize(sys_g, S.SolverConfig(b=b, keep_T=True))
+    ub = S.solve(fb, f)
+    for j in range(fa.stats.interfaces):
+        assert relerr(fa.T_block("diag", j), fb.T_block("diag", j)) < 1e-12
+        if j + 1 < fa.stats.interfaces:
+            assert relerr(fa.T_block("super", j), fb.T_block("super", j)) < 1e-12
+    assert relerr(ua, ub) < 1e-12
