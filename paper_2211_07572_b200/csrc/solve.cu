@@ -59,6 +59,9 @@ __host__ __device__ inline SolveLay solve_lay(int Wp, int64_t n2) {
   return L;
 }
 
+// backward level needs the full H (kb slices): U13 != 0 and not representable as <= 8 columns
+__device__ __forceinline__ bool bwd_full(uint8_t f, int bsc) { return (f & 1) && !(bsc && !(f & 64) && ((f >> 2) & 15) <= 8); }
+
 __device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release;\n" ::: "memory"); }
 // Level barrier for shared-memory-only exchange: the CTA-scope fence performs this CTA's shared
 // stores before the relaxed arrive, so peers reading them after the wait observe them.
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
         ls = 0;
         lph ^= 1u;
       }
-      const int nsl = fwd ? kf : ((su13[l] & 1) ? kb : kb / 2);
+      const int nsl = fwd ? kf : (bwd_full(su13[l], a.bsc) ? kb : kb / 2);
       const double* base = fac + l * lvl + (fwd ? 0 : 2LL * Wp * Wp);
       for (int j = 0; j < nsl; j++) {
         QS()
@@ -389,7 +392,9 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
   consumer_bar();
   int i1 = 1, i2 = 2, i0 = 0;  // x_{l+1} in xb[i1], x_{l+2} in xb[i2], x_l written into xb[i0]
   for (int64_t l = n2 - 1; l >= 0; l--) {
-    const int kbl = (su13[l] & 1) ? kb : kb / 2;
+    const uint8_t fl = su13[l];
+    const int kbl = bwd_full(fl, a.bsc) ? kb : kb / 2;
+    const int nhc = ((fl & 1) && !bwd_full(fl, a.bsc)) ? ((fl >> 2) & 15) : 0;
     const double* x1 = xb + i1 * WC;
     const double* x2 = xb + i2 * WC;
     double* x0 = xb + i0 * WC;
@@ -432,6 +437,20 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
       if (++slot == STAGES) {
         slot = 0;
         fph ^= 1u;
+      }
+    }
+    if (nhc > 0) {  // x_{l+2} half of H: the columns of the rows pivoted up (schur.cu)
+      const int64_t li = (int64_t)s * n2 + l;
+      for (int e = 0; e < nhc; e++) {
+        const int r = a.hidx[li * 8 + e];
+        const double* hc = a.hcol + (li * 8 + e) * Wp;
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+          if (lts[u] < 0) continue;
+          const double hv = hc[(bm0 + lts[u]) * 8 + g];
+          acc[u][0] = fma(hv, x2[r * C + 2 * t], acc[u][0]);
+          acc[u][1] = fma(hv, x2[r * C + 2 * t + 1], acc[u][1]);
+        }
       }
     }
 #pragma unroll
