@@ -21,6 +21,8 @@
 // used by the Schur kernel (schur.cu) and the solves (solve.cu).
 #include <climits>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -497,6 +499,308 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   }
 }
 
+// Look-ahead form of level_lu_kernel (same arithmetic and outputs).  Per 8-column block kb:
+//   X  trailing update of block kb on the next panel's 8 columns (all warps)
+//   Y  warps 0-3 factor panel kb+8 (its entering rows read from the staging buffer) while
+//      warps 4-15 finish the trailing update of block kb on the remaining columns
+//   R  rows kb..kb+7 retire to LU11, the entering rows take their physical rows
+//   S  panel kb+8's interchanges on the other columns;  U  its U block
+// so the serial pivot search of panel kb+8 runs beside the DMMA update of block kb.
+__global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
+  extern __shared__ double smem[];
+  const int Wp = a.Wp, NW = Wp + 8;
+  const int RS = ((Wp + 15) / 16) * 16 + 4;
+  double* win = smem;
+  double* pcand = win + NW * RS;  // [2][4] values, [2][4] positions, [2][8] pivot rows
+  double* ent = pcand + 32;       // [2][8 x Wp] entering rows
+  int* perm = reinterpret_cast<int*>(ent + 16 * Wp);
+  __shared__ int s_sing;
+  __shared__ int s_piv[8];
+  constexpr int PW = 4, NT = PW * 32, RPL = 2;
+
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const double* SV = a.sv_in + s * a.sSV;
+  const double* NX = a.has_next ? a.nx + s * a.sNX : nullptr;
+  double* slot = a.slot + s * a.sF;
+  double* LU11 = slot;
+  double* L21 = slot + (int64_t)Wp * Wp;
+  const int rows_total = a.has_next ? 2 * Wp : Wp;
+  auto rowp = [&](int pos) -> double* { return win + (pos < NW ? pos : pos - NW) * RS; };
+  auto Pval = [&](int p, int j) -> double {
+    return p < Wp ? SV[(int64_t)j * Wp + p] : NX[(int64_t)j * Wp + (p - Wp)];
+  };
+  if (tid == 0) s_sing = 0;
+  const int init_rows = rows_total < NW ? rows_total : NW;
+  for (int idx = tid; idx < init_rows * Wp; idx += blockDim.x) {
+    const int j = idx / init_rows, p = idx % init_rows;
+    rowp(p)[j] = Pval(p, j);
+  }
+  for (int p = tid; p < 2 * Wp; p += blockDim.x) perm[p] = p;
+
+  auto prefetch = [&](int kb_in, int buf) {  // rows entering at positions kb_in + Wp + q
+    for (int idx = tid; idx < 8 * Wp; idx += blockDim.x) {
+      const int q = idx / Wp, j = idx % Wp;
+      const int pe = kb_in + Wp + q;
+      if (pe < rows_total) cp_async8(ent + buf * 8 * Wp + idx, NX + (int64_t)j * Wp + (pe - Wp), true);
+    }
+    cp_async_commit();
+  };
+  // panel [kb, kb+8) on warps 0..PW-1; rows at positions >= kb + Wp live in entp (if given)
+  auto panel = [&](int kb, double* entp) {
+    const int pt = tid;
+    const int rlast = min(kb + 7 + Wp, rows_total - 1);
+    auto rowsrc = [&](int P) -> double* { return (entp && P >= kb + Wp) ? entp + (P - kb - Wp) * Wp : rowp(P); };
+    double v[RPL][8];
+    int pos[RPL];
+#pragma unroll
+    for (int i = 0; i < RPL; i++) {
+      pos[i] = kb + pt + NT * i;
+      if (pos[i] <= rlast) {
+        const double* row = rowsrc(pos[i]);
+#pragma unroll
+        for (int q = 0; q < 8; q++) v[i][q] = row[kb + q];
+      } else {
+        pos[i] = 0x3fffffff;
+#pragma unroll
+        for (int q = 0; q < 8; q++) v[i][q] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int c = kb + q, par = q & 1;
+      const int hi = min(c + Wp, rows_total - 1);
+      double best = 0.0;
+      int bpos = 0x7fffffff;
+#pragma unroll
+      for (int i = 0; i < RPL; i++) {
+        const double av = fabs(v[i][q]);
+        if (pos[i] >= c && pos[i] <= hi && (av > best || (av == best && pos[i] < bpos))) {
+          best = av;
+          bpos = pos[i];
+        }
+      }
+      const unsigned long long key = (unsigned long long)__double_as_longlong(best);
+      const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+      const unsigned mhi = __reduce_max_sync(0xffffffffu, khi);
+      const unsigned mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
+      const bool ismax = khi == mhi && klo == mlo;
+      const int rw = (int)__reduce_min_sync(0xffffffffu, ismax ? (unsigned)bpos : 0x7fffffffu);
+      const double mx = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+      if (lane == 0) {
+        pcand[par * 4 + warp] = mx;
+        pcand[8 + par * 4 + warp] = (double)rw;
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
+      double gm = pcand[par * 4];
+      int r = (int)pcand[8 + par * 4];
+#pragma unroll
+      for (int w2 = 1; w2 < PW; w2++) {
+        const double cv = pcand[par * 4 + w2];
+        const int cr = (int)pcand[8 + par * 4 + w2];
+        if (cv > gm || (cv == gm && cr < r)) {
+          gm = cv;
+          r = cr;
+        }
+      }
+      if (!(gm > 0.0)) {
+        r = c;
+        if (pt == 0) s_sing = 1;
+      }
+#pragma unroll
+      for (int i = 0; i < RPL; i++)
+        if (pos[i] == r)
+#pragma unroll
+          for (int qq = 0; qq < 8; qq++) pcand[16 + par * 8 + qq] = v[i][qq];
+#pragma unroll
+      for (int i = 0; i < RPL; i++) {
+        if (pos[i] == r) pos[i] = c;
+        else if (pos[i] == c) pos[i] = r;
+      }
+      if (pt == 0) s_piv[q] = r;
+      asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
+      double pr[8];
+#pragma unroll
+      for (int qq = 0; qq < 8; qq++) pr[qq] = pcand[16 + par * 8 + qq];
+      const double inv = pr[q] != 0.0 ? __drcp_rn(pr[q]) : 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; i++) {
+        if (pos[i] > c && pos[i] <= hi) {
+          const double m = v[i][q] * inv;
+          v[i][q] = m;
+#pragma unroll
+          for (int qq = q + 1; qq < 8; qq++) v[i][qq] = fma(-m, pr[qq], v[i][qq]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RPL; i++) {
+      if (pos[i] <= rlast) {
+        double* row = rowsrc(pos[i]);
+#pragma unroll
+        for (int q = 0; q < 8; q++) row[kb + q] = v[i][q];
+      }
+    }
+  };
+  auto swaps = [&](int kb) {  // panel kb's interchanges on the other columns; pivot-order bookkeeping
+    if (tid == blockDim.x - 1)
+      for (int q = 0; q < 8; q++) {
+        const int c = kb + q, r = s_piv[q];
+        if (r != c) {
+          const int tp = perm[c];
+          perm[c] = perm[r];
+          perm[r] = tp;
+        }
+      }
+    for (int jj = tid; jj < Wp - 8; jj += blockDim.x) {
+      const int col = jj < kb ? jj : jj + 8;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const int c = kb + q, r = s_piv[q];
+        if (r != c) {
+          double* rc = rowp(c);
+          double* rr = rowp(r);
+          const double tv = rc[col];
+          rc[col] = rr[col];
+          rr[col] = tv;
+        }
+      }
+    }
+  };
+  auto ublock = [&](int kb) {
+    for (int j = kb + 8 + tid; j < Wp; j += blockDim.x) {
+      double u[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++) u[q] = rowp(kb + q)[j];
+#pragma unroll
+      for (int q = 1; q < 8; q++) {
+        const double* lq = rowp(kb + q);
+#pragma unroll
+        for (int p = 0; p < 8; p++)
+          if (p < q) u[q] = fma(-lq[kb + p], u[p], u[q]);
+      }
+#pragma unroll
+      for (int q = 1; q < 8; q++) rowp(kb + q)[j] = u[q];
+    }
+  };
+  // rank-8 update of block kb on columns [c0, c1), rows kb+8..kb+7+Wp, by warps w0, w0+1, ...
+  auto trailing = [&](int kb, int c0, int c1, int w0, int nw) {
+    if (c1 <= c0 || warp < w0) return;
+    const int kend = kb + 8;
+    const int rlast = min(kb + 7 + Wp, rows_total - 1);
+    const int mt_n = (rlast - kend + 1 + 7) / 8;
+    const int nt_n = (c1 - c0) / 8;
+    const double* u0 = rowp(kb + t);
+    const double* u1 = rowp(kb + 4 + t);
+    const int nh = (nt_n + 1) / 2;
+    for (int unit = warp - w0; unit < 2 * mt_n; unit += nw) {
+      const int mi = unit >> 1;
+      const int nbeg = (unit & 1) * nh, nend = min(nt_n, nbeg + nh);
+      const int p = kend + mi * 8 + g;
+      const bool ok = p <= rlast;
+      double* row = rowp(ok ? p : kend);
+      const double a0 = ok ? -row[kb + t] : 0.0, a1 = ok ? -row[kb + 4 + t] : 0.0;
+      int ni = nbeg;
+      for (; ni + 4 <= nend; ni += 4) {
+        double b0[4], b1[4], d0[4], d1[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int cc = c0 + (ni + u) * 8;
+          b0[u] = u0[cc + g];
+          b1[u] = u1[cc + g];
+          d0[u] = row[cc + 2 * t];
+          d1[u] = row[cc + 2 * t + 1];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          dmma884(d0[u], d1[u], a0, b0[u]);
+          dmma884(d0[u], d1[u], a1, b1[u]);
+        }
+        if (ok) {
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int cc = c0 + (ni + u) * 8;
+            row[cc + 2 * t] = d0[u];
+            row[cc + 2 * t + 1] = d1[u];
+          }
+        }
+      }
+      for (; ni < nend; ni++) {
+        const int cc = c0 + ni * 8;
+        const double b0 = u0[cc + g], b1 = u1[cc + g];
+        double d0 = row[cc + 2 * t], d1 = row[cc + 2 * t + 1];
+        dmma884(d0, d1, a0, b0);
+        dmma884(d0, d1, a1, b1);
+        if (ok) {
+          row[cc + 2 * t] = d0;
+          row[cc + 2 * t + 1] = d1;
+        }
+      }
+    }
+  };
+
+  if (8 < Wp) prefetch(8, 0);
+  __syncthreads();
+  if (warp < PW) panel(0, nullptr);  // block 0: every row is in the window
+  __syncthreads();
+  swaps(0);
+  __syncthreads();
+  ublock(0);
+  __syncthreads();
+  int eb = 0;
+  for (int kb = 0; kb < Wp; kb += 8) {
+    const int kend = kb + 8;
+    const bool more = kend < Wp;
+    if (more) trailing(kb, kend, kend + 8, 0, nwarps);  // X
+    cp_async_wait<0>();
+    __syncthreads();
+    if (warp < PW) {  // Y
+      if (more) panel(kend, ent + eb * 8 * Wp);
+    } else {
+      trailing(kb, more ? kend + 8 : kend, Wp, PW, nwarps - PW);
+    }
+    __syncthreads();
+    for (int idx = tid; idx < 8 * Wp; idx += blockDim.x) {  // R
+      const int q = idx / Wp, j = idx % Wp;
+      double* rr = rowp(kb + q);
+      LU11[(int64_t)(kb + q) * Wp + j] = rr[j];
+      if (kend + Wp + q < rows_total) rr[j] = ent[eb * 8 * Wp + idx];
+    }
+    __syncthreads();
+    if (more) {
+      if (kend + 8 < Wp) prefetch(kend + 8, eb ^ 1);
+      swaps(kend);  // S
+      __syncthreads();
+      ublock(kend);  // U
+      __syncthreads();
+    }
+    eb ^= 1;
+  }
+
+  int32_t* perm_out = a.perm + s * a.sP;
+  for (int p = tid; p < 2 * Wp; p += blockDim.x) perm_out[p] = perm[p];
+  {
+    const int nup = __syncthreads_count(tid < Wp && perm[tid] >= Wp);
+    const int nd = a.has_next ? a.lnd[s * a.sU13] : 0;
+    const int ud = a.has_next ? a.lnd[(a.nstrips + s) * a.sU13] : 0;
+    if (tid == 0)
+      a.u13[s * a.sU13] = (uint8_t)((nup ? 1 : 0) | (nd ? 2 : 0) | (min(nup, 15) << 2) | (ud ? 64 : 0));
+  }
+  if (a.has_next) {
+    for (int idx = tid; idx < Wp * Wp; idx += blockDim.x) {
+      const int i = idx / Wp, j = idx % Wp;
+      L21[idx] = rowp(Wp + i)[j];
+    }
+  } else {
+    for (int idx = tid; idx < 3 * Wp * Wp; idx += blockDim.x) L21[idx] = 0.0;  // L21 and U1213
+  }
+  if (tid == 0 && s_sing) {
+    atomicOr(&a.status->flags, ERR_SINGULAR);
+    atomicMin(&a.status->singular_strip, s);
+  }
+}
+
 // R = perm_l [V_l 0 ; D_{l+1} Usup_{l+1}]: R1 -> U1213 slot, R2 -> sv_out.
 __global__ void gather_r_kernel(LevelArgs a) {
   const int s = blockIdx.y, Wp = a.Wp;
@@ -591,7 +895,18 @@ void level_lu(cudaStream_t st, const LevelArgs& a) {
     attr = smem;
   }
   // 4 panel warps: measured faster than one warp with 5 rows per lane (register pressure)
-  level_lu_kernel<4><<<a.nstrips, 512, smem, st>>>(a); count_launch();
+  static const bool no_la = getenv("SLB_LU_NOLA") != nullptr;
+  if (no_la) {
+    level_lu_kernel<4><<<a.nstrips, 512, smem, st>>>(a); count_launch();
+  } else {
+    const size_t smem2 = (size_t)((Wp + 8) * RS + 32 + 16 * Wp) * sizeof(double) + 2 * Wp * sizeof(int);
+    static size_t attr2 = 0;
+    if (smem2 > attr2) {
+      SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_la_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      attr2 = smem2;
+    }
+    level_lu_la_kernel<<<a.nstrips, 512, smem2, st>>>(a); count_launch();
+  }
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
