@@ -75,8 +75,11 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
   __shared__ int s_ci[2];
   __shared__ double s_crow[2][PNB];  // this CTA's candidate row
   __shared__ double s_krow[2][PNB];  // row k (owner CTA only)
-  __shared__ double s_prow[NW][PNB];  // per-warp copies of the pivot row
-  __shared__ double s_kloc[NW][PNB];  // per-warp copies of row k
+  // pushed by every CTA of the cluster before the barrier (so the resolve reads only local memory)
+  __shared__ double s_allv[2][16];
+  __shared__ int s_alli[2][16];
+  __shared__ double s_allrow[2][16][PNB];  // candidate rows of all CTAs
+  __shared__ double s_allk[2][PNB];        // row k
 
   double r[PNB];
 #pragma unroll
@@ -123,14 +126,27 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
     if (own && i == k)
 #pragma unroll
       for (int c = 0; c < PNB; c++) s_krow[pb][c] = r[c];
-    panel_cluster_barrier<RELAXED>();
+    __syncthreads();
+    // push candidate (value, row index, row) and row k into every CTA of the cluster
+    if (warp == 0) {
+      const double cr = s_crow[pb][lane];  // PNB == 32 == warp size
+      for (int r2 = 0; r2 < ncta; r2++) dsmem_st_f64(dsmem_map(&s_allrow[pb][rank][lane], r2), cr);
+      if (lane < ncta) {
+        dsmem_st_f64(dsmem_map(&s_allv[pb][rank], lane), s_cv[pb]);
+        dsmem_st_s32(dsmem_map(&s_alli[pb][rank], lane), s_ci[pb]);
+      }
+    } else if (warp == 1 && k / PTHREADS == rank) {
+      const double kr = s_krow[pb][lane];
+      for (int r2 = 0; r2 < ncta; r2++) dsmem_st_f64(dsmem_map(&s_allk[pb][lane], r2), kr);
+    }
+    panel_cluster_barrier<false>();  // release / acquire: the pushed data is visible after it
     PP(1)
-    // (3) every warp resolves the same pivot and copies both rows into its own slot
+    // (3) every warp resolves the same pivot from local copies
     double bv = -1.0;
     int bi = INT_MAX, bc = 0;
     if (lane < ncta) {
-      bv = dsmem_ld_f64(dsmem_map(&s_cv[pb], lane));
-      bi = dsmem_ld_s32(dsmem_map(&s_ci[pb], lane));
+      bv = s_allv[pb][lane];
+      bi = s_alli[pb][lane];
       bc = lane;
     }
 #pragma unroll
@@ -155,18 +171,12 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
         atomicMin(&status->singular_block, block_index);
       }
     }
-    const uint32_t krow = dsmem_map(&s_krow[pb][lane], k / PTHREADS);  // PNB == 32 == warp size
-    const uint32_t prow_addr = (bi == k) ? krow : dsmem_map(&s_crow[pb][lane], bc);
-    const double pval = dsmem_ld_f64(prow_addr), kval = dsmem_ld_f64(krow);
-    s_prow[warp][lane] = pval;
-    s_kloc[warp][lane] = kval;
     if (tid == 0 && rank == 0) ipiv[j + k] = (int32_t)(j + bi);
-    __syncwarp();
     PP(2)
     const int p = bi;
-    const double* prow = s_prow[warp];
+    const double* prow = (bi == k) ? s_allk[pb] : s_allrow[pb][bc];
     if (p != k) {
-      const double* src_row = (own && i == k) ? prow : s_kloc[warp];
+      const double* src_row = (own && i == k) ? prow : s_allk[pb];
       if (own && (i == k || i == p)) {
 #pragma unroll
         for (int c = 0; c < PNB; c++) r[c] = src_row[c];
