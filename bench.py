@@ -38,7 +38,7 @@ CONFIGS = {
     "cfg4": (1, 2000, 2000, 100, 10.0, "5-point FD Helmholtz 2000x2000 (rectangle stand-in), 10 ppw, b=100, 64 RHS"),
 }
 # DRAM bytes of one Schur-sweep launch (ncu --set full capture, profiles/ncu_schur_cfg3_r01.txt)
-SCHUR_DRAM_BYTES = {"cfg3": 2.367801e12 + 0.521072e12}
+SCHUR_DRAM_BYTES = {"cfg3": 1.833542e12 + 0.521007e12}
 FP64_PEAK_TFLOPS = 37.067  # measured DMMA peak on this pool's B200 (profiles/fp64_peak_r01.json)
 
 
