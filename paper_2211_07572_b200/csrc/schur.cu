@@ -476,6 +476,11 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     int p_buf = 0;                    // buffer holding x_{l+1}; the other holds x_{l+2}
     for (int64_t l = n2 - 1; l >= T.lstop; l--) {
       const double* ylev = ybase + (l - T.l0) * (int64_t)Wp * C;
+      if (l - 1 >= T.lstop) {  // y_{l-1} was written long ago (HBM): pull it into L2 one level ahead
+        const char* yn = reinterpret_cast<const char*>(ylev - (int64_t)Wp * C);
+        for (int off = tid * 128; off < Wp * C * 8; off += THREADS * 128)
+          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(yn + off));
+      }
       const uint8_t fl = su13[l];
       const int kbl = bwd_full(fl) ? kb : kb / 2;  // else x_{l+2} enters through <= 8 columns of H
       const int nhc = ((fl & 1) && !bwd_full(fl)) ? ((fl >> 2) & 15) : 0;
