@@ -9,6 +9,7 @@
 //   SolverConfig, CompressionChoice, choose_b      driver.hpp:37-66
 //   GridStrip, SlabPartition, partition            partition.hpp:27-91
 //   Factorization, factorize, solve                driver.hpp:72-179
+//   Shard (multi-GPU split, engine extension)      include/slablu_gpu.h slablu_gpu_shard_*
 //
 // Matrices are column major std::vector<double> (the reference uses
 // Eigen::MatrixXd, also column major; INTEGRATION.md shows the Eigen shim).
@@ -257,6 +258,37 @@ inline std::vector<double> solve(const Factorization& fact, const std::vector<do
   detail::check(slablu_gpu_solve(fact.handle(), f.data(), n, nrhs, u.data(), n));
   return u;
 }
+
+// ---- multi-GPU shards (no reference counterpart) -------------------
+// One process per GPU.  All pointers are device memory of the shard's device; the caller moves
+// the n2 x n2 (sweep) and n2 x nrhs (solve) messages between neighbouring ranks, e.g. with
+// ncclSend/ncclRecv, in the order: sweep (r-1 -> r), solve_forward (r-1 -> r),
+// solve_backward (r+1 -> r).
+class Shard {
+ public:
+  Shard(int64_t n1, int64_t n2, int64_t nnz, const int32_t* d_row_ptr, const int32_t* d_col_idx,
+        const double* d_val, const SolverConfig& config, int rank, int nranks) {
+    const slablu_gpu_config c = config.c_config();
+    slablu_gpu_fact* raw = nullptr;
+    detail::check(slablu_gpu_shard_factorize_device(n1, n2, nnz, d_row_ptr, d_col_idx, d_val, &c, rank, nranks, &raw));
+    h_.reset(raw, [](slablu_gpu_fact* f) { slablu_gpu_destroy(f); });
+    slablu_gpu_stats_t st{};
+    detail::check(slablu_gpu_stats(raw, &st));
+    detail::check(slablu_gpu_shard_plan(n1, n2, st.b, rank, nranks, &plan_));
+  }
+  const slablu_gpu_shard_t& plan() const { return plan_; }
+  void sweep(const double* d_in, double* d_out) { detail::check(slablu_gpu_shard_sweep(h_.get(), d_in, d_out)); }
+  void solve_forward(const double* d_f, int64_t ldf, int64_t nrhs, const double* d_in, double* d_out) {
+    detail::check(slablu_gpu_shard_solve_forward(h_.get(), d_f, ldf, nrhs, d_in, d_out));
+  }
+  void solve_backward(const double* d_in, double* d_out, double* d_u, int64_t ldu) {
+    detail::check(slablu_gpu_shard_solve_backward(h_.get(), d_in, d_out, d_u, ldu));
+  }
+
+ private:
+  std::shared_ptr<slablu_gpu_fact> h_;
+  slablu_gpu_shard_t plan_{};
+};
 
 }  // namespace slablu_b200
 
