@@ -503,4 +503,210 @@ void dgemv_batched_rhs(cudaStream_t st, int64_t m, int64_t n, int64_t nrhs, doub
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------------------
+// dgetrs for a few right-hand sides (the stage-two sweep solve, stage_two.hpp:
+// 176-186: S_j^{-1} r applied from the LU factors, never an explicit inverse
+// of S_j).  One launch runs both triangular solves as a chain of 64-row
+// blocks: CTA i of the first half solves block i of L y = P b, CTA i of the
+// second half block i of U z = y (bottom block first).  Every CTA streams its
+// off-diagonal row of 64x64 tiles while the chain is still upstream (tiles
+// are read as soon as the block they multiply is published), so the critical
+// path per block is one flag hop plus two 64x64 GEMVs from registers: the
+// diagonal blocks are applied through their inverses (64x64, computed once at
+// factorization by getrs_prepare from the LU factors, as MAGMA's trsv does).
+// Blocks are published with a release store of the call's epoch; waits only
+// ever target lower CTA indices, so the chain is deadlock-free for any
+// residency.
+namespace {
+constexpr int CT = 64;
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// perm[r] = source row of row r after the interchanges ipiv[0..n); one CTA per call.
+// dinv: per 64-row block b, [inv(L_bb) | inv(U_bb)] (64x64 col-major each, padded with identity).
+__global__ void __launch_bounds__(64) diag_inverse_kernel(int n, const double* __restrict__ lu, double* dinv) {
+  __shared__ double T[CT][CT + 1];
+  const int blk = blockIdx.x, upper = blockIdx.y, c = threadIdx.x;
+  const int r0 = blk * CT, m = min(CT, n - r0);
+  for (int k = 0; k < CT; k++)
+    T[c][k] = (c < m && k < m) ? lu[(int64_t)(r0 + k) * n + r0 + c] : (c == k ? 1.0 : 0.0);
+  __syncthreads();
+  double X[CT];  // thread c solves for column c of the inverse (fully unrolled: registers)
+#pragma unroll
+  for (int r = 0; r < CT; r++) X[r] = (r == c) ? 1.0 : 0.0;
+  if (!upper) {
+#pragma unroll
+    for (int k = 0; k < CT; k++) {
+#pragma unroll
+      for (int r = k + 1; r < CT; r++) X[r] -= T[r][k] * X[k];
+    }
+  } else {
+#pragma unroll
+    for (int k = CT - 1; k >= 0; k--) {
+      X[k] = X[k] / T[k][k];
+#pragma unroll
+      for (int r = 0; r < k; r++) X[r] -= T[r][k] * X[k];
+    }
+  }
+  double* out = dinv + ((int64_t)blk * 2 + upper) * CT * CT;
+#pragma unroll
+  for (int r = 0; r < CT; r++) out[(int64_t)c * CT + r] = X[r];
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) getrs_chain_kernel(int n, int nb, const double* __restrict__ lu,
+                                                          const double* __restrict__ dinv,
+                                                          const int32_t* __restrict__ perm, const double* b,
+                                                          int64_t ldb, double* x, int64_t ldx, double alpha,
+                                                          double beta, double* y, double* z, int* flags, int epoch) {
+  __shared__ double red[4][CT][NR];
+  __shared__ double vs[CT][NR];
+  __shared__ int s_ready;
+  const int t = threadIdx.x, r = t & (CT - 1), kq = t >> 6;
+  const bool lower = (int)blockIdx.x < nb;
+  const int i = lower ? (int)blockIdx.x : nb - 1 - ((int)blockIdx.x - nb);
+  const int r0 = i * CT, mrow = min(CT, n - r0);
+  const double* src = lower ? y : z;  // published blocks this CTA multiplies
+  int* myflags = lower ? flags : flags + nb;
+  // the diagonal block's inverse, prefetched (independent of the chain)
+  double d[16];
+  {
+    const double* D = dinv + ((int64_t)i * 2 + (lower ? 0 : 1)) * CT * CT;
+#pragma unroll
+    for (int u = 0; u < 16; u++) d[u] = D[(int64_t)(kq * 16 + u) * CT + r];
+  }
+  double acc[NR];
+#pragma unroll
+  for (int c = 0; c < NR; c++) acc[c] = 0.0;
+  const int ntiles = lower ? i : nb - 1 - i;
+  int ready = 0;
+  for (int q = 0; q < ntiles; q++) {
+    const int j = lower ? q : nb - 1 - q;
+    const int c0 = j * CT, ncol = min(CT, n - c0);
+    double a[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const int k = kq * 16 + u;
+      a[u] = (r < mrow && k < ncol) ? __ldg(&lu[(int64_t)(c0 + k) * n + r0 + r]) : 0.0;
+    }
+    if (q >= ready) {  // wait for block j, then take every further block already published
+      __syncthreads();
+      if (t == 0) {
+        while (ld_acquire_gpu(&myflags[j]) != epoch) {
+        }
+        int qq = q + 1;
+        while (qq < ntiles && ld_acquire_gpu(&myflags[lower ? qq : nb - 1 - qq]) == epoch) qq++;
+        __threadfence();
+        s_ready = qq;
+      }
+      __syncthreads();
+      ready = s_ready;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const int k = kq * 16 + u;
+      if (k < ncol) {
+#pragma unroll
+        for (int c = 0; c < NR; c++) acc[c] = fma(a[u], __ldcg(&src[(int64_t)c * n + c0 + k]), acc[c]);
+      }
+    }
+  }
+  // this block's right-hand side: lower P b, upper y_i (published by lower CTA i)
+  if (!lower) {
+    __syncthreads();
+    if (t == 0) {
+      while (ld_acquire_gpu(&flags[i]) != epoch) {
+      }
+      __threadfence();
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NR; c++) red[kq][r][c] = acc[c];
+  __syncthreads();
+  if (t < CT) {
+#pragma unroll
+    for (int c = 0; c < NR; c++) {
+      double v = 0.0;
+      if (r < mrow) {
+        const double s = red[0][r][c] + red[1][r][c] + red[2][r][c] + red[3][r][c];
+        const double rhs = lower ? b[(int64_t)c * ldb + perm[r0 + r]] : __ldcg(&y[(int64_t)c * n + r0 + r]);
+        v = rhs - s;
+      }
+      vs[r][c] = v;
+    }
+  }
+  __syncthreads();
+  // out = Dinv_i * rhs
+#pragma unroll
+  for (int c = 0; c < NR; c++) {
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; u++) s = fma(d[u], vs[kq * 16 + u][c], s);
+    red[kq][r][c] = s;
+  }
+  __syncthreads();
+  if (t < CT && r < mrow) {
+#pragma unroll
+    for (int c = 0; c < NR; c++) {
+      const double o = red[0][r][c] + red[1][r][c] + red[2][r][c] + red[3][r][c];
+      if (lower) {
+        y[(int64_t)c * n + r0 + r] = o;
+      } else {
+        z[(int64_t)c * n + r0 + r] = o;
+        double* xo = x + (int64_t)c * ldx + r0 + r;
+        *xo = beta == 0.0 ? alpha * o : fma(alpha, o, beta * *xo);
+      }
+    }
+  }
+  __syncthreads();
+  if (t == 0) {
+    __threadfence();
+    st_release_gpu(&myflags[i], epoch);
+  }
+}
+}  // namespace
+
+void getrs_prepare(cudaStream_t st, int64_t n, const double* lu, const int32_t* ipiv, int32_t* perm,
+                   double* dinv) {
+  if (n <= 0) return;
+  if (n > 8192) throw CudaFailure(cudaErrorInvalidValue, "getrs_prepare: n must be <= 8192", __FILE__, __LINE__);
+  swap_perm_kernel<<<1, 1024, n * sizeof(int32_t), st>>>(ipiv, n, 0, n, perm); count_launch();
+  SLB_CUDA_CHECK(cudaGetLastError());
+  diag_inverse_kernel<<<dim3((unsigned)cdiv(n, CT), 2), CT, 0, st>>>((int)n, lu, dinv); count_launch();
+  SLB_CUDA_CHECK(cudaGetLastError());
+}
+
+void getrs_chain(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const double* dinv,
+                 const int32_t* perm, const double* b, int64_t ldb, double* x, int64_t ldx, double alpha,
+                 double beta, double* yz, int* flags, int epoch) {
+  if (n <= 0 || nrhs <= 0) return;
+  const int nb = (int)cdiv(n, CT);
+  double* y = yz;
+  double* z = yz + n * nrhs;
+  const dim3 grid((unsigned)(2 * nb));
+#define SLB_CHAIN(NR)                                                                                      \
+  getrs_chain_kernel<NR><<<grid, 256, 0, st>>>((int)n, nb, lu, dinv, perm, b, ldb, x, ldx, alpha, beta, y, z, \
+                                               flags, epoch)
+  switch (nrhs) {
+    case 1: SLB_CHAIN(1); break;
+    case 2: SLB_CHAIN(2); break;
+    case 3: SLB_CHAIN(3); break;
+    case 4: SLB_CHAIN(4); break;
+    case 5: SLB_CHAIN(5); break;
+    case 6: SLB_CHAIN(6); break;
+    case 7: SLB_CHAIN(7); break;
+    case 8: SLB_CHAIN(8); break;
+    default: throw CudaFailure(cudaErrorInvalidValue, "getrs_chain: nrhs must be <= 8", __FILE__, __LINE__);
+  }
+#undef SLB_CHAIN
+  count_launch();
+  SLB_CUDA_CHECK(cudaGetLastError());
+}
+
 }  // namespace slb

@@ -145,11 +145,12 @@ __global__ void combine_reduce_kernel(double* red, int64_t K, int64_t nrhs, int6
   red[idx] = v;
 }
 // y[:, c] += x[:, c] for an n x nrhs block (lds, ldd)
-__global__ void add2d_kernel(const double* x, int64_t ldx, double* y, int64_t ldy, int64_t rows, int64_t cols) {
+__global__ void add2d_kernel(const double* x, int64_t ldx, double* y, int64_t ldy, int64_t rows, int64_t cols,
+                             double alpha) {
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < rows * cols;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = idx % rows, c = idx / rows;
-    y[c * ldy + r] += x[c * ldx + r];
+    y[c * ldy + r] += alpha * x[c * ldx + r];
   }
 }
 // r = f - A u (CSR, one thread per row and column), then u stays; used for refinement.
@@ -175,9 +176,11 @@ __global__ void copy2d_kernel(const double* src, int64_t lds, double* dst, int64
   }
 }
 
-void add2d(cudaStream_t st, const double* x, int64_t ldx, double* y, int64_t ldy, int64_t rows, int64_t cols) {
+void add2d(cudaStream_t st, const double* x, int64_t ldx, double* y, int64_t ldy, int64_t rows, int64_t cols,
+           double alpha = 1.0) {
   if (rows <= 0 || cols <= 0) return;
-  add2d_kernel<<<(unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 8192), 256, 0, st>>>(x, ldx, y, ldy, rows, cols); count_launch();
+  add2d_kernel<<<(unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 8192), 256, 0, st>>>(x, ldx, y, ldy, rows, cols,
+                                                                                     alpha); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -229,7 +232,11 @@ struct slablu_gpu_fact {
   DBuf<int32_t> excpos; // their positions: 8 per (strip, level)
   DBuf<double> hcol;    // x_{l+2} columns of H per (strip, level): 8 x Wp
   DBuf<int32_t> hidx;   // their column indices
-  DBuf<double> T;       // [diag k | super k-1 | sub k-1] blocks, n2 x n2; diag holds S_j^{-1}
+  DBuf<double> T;       // [diag k | super k-1 | sub k-1] blocks, n2 x n2; diag holds LU(S_j) (ipivT)
+                        // or, in a sharded factorization, S_j^{-1}
+  DBuf<int32_t> ipivT;  // pivots of LU(S_j), n2 per interface (unsharded)
+  DBuf<int32_t> permT;  // the same interchanges as a row permutation (getrs_chain)
+  DBuf<double> dinvT;   // inverses of the 64x64 diagonal blocks of L_j, U_j (getrs_chain)
   DBuf<double> Tkeep;   // optional copy of the reduced blocks
   DBuf<DevStatus> status;
   DBuf<int32_t> a_rp, a_ci;  // the original operator (iterative refinement)
@@ -614,23 +621,27 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     SLB_CUDA_CHECK(cudaEventRecord(e1, st));
 
     // ---- stage two: sweeping block LU (stage_two.hpp:131-150) --------------------------
+    // S_j stays in LU form (as DenseLU in the reference): X = S_{j-1}^{-1} super_{j-1} by getrs,
+    // the solve applies S_j^{-1} by getrs too (stage_two.hpp:138-147, 176-186)
     const int64_t bs = n2 * n2;
-    DBuf<double> X, I;
-    DBuf<int32_t> ipiv;
+    DBuf<double> X;
     X.alloc(dev, bs);
-    I.alloc(dev, bs);
-    ipiv.alloc(dev, n2);
+    const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
+    if (!sharded) {
+      F->ipivT.alloc(dev, (size_t)std::max(K, 1) * n2);
+      F->permT.alloc(dev, (size_t)std::max(K, 1) * n2);
+      F->dinvT.alloc(dev, (size_t)std::max(K, 1) * dinv_sz);
+    }
     for (int j = 0; j < (sharded ? 0 : K); j++) {  // sharded: slablu_gpu_shard_sweep
       double* Sj = F->Tdiag() + j * bs;
       if (j > 0) {
-        dgemm_batched(st, n2, n2, n2, 1.0, F->Tdiag() + (j - 1) * bs, n2, 0, F->Tsup() + (j - 1) * bs, n2, 0, 0.0,
-                      X.p, n2, 0, 1);
+        SLB_CUDA_CHECK(cudaMemcpyAsync(X.p, F->Tsup() + (j - 1) * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        dgetrs(st, n2, n2, F->Tdiag() + (j - 1) * bs, F->ipivT.p + (size_t)(j - 1) * n2, X.p, n2, nullptr);
         dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X.p, n2, 0, 1.0, Sj, n2, 0, 1);
       }
-      dgetrf(st, n2, Sj, ipiv.p, nullptr, F->status.p, j);
-      dset_identity(st, I.p, n2);
-      dgetrs(st, n2, n2, Sj, ipiv.p, I.p, n2, nullptr);
-      SLB_CUDA_CHECK(cudaMemcpyAsync(Sj, I.p, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      dgetrf(st, n2, Sj, F->ipivT.p + (size_t)j * n2, nullptr, F->status.p, j);
+      getrs_prepare(st, n2, Sj, F->ipivT.p + (size_t)j * n2, F->permT.p + (size_t)j * n2,
+                    F->dinvT.p + (size_t)j * dinv_sz);
     }
   } else {
     SLB_CUDA_CHECK(cudaEventRecord(es, st));
@@ -778,18 +789,40 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     run_sweep(sa);
     SLB_CUDA_CHECK(cudaEventRecord(s1, st));
     combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, S, F->strips.p, contrib.p, 0); count_launch();
-    // sweep solve (stage_two.hpp:170-188) with S_j^{-1}
+    // sweep solve (stage_two.hpp:170-188) with the LU factors of S_j
+    // S_j^{-1} v: chained getrs for nrhs <= 8, TRSM/GEMM getrs beyond
     const int64_t bs = n2 * n2;
+    const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
+    const bool chain = nrhs <= 8;
+    DBuf<double> yz;
+    DBuf<int> flags;
+    int epoch = 0;
+    if (chain) {
+      yz.alloc(dev, (size_t)2 * n2 * nrhs);
+      flags.alloc(dev, (size_t)2 * cdiv(n2, 64));
+      SLB_CUDA_CHECK(cudaMemsetAsync(flags.p, 0, flags.bytes(), st));
+    }
+    auto apply_Sinv = [&](int j, const double* v, int64_t ldv, double* out, double alpha, double beta) {
+      if (chain) {
+        getrs_chain(st, n2, nrhs, F->Tdiag() + j * bs, F->dinvT.p + (size_t)j * dinv_sz,
+                    F->permT.p + (size_t)j * n2, v, ldv, out, K, alpha, beta, yz.p, flags.p, ++epoch);
+      } else {  // out = beta*out + alpha*S^{-1} v, v is scratch (tmp)
+        double* w = const_cast<double*>(v);
+        dgetrs(st, n2, nrhs, F->Tdiag() + j * bs, F->ipivT.p + (size_t)j * n2, w, ldv, nullptr);
+        if (beta == 0.0) copy2d(st, w, ldv, out, K, n2, nrhs);
+        else add2d(st, w, ldv, out, K, n2, nrhs, alpha);
+      }
+    };
     for (int j = 0; j < F->K; j++) {
       double* rj = red.p + j * n2;
       if (j > 0) dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j - 1) * bs, n2, uifc.p + (j - 1) * n2, K,
                                    1.0, rj, K, part.p);
-      dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tdiag() + j * bs, n2, rj, K, 0.0, uifc.p + j * n2, K, part.p);
+      apply_Sinv(j, rj, K, uifc.p + j * n2, 1.0, 0.0);
     }
     for (int j = F->K - 2; j >= 0; j--) {
       dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tsup() + j * bs, n2, uifc.p + (j + 1) * n2, K, 0.0, tmp.p, n2,
                         part.p);
-      dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tdiag() + j * bs, n2, tmp.p, n2, 1.0, uifc.p + j * n2, K, part.p);
+      apply_Sinv(j, tmp.p, n2, uifc.p + j * n2, -1.0, 1.0);
     }
     // recover_interiors (stage_one.hpp:438-462)
     SLB_CUDA_CHECK(cudaEventRecord(s2, st));
@@ -1405,6 +1438,68 @@ int slablu_gpu_debug_dense_bench(int64_t n, int device, double* out) {
     return 0;
   } catch (const CudaFailure& f) {
     fprintf(stderr, "debug_dense_bench: %s at %s:%d (%s)\n", cudaGetErrorString(f.err), f.file, f.line, f.expr);
+    return 1;
+  } catch (...) {
+    return 1;
+  }
+}
+
+// Test hook for the stage-two solve kernel: LU-factor the n x n column-major a (host),
+// then x = A^{-1} b (n x nrhs, host) through getrs_chain (nrhs <= 8) or the TRSM getrs.
+// t_out[0] = average device seconds per getrs over `reps` calls.
+int slablu_gpu_debug_getrs(int64_t n, int64_t nrhs, const double* a, const double* b, double* x, int reps,
+                           int device, double* t_out) {
+  try {
+    SLB_CUDA_CHECK(cudaSetDevice(device));
+    cudaStream_t st;
+    SLB_CUDA_CHECK(cudaStreamCreate(&st));
+    const int64_t dinv_sz = cdiv(n, 64) * 2 * 64 * 64;
+    DBuf<double> A, B, X, D, yz;
+    DBuf<int32_t> ipiv, perm;
+    DBuf<int> flags;
+    DBuf<DevStatus> status;
+    A.alloc(device, n * n);
+    B.alloc(device, n * nrhs);
+    X.alloc(device, n * nrhs);
+    D.alloc(device, dinv_sz);
+    yz.alloc(device, 2 * n * nrhs);
+    ipiv.alloc(device, n);
+    perm.alloc(device, n);
+    flags.alloc(device, 2 * cdiv(n, 64));
+    status.alloc(device, 1);
+    DevStatus st0{0, INT_MAX, INT_MAX, 0};
+    SLB_CUDA_CHECK(cudaMemcpy(status.p, &st0, sizeof(st0), cudaMemcpyHostToDevice));
+    SLB_CUDA_CHECK(cudaMemcpy(A.p, a, n * n * sizeof(double), cudaMemcpyHostToDevice));
+    SLB_CUDA_CHECK(cudaMemcpy(B.p, b, n * nrhs * sizeof(double), cudaMemcpyHostToDevice));
+    SLB_CUDA_CHECK(cudaMemset(flags.p, 0, flags.bytes()));
+    dgetrf(st, n, A.p, ipiv.p, nullptr, status.p, 0);
+    getrs_prepare(st, n, A.p, ipiv.p, perm.p, D.p);
+    cudaEvent_t e0, e1;
+    SLB_CUDA_CHECK(cudaEventCreate(&e0));
+    SLB_CUDA_CHECK(cudaEventCreate(&e1));
+    int epoch = 0;
+    reps = std::max(reps, 1);
+    SLB_CUDA_CHECK(cudaEventRecord(e0, st));
+    for (int r = 0; r < reps; r++) {
+      if (nrhs <= 8) {
+        getrs_chain(st, n, nrhs, A.p, D.p, perm.p, B.p, n, X.p, n, 1.0, 0.0, yz.p, flags.p, ++epoch);
+      } else {
+        copy2d(st, B.p, n, X.p, n, n, nrhs);
+        dgetrs(st, n, nrhs, A.p, ipiv.p, X.p, n, nullptr);
+      }
+    }
+    SLB_CUDA_CHECK(cudaEventRecord(e1, st));
+    SLB_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms;
+    SLB_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    if (t_out) t_out[0] = ms * 1e-3 / reps;
+    SLB_CUDA_CHECK(cudaMemcpy(x, X.p, n * nrhs * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+    return 0;
+  } catch (const CudaFailure& f) {
+    fprintf(stderr, "debug_getrs: %s at %s:%d (%s)\n", cudaGetErrorString(f.err), f.file, f.line, f.expr);
     return 1;
   } catch (...) {
     return 1;

@@ -157,6 +157,16 @@ void dgetrf(cudaStream_t st, int64_t n, double* a, int32_t* ipiv, double* work, 
 void dgetrs(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const int32_t* ipiv,
             double* b, int64_t ldb, double* work);
 void check_finite(cudaStream_t st, const double* a, int64_t count, DevStatus* status);
+// From the dgetrf factors: perm (n, source row of each row after the interchanges) and the
+// inverses of the 64x64 diagonal blocks of L and U (dinv: cdiv(n,64) * 2 * 64 * 64).
+void getrs_prepare(cudaStream_t st, int64_t n, const double* lu, const int32_t* ipiv, int32_t* perm,
+                   double* dinv);
+// x = beta*x + alpha * A^{-1} b for nrhs <= 8 with the dgetrf factors (one chained launch).
+// b and x must not alias; yz: 2*n*nrhs scratch; flags: 2*cdiv(n,64) ints, zeroed before the
+// first call; epoch: distinct positive value per call on the same flags.
+void getrs_chain(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const double* dinv,
+                 const int32_t* perm, const double* b, int64_t ldb, double* x, int64_t ldx, double alpha,
+                 double beta, double* yz, int* flags, int epoch);
 
 // ---- solve.cu ---------------------------------------------------------------------
 

@@ -258,3 +258,28 @@ def test_backward_columns_match_full_operator(monkeypatch):
         if j + 1 < fa.stats.interfaces:
             assert relerr(fa.T_block("super", j), fb.T_block("super", j)) < 1e-12
     assert relerr(ua, ub) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,nrhs", [(1, 1), (37, 3), (64, 1), (100, 8), (333, 2), (1000, 5), (4000, 1), (700, 12)])
+def test_stage_two_getrs_vs_numpy(n, nrhs):
+    """The stage-two solve applies S_j^{-1} from its LU factors (stage_two.hpp:176-186,
+    DenseLU::solve dense.hpp:48-61): chained getrs for nrhs <= 8, TRSM getrs beyond.
+    Checked against numpy's LAPACK solve of the same matrix (relative 1e-10)."""
+    import ctypes
+    from paper_2211_07572_b200 import _lib
+    L = _lib.lib()
+    P = ctypes.POINTER(ctypes.c_double)
+    L.slablu_gpu_debug_getrs.restype = ctypes.c_int
+    L.slablu_gpu_debug_getrs.argtypes = [ctypes.c_int64, ctypes.c_int64, P, P, P, ctypes.c_int, ctypes.c_int, P]
+    rng = np.random.default_rng(n * 31 + nrhs)
+    A = np.asfortranarray(rng.standard_normal((n, n)) + 0.0)
+    B = np.asfortranarray(rng.standard_normal((n, nrhs)))
+    X = np.zeros((n, nrhs), order="F")
+    t = np.zeros(1)
+    assert L.slablu_gpu_debug_getrs(n, nrhs, A.ctypes.data_as(P), B.ctypes.data_as(P), X.ctypes.data_as(P), 3, 0,
+                                    t.ctypes.data_as(P)) == 0
+    ref = np.linalg.solve(A, B)
+    cond = np.linalg.cond(A)
+    assert np.linalg.norm(X - ref) / np.linalg.norm(ref) <= max(1e-10, 1e-14 * cond)
+    assert np.linalg.norm(A @ X - B) / (np.linalg.norm(A) * np.linalg.norm(X)) <= 1e-13
