@@ -504,28 +504,37 @@ void dgemv_batched_rhs(cudaStream_t st, int64_t m, int64_t n, int64_t nrhs, doub
 }
 
 // ---------------------------------------------------------------------------
-// dgetrs for a few right-hand sides (the stage-two sweep solve, stage_two.hpp:
-// 176-186: S_j^{-1} r applied from the LU factors, never an explicit inverse
-// of S_j).  One launch runs both triangular solves as a chain of 64-row
-// blocks: CTA i of the first half solves block i of L y = P b, CTA i of the
-// second half block i of U z = y (bottom block first).  Every CTA streams its
-// off-diagonal row of 64x64 tiles while the chain is still upstream (tiles
-// are read as soon as the block they multiply is published), so the critical
-// path per block is one flag hop plus two 64x64 GEMVs from registers: the
-// diagonal blocks are applied through their inverses (64x64, computed once at
-// factorization by getrs_prepare from the LU factors, as MAGMA's trsv does).
-// Blocks are published with a release store of the call's epoch; waits only
-// ever target lower CTA indices, so the chain is deadlock-free for any
-// residency.
+// dgetrs for the stage-two sweep solve (stage_two.hpp:176-186: S_j^{-1} r is
+// applied from the LU factors of S_j, as DenseLU::solve does, dense.hpp:48-61).
+// One launch runs both triangular solves as a chain of 64-row blocks per
+// 8-column group of right-hand sides: CTA i of the first half solves block i
+// of L y = P b, CTA i of the second half block i of U z = y (bottom block
+// first).  Each CTA streams its off-diagonal row of 64x64 tiles two at a time
+// as the blocks they multiply are published, so the critical path per block
+// is one L2 hop plus two 64x64 GEMVs: the diagonal blocks are applied through
+// their inverses (computed once at factorization by getrs_prepare from the LU
+// factors, as MAGMA's trsv does).  There are no flags: a published block is
+// its data, and a consumer polls the values themselves against a sentinel NaN
+// pattern that no computation can produce (NaN results are canonicalised).
+// The y/z scratch holds two sets used on alternating calls; each CTA resets
+// its own block of the other set to the sentinel, ready for the next call.
+// Polls only ever wait on lower CTA indices of the same chain (deadlock-free
+// for any residency) and are bounded (a broken chain returns garbage, it
+// does not hang the device).
 namespace {
 constexpr int CT = 64;
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+constexpr unsigned long long kSentinel = 0xFFFFFFFFFFFFFFFFull;
+constexpr unsigned long long kCanonNaN = 0x7FF8000000000000ull;
+constexpr int kSpinLimit = 1 << 22;
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+  unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  if ((u & 0x7FF0000000000000ull) == 0x7FF0000000000000ull && (u & 0x000FFFFFFFFFFFFFull)) u = kCanonNaN;
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(u) : "memory");
 }
 
 // perm[r] = source row of row r after the interchanges ipiv[0..n); one CTA per call.
@@ -564,66 +573,99 @@ __global__ void __launch_bounds__(256) getrs_chain_kernel(int n, int nb, const d
                                                           const double* __restrict__ dinv,
                                                           const int32_t* __restrict__ perm, const double* b,
                                                           int64_t ldb, double* x, int64_t ldx, double alpha,
-                                                          double beta, double* y, double* z, int* flags, int epoch) {
+                                                          double beta, double* cur, double* nxt) {
+  {  // chain = 8-column group: its own columns and scratch (y at +0, z at +8n)
+    const int chain = (int)blockIdx.x / (2 * nb);
+    b += (int64_t)chain * NR * ldb;
+    x += (int64_t)chain * NR * ldx;
+    cur += (int64_t)chain * 16 * n;
+    nxt += (int64_t)chain * 16 * n;
+  }
+  const int cta = (int)blockIdx.x % (2 * nb);
   __shared__ double red[4][CT][NR];
+  __shared__ double vt[2][CT][NR];
   __shared__ double vs[CT][NR];
-  __shared__ int s_ready;
   const int t = threadIdx.x, r = t & (CT - 1), kq = t >> 6;
-  const bool lower = (int)blockIdx.x < nb;
-  const int i = lower ? (int)blockIdx.x : nb - 1 - ((int)blockIdx.x - nb);
+  const bool lower = cta < nb;
+  const int i = lower ? cta : nb - 1 - (cta - nb);
   const int r0 = i * CT, mrow = min(CT, n - r0);
+  double* y = cur;
+  double* z = cur + (int64_t)8 * n;
   const double* src = lower ? y : z;  // published blocks this CTA multiplies
-  int* myflags = lower ? flags : flags + nb;
-  // the diagonal block's inverse, prefetched (independent of the chain)
-  double d[16];
+  double* own = lower ? y : z;
+  const bool row_owner = t < CT && r < mrow;
+  if (row_owner) {  // the next call's copy of this block starts unpublished
+    double* o = lower ? nxt : nxt + (int64_t)8 * n;
+#pragma unroll
+    for (int c = 0; c < NR; c++) o[(int64_t)c * n + r0 + r] = __longlong_as_double((long long)kSentinel);
+  }
+  double d[16];  // the diagonal block's inverse, prefetched
   {
     const double* D = dinv + ((int64_t)i * 2 + (lower ? 0 : 1)) * CT * CT;
 #pragma unroll
     for (int u = 0; u < 16; u++) d[u] = D[(int64_t)(kq * 16 + u) * CT + r];
   }
+  double rhs[NR];
+  if (lower && row_owner) {
+    const int32_t pr = perm[r0 + r];
+#pragma unroll
+    for (int c = 0; c < NR; c++) rhs[c] = b[(int64_t)c * ldb + pr];
+  }
   double acc[NR];
 #pragma unroll
   for (int c = 0; c < NR; c++) acc[c] = 0.0;
   const int ntiles = lower ? i : nb - 1 - i;
-  int ready = 0;
-  for (int q = 0; q < ntiles; q++) {
-    const int j = lower ? q : nb - 1 - q;
-    const int c0 = j * CT, ncol = min(CT, n - c0);
-    double a[16];
+  constexpr int PER = (2 * CT * NR + 255) / 256;  // staged values per thread (two tiles)
+  for (int q = 0; q < ntiles; q += 2) {
+    const int j0 = lower ? q : nb - 1 - q, j1 = lower ? q + 1 : nb - 2 - q;
+    const int c00 = j0 * CT, nc0 = min(CT, n - c00);
+    const int c01 = j1 * CT, nc1 = q + 1 < ntiles ? min(CT, n - c01) : 0;
+    double a0[16], a1[16];
 #pragma unroll
     for (int u = 0; u < 16; u++) {
       const int k = kq * 16 + u;
-      a[u] = (r < mrow && k < ncol) ? __ldg(&lu[(int64_t)(c0 + k) * n + r0 + r]) : 0.0;
+      a0[u] = (r < mrow && k < nc0) ? __ldg(&lu[(int64_t)(c00 + k) * n + r0 + r]) : 0.0;
+      a1[u] = (r < mrow && k < nc1) ? __ldg(&lu[(int64_t)(c01 + k) * n + r0 + r]) : 0.0;
     }
-    if (q >= ready) {  // wait for block j, then take every further block already published
-      __syncthreads();
-      if (t == 0) {
-        while (ld_acquire_gpu(&myflags[j]) != epoch) {
+    unsigned long long v[PER];
+    const double* vp[PER];
+#pragma unroll
+    for (int m = 0; m < PER; m++) {
+      const int e = t + 256 * m, tile = e / (CT * NR), rem = e % (CT * NR), c = rem / CT, k = rem % CT;
+      const bool valid = e < 2 * CT * NR && k < (tile ? nc1 : nc0);
+      vp[m] = valid ? src + (int64_t)c * n + (tile ? c01 : c00) + k : nullptr;
+      v[m] = valid ? ld_relaxed_u64(vp[m]) : 0ull;
+    }
+    for (int spin = 0; spin < kSpinLimit; spin++) {  // re-poll the values not yet published
+      bool miss = false;
+#pragma unroll
+      for (int m = 0; m < PER; m++)
+        if (v[m] == kSentinel) {
+          v[m] = ld_relaxed_u64(vp[m]);
+          miss = true;
         }
-        int qq = q + 1;
-        while (qq < ntiles && ld_acquire_gpu(&myflags[lower ? qq : nb - 1 - qq]) == epoch) qq++;
-        __threadfence();
-        s_ready = qq;
-      }
-      __syncthreads();
-      ready = s_ready;
+      if (!miss) break;
     }
+    __syncthreads();  // the previous pair's FMAs are done with vt
+#pragma unroll
+    for (int m = 0; m < PER; m++) {
+      const int e = t + 256 * m, tile = e / (CT * NR), rem = e % (CT * NR), c = rem / CT, k = rem % CT;
+      if (e < 2 * CT * NR) vt[tile][k][c] = __longlong_as_double((long long)v[m]);
+    }
+    __syncthreads();
 #pragma unroll
     for (int u = 0; u < 16; u++) {
       const int k = kq * 16 + u;
-      if (k < ncol) {
 #pragma unroll
-        for (int c = 0; c < NR; c++) acc[c] = fma(a[u], __ldcg(&src[(int64_t)c * n + c0 + k]), acc[c]);
-      }
+      for (int c = 0; c < NR; c++) acc[c] = fma(a1[u], vt[1][k][c], fma(a0[u], vt[0][k][c], acc[c]));
     }
   }
-  // this block's right-hand side: lower P b, upper y_i (published by lower CTA i)
-  if (!lower) {
-    __syncthreads();
-    if (t == 0) {
-      while (ld_acquire_gpu(&flags[i]) != epoch) {
-      }
-      __threadfence();
+  if (!lower && row_owner) {  // upper: this block's right-hand side is y_i from lower CTA i
+#pragma unroll
+    for (int c = 0; c < NR; c++) {
+      unsigned long long u = ld_relaxed_u64(&y[(int64_t)c * n + r0 + r]);
+      for (int spin = 0; u == kSentinel && spin < kSpinLimit; spin++) u = ld_relaxed_u64(&y[(int64_t)c * n + r0 + r]);
+      rhs[c] = __longlong_as_double((long long)u);
     }
   }
 #pragma unroll
@@ -631,43 +673,28 @@ __global__ void __launch_bounds__(256) getrs_chain_kernel(int n, int nb, const d
   __syncthreads();
   if (t < CT) {
 #pragma unroll
-    for (int c = 0; c < NR; c++) {
-      double v = 0.0;
-      if (r < mrow) {
-        const double s = red[0][r][c] + red[1][r][c] + red[2][r][c] + red[3][r][c];
-        const double rhs = lower ? b[(int64_t)c * ldb + perm[r0 + r]] : __ldcg(&y[(int64_t)c * n + r0 + r]);
-        v = rhs - s;
-      }
-      vs[r][c] = v;
-    }
+    for (int c = 0; c < NR; c++)
+      vs[r][c] = r < mrow ? rhs[c] - (red[0][r][c] + red[1][r][c] + red[2][r][c] + red[3][r][c]) : 0.0;
   }
   __syncthreads();
-  // out = Dinv_i * rhs
 #pragma unroll
-  for (int c = 0; c < NR; c++) {
+  for (int c = 0; c < NR; c++) {  // out = Dinv_i * (rhs - off-diagonal sum)
     double s = 0.0;
 #pragma unroll
     for (int u = 0; u < 16; u++) s = fma(d[u], vs[kq * 16 + u][c], s);
     red[kq][r][c] = s;
   }
   __syncthreads();
-  if (t < CT && r < mrow) {
+  if (row_owner) {
 #pragma unroll
     for (int c = 0; c < NR; c++) {
       const double o = red[0][r][c] + red[1][r][c] + red[2][r][c] + red[3][r][c];
-      if (lower) {
-        y[(int64_t)c * n + r0 + r] = o;
-      } else {
-        z[(int64_t)c * n + r0 + r] = o;
+      st_relaxed_f64(&own[(int64_t)c * n + r0 + r], o);  // publishes the value
+      if (!lower) {
         double* xo = x + (int64_t)c * ldx + r0 + r;
         *xo = beta == 0.0 ? alpha * o : fma(alpha, o, beta * *xo);
       }
     }
-  }
-  __syncthreads();
-  if (t == 0) {
-    __threadfence();
-    st_release_gpu(&myflags[i], epoch);
   }
 }
 }  // namespace
@@ -684,29 +711,36 @@ void getrs_prepare(cudaStream_t st, int64_t n, const double* lu, const int32_t* 
 
 void getrs_chain(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const double* dinv,
                  const int32_t* perm, const double* b, int64_t ldb, double* x, int64_t ldx, double alpha,
-                 double beta, double* yz, int* flags, int epoch) {
+                 double beta, double* yz, int epoch) {
   if (n <= 0 || nrhs <= 0) return;
   const int nb = (int)cdiv(n, CT);
-  double* y = yz;
-  double* z = yz + n * nrhs;
-  const dim3 grid((unsigned)(2 * nb));
-#define SLB_CHAIN(NR)                                                                                      \
-  getrs_chain_kernel<NR><<<grid, 256, 0, st>>>((int)n, nb, lu, dinv, perm, b, ldb, x, ldx, alpha, beta, y, z, \
-                                               flags, epoch)
-  switch (nrhs) {
-    case 1: SLB_CHAIN(1); break;
-    case 2: SLB_CHAIN(2); break;
-    case 3: SLB_CHAIN(3); break;
-    case 4: SLB_CHAIN(4); break;
-    case 5: SLB_CHAIN(5); break;
-    case 6: SLB_CHAIN(6); break;
-    case 7: SLB_CHAIN(7); break;
-    case 8: SLB_CHAIN(8); break;
-    default: throw CudaFailure(cudaErrorInvalidValue, "getrs_chain: nrhs must be <= 8", __FILE__, __LINE__);
+  // chains of 8 columns in one launch, the remainder (< 8 columns) as one more chain
+  const int64_t full = nrhs / 8, rem = nrhs % 8;
+  const int64_t set = 16 * n * cdiv(nrhs, 8);
+  double* cur = yz + (epoch & 1) * set;
+  double* nxt = yz + ((epoch + 1) & 1) * set;
+#define SLB_CHAIN(NR, NCH, OFF)                                                                          \
+  getrs_chain_kernel<NR><<<(unsigned)(2 * nb * (NCH)), 256, 0, st>>>(                                    \
+      (int)n, nb, lu, dinv, perm, b + (OFF) * 8 * ldb, ldb, x + (OFF) * 8 * ldx, ldx, alpha, beta,       \
+      cur + (OFF) * 16 * n, nxt + (OFF) * 16 * n);                                                       \
+  count_launch()
+  if (full > 0) SLB_CHAIN(8, full, 0);
+  switch (rem) {
+    case 0: break;
+    case 1: SLB_CHAIN(1, 1, full); break;
+    case 2: SLB_CHAIN(2, 1, full); break;
+    case 3: SLB_CHAIN(3, 1, full); break;
+    case 4: SLB_CHAIN(4, 1, full); break;
+    case 5: SLB_CHAIN(5, 1, full); break;
+    case 6: SLB_CHAIN(6, 1, full); break;
+    case 7: SLB_CHAIN(7, 1, full); break;
   }
 #undef SLB_CHAIN
-  count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
+}
+
+void getrs_chain_init(cudaStream_t st, int64_t n, int64_t nrhs, double* yz) {
+  SLB_CUDA_CHECK(cudaMemsetAsync(yz, 0xFF, getrs_chain_scratch(n, nrhs) * sizeof(double), st));
 }
 
 }  // namespace slb

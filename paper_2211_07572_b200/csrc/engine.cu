@@ -790,28 +790,16 @@ void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
     SLB_CUDA_CHECK(cudaEventRecord(s1, st));
     combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, S, F->strips.p, contrib.p, 0); count_launch();
     // sweep solve (stage_two.hpp:170-188) with the LU factors of S_j
-    // S_j^{-1} v: chained getrs for nrhs <= 8, TRSM/GEMM getrs beyond
+    // S_j^{-1} v from the LU factors of S_j: chained getrs (8-column chains)
     const int64_t bs = n2 * n2;
     const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
-    const bool chain = nrhs <= 8;
     DBuf<double> yz;
-    DBuf<int> flags;
     int epoch = 0;
-    if (chain) {
-      yz.alloc(dev, (size_t)2 * n2 * nrhs);
-      flags.alloc(dev, (size_t)2 * cdiv(n2, 64));
-      SLB_CUDA_CHECK(cudaMemsetAsync(flags.p, 0, flags.bytes(), st));
-    }
+    yz.alloc(dev, (size_t)getrs_chain_scratch(n2, nrhs));
+    getrs_chain_init(st, n2, nrhs, yz.p);
     auto apply_Sinv = [&](int j, const double* v, int64_t ldv, double* out, double alpha, double beta) {
-      if (chain) {
-        getrs_chain(st, n2, nrhs, F->Tdiag() + j * bs, F->dinvT.p + (size_t)j * dinv_sz,
-                    F->permT.p + (size_t)j * n2, v, ldv, out, K, alpha, beta, yz.p, flags.p, ++epoch);
-      } else {  // out = beta*out + alpha*S^{-1} v, v is scratch (tmp)
-        double* w = const_cast<double*>(v);
-        dgetrs(st, n2, nrhs, F->Tdiag() + j * bs, F->ipivT.p + (size_t)j * n2, w, ldv, nullptr);
-        if (beta == 0.0) copy2d(st, w, ldv, out, K, n2, nrhs);
-        else add2d(st, w, ldv, out, K, n2, nrhs, alpha);
-      }
+      getrs_chain(st, n2, nrhs, F->Tdiag() + j * bs, F->dinvT.p + (size_t)j * dinv_sz, F->permT.p + (size_t)j * n2,
+                  v, ldv, out, K, alpha, beta, yz.p, ++epoch);
     };
     for (int j = 0; j < F->K; j++) {
       double* rj = red.p + j * n2;
@@ -1445,7 +1433,7 @@ int slablu_gpu_debug_dense_bench(int64_t n, int device, double* out) {
 }
 
 // Test hook for the stage-two solve kernel: LU-factor the n x n column-major a (host),
-// then x = A^{-1} b (n x nrhs, host) through getrs_chain (nrhs <= 8) or the TRSM getrs.
+// then x = A^{-1} b (n x nrhs, host) through getrs_chain.
 // t_out[0] = average device seconds per getrs over `reps` calls.
 int slablu_gpu_debug_getrs(int64_t n, int64_t nrhs, const double* a, const double* b, double* x, int reps,
                            int device, double* t_out) {
@@ -1456,22 +1444,20 @@ int slablu_gpu_debug_getrs(int64_t n, int64_t nrhs, const double* a, const doubl
     const int64_t dinv_sz = cdiv(n, 64) * 2 * 64 * 64;
     DBuf<double> A, B, X, D, yz;
     DBuf<int32_t> ipiv, perm;
-    DBuf<int> flags;
     DBuf<DevStatus> status;
     A.alloc(device, n * n);
     B.alloc(device, n * nrhs);
     X.alloc(device, n * nrhs);
     D.alloc(device, dinv_sz);
-    yz.alloc(device, 2 * n * nrhs);
+    yz.alloc(device, getrs_chain_scratch(n, nrhs));
     ipiv.alloc(device, n);
     perm.alloc(device, n);
-    flags.alloc(device, 2 * cdiv(n, 64));
     status.alloc(device, 1);
     DevStatus st0{0, INT_MAX, INT_MAX, 0};
     SLB_CUDA_CHECK(cudaMemcpy(status.p, &st0, sizeof(st0), cudaMemcpyHostToDevice));
     SLB_CUDA_CHECK(cudaMemcpy(A.p, a, n * n * sizeof(double), cudaMemcpyHostToDevice));
     SLB_CUDA_CHECK(cudaMemcpy(B.p, b, n * nrhs * sizeof(double), cudaMemcpyHostToDevice));
-    SLB_CUDA_CHECK(cudaMemset(flags.p, 0, flags.bytes()));
+    getrs_chain_init(st, n, nrhs, yz.p);
     dgetrf(st, n, A.p, ipiv.p, nullptr, status.p, 0);
     getrs_prepare(st, n, A.p, ipiv.p, perm.p, D.p);
     cudaEvent_t e0, e1;
@@ -1481,12 +1467,7 @@ int slablu_gpu_debug_getrs(int64_t n, int64_t nrhs, const double* a, const doubl
     reps = std::max(reps, 1);
     SLB_CUDA_CHECK(cudaEventRecord(e0, st));
     for (int r = 0; r < reps; r++) {
-      if (nrhs <= 8) {
-        getrs_chain(st, n, nrhs, A.p, D.p, perm.p, B.p, n, X.p, n, 1.0, 0.0, yz.p, flags.p, ++epoch);
-      } else {
-        copy2d(st, B.p, n, X.p, n, n, nrhs);
-        dgetrs(st, n, nrhs, A.p, ipiv.p, X.p, n, nullptr);
-      }
+      getrs_chain(st, n, nrhs, A.p, D.p, perm.p, B.p, n, X.p, n, 1.0, 0.0, yz.p, ++epoch);
     }
     SLB_CUDA_CHECK(cudaEventRecord(e1, st));
     SLB_CUDA_CHECK(cudaEventSynchronize(e1));

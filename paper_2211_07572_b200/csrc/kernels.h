@@ -161,12 +161,15 @@ void check_finite(cudaStream_t st, const double* a, int64_t count, DevStatus* st
 // inverses of the 64x64 diagonal blocks of L and U (dinv: cdiv(n,64) * 2 * 64 * 64).
 void getrs_prepare(cudaStream_t st, int64_t n, const double* lu, const int32_t* ipiv, int32_t* perm,
                    double* dinv);
-// x = beta*x + alpha * A^{-1} b for nrhs <= 8 with the dgetrf factors (one chained launch).
-// b and x must not alias; yz: 2*n*nrhs scratch; flags: 2*cdiv(n,64) ints, zeroed before the
-// first call; epoch: distinct positive value per call on the same flags.
+// x = beta*x + alpha * A^{-1} b with the dgetrf factors: chains of 8 columns, one launch
+// (plus one for a remainder).  b and x must not alias.  yz: getrs_chain_scratch(n, nrhs)
+// doubles, set up once by getrs_chain_init; epoch: 1, 2, 3, ... on consecutive calls that
+// share yz (stream-ordered).
+inline int64_t getrs_chain_scratch(int64_t n, int64_t nrhs) { return 2 * 16 * n * ((nrhs + 7) / 8); }
+void getrs_chain_init(cudaStream_t st, int64_t n, int64_t nrhs, double* yz);
 void getrs_chain(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const double* dinv,
                  const int32_t* perm, const double* b, int64_t ldb, double* x, int64_t ldx, double alpha,
-                 double beta, double* yz, int* flags, int epoch);
+                 double beta, double* yz, int epoch);
 
 // ---- solve.cu ---------------------------------------------------------------------
 

@@ -15,7 +15,7 @@ L.slablu_gpu_debug_getrs.argtypes = [ctypes.c_int64, ctypes.c_int64, P, P, P, ct
 rng = np.random.default_rng(0)
 for n in [int(a) for a in (sys.argv[1:] or ["1000", "4000"])]:
     A = np.asfortranarray(rng.standard_normal((n, n)))
-    for nrhs in (1, 8, 16):
+    for nrhs in (1, 8, 16, 64):
         B = np.asfortranarray(rng.standard_normal((n, nrhs)))
         X = np.zeros((n, nrhs), order="F")
         t = np.zeros(1)
