@@ -211,21 +211,23 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
 // [k1, n): idx[r - k1] = source row of row r.  One CTA, swaps replayed in
 // shared memory by one thread (n - k1 <= 8192).
 __global__ void swap_perm_kernel(const int32_t* ipiv, int64_t n, int64_t k1, int64_t k2, int32_t* idx) {
-  extern __shared__ int32_t sidx[];
+  // rows and pivots as int16 in shared memory (n - k1 <= 8192): the serial replay touches
+  // shared memory only
+  extern __shared__ int16_t sidx[];
+  int16_t* spiv = sidx + (n - k1);
   const int64_t m = n - k1;
-  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) sidx[r] = (int32_t)(k1 + r);
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) sidx[r] = (int16_t)r;
+  for (int64_t k = k1 + threadIdx.x; k < k2; k += blockDim.x) spiv[k - k1] = (int16_t)(ipiv[k] - k1);
   __syncthreads();
   if (threadIdx.x == 0)
-    for (int64_t k = k1; k < k2; k++) {
-      const int64_t p = ipiv[k];
-      if (p != k) {
-        const int32_t t = sidx[k - k1];
-        sidx[k - k1] = sidx[p - k1];
-        sidx[p - k1] = t;
-      }
+    for (int64_t k = 0; k < k2 - k1; k++) {
+      const int p = spiv[k];
+      const int16_t t = sidx[k];
+      sidx[k] = sidx[p];
+      sidx[p] = t;
     }
   __syncthreads();
-  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) idx[r] = sidx[r];
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) idx[r] = (int32_t)(k1 + sidx[r]);
 }
 // tmp[c][r] = A[c][idx[r]] for rows [k1, n) of columns [c0, c1)
 __global__ void gather_rows_kernel(const double* A, int64_t lda, int64_t c0, int64_t c1, int64_t k1, int64_t m,
@@ -340,7 +342,7 @@ void laswp(cudaStream_t st, double* A, int64_t lda, int64_t c0, int64_t c1, cons
     SLB_CUDA_CHECK(cudaMalloc(&S.tmp, m * nc * sizeof(double)));
     S.tmp_n = m * nc;
   }
-  swap_perm_kernel<<<1, 1024, m * sizeof(int32_t), st>>>(ipiv, n, k1, k2, S.idx); count_launch();
+  swap_perm_kernel<<<1, 1024, (m + (k2 - k1)) * sizeof(int16_t), st>>>(ipiv, n, k1, k2, S.idx); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
   for (int64_t cb = 0; cb < nc; cb += 65535) {
     const int64_t ncb = std::min<int64_t>(65535, nc - cb);
@@ -703,7 +705,7 @@ void getrs_prepare(cudaStream_t st, int64_t n, const double* lu, const int32_t* 
                    double* dinv) {
   if (n <= 0) return;
   if (n > 8192) throw CudaFailure(cudaErrorInvalidValue, "getrs_prepare: n must be <= 8192", __FILE__, __LINE__);
-  swap_perm_kernel<<<1, 1024, n * sizeof(int32_t), st>>>(ipiv, n, 0, n, perm); count_launch();
+  swap_perm_kernel<<<1, 1024, 2 * n * sizeof(int16_t), st>>>(ipiv, n, 0, n, perm); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
   diag_inverse_kernel<<<dim3((unsigned)cdiv(n, CT), 2), CT, 0, st>>>((int)n, lu, dinv); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
