@@ -233,8 +233,7 @@ struct slablu_gpu_fact {
   DBuf<double> hcol;    // x_{l+2} columns of H per (strip, level): 8 x Wp
   DBuf<int32_t> hidx;   // their column indices
   DBuf<double> T;       // [diag k | super k-1 | sub k-1] blocks, n2 x n2; diag holds LU(S_j) (ipivT)
-                        // or, in a sharded factorization, S_j^{-1}
-  DBuf<int32_t> ipivT;  // pivots of LU(S_j), n2 per interface (unsharded)
+  DBuf<int32_t> ipivT;  // pivots of LU(S_j), n2 per interface
   DBuf<int32_t> permT;  // the same interchanges as a row permutation (getrs_chain)
   DBuf<double> dinvT;   // inverses of the 64x64 diagonal blocks of L_j, U_j (getrs_chain)
   DBuf<double> Tkeep;   // optional copy of the reduced blocks
@@ -936,30 +935,28 @@ void shard_sweep_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
   SLB_CUDA_CHECK(cudaEventCreate(&e1));
   SLB_CUDA_CHECK(cudaEventRecord(e0, st));
   if (F->rank > 0) add2d(st, d_in, n2, F->Tdiag() + j0 * bs, n2, n2, n2);
-  DBuf<double> X, I;
-  DBuf<int32_t> ipiv;
+  // S_j in LU form as in the unsharded sweep (DenseLU, stage_two.hpp:138-147)
+  const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
+  F->ipivT.alloc(dev, (size_t)std::max(F->K, 1) * n2);
+  F->permT.alloc(dev, (size_t)std::max(F->K, 1) * n2);
+  F->dinvT.alloc(dev, (size_t)std::max(F->K, 1) * dinv_sz);
+  DBuf<double> X;
   X.alloc(dev, bs);
-  I.alloc(dev, bs);
-  ipiv.alloc(dev, n2);
+  auto sub_Sinv_super = [&](int j, double* target) {  // target -= sub_j S_j^{-1} super_j
+    SLB_CUDA_CHECK(cudaMemcpyAsync(X.p, F->Tsup() + j * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    dgetrs(st, n2, n2, F->Tdiag() + j * bs, F->ipivT.p + (size_t)j * n2, X.p, n2, nullptr);
+    dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + j * bs, n2, 0, X.p, n2, 0, 1.0, target, n2, 0, 1);
+  };
   for (int j = j0; j < j1; j++) {
     double* Sj = F->Tdiag() + j * bs;
-    if (j > j0) {
-      dgemm_batched(st, n2, n2, n2, 1.0, F->Tdiag() + (j - 1) * bs, n2, 0, F->Tsup() + (j - 1) * bs, n2, 0, 0.0, X.p,
-                    n2, 0, 1);
-      dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X.p, n2, 0, 1.0, Sj, n2, 0, 1);
-    }
-    dgetrf(st, n2, Sj, ipiv.p, nullptr, F->status.p, j);
-    dset_identity(st, I.p, n2);
-    dgetrs(st, n2, n2, Sj, ipiv.p, I.p, n2, nullptr);
-    SLB_CUDA_CHECK(cudaMemcpyAsync(Sj, I.p, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (j > j0) sub_Sinv_super(j - 1, Sj);
+    dgetrf(st, n2, Sj, F->ipivT.p + (size_t)j * n2, nullptr, F->status.p, j);
+    getrs_prepare(st, n2, Sj, F->ipivT.p + (size_t)j * n2, F->permT.p + (size_t)j * n2,
+                  F->dinvT.p + (size_t)j * dinv_sz);
   }
   if (F->rank < F->nranks - 1) {
     SLB_CUDA_CHECK(cudaMemcpyAsync(d_out, F->Tdiag() + j1 * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    if (j1 > j0) {
-      dgemm_batched(st, n2, n2, n2, 1.0, F->Tdiag() + (j1 - 1) * bs, n2, 0, F->Tsup() + (j1 - 1) * bs, n2, 0, 0.0,
-                    X.p, n2, 0, 1);
-      dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j1 - 1) * bs, n2, 0, X.p, n2, 0, 1.0, d_out, n2, 0, 1);
-    }
+    if (j1 > j0) sub_Sinv_super(j1 - 1, d_out);
   }
   SLB_CUDA_CHECK(cudaEventRecord(e1, st));
   SLB_CUDA_CHECK(cudaEventSynchronize(e1));
@@ -1010,13 +1007,19 @@ void shard_solve_fwd_impl(slablu_gpu_fact* F, const double* d_f, int64_t ldf, in
   double* red = F->sh_red.p;
   double* uifc = F->sh_uifc.p;
   if (F->rank > 0) add2d(st, d_in, n2, red + j0 * n2, Kn, n2, nrhs);
+  const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
+  DBuf<double> yz;
+  yz.alloc(dev, (size_t)getrs_chain_scratch(n2, nrhs));
+  getrs_chain_init(st, n2, nrhs, yz.p);
+  int epoch = 0;
   for (int j = j0; j < j1; j++) {
     double* rj = red + j * n2;
     if (j > j0) {
       dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j - 1) * bs, n2, uifc + (j - 1) * n2, Kn, 1.0, rj, Kn,
                         part.p);
     }
-    dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tdiag() + j * bs, n2, rj, Kn, 0.0, uifc + j * n2, Kn, part.p);
+    getrs_chain(st, n2, nrhs, F->Tdiag() + j * bs, F->dinvT.p + (size_t)j * dinv_sz, F->permT.p + (size_t)j * n2, rj,
+                Kn, uifc + j * n2, Kn, 1.0, 0.0, yz.p, ++epoch);
   }
   if (F->rank < F->nranks - 1) {
     copy2d(st, red + j1 * n2, Kn, d_out, n2, n2, nrhs);
@@ -1050,10 +1053,16 @@ void shard_solve_bwd_impl(slablu_gpu_fact* F, const double* d_in, double* d_out,
   tmp.alloc(dev, (size_t)n2 * nrhs);
   part.alloc(dev, (size_t)8 * n2 * nrhs);
   if (F->rank < F->nranks - 1) copy2d(st, d_in, n2, uifc + j1 * n2, Kn, n2, nrhs);
+  const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
+  DBuf<double> yz;
+  yz.alloc(dev, (size_t)getrs_chain_scratch(n2, nrhs));
+  getrs_chain_init(st, n2, nrhs, yz.p);
+  int epoch = 0;
   for (int j = j1 - 1; j >= j0; j--) {
     if (j + 1 >= F->K) continue;
     dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tsup() + j * bs, n2, uifc + (j + 1) * n2, Kn, 0.0, tmp.p, n2, part.p);
-    dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tdiag() + j * bs, n2, tmp.p, n2, 1.0, uifc + j * n2, Kn, part.p);
+    getrs_chain(st, n2, nrhs, F->Tdiag() + j * bs, F->dinvT.p + (size_t)j * dinv_sz, F->permT.p + (size_t)j * n2,
+                tmp.p, n2, uifc + j * n2, Kn, -1.0, 1.0, yz.p, ++epoch);
   }
   if (F->rank > 0) copy2d(st, uifc + j0 * n2, Kn, d_out, n2, n2, nrhs);
   StripSweeper sw(F, F->sh_f.p, nrhs);
