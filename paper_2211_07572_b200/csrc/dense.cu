@@ -584,9 +584,10 @@ __global__ void __launch_bounds__(256) getrs_chain_kernel(int n, int nb, const d
     nxt += (int64_t)chain * 16 * n;
   }
   const int cta = (int)blockIdx.x % (2 * nb);
-  __shared__ double red[4][CT][NR];
-  __shared__ double vt[2][CT][NR];
-  __shared__ double vs[CT][NR];
+  // row / k index innermost: lanes touch consecutive words (no bank conflicts)
+  __shared__ double red[4][NR][CT];
+  __shared__ double vt[2][NR][CT];
+  __shared__ double vs[NR][CT];
   const int t = threadIdx.x, r = t & (CT - 1), kq = t >> 6;
   const bool lower = cta < nb;
   const int i = lower ? cta : nb - 1 - (cta - nb);
@@ -652,14 +653,14 @@ __global__ void __launch_bounds__(256) getrs_chain_kernel(int n, int nb, const d
 #pragma unroll
     for (int m = 0; m < PER; m++) {
       const int e = t + 256 * m, tile = e / (CT * NR), rem = e % (CT * NR), c = rem / CT, k = rem % CT;
-      if (e < 2 * CT * NR) vt[tile][k][c] = __longlong_as_double((long long)v[m]);
+      if (e < 2 * CT * NR) vt[tile][c][k] = __longlong_as_double((long long)v[m]);
     }
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < 16; u++) {
       const int k = kq * 16 + u;
 #pragma unroll
-      for (int c = 0; c < NR; c++) acc[c] = fma(a1[u], vt[1][k][c], fma(a0[u], vt[0][k][c], acc[c]));
+      for (int c = 0; c < NR; c++) acc[c] = fma(a1[u], vt[1][c][k], fma(a0[u], vt[0][c][k], acc[c]));
     }
   }
   if (!lower && row_owner) {  // upper: this block's right-hand side is y_i from lower CTA i
@@ -671,26 +672,26 @@ __global__ void __launch_bounds__(256) getrs_chain_kernel(int n, int nb, const d
     }
   }
 #pragma unroll
-  for (int c = 0; c < NR; c++) red[kq][r][c] = acc[c];
+  for (int c = 0; c < NR; c++) red[kq][c][r] = acc[c];
   __syncthreads();
   if (t < CT) {
 #pragma unroll
     for (int c = 0; c < NR; c++)
-      vs[r][c] = r < mrow ? rhs[c] - (red[0][r][c] + red[1][r][c] + red[2][r][c] + red[3][r][c]) : 0.0;
+      vs[c][r] = r < mrow ? rhs[c] - (red[0][c][r] + red[1][c][r] + red[2][c][r] + red[3][c][r]) : 0.0;
   }
   __syncthreads();
 #pragma unroll
   for (int c = 0; c < NR; c++) {  // out = Dinv_i * (rhs - off-diagonal sum)
     double s = 0.0;
 #pragma unroll
-    for (int u = 0; u < 16; u++) s = fma(d[u], vs[kq * 16 + u][c], s);
-    red[kq][r][c] = s;
+    for (int u = 0; u < 16; u++) s = fma(d[u], vs[c][kq * 16 + u], s);
+    red[kq][c][r] = s;
   }
   __syncthreads();
   if (row_owner) {
 #pragma unroll
     for (int c = 0; c < NR; c++) {
-      const double o = red[0][r][c] + red[1][r][c] + red[2][r][c] + red[3][r][c];
+      const double o = red[0][c][r] + red[1][c][r] + red[2][c][r] + red[3][c][r];
       st_relaxed_f64(&own[(int64_t)c * n + r0 + r], o);  // publishes the value
       if (!lower) {
         double* xo = x + (int64_t)c * ldx + r0 + r;
