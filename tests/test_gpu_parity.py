@@ -283,3 +283,28 @@ def test_stage_two_getrs_vs_numpy(n, nrhs):
     cond = np.linalg.cond(A)
     assert np.linalg.norm(X - ref) / np.linalg.norm(ref) <= max(1e-10, 1e-14 * cond)
     assert np.linalg.norm(A @ X - B) / (np.linalg.norm(A) * np.linalg.norm(X)) <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(120)
+def test_stage_two_getrs_nonfinite_rhs_terminates():
+    """Blocks of the chained getrs are published as data against a sentinel NaN pattern;
+    NaN/Inf right-hand sides must propagate (canonicalised NaN), never stall the chain."""
+    import ctypes
+    from paper_2211_07572_b200 import _lib
+    L = _lib.lib()
+    P = ctypes.POINTER(ctypes.c_double)
+    L.slablu_gpu_debug_getrs.restype = ctypes.c_int
+    L.slablu_gpu_debug_getrs.argtypes = [ctypes.c_int64, ctypes.c_int64, P, P, P, ctypes.c_int, ctypes.c_int, P]
+    n, nrhs = 300, 3
+    rng = np.random.default_rng(7)
+    A = np.asfortranarray(rng.standard_normal((n, n)))
+    B = np.asfortranarray(rng.standard_normal((n, nrhs)))
+    B[5, 0] = np.nan
+    B[7, 1] = np.inf
+    B.view(np.uint64)[11, 2] = np.uint64(0xFFFFFFFFFFFFFFFF)  # the sentinel pattern itself
+    X = np.zeros((n, nrhs), order="F")
+    t = np.zeros(1)
+    assert L.slablu_gpu_debug_getrs(n, nrhs, A.ctypes.data_as(P), B.ctypes.data_as(P), X.ctypes.data_as(P), 2, 0,
+                                    t.ctypes.data_as(P)) == 0
+    assert np.isnan(X).any(axis=0).all()
