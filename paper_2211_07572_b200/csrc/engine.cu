@@ -512,10 +512,17 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     }
   };
   int cur = 0;
+  int64_t conv_done = 0;  // levels [0, conv_done) handed to the conversion stream
   for (int64_t l = 0; l < n2; l++) {
     const int64_t nxt = l + 1;
     const bool has_next = nxt < n2;
-    if (l > 0 && l % CCH == 0 && !defer_conv) convert_chunk(l - CCH, l);
+    // chunks of CCH levels; 64-level chunks over the last 2 CCH levels so that little
+    // conversion is left once the chain ends
+    const int64_t cch = (n2 - l <= 2 * CCH) ? std::min<int64_t>(CCH, 64) : CCH;
+    if (!defer_conv && l - conv_done >= cch) {
+      convert_chunk(conv_done, l);
+      conv_done = l;
+    }
     if (has_next && nxt % LCH == 0) {
       extract_levels(st, A, F->strips.p, S, n2, Wp, nxt, std::min(LCH, n2 - nxt), nx.p, sNX, F->status.p,
                      F->dsub.p, F->lnd.p);
@@ -550,7 +557,8 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     SLB_CUDA_CHECK(cudaEventRecord(chain_end, st));
     for (int64_t c0 = 0; c0 + CCH < n2; c0 += CCH) convert_chunk(c0, c0 + CCH);
   }
-  convert_chunk(((n2 - 1) / CCH) * CCH, n2);
+  if (!defer_conv) convert_chunk(conv_done, n2);
+  else convert_chunk(((n2 - 1) / CCH) * CCH, n2);
   SLB_CUDA_CHECK(cudaEventRecord(chunk_ev, cst));
   SLB_CUDA_CHECK(cudaStreamWaitEvent(st, chunk_ev, 0));
   SLB_CUDA_CHECK(cudaEventDestroy(chunk_ev));
