@@ -42,13 +42,21 @@ __device__ __forceinline__ void panel_cluster_barrier() {
   asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory");
 }
 
-// r[k] for a runtime k without local memory or branches (selects over the unrolled row)
+// r[k] for a runtime k without local memory or branches: a select tree on the bits of k
+// (depth log2 N instead of a chain of N dependent selects)
 template <int N>
 __device__ __forceinline__ double pick(const double (&r)[N], int k) {
-  double x = 0.0;
+  static_assert(N == 32, "pick: 32-wide rows");
+  double t16[16], t8[8], t4[4], t2[2];
 #pragma unroll
-  for (int c = 0; c < N; c++) x = c == k ? r[c] : x;
-  return x;
+  for (int c = 0; c < 16; c++) t16[c] = (k & 16) ? r[c + 16] : r[c];
+#pragma unroll
+  for (int c = 0; c < 8; c++) t8[c] = (k & 8) ? t16[c + 8] : t16[c];
+#pragma unroll
+  for (int c = 0; c < 4; c++) t4[c] = (k & 4) ? t8[c + 4] : t8[c];
+#pragma unroll
+  for (int c = 0; c < 2; c++) t2[c] = (k & 2) ? t4[c + 2] : t4[c];
+  return (k & 1) ? t2[1] : t2[0];
 }
 
 __device__ __forceinline__ void better(double& v, int& vi, double ov, int oi) {
