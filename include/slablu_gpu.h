@@ -12,6 +12,10 @@
  *   slablu_gpu_stats           <- Factorization fields    (driver.hpp:72-87)
  *   slablu_gpu_T_block         <- ReducedSystem blocks    (stage_one.hpp:303-338, staged parity)
  *   slablu_gpu_reduce_rhs      <- reduce_rhs              (stage_one.hpp:415-433, staged parity)
+ *   slablu_gpu_sweep_solve     <- sweep_solve             (stage_two.hpp:245-248 -> 170-188, staged)
+ *   slablu_gpu_recover         <- recover_interiors       (stage_one.hpp:438-462, staged)
+ *   slablu_gpu_sweep_build     <- sweep_build / SweepFactorization(BlockTridiagonal)
+ *                                                         (stage_two.hpp:41-56, 131-150, 241-243)
  *   slablu_gpu_destroy         <- ~Factorization
  *   slablu_gpu_shard_*         <- (no reference counterpart: the multi-GPU split of
  *                                 factorize/solve designed in SURVEY.md §8(e))
@@ -144,6 +148,19 @@ slablu_gpu_status slablu_gpu_T_block(const slablu_gpu_fact* fact, int which, int
 /* Staged reduce_rhs: out (k*n2 x nrhs) from host f (n x nrhs, ld n). */
 slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* fact, const double* f, int64_t nrhs,
                                         double* out);
+/* Staged sweep solve: u_ifc (k*n2 x nrhs) = T^{-1} red through the LU factors of S_j (host buffers). */
+slablu_gpu_status slablu_gpu_sweep_solve(const slablu_gpu_fact* fact, const double* red, int64_t nrhs,
+                                         double* u_ifc);
+/* sweep_build on a caller's block-tridiagonal system (host): blocks = [diag 0..k-1 | super
+ * 0..k-2 | sub 0..k-2], each m x m column major.  Rejects k < 1 (ConfigError) and non-finite
+ * entries (Error); a singular S_j raises SingularMatrixError(j).  The handle serves
+ * slablu_gpu_sweep_solve (m*k x nrhs) and slablu_gpu_stats; release with slablu_gpu_destroy. */
+slablu_gpu_status slablu_gpu_sweep_build(int64_t m, int64_t k, const double* blocks, int device,
+                                         slablu_gpu_fact** out);
+/* Staged recover_interiors: u (n x nrhs, ld n) from f (n x nrhs, ld n) and u_ifc (k*n2 x nrhs);
+ * interface entries of u are copied from u_ifc (host buffers). */
+slablu_gpu_status slablu_gpu_recover(const slablu_gpu_fact* fact, const double* f, const double* u_ifc,
+                                     int64_t nrhs, double* u);
 void slablu_gpu_destroy(slablu_gpu_fact* fact);
 
 /* ---- multi-GPU: strip-sharded factorization and solve ----------------------

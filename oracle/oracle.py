@@ -78,6 +78,12 @@ def lib():
         L.orc_time_slab_sample.argtypes = [P, Lg, Lg, Lg, P, P]
         L.orc_time_sweep_step.argtypes = [Lg, P]
         L.orc_gaussian_matrix.argtypes = [Lg, Lg, ctypes.c_uint64, P]
+        L.orc_slab_factor.argtypes = [P, Lg, Lg, P]
+        L.orc_slab_free.argtypes = [P]
+        L.orc_slab_info.argtypes = [P, P]
+        L.orc_slab_contrib.argtypes = [P, P, Lg, P, P]
+        L.orc_slab_T_columns.argtypes = [P, I, P, Lg, P, P]
+        L.orc_slab_recover.argtypes = [P, P, P, Lg, P]
         L.orc_set_blas_threads.argtypes = [I]
         L.orc_get_blas_threads.restype = I
         _lib = L
@@ -254,6 +260,56 @@ def factorize(system, b=0, c=0.6, threads=1, chunk=0, keep_T=False):
     hdl = ctypes.c_void_p()
     _check(lib().orc_factorize(system._h, int(b), float(c), int(threads), int(chunk), int(keep_T), ctypes.byref(hdl)))
     return Factorization(hdl.value, system)
+
+
+class Slab:
+    """One slab interior factored alone (factor_one_interior, inc/stage_one.hpp:163-238) and
+    its per-slab stage-one / solve terms, for staged parity at sizes where the whole oracle
+    factorization does not fit (tests only)."""
+
+    def __init__(self, system, b, strip):
+        hdl = ctypes.c_void_p()
+        _check(lib().orc_slab_factor(system._h, int(b), int(strip), ctypes.byref(hdl)))
+        self._h = ctypes.c_void_p(hdl.value)
+        self.system = system
+        info = np.zeros(4, np.int64)
+        lib().orc_slab_info(self._h, _ptr(info))
+        self.first_col, self.width, self.left_ifc, self.right_ifc = (int(v) for v in info)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                lib().orc_slab_free(self._h)
+            except Exception:
+                pass
+            self._h = None
+
+    def contrib(self, f):
+        """(to_left A^-1 f_i, to_right A^-1 f_i), each n2 x nrhs (reduce_rhs :423-432)."""
+        n, n2 = self.system.dim, self.system.n2
+        f = np.asfortranarray(np.asarray(f, np.float64).reshape(n, -1))
+        oL = np.empty((n2, f.shape[1]), order="F")
+        oR = np.empty((n2, f.shape[1]), order="F")
+        _check(lib().orc_slab_contrib(self._h, _ptr(f), f.shape[1], _ptr(oL), _ptr(oR)))
+        return oL, oR
+
+    def T_columns(self, side, cols):
+        """(to_left, to_right) . A^-1 . from_side[:, cols] (side 'left' | 'right')."""
+        n2 = self.system.n2
+        c = np.ascontiguousarray(cols, np.int64)
+        oL = np.empty((n2, c.size), order="F")
+        oR = np.empty((n2, c.size), order="F")
+        _check(lib().orc_slab_T_columns(self._h, 0 if side == "left" else 1, _ptr(c), c.size, _ptr(oL), _ptr(oR)))
+        return oL, oR
+
+    def recover(self, f, u_ifc):
+        """A^-1 (f_i - from_L u_L - from_R u_R) in natural order ((width*n2) x nrhs)."""
+        n, n2 = self.system.dim, self.system.n2
+        f = np.asfortranarray(np.asarray(f, np.float64).reshape(n, -1))
+        u_ifc = np.asfortranarray(np.asarray(u_ifc, np.float64).reshape(-1, f.shape[1]))
+        out = np.empty((self.width * n2, f.shape[1]), order="F")
+        _check(lib().orc_slab_recover(self._h, _ptr(f), _ptr(u_ifc), f.shape[1], _ptr(out)))
+        return out
 
 
 def time_slab_sample(system, b, strip, nrhs_sample):

@@ -1075,4 +1075,91 @@ void orc_gaussian_matrix(long rows, long cols, uint64_t seed, double* out) {
     for (long i = 0; i < rows; i++) out[j * rows + i] = gauss(rng);
 }
 
+// ---------------------------------------------------------------------------
+// Per-slab staged checks (test infrastructure): one slab interior factored on
+// its own (factor_one_interior, inc/stage_one.hpp:163-238), then the three
+// per-slab terms of the reference's stage one / solve, so that parity can be
+// checked at sizes where the whole oracle factorization does not fit:
+//   contrib  : to_left/to_right . A_ii^{-1} permute_in(f_i)   (reduce_rhs :423-432)
+//   T columns: to_X . A_ii^{-1} from_Y[:, cols]                (apply_T_block :276-283)
+//   recover  : A_ii^{-1}(f_i - from_L u_L - from_R u_R)        (recover_interiors :447-459)
+struct orc_slab {
+  SlabFactor f;
+  long N = 0, K = 0;
+};
+int orc_slab_factor(const orc_system* s, long b, long strip, orc_slab** out) {
+  ORC_TRY({
+    Partition p = partition(s->sys.n1, s->sys.n2, b);
+    if (strip < 0 || strip >= p.nint()) fail(ERR_GENERIC, "slab_factor: strip out of range");
+    auto* h = new orc_slab;
+    try {
+      h->f = factor_one_interior(s->sys, p, strip);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    h->N = p.dim();
+    h->K = p.nifc() * p.n2;
+    *out = h;
+  })
+}
+void orc_slab_free(orc_slab* h) { delete h; }
+// [first_col, width, left_ifc, right_ifc]
+void orc_slab_info(const orc_slab* h, long* info) {
+  info[0] = h->f.first_col;
+  info[1] = h->f.width;
+  info[2] = h->f.left_ifc;
+  info[3] = h->f.right_ifc;
+}
+// f: N x nrhs (ld N) natural order; outL/outR: n2 x nrhs (zero for an absent side)
+int orc_slab_contrib(const orc_slab* h, const double* f, long nrhs, double* outL, double* outR) {
+  ORC_TRY({
+    const SlabFactor& fc = h->f;
+    const long m = fc.rows(), n2 = fc.n2;
+    std::vector<double> g(m * nrhs);
+    fc.permute_in(f + fc.first_col * n2, h->N, nrhs, g.data());
+    fc.lu.solve(g.data(), nrhs, false);
+    std::fill(outL, outL + n2 * nrhs, 0.0);
+    std::fill(outR, outR + n2 * nrhs, 0.0);
+    if (fc.left_ifc >= 0) sparse_apply(fc.to_left, false, g.data(), nrhs, outL);
+    if (fc.right_ifc >= 0) sparse_apply(fc.to_right, false, g.data(), nrhs, outR);
+  })
+}
+// side: 0 from_left, 1 from_right; cols: ncol interface row indices (identity columns);
+// outL/outR: n2 x ncol = to_left / to_right . A_ii^{-1} from_side[:, cols]
+int orc_slab_T_columns(const orc_slab* h, int side, const long* cols, long ncol, double* outL, double* outR) {
+  ORC_TRY({
+    const SlabFactor& fc = h->f;
+    const long m = fc.rows(), n2 = fc.n2;
+    const Sparse& in_blk = side == 0 ? fc.from_left : fc.from_right;
+    if ((side == 0 ? fc.left_ifc : fc.right_ifc) < 0) fail(ERR_GENERIC, "slab_T_columns: no interface on that side");
+    std::vector<double> x(n2 * ncol, 0.0), tmp(m * ncol);
+    for (long c = 0; c < ncol; c++) x[c * n2 + cols[c]] = 1.0;
+    sparse_apply(in_blk, false, x.data(), ncol, tmp.data());
+    fc.lu.solve(tmp.data(), ncol, false);
+    std::fill(outL, outL + n2 * ncol, 0.0);
+    std::fill(outR, outR + n2 * ncol, 0.0);
+    if (fc.left_ifc >= 0) sparse_apply(fc.to_left, false, tmp.data(), ncol, outL);
+    if (fc.right_ifc >= 0) sparse_apply(fc.to_right, false, tmp.data(), ncol, outR);
+  })
+}
+// u_ifc: K x nrhs (ld K); out: (width*n2) x nrhs in natural order (ix*n2 + iy)
+int orc_slab_recover(const orc_slab* h, const double* f, const double* u_ifc, long nrhs, double* out) {
+  ORC_TRY({
+    const SlabFactor& fc = h->f;
+    const long m = fc.rows(), n2 = fc.n2;
+    std::vector<double> rhs(m * nrhs), tmp(m * nrhs), ui(n2 * nrhs);
+    fc.permute_in(f + fc.first_col * n2, h->N, nrhs, rhs.data());
+    auto sub_coupling = [&](const Sparse& sp, long ifc) {
+      for (long c = 0; c < nrhs; c++) std::memcpy(&ui[c * n2], u_ifc + c * h->K + ifc * n2, n2 * sizeof(double));
+      sparse_apply(sp, false, ui.data(), nrhs, tmp.data());
+      for (long i = 0; i < m * nrhs; i++) rhs[i] -= tmp[i];
+    };
+    if (fc.left_ifc >= 0) sub_coupling(fc.from_left, fc.left_ifc);
+    if (fc.right_ifc >= 0) sub_coupling(fc.from_right, fc.right_ifc);
+    fc.lu.solve(rhs.data(), nrhs, false);
+    fc.permute_out(rhs.data(), nrhs, out, m);
+  })
+}
+
 }  // extern "C"

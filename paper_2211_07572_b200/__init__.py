@@ -5,8 +5,8 @@ solve); compute runs in hand-written sm_100a kernels behind the C ABI in
 include/slablu_gpu.h (libslablu_gpu.so, built in-tree).
 """
 from .slablu import (  # noqa: F401
-    CompressionChoice, ConfigError, Error, ErrorReport, Factorization, GridStrip, ProblemSpec,
-    SingularMatrixError, SlabPartition, SolverConfig, SparseSystem, UnsupportedError, assemble_fd5,
+    BlockTridiagonal, CompressionChoice, ConfigError, Error, ErrorReport, Factorization, GridStrip, ProblemSpec,
+    SingularMatrixError, SlabPartition, SweepFactorization, sweep_build, SolverConfig, SparseSystem, UnsupportedError, assemble_fd5,
     bessel_j0, choose_b, device_count, error_report, factorize, factorize_device, gaussian_matrix,
     helmholtz_bump_problem, helmholtz_problem, kappa_from_ppw, partition, poisson_log_problem,
     run_problem, sample_field, sample_solution, solve, solve_device, true_solution_helmholtz,

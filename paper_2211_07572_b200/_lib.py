@@ -50,7 +50,8 @@ EXPORTS = [
     "slablu_gpu_stats", "slablu_gpu_T_block", "slablu_gpu_reduce_rhs", "slablu_gpu_destroy",
     "slablu_gpu_device_count", "slablu_gpu_shard_plan", "slablu_gpu_shard_factorize_device",
     "slablu_gpu_shard_sweep", "slablu_gpu_shard_solve_forward", "slablu_gpu_shard_solve_backward",
-    "slablu_gpu_residual",
+    "slablu_gpu_residual", "slablu_gpu_sweep_solve", "slablu_gpu_recover",
+    "slablu_gpu_sweep_build",
 ]
 
 _lib = None

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   auto Pval = [&](int p, int j) -> double {
     return p < Wp ? SV[(int64_t)j * Wp + p] : NX[(int64_t)j * Wp + (p - Wp)];
   };
-  if (tid == 0) s_sing = 0;
+  if (tid == 0) s_sing = -1;
 
   const int init_rows = rows_total < NW ? rows_total : NW;
   for (int idx = tid; idx < init_rows * Wp; idx += blockDim.x) {
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
         QP(1)
         if (!(gm > 0.0)) {
           r = c;
-          if (pt == 0) s_sing = 1;
+          if (pt == 0 && s_sing < 0) s_sing = c;  // first zero pivot column of this level
         }
         // the winner publishes its row; positions c and r exchange
 #pragma unroll
@@ -493,9 +493,10 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   } else {
     for (int idx = tid; idx < 3 * Wp * Wp; idx += blockDim.x) L21[idx] = 0.0;  // L21 and U1213
   }
-  if (tid == 0 && s_sing) {
+  if (tid == 0 && s_sing >= 0) {
     atomicOr(&a.status->flags, ERR_SINGULAR);
     atomicMin(&a.status->singular_strip, s);
+    if (a.nstrips == 1) atomicMin(&a.status->singular_pos, a.level * Wp + s_sing);  // single-slab path
   }
 }
 
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
   auto Pval = [&](int p, int j) -> double {
     return p < Wp ? SV[(int64_t)j * Wp + p] : NX[(int64_t)j * Wp + (p - Wp)];
   };
-  if (tid == 0) s_sing = 0;
+  if (tid == 0) s_sing = -1;
   const int init_rows = rows_total < NW ? rows_total : NW;
   for (int idx = tid; idx < init_rows * Wp; idx += blockDim.x) {
     const int j = idx / init_rows, p = idx % init_rows;
@@ -606,7 +607,7 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
       }
       if (!(gm > 0.0)) {
         r = c;
-        if (pt == 0) s_sing = 1;
+        if (pt == 0 && s_sing < 0) s_sing = c;  // first zero pivot column of this level
       }
 #pragma unroll
       for (int i = 0; i < RPL; i++)
@@ -795,9 +796,10 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
   } else {
     for (int idx = tid; idx < 3 * Wp * Wp; idx += blockDim.x) L21[idx] = 0.0;  // L21 and U1213
   }
-  if (tid == 0 && s_sing) {
+  if (tid == 0 && s_sing >= 0) {
     atomicOr(&a.status->flags, ERR_SINGULAR);
     atomicMin(&a.status->singular_strip, s);
+    if (a.nstrips == 1) atomicMin(&a.status->singular_pos, a.level * Wp + s_sing);  // single-slab path
   }
 }
 

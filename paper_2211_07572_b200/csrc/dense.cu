@@ -9,6 +9,7 @@
 // registers, pivot search reduced through distributed shared memory).  All
 // bulk work is DMMA GEMM (gemm.cu) with large K from the recursion.
 // trsm: recursive, 64-row leaves solved per right-hand-side column.
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cooperative_groups.h>
@@ -528,9 +529,13 @@ void dgemv_batched_rhs(cudaStream_t st, int64_t m, int64_t n, int64_t nrhs, doub
 // pattern that no computation can produce (NaN results are canonicalised).
 // The y/z scratch holds two sets used on alternating calls; each CTA resets
 // its own block of the other set to the sentinel, ready for the next call.
-// Polls only ever wait on lower CTA indices of the same chain (deadlock-free
-// for any residency) and are bounded (a broken chain returns garbage, it
-// does not hang the device).
+// Polls only ever wait on lower CTA indices of the same chain.  That is
+// deadlock-free when every CTA of a launch is resident at once, which the
+// launcher guarantees by sizing each launch to the occupancy limit (CTAs are
+// not guaranteed to be dispatched in blockIdx order, so a launch larger than
+// the resident capacity could park waiting CTAs ahead of the ones they wait
+// on).  Polls are bounded: an expired spin raises ERR_CHAIN_TIMEOUT in the
+// status word, which the solve reports as an error instead of returning data.
 namespace {
 constexpr int CT = 64;
 constexpr unsigned long long kSentinel = 0xFFFFFFFFFFFFFFFFull;
@@ -583,7 +588,8 @@ __global__ void __launch_bounds__(256) getrs_chain_kernel(int n, int nb, const d
                                                           const double* __restrict__ dinv,
                                                           const int32_t* __restrict__ perm, const double* b,
                                                           int64_t ldb, double* x, int64_t ldx, double alpha,
-                                                          double beta, double* cur, double* nxt) {
+                                                          double beta, double* cur, double* nxt,
+                                                          DevStatus* status) {
   {  // chain = 8-column group: its own columns and scratch (y at +0, z at +8n)
     const int chain = (int)blockIdx.x / (2 * nb);
     b += (int64_t)chain * NR * ldb;
@@ -647,7 +653,7 @@ __global__ void __launch_bounds__(256) getrs_chain_kernel(int n, int nb, const d
       vp[m] = valid ? src + (int64_t)c * n + (tile ? c01 : c00) + k : nullptr;
       v[m] = valid ? ld_relaxed_u64(vp[m]) : 0ull;
     }
-    for (int spin = 0; spin < kSpinLimit; spin++) {  // re-poll the values not yet published
+    for (int spin = 0;; spin++) {  // re-poll the values not yet published
       bool miss = false;
 #pragma unroll
       for (int m = 0; m < PER; m++)
@@ -656,6 +662,10 @@ __global__ void __launch_bounds__(256) getrs_chain_kernel(int n, int nb, const d
           miss = true;
         }
       if (!miss) break;
+      if (spin == kSpinLimit) {
+        if (status) atomicOr(&status->flags, ERR_CHAIN_TIMEOUT);
+        break;
+      }
     }
     __syncthreads();  // the previous pair's FMAs are done with vt
 #pragma unroll
@@ -675,7 +685,13 @@ __global__ void __launch_bounds__(256) getrs_chain_kernel(int n, int nb, const d
 #pragma unroll
     for (int c = 0; c < NR; c++) {
       unsigned long long u = ld_relaxed_u64(&y[(int64_t)c * n + r0 + r]);
-      for (int spin = 0; u == kSentinel && spin < kSpinLimit; spin++) u = ld_relaxed_u64(&y[(int64_t)c * n + r0 + r]);
+      for (int spin = 0; u == kSentinel; spin++) {
+        if (spin == kSpinLimit) {
+          if (status) atomicOr(&status->flags, ERR_CHAIN_TIMEOUT);
+          break;
+        }
+        u = ld_relaxed_u64(&y[(int64_t)c * n + r0 + r]);
+      }
       rhs[c] = __longlong_as_double((long long)u);
     }
   }
@@ -722,20 +738,32 @@ void getrs_prepare(cudaStream_t st, int64_t n, const double* lu, const int32_t* 
 
 void getrs_chain(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const double* dinv,
                  const int32_t* perm, const double* b, int64_t ldb, double* x, int64_t ldx, double alpha,
-                 double beta, double* yz, int epoch) {
+                 double beta, double* yz, int epoch, DevStatus* status) {
   if (n <= 0 || nrhs <= 0) return;
   const int nb = (int)cdiv(n, CT);
-  // chains of 8 columns in one launch, the remainder (< 8 columns) as one more chain
+  // chains of 8 columns, the remainder (< 8 columns) as one more chain; each launch holds at
+  // most as many chains as can be resident at once (a chain's CTAs wait on each other)
   const int64_t full = nrhs / 8, rem = nrhs % 8;
   const int64_t set = 16 * n * cdiv(nrhs, 8);
   double* cur = yz + (epoch & 1) * set;
   double* nxt = yz + ((epoch + 1) & 1) * set;
+  static int resident = 0;  // CTAs of getrs_chain_kernel<8> resident at once on this device
+  if (resident == 0) {
+    int dev = 0, sms = 0, per = 0;
+    SLB_CUDA_CHECK(cudaGetDevice(&dev));
+    SLB_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SLB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, getrs_chain_kernel<8>, 256, 0));
+    resident = std::max(1, sms * per);
+  }
+  if (2 * nb > resident)
+    throw CudaFailure(cudaErrorInvalidValue, "getrs_chain: block too large for one resident chain", __FILE__, __LINE__);
+  const int64_t per_launch = std::max<int64_t>(1, resident / (2 * nb));
 #define SLB_CHAIN(NR, NCH, OFF)                                                                          \
   getrs_chain_kernel<NR><<<(unsigned)(2 * nb * (NCH)), 256, 0, st>>>(                                    \
       (int)n, nb, lu, dinv, perm, b + (OFF) * 8 * ldb, ldb, x + (OFF) * 8 * ldx, ldx, alpha, beta,       \
-      cur + (OFF) * 16 * n, nxt + (OFF) * 16 * n);                                                       \
+      cur + (OFF) * 16 * n, nxt + (OFF) * 16 * n, status);                                               \
   count_launch()
-  if (full > 0) SLB_CHAIN(8, full, 0);
+  for (int64_t c0 = 0; c0 < full; c0 += per_launch) SLB_CHAIN(8, std::min(per_launch, full - c0), c0);
   switch (rem) {
     case 0: break;
     case 1: SLB_CHAIN(1, 1, full); break;

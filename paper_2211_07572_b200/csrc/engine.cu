@@ -6,8 +6,8 @@
 //                the Schur sweep (schur.cu) and T assembly;
 //   stage two  = sweeping block LU of the reduced block tridiagonal system
 //                (stage_two.hpp:131-150) with dense LU on the device
-//                (dense.cu); each S_j is kept as its explicit inverse so the
-//                stage-two solve is bandwidth-bound GEMV.
+//                (dense.cu); each S_j is kept in LU form (DenseLU,
+//                dense.hpp:31-61) and applied by the chained getrs.
 // solve (driver.hpp:171-179): reduce_rhs -> sweep solve -> recover_interiors,
 // all on the device.
 #include <algorithm>
@@ -38,9 +38,41 @@ namespace {
 // ---------------------------------------------------------------------------
 // Exact-size caching device allocator (repeated factorizations of the same
 // problem reuse their buffers instead of paying cudaMalloc/cudaFree).
+//
+// Reuse is stream-ordered: a block released while the thread is inside a StreamScope records
+// an event on that stream.  The same stream may take the block back at once (its later work is
+// ordered after the earlier user's); any other stream takes it only once the event has
+// completed.  Blocks released outside a scope (after a synchronize) carry no event.
+thread_local cudaStream_t t_scope_stream = nullptr;
+struct StreamScope {
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(t_scope_stream) { t_scope_stream = s; }
+  ~StreamScope() { t_scope_stream = prev; }
+};
+// Sets the current device for the lifetime of the guard and restores the caller's.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+    }
+    if (prev != dev) SLB_CUDA_CHECK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 struct DevPool {
+  struct Block {
+    void* p;
+    cudaStream_t stream;  // stream of the last user (nullptr: no pending work)
+    cudaEvent_t ev;       // completes when that work is done (nullptr: nothing pending)
+  };
   std::mutex mu;
-  std::multimap<std::pair<int, size_t>, void*> free_blocks;
+  std::multimap<std::pair<int, size_t>, Block> free_blocks;
   size_t cached_bytes(int dev) {
     std::lock_guard<std::mutex> g(mu);
     size_t s = 0;
@@ -50,12 +82,28 @@ struct DevPool {
   }
   void* get(int dev, size_t bytes) {
     if (bytes == 0) return nullptr;
+    DeviceGuard dg(dev);
     {
       std::lock_guard<std::mutex> g(mu);
-      auto it = free_blocks.find({dev, bytes});
-      if (it != free_blocks.end()) {
-        void* p = it->second;
-        free_blocks.erase(it);
+      auto range = free_blocks.equal_range({dev, bytes});
+      auto pick = free_blocks.end();
+      for (auto it = range.first; it != range.second; ++it) {
+        const Block& b = it->second;
+        if (!b.ev || (t_scope_stream && b.stream == t_scope_stream)) {
+          pick = it;
+          break;
+        }
+        const cudaError_t q = cudaEventQuery(b.ev);
+        if (q == cudaSuccess) {
+          pick = it;
+          break;
+        }
+        if (q != cudaErrorNotReady) cudaGetLastError();
+      }
+      if (pick != free_blocks.end()) {
+        void* p = pick->second.p;
+        if (pick->second.ev) cudaEventDestroy(pick->second.ev);
+        free_blocks.erase(pick);
         return p;
       }
     }
@@ -74,19 +122,40 @@ struct DevPool {
   }
   void put(int dev, size_t bytes, void* p) {
     if (!p) return;
+    Block b{p, nullptr, nullptr};
+    if (t_scope_stream) {
+      DeviceGuard dg(dev);
+      if (cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) == cudaSuccess &&
+          cudaEventRecord(b.ev, t_scope_stream) == cudaSuccess) {
+        b.stream = t_scope_stream;
+      } else {
+        cudaGetLastError();
+        if (b.ev) cudaEventDestroy(b.ev);
+        b.ev = nullptr;
+        cudaStreamSynchronize(t_scope_stream);  // cannot order the reuse: wait for the user
+        cudaGetLastError();
+      }
+    }
     std::lock_guard<std::mutex> g(mu);
-    free_blocks.insert({{dev, bytes}, p});
+    free_blocks.insert({{dev, bytes}, b});
   }
+  // Frees every cached block of dev (waiting for pending users first).
   void trim(int dev) {
+    DeviceGuard dg(dev);
     std::lock_guard<std::mutex> g(mu);
     for (auto it = free_blocks.begin(); it != free_blocks.end();) {
       if (it->first.first == dev) {
-        cudaFree(it->second);
+        if (it->second.ev) {
+          cudaEventSynchronize(it->second.ev);
+          cudaEventDestroy(it->second.ev);
+        }
+        cudaFree(it->second.p);
         it = free_blocks.erase(it);
       } else {
         ++it;
       }
     }
+    cudaGetLastError();
   }
 };
 DevPool& pool() {
@@ -206,6 +275,11 @@ cudaStream_t green_partition_stream(int dev, int conv_sms) {
   if (it != made.end()) return it->second;
   made[dev] = nullptr;
   if (getenv("SLB_NO_GREEN")) return nullptr;
+  // under a profiler (ncu/nsys inject through these variables) a green context ends the
+  // profiled process; the priority-stream fallback runs the same kernels
+  if (getenv("CUDA_INJECTION64_PATH") || getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") ||
+      getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE"))
+    return nullptr;
   using FnDeviceGet = CUresult (*)(CUdevice*, int);
   using FnGetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
   using FnSplit = CUresult (*)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*, unsigned int,
@@ -249,6 +323,8 @@ cudaStream_t green_partition_stream(int dev, int conv_sms) {
   return made[dev];
 }
 
+constexpr int64_t kMaxIfc = 4096;  // stage-two block dimension limit (dgetrf panel cluster, dense.cu)
+
 int sm_count(int dev) {
   int v = 0;
   SLB_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
@@ -272,6 +348,7 @@ struct slablu_gpu_fact {
   // s - s0), interfaces [j0, j1) are owned; K and every interface-indexed array stay global
   int rank = 0, nranks = 1, Sg = 0, s0 = 0, s1 = 0, j0 = 0, j1 = 0;
   bool sharded = false, swept = false;
+  bool stage2_only = false;  // slablu_gpu_sweep_build: a block-tridiagonal system only
   // shard solve state between the forward and backward phases
   DBuf<double> sh_f, sh_red, sh_uifc;
   int64_t sh_nrhs = 0;
@@ -297,6 +374,7 @@ struct slablu_gpu_fact {
   DBuf<double> dinvT;   // inverses of the 64x64 diagonal blocks of L_j, U_j (getrs_chain)
   DBuf<double> Tkeep;   // optional copy of the reduced blocks
   DBuf<DevStatus> status;
+  DBuf<DevStatus> sstatus;   // solve-time status (getrs_chain timeouts)
   DBuf<int32_t> a_rp, a_ci;  // the original operator (iterative refinement)
   DBuf<double> a_v;
   int refine = 0;
@@ -344,6 +422,32 @@ void shard_ranges(int Sg, int K, int rank, int nranks, int* s0, int* s1, int* j0
   *j1 = rank == nranks - 1 ? K : *s1 - 1;
 }
 
+// Stage two (stage_two.hpp:131-150) on F->T: S_0 = T_00, S_j = T_jj - sub_{j-1} S_{j-1}^{-1} super_{j-1}.
+// S_j stays in LU form (as DenseLU in the reference): X = S_{j-1}^{-1} super_{j-1} by getrs, the
+// solve applies S_j^{-1} by the chained getrs (stage_two.hpp:138-147, 176-186).  Singular S_j raise
+// ERR_SINGULAR with the block index in F->status (checked by the caller).
+void stage_two_build(slablu_gpu_fact* F) {
+  cudaStream_t st = F->stream;
+  const int dev = F->device, K = F->K;
+  const int64_t n2 = F->n2, bs = n2 * n2;
+  DBuf<double> X;
+  X.alloc(dev, bs);
+  const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
+  F->ipivT.alloc(dev, (size_t)std::max(K, 1) * n2);
+  F->permT.alloc(dev, (size_t)std::max(K, 1) * n2);
+  F->dinvT.alloc(dev, (size_t)std::max(K, 1) * dinv_sz);
+  for (int j = 0; j < K; j++) {
+    double* Sj = F->Tdiag() + j * bs;
+    if (j > 0) {
+      SLB_CUDA_CHECK(cudaMemcpyAsync(X.p, F->Tsup() + (j - 1) * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      dgetrs(st, n2, n2, F->Tdiag() + (j - 1) * bs, F->ipivT.p + (size_t)(j - 1) * n2, X.p, n2, nullptr);
+      dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X.p, n2, 0, 1.0, Sj, n2, 0, 1);
+    }
+    dgetrf(st, n2, Sj, F->ipivT.p + (size_t)j * n2, nullptr, F->status.p, j);
+    getrs_prepare(st, n2, Sj, F->ipivT.p + (size_t)j * n2, F->permT.p + (size_t)j * n2, F->dinvT.p + (size_t)j * dinv_sz);
+  }
+}
+
 slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32_t* rp, const int32_t* ci,
                                 const double* v, const slablu_gpu_config* cfg, int rank = 0, int nranks = 1,
                                 bool sharded = false) {
@@ -356,7 +460,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   const int64_t launches0 = slb::g_kernel_count.load();
   auto F = std::make_unique<slablu_gpu_fact>();
   F->device = c.device;
-  SLB_CUDA_CHECK(cudaSetDevice(c.device));
+  DeviceGuard dg(c.device);
   {
     // the level chain is latency-bound: its stream gets the greatest priority so that its CTAs
     // are scheduled ahead of the conversion kernels running beside it (which use the least)
@@ -365,6 +469,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     SLB_CUDA_CHECK(cudaStreamCreateWithPriority(&F->stream, cudaStreamNonBlocking, greatest));
   }
   cudaStream_t st = F->stream;
+  StreamScope scope(st);
   F->n1 = n1;
   F->n2 = n2;
   F->N = n1 * n2;
@@ -401,6 +506,10 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   F->Wp = (int)round_up(wmax, 8);
   if (F->Wp > 160)
     throw HostError(SLABLU_ERR_UNSUPPORTED, "factorize: slab width " + std::to_string(wmax) + " exceeds the engine's 160-column envelope");
+  if (!F->single && n2 > kMaxIfc)
+    throw HostError(SLABLU_ERR_UNSUPPORTED, "factorize: interface length n2 = " + std::to_string(n2) +
+                                                " exceeds the engine's " + std::to_string(kMaxIfc) +
+                                                "-row stage-two envelope");
   const int Wp = F->Wp, S = F->S, K = F->K;
   for (int s = 0; s < S; s++) {
     StripDesc d;
@@ -430,8 +539,10 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     SLB_CUDA_CHECK(cudaMemcpyAsync(F->ifc_off.p, F->ifc_off_h.data(), K * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   }
   F->status.alloc(dev, 1);
-  DevStatus st0{0, INT_MAX, INT_MAX, 0};
+  F->sstatus.alloc(dev, 1);
+  static const DevStatus st0{0, INT_MAX, INT_MAX, INT_MAX};
   SLB_CUDA_CHECK(cudaMemcpyAsync(F->status.p, &st0, sizeof(DevStatus), cudaMemcpyHostToDevice, st));
+  SLB_CUDA_CHECK(cudaMemcpyAsync(F->sstatus.p, &st0, sizeof(DevStatus), cudaMemcpyHostToDevice, st));
   CsrDev A{rp, ci, v, F->N};
   F->refine = std::max(0, c.refine);
   if (F->refine > 0) {
@@ -485,7 +596,8 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   // conversion; smaller partitions no longer hide the conversion behind the chain.
   cudaStream_t cst = nullptr;
   bool cst_owned = false;
-  {
+  // the partition pays only when the chain is long and the conversion large (cfg3-sized)
+  if (S * n2 >= 16384 && n2 >= 1024) {
     const char* e = getenv("SLB_GREEN_SMS");
     const int want = e ? atoi(e) : sm_count(dev) - (int)round_up(S + 4, 8);
     cst = green_partition_stream(dev, want);
@@ -580,8 +692,14 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     SLB_CUDA_CHECK(cudaStreamSynchronize(st));
     throw_status(hs);
     if (hs.flags & ERR_SINGULAR) {
-      if (F->single) throw HostError(SLABLU_ERR_SINGULAR, "BandedLU: exactly singular pivot", hs.singular_strip);
-      throw HostError(SLABLU_ERR_SINGULAR, "factor_one_interior: singular slab interior", hs.singular_strip);
+      // single slab: the natural index (ix * n2 + iy) of the first zero pivot, as BandedLU reports
+      // dgbtrf's info - 1 (banded.hpp:103-109); else the global strip index (stage_one.hpp:234-237)
+      if (F->single) {
+        const int64_t lvl_ = hs.singular_pos / Wp, col_ = hs.singular_pos % Wp;
+        throw HostError(SLABLU_ERR_SINGULAR, "BandedLU: exactly singular pivot", col_ * n2 + lvl_);
+      }
+      throw HostError(SLABLU_ERR_SINGULAR, "factor_one_interior: singular slab interior",
+                      (int64_t)hs.singular_strip + F->s0);
     }
     if (getenv("SLB_U13_STATS")) {
       std::vector<uint8_t> h((size_t)S * n2);
@@ -698,28 +816,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     SLB_CUDA_CHECK(cudaEventRecord(e1, st));
 
     // ---- stage two: sweeping block LU (stage_two.hpp:131-150) --------------------------
-    // S_j stays in LU form (as DenseLU in the reference): X = S_{j-1}^{-1} super_{j-1} by getrs,
-    // the solve applies S_j^{-1} by getrs too (stage_two.hpp:138-147, 176-186)
-    const int64_t bs = n2 * n2;
-    DBuf<double> X;
-    X.alloc(dev, bs);
-    const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
-    if (!sharded) {
-      F->ipivT.alloc(dev, (size_t)std::max(K, 1) * n2);
-      F->permT.alloc(dev, (size_t)std::max(K, 1) * n2);
-      F->dinvT.alloc(dev, (size_t)std::max(K, 1) * dinv_sz);
-    }
-    for (int j = 0; j < (sharded ? 0 : K); j++) {  // sharded: slablu_gpu_shard_sweep
-      double* Sj = F->Tdiag() + j * bs;
-      if (j > 0) {
-        SLB_CUDA_CHECK(cudaMemcpyAsync(X.p, F->Tsup() + (j - 1) * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
-        dgetrs(st, n2, n2, F->Tdiag() + (j - 1) * bs, F->ipivT.p + (size_t)(j - 1) * n2, X.p, n2, nullptr);
-        dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X.p, n2, 0, 1.0, Sj, n2, 0, 1);
-      }
-      dgetrf(st, n2, Sj, F->ipivT.p + (size_t)j * n2, nullptr, F->status.p, j);
-      getrs_prepare(st, n2, Sj, F->ipivT.p + (size_t)j * n2, F->permT.p + (size_t)j * n2,
-                    F->dinvT.p + (size_t)j * dinv_sz);
-    }
+    if (!sharded) stage_two_build(F.get());  // sharded: slablu_gpu_shard_sweep
   } else {
     SLB_CUDA_CHECK(cudaEventRecord(es, st));
     SLB_CUDA_CHECK(cudaEventRecord(e1, st));
@@ -760,165 +857,22 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   return F.release();
 }
 
-void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu) {
-  const int64_t launches0 = slb::g_kernel_count.load();
-  SLB_CUDA_CHECK(cudaSetDevice(F->device));
-  cudaStream_t st = F->stream;
-  const int dev = F->device;
-  const int64_t n2 = F->n2, N = F->N, K = (int64_t)F->K * n2;
-  const int S = F->S;
-  // compact f (ld N)
-  DBuf<double> f;
-  const double* fp = d_f;
-  if (ldf != N) {
-    f.alloc(dev, (size_t)N * nrhs);
-    copy2d(st, d_f, ldf, f.p, N, N, nrhs);
-    fp = f.p;
+// Raises the solve-time device status (bounded waits of getrs_chain that expired) and re-arms it.
+void check_solve_status(const slablu_gpu_fact* F) {
+  DevStatus hs;
+  SLB_CUDA_CHECK(cudaMemcpyAsync(&hs, F->sstatus.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, F->stream));
+  SLB_CUDA_CHECK(cudaStreamSynchronize(F->stream));
+  if (hs.flags) {
+    static const DevStatus st0{0, INT_MAX, INT_MAX, INT_MAX};
+    SLB_CUDA_CHECK(cudaMemcpyAsync(F->sstatus.p, &st0, sizeof(DevStatus), cudaMemcpyHostToDevice, F->stream));
+    SLB_CUDA_CHECK(cudaStreamSynchronize(F->stream));
+    throw HostError(SLABLU_ERR_CUDA, "solve: stage-two block chain timed out (a published block never arrived)");
   }
-  DBuf<double> u;
-  double* up = d_u;
-  if (ldu != N) {
-    u.alloc(dev, (size_t)N * nrhs);
-    up = u.p;
-  }
-  cudaEvent_t s0, s1, s2, s3, s4;
-  for (cudaEvent_t* ev : {&s0, &s1, &s2, &s3, &s4}) SLB_CUDA_CHECK(cudaEventCreate(ev));
-  SLB_CUDA_CHECK(cudaEventRecord(s0, st));
-  SLB_CUDA_CHECK(cudaEventRecord(s1, st));
-  SLB_CUDA_CHECK(cudaEventRecord(s2, st));
-  SLB_CUDA_CHECK(cudaEventRecord(s3, st));
-  const int CH = nrhs <= 8 ? 8 : kSweepChunk;
-  const int64_t nch = cdiv(nrhs, CH);
-  std::vector<int32_t> tasks;
-  for (int s = 0; s < S; s++)
-    for (int64_t cch = 0; cch < nch; cch++) {
-      tasks.push_back(s);
-      tasks.push_back(0);
-      tasks.push_back((int32_t)(cch * CH));
-    }
-  const int ntasks = (int)(tasks.size() / 3);
-  DBuf<int32_t> dtasks, counter;
-  dtasks.alloc(dev, tasks.size());
-  counter.alloc(dev, 1);
-  SLB_CUDA_CHECK(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  const bool clustered = CH == 8 && strip_solve_fits(F->Wp, n2);  // cluster sweeps for small nrhs (solve.cu)
-  const int nslots = clustered ? ntasks : std::min(sm_count(dev), ntasks);
-  const int64_t sY = n2 * F->Wp * CH;
-  DBuf<double> ybuf;
-  ybuf.alloc(dev, (size_t)nslots * sY);
-  auto run_sweep = [&](const SchurArgs& args) {
-    if (clustered) {
-      strip_solve(st, args, ntasks);  // rhs pack + cluster sweep
-    } else {
-      sweep(st, args, nslots);
-    }
-  };
-  SchurArgs sa{};
-  sa.chunk = CH;
-  sa.u13 = F->u13.p;
-    sa.dsub = F->dsub.p;
-    sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
-    sa.exc = F->exc.p;
-    sa.excpos = F->excpos.p;
-    sa.bsc = getenv("SLB_NO_BSC") ? 0 : 1;  // backward shortcut (SLB_NO_BSC=1 disables, for A/B runs)
-    sa.hcol = F->hcol.p;
-    sa.hidx = F->hidx.p;
-  sa.Wp = F->Wp;
-  sa.n2 = n2;
-  sa.nstrips = S;
-  sa.strips = F->strips.p;
-  sa.fac = F->fac.p;
-  sa.sF = F->sF;
-  sa.perm = F->perm.p;
-  sa.sP = F->sP;
-  sa.cpl = F->cpl.p;
-  sa.sCPL = F->sCPL;
-  sa.sym = F->sym.p;
-  sa.ybuf = ybuf.p;
-  sa.sY = sY;
-  sa.task_counter = counter.p;
-  sa.ntasks = ntasks;
-  sa.tasks = dtasks.p;
-  sa.N = N;
-  sa.K = K;
-  sa.nrhs = nrhs;
-  sa.f = fp;
-
-  if (F->single) {
-    SLB_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
-    sa.mode = SWEEP_RECOVER;
-    sa.u_ifc = nullptr;
-    sa.out = up;
-    run_sweep(sa);
-  } else {
-    DBuf<double> red, uifc, contrib, tmp, part;
-    red.alloc(dev, (size_t)K * nrhs);
-    uifc.alloc(dev, (size_t)K * nrhs);
-    contrib.alloc(dev, (size_t)S * 2 * nrhs * n2);
-    tmp.alloc(dev, (size_t)n2 * nrhs);
-    part.alloc(dev, (size_t)8 * n2 * nrhs);
-    const unsigned gb = (unsigned)cdiv(K * nrhs, 256);
-    // reduce_rhs (stage_one.hpp:415-433)
-    gather_ifc_kernel<<<gb, 256, 0, st>>>(fp, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K, 0, F->K); count_launch();
-    SLB_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
-    sa.mode = SWEEP_REDUCE;
-    sa.out = contrib.p;
-    run_sweep(sa);
-    SLB_CUDA_CHECK(cudaEventRecord(s1, st));
-    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, S, F->strips.p, contrib.p, 0); count_launch();
-    // sweep solve (stage_two.hpp:170-188) with the LU factors of S_j
-    // S_j^{-1} v from the LU factors of S_j: chained getrs (8-column chains)
-    const int64_t bs = n2 * n2;
-    const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
-    DBuf<double> yz;
-    int epoch = 0;
-    yz.alloc(dev, (size_t)getrs_chain_scratch(n2, nrhs));
-    getrs_chain_init(st, n2, nrhs, yz.p);
-    auto apply_Sinv = [&](int j, const double* v, int64_t ldv, double* out, double alpha, double beta) {
-      getrs_chain(st, n2, nrhs, F->Tdiag() + j * bs, F->dinvT.p + (size_t)j * dinv_sz, F->permT.p + (size_t)j * n2,
-                  v, ldv, out, K, alpha, beta, yz.p, ++epoch);
-    };
-    for (int j = 0; j < F->K; j++) {
-      double* rj = red.p + j * n2;
-      if (j > 0) dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j - 1) * bs, n2, uifc.p + (j - 1) * n2, K,
-                                   1.0, rj, K, part.p);
-      apply_Sinv(j, rj, K, uifc.p + j * n2, 1.0, 0.0);
-    }
-    for (int j = F->K - 2; j >= 0; j--) {
-      dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tsup() + j * bs, n2, uifc.p + (j + 1) * n2, K, 0.0, tmp.p, n2,
-                        part.p);
-      apply_Sinv(j, tmp.p, n2, uifc.p + j * n2, -1.0, 1.0);
-    }
-    // recover_interiors (stage_one.hpp:438-462)
-    SLB_CUDA_CHECK(cudaEventRecord(s2, st));
-    SLB_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(int32_t), st));
-    sa.mode = SWEEP_RECOVER;
-    sa.u_ifc = uifc.p;
-    sa.out = up;
-    run_sweep(sa);
-    SLB_CUDA_CHECK(cudaEventRecord(s3, st));
-    scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc.p, K, nrhs, F->ifc_off.p, n2, up, N, 0, F->K); count_launch();
-    SLB_CUDA_CHECK(cudaGetLastError());
-    SLB_CUDA_CHECK(cudaStreamSynchronize(st));
-  }
-  if (up != d_u) copy2d(st, up, N, d_u, ldu, N, nrhs);
-  SLB_CUDA_CHECK(cudaEventRecord(s4, st));
-  SLB_CUDA_CHECK(cudaStreamSynchronize(st));
-  float a = 0, b = 0, c = 0;
-  SLB_CUDA_CHECK(cudaEventElapsedTime(&a, s0, s4));
-  SLB_CUDA_CHECK(cudaEventElapsedTime(&b, s0, s1));
-  SLB_CUDA_CHECK(cudaEventElapsedTime(&c, s2, s3));
-  F->t_solve = a * 1e-3;
-  F->t_solve_strips = F->single ? a * 1e-3 : (b + c) * 1e-3;
-  for (cudaEvent_t ev : {s0, s1, s2, s3, s4}) cudaEventDestroy(ev);
-  F->launches_solve = slb::g_kernel_count.load() - launches0;
 }
 
-// solve with F->refine steps of iterative refinement against the original
-// operator: u += A~^{-1} (f - A u).  Restores componentwise backward stability
-// lost to the explicit level/Schur inverses.
 // Slab sweeps of the solve for the factorization's (local) strips: reduce (contributions
-// to_X A_ii^{-1} f_i) or recover (A_ii^{-1}(f_i - couplings u)), as in solve_once.
+// to_X A_ii^{-1} f_i) or recover (A_ii^{-1}(f_i - couplings u)).  nrhs <= 8: cluster sweeps
+// (solve.cu); more columns: the 64-column persistent sweep kernel (schur.cu).
 struct StripSweeper {
   const slablu_gpu_fact* F;
   cudaStream_t st;
@@ -990,6 +944,131 @@ struct StripSweeper {
   }
 };
 
+// reduce_rhs (stage_one.hpp:415-433): red (K n2 x nrhs, ld K n2) = f on the interfaces [jlo, jhi)
+// minus the adjacent local strips' terms to_X A_ii^{-1} f_i.  fp: N x nrhs, ld N (device).
+void reduce_phase(const slablu_gpu_fact* F, StripSweeper& sw, const double* fp, int64_t nrhs, double* red, int jlo,
+                  int jhi) {
+  cudaStream_t st = F->stream;
+  const int64_t n2 = F->n2, N = F->N, Kn = (int64_t)F->K * n2;
+  DBuf<double> contrib;
+  contrib.alloc(F->device, (size_t)F->S * 2 * nrhs * n2);
+  const unsigned gb = (unsigned)cdiv(Kn * nrhs, 256);
+  gather_ifc_kernel<<<gb, 256, 0, st>>>(fp, N, nrhs, F->K, F->ifc_off.p, n2, red, Kn, jlo, jhi); count_launch();
+  sw.run(SWEEP_REDUCE, nullptr, contrib.p);
+  combine_reduce_kernel<<<gb, 256, 0, st>>>(red, Kn, nrhs, n2, F->S, F->strips.p, contrib.p, F->s0); count_launch();
+  SLB_CUDA_CHECK(cudaGetLastError());
+}
+
+// Sweep solve over the interfaces [jlo, jhi) (stage_two.hpp:170-188) with the LU factors of S_j:
+// forward u_j = S_j^{-1}(red_j - sub_{j-1} u_{j-1}), backward u_j -= S_j^{-1} super_j u_{j+1}.
+// red and uifc are K n2 x nrhs (ld K n2); red is consumed (overwritten).
+struct SweepSolver {
+  const slablu_gpu_fact* F;
+  int64_t nrhs;
+  DBuf<double> yz, tmp, part;
+  int epoch = 0;
+  SweepSolver(const slablu_gpu_fact* F_, int64_t nrhs_) : F(F_), nrhs(nrhs_) {
+    const int64_t n2 = F->n2;
+    yz.alloc(F->device, (size_t)getrs_chain_scratch(n2, nrhs));
+    tmp.alloc(F->device, (size_t)n2 * nrhs);
+    part.alloc(F->device, (size_t)8 * n2 * nrhs);
+    getrs_chain_init(F->stream, n2, nrhs, yz.p);
+  }
+  int64_t dinv_sz() const { return cdiv(F->n2, 64) * 2 * 64 * 64; }
+  // out = beta out + alpha S_j^{-1} v
+  void apply_Sinv(int j, const double* v, int64_t ldv, double* out, int64_t ldo, double alpha, double beta) {
+    getrs_chain(F->stream, F->n2, nrhs, F->Tdiag() + (size_t)j * F->n2 * F->n2, F->dinvT.p + (size_t)j * dinv_sz(),
+                F->permT.p + (size_t)j * F->n2, v, ldv, out, ldo, alpha, beta, yz.p, ++epoch, F->sstatus.p);
+  }
+  void forward(double* red, double* uifc, int jlo, int jhi) {
+    const int64_t n2 = F->n2, Kn = (int64_t)F->K * n2, bs = n2 * n2;
+    for (int j = jlo; j < jhi; j++) {
+      double* rj = red + j * n2;
+      if (j > jlo)
+        dgemv_batched_rhs(F->stream, n2, n2, nrhs, -1.0, F->Tsub() + (j - 1) * bs, n2, uifc + (j - 1) * n2, Kn, 1.0,
+                          rj, Kn, part.p);
+      apply_Sinv(j, rj, Kn, uifc + j * n2, Kn, 1.0, 0.0);
+    }
+  }
+  void backward(double* uifc, int jlo, int jhi) {
+    const int64_t n2 = F->n2, Kn = (int64_t)F->K * n2, bs = n2 * n2;
+    for (int j = jhi - 1; j >= jlo; j--) {
+      if (j + 1 >= F->K) continue;
+      dgemv_batched_rhs(F->stream, n2, n2, nrhs, 1.0, F->Tsup() + j * bs, n2, uifc + (j + 1) * n2, Kn, 0.0, tmp.p,
+                        n2, part.p);
+      apply_Sinv(j, tmp.p, n2, uifc + j * n2, Kn, -1.0, 1.0);
+    }
+  }
+};
+
+// recover_interiors (stage_one.hpp:438-462) on the local strips, then the owned interface
+// values [jlo, jhi) copied in: up is N x nrhs (ld N).
+void recover_phase(const slablu_gpu_fact* F, StripSweeper& sw, const double* uifc, int64_t nrhs, double* up, int jlo,
+                   int jhi) {
+  cudaStream_t st = F->stream;
+  const int64_t n2 = F->n2, N = F->N, Kn = (int64_t)F->K * n2;
+  sw.run(SWEEP_RECOVER, uifc, up);
+  if (Kn > 0) {
+    const unsigned gb = (unsigned)cdiv(Kn * nrhs, 256);
+    scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc, Kn, nrhs, F->ifc_off.p, n2, up, N, jlo, jhi); count_launch();
+  }
+  SLB_CUDA_CHECK(cudaGetLastError());
+}
+
+void solve_once(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu) {
+  const int64_t launches0 = slb::g_kernel_count.load();
+  cudaStream_t st = F->stream;
+  const int dev = F->device;
+  const int64_t n2 = F->n2, N = F->N, Kn = (int64_t)F->K * n2;
+  // compact f (ld N)
+  DBuf<double> f;
+  const double* fp = d_f;
+  if (ldf != N) {
+    f.alloc(dev, (size_t)N * nrhs);
+    copy2d(st, d_f, ldf, f.p, N, N, nrhs);
+    fp = f.p;
+  }
+  DBuf<double> u;
+  double* up = d_u;
+  if (ldu != N) {
+    u.alloc(dev, (size_t)N * nrhs);
+    up = u.p;
+  }
+  cudaEvent_t s0, s1, s2, s3, s4;
+  for (cudaEvent_t* ev : {&s0, &s1, &s2, &s3, &s4}) SLB_CUDA_CHECK(cudaEventCreate(ev));
+  SLB_CUDA_CHECK(cudaEventRecord(s0, st));
+  SLB_CUDA_CHECK(cudaEventRecord(s1, st));
+  SLB_CUDA_CHECK(cudaEventRecord(s2, st));
+  SLB_CUDA_CHECK(cudaEventRecord(s3, st));
+  StripSweeper sw(F, fp, nrhs);
+  if (F->single) {
+    sw.run(SWEEP_RECOVER, nullptr, up);
+  } else {
+    DBuf<double> red, uifc;
+    red.alloc(dev, (size_t)Kn * nrhs);
+    uifc.alloc(dev, (size_t)Kn * nrhs);
+    reduce_phase(F, sw, fp, nrhs, red.p, 0, F->K);
+    SLB_CUDA_CHECK(cudaEventRecord(s1, st));
+    SweepSolver ss(F, nrhs);
+    ss.forward(red.p, uifc.p, 0, F->K);
+    ss.backward(uifc.p, 0, F->K);
+    SLB_CUDA_CHECK(cudaEventRecord(s2, st));
+    recover_phase(F, sw, uifc.p, nrhs, up, 0, F->K);
+    SLB_CUDA_CHECK(cudaEventRecord(s3, st));
+  }
+  if (up != d_u) copy2d(st, up, N, d_u, ldu, N, nrhs);
+  SLB_CUDA_CHECK(cudaEventRecord(s4, st));
+  SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+  float a = 0, b = 0, c = 0;
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&a, s0, s4));
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&b, s0, s1));
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&c, s2, s3));
+  F->t_solve = a * 1e-3;
+  F->t_solve_strips = F->single ? a * 1e-3 : (b + c) * 1e-3;
+  for (cudaEvent_t ev : {s0, s1, s2, s3, s4}) cudaEventDestroy(ev);
+  F->launches_solve = slb::g_kernel_count.load() - launches0;
+}
+
 void require_shard(const slablu_gpu_fact* F, const char* who) {
   if (!F->sharded) throw HostError(SLABLU_ERR_CONFIG, std::string(who) + ": not a sharded factorization");
 }
@@ -1002,8 +1081,9 @@ void shard_sweep_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
   if (F->rank > 0 && !d_in) throw HostError(SLABLU_ERR_CONFIG, "shard_sweep: rank > 0 needs the message of rank - 1");
   if (F->rank < F->nranks - 1 && !d_out)
     throw HostError(SLABLU_ERR_CONFIG, "shard_sweep: rank < nranks - 1 needs an output message buffer");
-  SLB_CUDA_CHECK(cudaSetDevice(F->device));
+  DeviceGuard dg(F->device);
   cudaStream_t st = F->stream;
+  StreamScope scope(st);
   const int dev = F->device;
   const int64_t n2 = F->n2, bs = n2 * n2;
   const int j0 = F->j0, j1 = F->j1;
@@ -1063,8 +1143,9 @@ void shard_solve_fwd_impl(slablu_gpu_fact* F, const double* d_f, int64_t ldf, in
   if (F->rank > 0 && !d_in) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_forward: rank > 0 needs the message of rank - 1");
   if (F->rank < F->nranks - 1 && !d_out)
     throw HostError(SLABLU_ERR_CONFIG, "shard_solve_forward: rank < nranks - 1 needs an output message buffer");
-  SLB_CUDA_CHECK(cudaSetDevice(F->device));
+  DeviceGuard dg(F->device);
   cudaStream_t st = F->stream;
+  StreamScope scope(st);
   const int dev = F->device;
   const int64_t n2 = F->n2, N = F->N, Kn = (int64_t)F->K * n2, bs = n2 * n2;
   const int j0 = F->j0, j1 = F->j1;
@@ -1074,36 +1155,20 @@ void shard_solve_fwd_impl(slablu_gpu_fact* F, const double* d_f, int64_t ldf, in
   F->sh_red.alloc(dev, (size_t)std::max<int64_t>(Kn, 1) * nrhs);
   F->sh_uifc.alloc(dev, (size_t)std::max<int64_t>(Kn, 1) * nrhs);
   SLB_CUDA_CHECK(cudaMemsetAsync(F->sh_uifc.p, 0, F->sh_uifc.bytes(), st));
-  DBuf<double> contrib, part;
-  contrib.alloc(dev, (size_t)F->S * 2 * nrhs * n2);
-  part.alloc(dev, (size_t)8 * n2 * nrhs);
-  const unsigned gb = (unsigned)cdiv(Kn * nrhs, 256);
-  gather_ifc_kernel<<<gb, 256, 0, st>>>(F->sh_f.p, N, nrhs, F->K, F->ifc_off.p, n2, F->sh_red.p, Kn, j0, j1); count_launch();
-  StripSweeper sw(F, F->sh_f.p, nrhs);
-  sw.run(SWEEP_REDUCE, nullptr, contrib.p);
-  combine_reduce_kernel<<<gb, 256, 0, st>>>(F->sh_red.p, Kn, nrhs, n2, F->S, F->strips.p, contrib.p, F->s0); count_launch();
   double* red = F->sh_red.p;
   double* uifc = F->sh_uifc.p;
-  if (F->rank > 0) add2d(st, d_in, n2, red + j0 * n2, Kn, n2, nrhs);
-  const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
-  DBuf<double> yz;
-  yz.alloc(dev, (size_t)getrs_chain_scratch(n2, nrhs));
-  getrs_chain_init(st, n2, nrhs, yz.p);
-  int epoch = 0;
-  for (int j = j0; j < j1; j++) {
-    double* rj = red + j * n2;
-    if (j > j0) {
-      dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j - 1) * bs, n2, uifc + (j - 1) * n2, Kn, 1.0, rj, Kn,
-                        part.p);
-    }
-    getrs_chain(st, n2, nrhs, F->Tdiag() + j * bs, F->dinvT.p + (size_t)j * dinv_sz, F->permT.p + (size_t)j * n2, rj,
-                Kn, uifc + j * n2, Kn, 1.0, 0.0, yz.p, ++epoch);
+  {
+    StripSweeper sw(F, F->sh_f.p, nrhs);
+    reduce_phase(F, sw, F->sh_f.p, nrhs, red, j0, j1);
   }
+  if (F->rank > 0) add2d(st, d_in, n2, red + j0 * n2, Kn, n2, nrhs);
+  SweepSolver ss(F, nrhs);
+  ss.forward(red, uifc, j0, j1);
   if (F->rank < F->nranks - 1) {
     copy2d(st, red + j1 * n2, Kn, d_out, n2, n2, nrhs);
     if (j1 > j0) {
       dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j1 - 1) * bs, n2, uifc + (j1 - 1) * n2, Kn, 1.0, d_out,
-                        n2, part.p);
+                        n2, ss.part.p);
     }
   }
   SLB_CUDA_CHECK(cudaGetLastError());
@@ -1121,36 +1186,24 @@ void shard_solve_bwd_impl(slablu_gpu_fact* F, const double* d_in, double* d_out,
   if (F->rank < F->nranks - 1 && !d_in)
     throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: rank < nranks - 1 needs u of interface j_end");
   if (F->rank > 0 && !d_out) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: rank > 0 needs an output buffer");
-  SLB_CUDA_CHECK(cudaSetDevice(F->device));
+  DeviceGuard dg(F->device);
   cudaStream_t st = F->stream;
-  const int dev = F->device;
-  const int64_t n2 = F->n2, N = F->N, Kn = (int64_t)F->K * n2, bs = n2 * n2, nrhs = F->sh_nrhs;
+  StreamScope scope(st);
+  const int64_t n2 = F->n2, Kn = (int64_t)F->K * n2, nrhs = F->sh_nrhs;
   const int j0 = F->j0, j1 = F->j1;
   double* uifc = F->sh_uifc.p;
-  DBuf<double> tmp, part;
-  tmp.alloc(dev, (size_t)n2 * nrhs);
-  part.alloc(dev, (size_t)8 * n2 * nrhs);
   if (F->rank < F->nranks - 1) copy2d(st, d_in, n2, uifc + j1 * n2, Kn, n2, nrhs);
-  const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
-  DBuf<double> yz;
-  yz.alloc(dev, (size_t)getrs_chain_scratch(n2, nrhs));
-  getrs_chain_init(st, n2, nrhs, yz.p);
-  int epoch = 0;
-  for (int j = j1 - 1; j >= j0; j--) {
-    if (j + 1 >= F->K) continue;
-    dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->Tsup() + j * bs, n2, uifc + (j + 1) * n2, Kn, 0.0, tmp.p, n2, part.p);
-    getrs_chain(st, n2, nrhs, F->Tdiag() + j * bs, F->dinvT.p + (size_t)j * dinv_sz, F->permT.p + (size_t)j * n2,
-                tmp.p, n2, uifc + j * n2, Kn, -1.0, 1.0, yz.p, ++epoch);
+  {
+    SweepSolver ss(F, nrhs);
+    ss.backward(uifc, j0, j1);
   }
   if (F->rank > 0) copy2d(st, uifc + j0 * n2, Kn, d_out, n2, n2, nrhs);
-  StripSweeper sw(F, F->sh_f.p, nrhs);
-  sw.run(SWEEP_RECOVER, uifc, d_u);
-  const unsigned gb = (unsigned)cdiv(Kn * nrhs, 256);
-  if (Kn > 0) {
-    scatter_ifc_kernel<<<gb, 256, 0, st>>>(uifc, Kn, nrhs, F->ifc_off.p, n2, d_u, N, j0, j1); count_launch();
+  {
+    StripSweeper sw(F, F->sh_f.p, nrhs);
+    recover_phase(F, sw, uifc, nrhs, d_u, j0, j1);
   }
-  SLB_CUDA_CHECK(cudaGetLastError());
   SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+  check_solve_status(F);
   F->sh_f.release();
   F->sh_red.release();
   F->sh_uifc.release();
@@ -1158,10 +1211,14 @@ void shard_solve_bwd_impl(slablu_gpu_fact* F, const double* d_in, double* d_out,
 }
 
 void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu) {
+  if (F->stage2_only)
+    throw HostError(SLABLU_ERR_CONFIG, "solve: a sweep_build handle holds stage two only, use slablu_gpu_sweep_solve");
   if (F->sharded)
     throw HostError(SLABLU_ERR_CONFIG, "solve: sharded factorization, use slablu_gpu_shard_solve_forward/backward");
   std::lock_guard<std::mutex> guard(F->solve_mu);
+  DeviceGuard dg(F->device);
   cudaStream_t st = F->stream;
+  StreamScope scope(st);
   const int dev = F->device;
   const int64_t N = F->N;
   cudaEvent_t e0, e1;
@@ -1200,6 +1257,7 @@ void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   F->launches_solve = slb::g_kernel_count.load() - l0;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  check_solve_status(F);
 }
 
 slablu_gpu_status status_from(const HostError& e) { return make_status(e.code, e.what(), e.index); }
@@ -1310,7 +1368,7 @@ slablu_gpu_status slablu_gpu_residual(const slablu_gpu_fact* fact, const double*
     if (!fact) throw HostError(SLABLU_ERR_GENERIC, "residual: null factorization");
     if (!fact->a_rp.p) throw HostError(SLABLU_ERR_CONFIG, "residual: factorize with config.refine > 0 to keep the operator");
     if (ldf != fact->N || ldu != fact->N || nrhs < 1) throw HostError(SLABLU_ERR_GENERIC, "residual: ld must equal n1*n2");
-    SLB_CUDA_CHECK(cudaSetDevice(fact->device));
+    DeviceGuard dg(fact->device);
     const int64_t N = fact->N;
     residual_kernel<<<(unsigned)cdiv(N * nrhs, 256), 256, 0, fact->stream>>>(fact->a_rp.p, fact->a_ci.p, fact->a_v.p, N,
                                                                          nrhs, d_f, d_u, d_r); count_launch();
@@ -1350,7 +1408,7 @@ slablu_gpu_status slablu_gpu_solve(const slablu_gpu_fact* fact, const double* f,
     if (nrhs < 0 || ldf < fact->N || ldu < fact->N)
       throw HostError(SLABLU_ERR_GENERIC, "solve: rhs length must equal the grid size");
     if (nrhs == 0) return make_status(SLABLU_OK, "", -1);
-    SLB_CUDA_CHECK(cudaSetDevice(fact->device));
+    DeviceGuard dg(fact->device);
     const int64_t N = fact->N;
     DBuf<double> df, du;
     df.alloc(fact->device, (size_t)N * nrhs);
@@ -1408,7 +1466,7 @@ slablu_gpu_status slablu_gpu_T_block(const slablu_gpu_fact* F, int which, int64_
     const int64_t nb = which == 0 ? F->K : F->K - 1;
     if (j < 0 || j >= nb || which < 0 || which > 2) throw HostError(SLABLU_ERR_GENERIC, "T_block: index out of range");
     const int64_t base = which == 0 ? j : which == 1 ? F->K + j : 2 * F->K - 1 + j;
-    SLB_CUDA_CHECK(cudaSetDevice(F->device));
+    DeviceGuard dg(F->device);
     SLB_CUDA_CHECK(cudaMemcpy(out, F->Tkeep.p + base * F->n2 * F->n2, F->n2 * F->n2 * sizeof(double),
                               cudaMemcpyDeviceToHost));
   })
@@ -1416,53 +1474,123 @@ slablu_gpu_status slablu_gpu_T_block(const slablu_gpu_fact* F, int which, int64_
 
 slablu_gpu_status slablu_gpu_reduce_rhs(const slablu_gpu_fact* F, const double* f, int64_t nrhs, double* out) {
   ABI_TRY({
-    if (!F || F->single) throw HostError(SLABLU_ERR_GENERIC, "reduce_rhs: no partition");
+    if (!F || F->single || F->stage2_only) throw HostError(SLABLU_ERR_GENERIC, "reduce_rhs: no partition");
+    if (F->sharded) throw HostError(SLABLU_ERR_CONFIG, "reduce_rhs: sharded factorization");
+    if (nrhs < 1) throw HostError(SLABLU_ERR_GENERIC, "reduce_rhs: nrhs must be positive");
     std::lock_guard<std::mutex> guard(F->solve_mu);
-    SLB_CUDA_CHECK(cudaSetDevice(F->device));
+    DeviceGuard dg(F->device);
+    StreamScope scope(F->stream);
+    const int64_t N = F->N, Kn = (int64_t)F->K * F->n2;
+    DBuf<double> df, red;
+    df.alloc(F->device, (size_t)N * nrhs);
+    red.alloc(F->device, (size_t)Kn * nrhs);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(df.p, f, N * nrhs * sizeof(double), cudaMemcpyHostToDevice, F->stream));
+    StripSweeper sw(F, df.p, nrhs);  // the solve's own dispatch (cluster sweeps for nrhs <= 8)
+    reduce_phase(F, sw, df.p, nrhs, red.p, 0, F->K);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(out, red.p, Kn * nrhs * sizeof(double), cudaMemcpyDeviceToHost, F->stream));
+    SLB_CUDA_CHECK(cudaStreamSynchronize(F->stream));
+  })
+}
+
+slablu_gpu_status slablu_gpu_sweep_solve(const slablu_gpu_fact* F, const double* red, int64_t nrhs, double* u_ifc) {
+  ABI_TRY({
+    if (!F || F->single) throw HostError(SLABLU_ERR_GENERIC, "sweep_solve: no partition");
+    if (F->sharded) throw HostError(SLABLU_ERR_CONFIG, "sweep_solve: sharded factorization");
+    if (nrhs < 1) throw HostError(SLABLU_ERR_GENERIC, "sweep_solve: nrhs must be positive");
+    std::lock_guard<std::mutex> guard(F->solve_mu);
+    DeviceGuard dg(F->device);
+    StreamScope scope(F->stream);
+    const int64_t Kn = (int64_t)F->K * F->n2;
+    DBuf<double> r, u;
+    r.alloc(F->device, (size_t)Kn * nrhs);
+    u.alloc(F->device, (size_t)Kn * nrhs);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(r.p, red, Kn * nrhs * sizeof(double), cudaMemcpyHostToDevice, F->stream));
+    SweepSolver ss(F, nrhs);
+    ss.forward(r.p, u.p, 0, F->K);
+    ss.backward(u.p, 0, F->K);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(u_ifc, u.p, Kn * nrhs * sizeof(double), cudaMemcpyDeviceToHost, F->stream));
+    SLB_CUDA_CHECK(cudaStreamSynchronize(F->stream));
+    check_solve_status(F);
+  })
+}
+
+// sweep_build (stage_two.hpp:131-150, validate :41-56) on a caller-supplied block-tridiagonal
+// system: blocks = [diag 0..k-1 | super 0..k-2 | sub 0..k-2], each m x m column major (host).
+slablu_gpu_status slablu_gpu_sweep_build(int64_t m, int64_t k, const double* blocks, int device,
+                                         slablu_gpu_fact** out) {
+  ABI_TRY({
+    require_device();
+    *out = nullptr;
+    if (k < 1) throw HostError(SLABLU_ERR_CONFIG, "BlockTridiagonal: no blocks");
+    if (m < 1) throw HostError(SLABLU_ERR_CONFIG, "BlockTridiagonal: inconsistent block dimensions");
+    if (m > kMaxIfc)
+      throw HostError(SLABLU_ERR_UNSUPPORTED, "sweep_build: block dimension exceeds the engine's envelope");
+    auto F = std::make_unique<slablu_gpu_fact>();
+    F->device = device;
+    DeviceGuard dg(device);
+    SLB_CUDA_CHECK(cudaStreamCreateWithFlags(&F->stream, cudaStreamNonBlocking));
     cudaStream_t st = F->stream;
-    const int dev = F->device;
-    const int64_t n2 = F->n2, N = F->N, K = (int64_t)F->K * n2;
-    DBuf<double> df, red, contrib, ybuf;
-    DBuf<int32_t> dtasks, counter;
-    df.alloc(dev, (size_t)N * nrhs);
-    SLB_CUDA_CHECK(cudaMemcpy(df.p, f, N * nrhs * sizeof(double), cudaMemcpyHostToDevice));
-    red.alloc(dev, (size_t)K * nrhs);
-    contrib.alloc(dev, (size_t)F->S * 2 * nrhs * n2);
-    std::vector<int32_t> tasks;
-    for (int s = 0; s < F->S; s++)
-      for (int64_t c0 = 0; c0 < nrhs; c0 += kSweepChunk) {
-        tasks.push_back(s);
-        tasks.push_back(0);
-        tasks.push_back((int32_t)c0);
-      }
-    dtasks.alloc(dev, tasks.size());
-    counter.alloc(dev, 1);
-    SLB_CUDA_CHECK(cudaMemcpy(dtasks.p, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    SLB_CUDA_CHECK(cudaMemset(counter.p, 0, sizeof(int32_t)));
-    const int ntasks = (int)(tasks.size() / 3);
-    const int nslots = std::min(sm_count(dev), ntasks);
-    const int64_t sY = n2 * F->Wp * kSweepChunk;
-    ybuf.alloc(dev, (size_t)nslots * sY);
-    SchurArgs sa{};
-    sa.chunk = kSweepChunk; sa.u13 = F->u13.p;
-    sa.dsub = F->dsub.p;
-    sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
-    sa.exc = F->exc.p;
-    sa.excpos = F->excpos.p;
-    sa.bsc = getenv("SLB_NO_BSC") ? 0 : 1;  // backward shortcut (SLB_NO_BSC=1 disables, for A/B runs)
-    sa.hcol = F->hcol.p;
-    sa.hidx = F->hidx.p;
-    sa.Wp = F->Wp; sa.n2 = n2; sa.nstrips = F->S; sa.strips = F->strips.p; sa.fac = F->fac.p; sa.sF = F->sF;
-    sa.perm = F->perm.p; sa.sP = F->sP; sa.cpl = F->cpl.p; sa.sCPL = F->sCPL; sa.sym = F->sym.p;
-    sa.ybuf = ybuf.p; sa.sY = sY; sa.task_counter = counter.p; sa.ntasks = ntasks; sa.tasks = dtasks.p;
-    sa.N = N; sa.K = K; sa.nrhs = nrhs; sa.f = df.p; sa.mode = SWEEP_REDUCE; sa.out = contrib.p;
-    const unsigned gb = (unsigned)cdiv(K * nrhs, 256);
-    gather_ifc_kernel<<<gb, 256, 0, st>>>(df.p, N, nrhs, F->K, F->ifc_off.p, n2, red.p, K, 0, F->K); count_launch();
-    sweep(st, sa, nslots);
-    combine_reduce_kernel<<<gb, 256, 0, st>>>(red.p, K, nrhs, n2, F->S, F->strips.p, contrib.p, 0); count_launch();
-    SLB_CUDA_CHECK(cudaGetLastError());
+    StreamScope scope(st);
+    F->stage2_only = true;
+    F->n1 = k;
+    F->n2 = m;
+    F->N = k * m;
+    F->K = (int)k;
+    F->status.alloc(device, 1);
+    F->sstatus.alloc(device, 1);
+    static const DevStatus st0{0, INT_MAX, INT_MAX, INT_MAX};
+    SLB_CUDA_CHECK(cudaMemcpyAsync(F->status.p, &st0, sizeof(DevStatus), cudaMemcpyHostToDevice, st));
+    SLB_CUDA_CHECK(cudaMemcpyAsync(F->sstatus.p, &st0, sizeof(DevStatus), cudaMemcpyHostToDevice, st));
+    const int64_t nb = 3 * k - 2;
+    F->T.alloc(device, (size_t)nb * m * m);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(F->T.p, blocks, (size_t)nb * m * m * sizeof(double), cudaMemcpyHostToDevice, st));
+    check_finite(st, F->T.p, nb * m * m, F->status.p);
+    DevStatus hs;
+    SLB_CUDA_CHECK(cudaMemcpyAsync(&hs, F->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
     SLB_CUDA_CHECK(cudaStreamSynchronize(st));
-    SLB_CUDA_CHECK(cudaMemcpy(out, red.p, K * nrhs * sizeof(double), cudaMemcpyDeviceToHost));
+    if (hs.flags & ERR_NONFINITE) throw HostError(SLABLU_ERR_GENERIC, "BlockTridiagonal: non-finite block entry");
+    cudaEvent_t e0, e1;
+    SLB_CUDA_CHECK(cudaEventCreate(&e0));
+    SLB_CUDA_CHECK(cudaEventCreate(&e1));
+    SLB_CUDA_CHECK(cudaEventRecord(e0, st));
+    const int64_t l0 = slb::g_kernel_count.load();
+    stage_two_build(F.get());
+    SLB_CUDA_CHECK(cudaEventRecord(e1, st));
+    SLB_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0;
+    SLB_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    F->t2 = ms * 1e-3;
+    F->launches_factor = slb::g_kernel_count.load() - l0;
+    F->storage2 = (k + 2 * (k - 1)) * m * m;
+    SLB_CUDA_CHECK(cudaMemcpy(&hs, F->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost));
+    if (hs.flags & ERR_SINGULAR)
+      throw HostError(SLABLU_ERR_SINGULAR, "sweep_build: singular Schur complement block", hs.singular_block);
+    *out = F.release();
+  })
+}
+
+slablu_gpu_status slablu_gpu_recover(const slablu_gpu_fact* F, const double* f, const double* u_ifc, int64_t nrhs,
+                                     double* u) {
+  ABI_TRY({
+    if (!F || F->single || F->stage2_only) throw HostError(SLABLU_ERR_GENERIC, "recover: no partition");
+    if (F->sharded) throw HostError(SLABLU_ERR_CONFIG, "recover: sharded factorization");
+    if (nrhs < 1) throw HostError(SLABLU_ERR_GENERIC, "recover: nrhs must be positive");
+    std::lock_guard<std::mutex> guard(F->solve_mu);
+    DeviceGuard dg(F->device);
+    StreamScope scope(F->stream);
+    const int64_t N = F->N, Kn = (int64_t)F->K * F->n2;
+    DBuf<double> df, du, dui;
+    df.alloc(F->device, (size_t)N * nrhs);
+    du.alloc(F->device, (size_t)N * nrhs);
+    dui.alloc(F->device, (size_t)Kn * nrhs);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(df.p, f, N * nrhs * sizeof(double), cudaMemcpyHostToDevice, F->stream));
+    SLB_CUDA_CHECK(cudaMemcpyAsync(dui.p, u_ifc, Kn * nrhs * sizeof(double), cudaMemcpyHostToDevice, F->stream));
+    StripSweeper sw(F, df.p, nrhs);
+    recover_phase(F, sw, dui.p, nrhs, du.p, 0, F->K);
+    SLB_CUDA_CHECK(cudaMemcpyAsync(u, du.p, N * nrhs * sizeof(double), cudaMemcpyDeviceToHost, F->stream));
+    SLB_CUDA_CHECK(cudaStreamSynchronize(F->stream));
   })
 }
 
@@ -1481,7 +1609,7 @@ int slablu_gpu_debug_dense_bench(int64_t n, int device, double* out) {
     C.alloc(device, n * n);
     ipiv.alloc(device, n);
     status.alloc(device, 1);
-    DevStatus st0{0, INT_MAX, INT_MAX, 0};
+    DevStatus st0{0, INT_MAX, INT_MAX, INT_MAX};
     SLB_CUDA_CHECK(cudaMemcpy(status.p, &st0, sizeof(st0), cudaMemcpyHostToDevice));
     std::vector<double> h(n * n);
     uint64_t x = 88172645463325252ULL;
@@ -1540,7 +1668,7 @@ int slablu_gpu_debug_getrs(int64_t n, int64_t nrhs, const double* a, const doubl
     ipiv.alloc(device, n);
     perm.alloc(device, n);
     status.alloc(device, 1);
-    DevStatus st0{0, INT_MAX, INT_MAX, 0};
+    DevStatus st0{0, INT_MAX, INT_MAX, INT_MAX};
     SLB_CUDA_CHECK(cudaMemcpy(status.p, &st0, sizeof(st0), cudaMemcpyHostToDevice));
     SLB_CUDA_CHECK(cudaMemcpy(A.p, a, n * n * sizeof(double), cudaMemcpyHostToDevice));
     SLB_CUDA_CHECK(cudaMemcpy(B.p, b, n * nrhs * sizeof(double), cudaMemcpyHostToDevice));
@@ -1554,7 +1682,7 @@ int slablu_gpu_debug_getrs(int64_t n, int64_t nrhs, const double* a, const doubl
     reps = std::max(reps, 1);
     SLB_CUDA_CHECK(cudaEventRecord(e0, st));
     for (int r = 0; r < reps; r++) {
-      getrs_chain(st, n, nrhs, A.p, D.p, perm.p, B.p, n, X.p, n, 1.0, 0.0, yz.p, ++epoch);
+      getrs_chain(st, n, nrhs, A.p, D.p, perm.p, B.p, n, X.p, n, 1.0, 0.0, yz.p, ++epoch, status.p);
     }
     SLB_CUDA_CHECK(cudaEventRecord(e1, st));
     SLB_CUDA_CHECK(cudaEventSynchronize(e1));

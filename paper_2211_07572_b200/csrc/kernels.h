@@ -36,12 +36,13 @@ enum ErrBits : int32_t {
   ERR_SINGULAR = 8,           // exactly singular pivot
   ERR_IFC_STRUCTURE = 16,     // interface row couples outside adjacent strips/interfaces
   ERR_NONFINITE = 32,         // non-finite reduced block entry
+  ERR_CHAIN_TIMEOUT = 64,     // getrs_chain: a published block never arrived (bounded spin expired)
 };
 struct DevStatus {
   int32_t flags;
   int32_t singular_strip;  // lowest strip index with a singular pivot (or INT_MAX)
   int32_t singular_block;  // lowest sweep block index with a singular pivot
-  int32_t pad;
+  int32_t singular_pos;    // single strip: lowest level * Wp + column of a zero pivot (or INT_MAX)
 };
 
 // ---- band_lu.cu --------------------------------------------------------------
@@ -169,7 +170,7 @@ inline int64_t getrs_chain_scratch(int64_t n, int64_t nrhs) { return 2 * 16 * n 
 void getrs_chain_init(cudaStream_t st, int64_t n, int64_t nrhs, double* yz);
 void getrs_chain(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const double* dinv,
                  const int32_t* perm, const double* b, int64_t ldb, double* x, int64_t ldx, double alpha,
-                 double beta, double* yz, int epoch);
+                 double beta, double* yz, int epoch, DevStatus* status);
 
 // ---- solve.cu ---------------------------------------------------------------------
 

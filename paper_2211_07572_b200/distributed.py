@@ -83,25 +83,37 @@ class Shard:
         self.plan = shard_plan(self.n1, self.n2, self.b, self.rank, self.nranks)
         self.stats = st
 
+    def _sync(self):
+        # The engine runs on its own stream.  torch.distributed recv/all_reduce and torch
+        # kernels (zeros_like, sums) complete on torch's current stream of this device, so
+        # every engine call first waits for that stream; the engine's calls return with
+        # their outputs complete (include/slablu_gpu.h), so no wait is needed after them.
+        if self.device.type == "cuda":
+            self.torch.cuda.current_stream(self.device).synchronize()
+
     def new_message(self, cols):
         """An n2 x cols column-major message buffer (torch shape (cols, n2))."""
         return self.torch.empty((cols, self.n2), dtype=self.torch.float64, device=self.device)
 
     def sweep(self, m_in, m_out):
+        self._sync()
         _check(lib().slablu_gpu_shard_sweep(self._h, _ptr(m_in), _ptr(m_out)))
 
     def solve_forward(self, f, m_in, m_out):
         """f: (nrhs, N) CUDA tensor (column-major N x nrhs)."""
         nrhs = f.shape[0] if f.dim() == 2 else 1
+        self._sync()
         _check(lib().slablu_gpu_shard_solve_forward(self._h, f.data_ptr(), self.N, nrhs, _ptr(m_in), _ptr(m_out)))
 
     def solve_backward(self, m_in, m_out, u):
         """u: (nrhs, N) CUDA tensor; receives this shard's unknowns (others untouched)."""
+        self._sync()
         _check(lib().slablu_gpu_shard_solve_backward(self._h, _ptr(m_in), _ptr(m_out), u.data_ptr(), self.N))
 
     def residual(self, f, u, r):
         """r = f - A u (all rows; f, u, r: (nrhs, N) CUDA tensors)."""
         nrhs = f.shape[0] if f.dim() == 2 else 1
+        self._sync()
         _check(lib().slablu_gpu_residual(self._h, f.data_ptr(), self.N, nrhs, u.data_ptr(), self.N, r.data_ptr()))
 
     def refresh_stats(self):

@@ -372,6 +372,24 @@ class Factorization:
         _check(lib().slablu_gpu_reduce_rhs(self._h, _p(f), f.shape[1], _p(out)))
         return out
 
+    def sweep_solve(self, red):
+        """Staged sweep solve (stage_two.hpp:170-188): interface values u_ifc (k*n2 x nrhs) from
+        the reduced right-hand side."""
+        red = np.asfortranarray(np.asarray(red, np.float64).reshape(self.stats.interfaces * self.n2, -1))
+        out = np.empty_like(red, order="F")
+        _check(lib().slablu_gpu_sweep_solve(self._h, _p(red), red.shape[1], _p(out)))
+        return out
+
+    def recover(self, f, u_ifc):
+        """Staged recover_interiors (stage_one.hpp:438-462): the full solution (N x nrhs) from f and
+        the interface values."""
+        n = self.n1 * self.n2
+        f = np.asfortranarray(np.asarray(f, np.float64).reshape(n, -1))
+        u_ifc = np.asfortranarray(np.asarray(u_ifc, np.float64).reshape(-1, f.shape[1]))
+        out = np.empty_like(f, order="F")
+        _check(lib().slablu_gpu_recover(self._h, _p(f), _p(u_ifc), f.shape[1], _p(out)))
+        return out
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             lib().slablu_gpu_destroy(self._h)
@@ -397,8 +415,88 @@ def factorize(system: SparseSystem, config: SolverConfig = SolverConfig()) -> Fa
     return Factorization(h.value, config)
 
 
+class BlockTridiagonal:
+    """stage_two.hpp:31-121: k diagonal blocks, k-1 sub (row j+1, col j) and super blocks, m x m."""
+
+    def __init__(self, diag, sup, sub):
+        self.diag, self.super, self.sub = list(diag), list(sup), list(sub)
+
+    def block_count(self):
+        return len(self.diag)
+
+    def block_dim(self):
+        return 0 if not self.diag else self.diag[0].shape[0]
+
+    def to_dense(self):
+        k, m = self.block_count(), self.block_dim()
+        a = np.zeros((k * m, k * m))
+        for j in range(k):
+            a[j * m:(j + 1) * m, j * m:(j + 1) * m] = self.diag[j]
+        for j in range(k - 1):
+            a[j * m:(j + 1) * m, (j + 1) * m:(j + 2) * m] = self.super[j]
+            a[(j + 1) * m:(j + 2) * m, j * m:(j + 1) * m] = self.sub[j]
+        return a
+
+
+class SweepFactorization:
+    """stage_two.hpp:126-232 on the GPU: LU factors of the sweep's S_j (slablu_gpu_sweep_build)."""
+
+    def __init__(self, t: BlockTridiagonal, device=0):
+        k = t.block_count()
+        if k == 0:
+            raise ConfigError("BlockTridiagonal: no blocks")
+        m = t.block_dim()
+        if len(t.super) != k - 1 or len(t.sub) != k - 1:
+            raise ConfigError("BlockTridiagonal: off-diagonal count must be k - 1")
+        for blk in t.diag + t.super + t.sub:
+            if np.shape(blk) != (m, m):
+                raise ConfigError("BlockTridiagonal: inconsistent block dimensions")
+        blocks = np.concatenate([np.asfortranarray(b, np.float64).ravel(order="F") for b in t.diag + t.super + t.sub])
+        h = ctypes.c_void_p()
+        _check(lib().slablu_gpu_sweep_build(int(m), int(k), _p(blocks), int(device), ctypes.byref(h)))
+        self._h = h
+        self.k, self.m = k, m
+        st = _lib.Stats()
+        _check(lib().slablu_gpu_stats(self._h, ctypes.byref(st)))
+        self.stats = st
+
+    def storage_scalars(self):
+        return int(self.stats.storage_stage2)
+
+    def solve(self, f):
+        f = np.asfortranarray(np.asarray(f, np.float64).reshape(self.k * self.m, -1))
+        out = np.empty_like(f, order="F")
+        _check(lib().slablu_gpu_sweep_solve(self._h, _p(f), f.shape[1], _p(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().slablu_gpu_destroy(self._h)
+            self._h = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def sweep_build(t: BlockTridiagonal, device=0) -> SweepFactorization:
+    """stage_two.hpp:241-243."""
+    return SweepFactorization(t, device)
+
+
+def _torch_sync(t):
+    """The engine runs on its own stream: work queued on torch's current stream that produces
+    an input (copies, kernels, NCCL receives) must be complete before the engine reads it."""
+    import torch
+    if t.is_cuda:
+        torch.cuda.current_stream(t.device).synchronize()
+
+
 def factorize_device(n1, n2, row_ptr, col_idx, values, config: SolverConfig = SolverConfig()) -> Factorization:
     """CSR already resident on the GPU (torch CUDA tensors int32/int32/float64)."""
+    _torch_sync(values)
     h = ctypes.c_void_p()
     cfg = config._c()
     _check(lib().slablu_gpu_factorize_device(int(n1), int(n2), int(values.numel()), row_ptr.data_ptr(),
@@ -423,6 +521,7 @@ def solve_device(fact: Factorization, f, u):
     """Device-resident solve: f, u are torch CUDA float64 tensors of shape (nrhs, N) (column-major N x nrhs)."""
     n = fact.n1 * fact.n2
     nrhs = f.shape[0] if f.dim() == 2 else 1
+    _torch_sync(f)
     _check(lib().slablu_gpu_solve_device(fact._h, f.data_ptr(), n, nrhs, u.data_ptr(), n))
     return u
 

@@ -225,7 +225,7 @@ def test_ten_ppw_helmholtz_vs_oracle(n, b):
     d = relerr(u, u_o)
     print(f"10ppw n={n}: diff vs oracle {d:.3e}, backward error gpu {eta_g:.3e} oracle {eta_o:.3e}")
     assert eta_g < 1e-14 and eta_g < 10 * eta_o + 1e-16
-    assert d < 1e-8
+    assert d < 1e-10
 
 
 def test_forward_shortcut_matches_full_operator(monkeypatch):
