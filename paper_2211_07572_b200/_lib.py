@@ -109,9 +109,18 @@ def lib():
     L.slablu_gpu_T_block.argtypes = [P, I, I64, P]
     L.slablu_gpu_reduce_rhs.restype = St
     L.slablu_gpu_reduce_rhs.argtypes = [P, P, I64, P]
+    L.slablu_gpu_sweep_solve.restype = St
+    L.slablu_gpu_sweep_solve.argtypes = [P, P, I64, P]
+    L.slablu_gpu_recover.restype = St
+    L.slablu_gpu_recover.argtypes = [P, P, P, I64, P]
+    L.slablu_gpu_sweep_build.restype = St
+    L.slablu_gpu_sweep_build.argtypes = [I64, I64, P, I, P]
     L.slablu_gpu_destroy.restype = None
     L.slablu_gpu_destroy.argtypes = [P]
     L.slablu_gpu_device_count.restype = I
     L.slablu_gpu_device_count.argtypes = []
+    for name in EXPORTS:  # every exported entry point has a declared signature
+        if getattr(L, name).argtypes is None:
+            raise ImportError(f"{name}: ctypes signature not declared in _lib.py")
     _lib = L
     return L

@@ -137,6 +137,14 @@ void sweep(cudaStream_t st, const SchurArgs& a, int nslots);
 // ybuf holds ntasks slabs of n2 * Wp * 8 doubles.
 bool strip_solve_fits(int Wp, int64_t n2);
 void strip_solve(cudaStream_t st, const SchurArgs& a, int ntasks);  // launches 2 kernels
+// b_l of every (task, level) packed level-major into ybuf (8 columns per task), recover-mode
+// couplings folded in.
+void strip_rhs_pack(cudaStream_t st, const SchurArgs& a, int ntasks);
+// Version 2 (solve2.cu): TMA tensor slices + st.async level exchange, cluster size chosen at run
+// time (2..8 CTAs); ybuf as for strip_solve.
+bool strip_solve2_fits(int Wp, int64_t n2, int G);
+int strip_solve2_cluster(int Wp, int64_t n2, int ntasks);
+void strip_solve2(cudaStream_t st, const SchurArgs& a, int ntasks);
 
 // T block assembly from per-strip G buffers (reference order: direct, left strip, right strip).
 // Interface-block ranges of a (possibly sharded) factorization: local strips are the global

@@ -509,6 +509,11 @@ __global__ void __launch_bounds__(THREADS, 1) strip_solve_kernel(SchurArgs a) {
 
 }  // namespace
 
+void strip_rhs_pack(cudaStream_t st, const SchurArgs& a, int ntasks) {
+  rhs_pack_kernel<<<dim3((unsigned)ntasks, (unsigned)cdiv(a.n2, 32)), 256, 0, st>>>(a); count_launch();
+  SLB_CUDA_CHECK(cudaGetLastError());
+}
+
 bool strip_solve_fits(int Wp, int64_t n2) {
   const int MTH = Wp / 8;
   if (MTH > 64 || (MTH + G - 1) / G > 8) return false;
