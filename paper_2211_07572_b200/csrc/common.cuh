@@ -87,6 +87,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// Same with a suspend-time hint: the waiting thread sleeps in hardware until the phase completes
+// (or the hint, in ns, expires) instead of re-polling; spinning warps otherwise take issue slots
+// from the warps doing the work on the same sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(1000000u)
+      : "memory");
+}
 // Distributed shared memory: address of `local` in CTA `rank` of the cluster, and 32-bit loads
 // through the shared::cluster window (cheaper than generic loads of a mapped pointer).
 __device__ __forceinline__ uint32_t dsmem_map(const void* local, int rank) {

@@ -372,6 +372,7 @@ struct slablu_gpu_fact {
   DBuf<int32_t> ipivT;  // pivots of LU(S_j), n2 per interface
   DBuf<int32_t> permT;  // the same interchanges as a row permutation (getrs_chain)
   DBuf<double> dinvT;   // inverses of the 64x64 diagonal blocks of L_j, U_j (getrs_chain)
+  DBuf<double> Xup;     // block upper factor X_j = S_j^{-1} super_j (n2 x n2 per interface j < K-1)
   DBuf<double> Tkeep;   // optional copy of the reduced blocks
   DBuf<DevStatus> status;
   DBuf<DevStatus> sstatus;   // solve-time status (getrs_chain timeouts)
@@ -430,18 +431,21 @@ void stage_two_build(slablu_gpu_fact* F) {
   cudaStream_t st = F->stream;
   const int dev = F->device, K = F->K;
   const int64_t n2 = F->n2, bs = n2 * n2;
-  DBuf<double> X;
-  X.alloc(dev, bs);
   const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
   F->ipivT.alloc(dev, (size_t)std::max(K, 1) * n2);
   F->permT.alloc(dev, (size_t)std::max(K, 1) * n2);
   F->dinvT.alloc(dev, (size_t)std::max(K, 1) * dinv_sz);
+  // The block LU T = L~ U~ keeps, besides LU(S_j), U~'s off-diagonal blocks X_j = S_j^{-1} super_j:
+  // the recurrence computes them anyway (stage_two.hpp:138-140), and the backward sweep of the
+  // solve is then u_j -= X_j u_{j+1}, one GEMV instead of a GEMV plus a triangular-solve chain.
+  F->Xup.alloc(dev, (size_t)std::max(K - 1, 1) * bs);
   for (int j = 0; j < K; j++) {
     double* Sj = F->Tdiag() + j * bs;
     if (j > 0) {
-      SLB_CUDA_CHECK(cudaMemcpyAsync(X.p, F->Tsup() + (j - 1) * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      dgetrs(st, n2, n2, F->Tdiag() + (j - 1) * bs, F->ipivT.p + (size_t)(j - 1) * n2, X.p, n2, nullptr);
-      dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X.p, n2, 0, 1.0, Sj, n2, 0, 1);
+      double* X = F->Xup.p + (size_t)(j - 1) * bs;
+      SLB_CUDA_CHECK(cudaMemcpyAsync(X, F->Tsup() + (j - 1) * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      dgetrs(st, n2, n2, F->Tdiag() + (j - 1) * bs, F->ipivT.p + (size_t)(j - 1) * n2, X, n2, nullptr);
+      dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X, n2, 0, 1.0, Sj, n2, 0, 1);
     }
     dgetrf(st, n2, Sj, F->ipivT.p + (size_t)j * n2, nullptr, F->status.p, j);
     getrs_prepare(st, n2, Sj, F->ipivT.p + (size_t)j * n2, F->permT.p + (size_t)j * n2, F->dinvT.p + (size_t)j * dinv_sz);
@@ -877,7 +881,7 @@ struct StripSweeper {
   const slablu_gpu_fact* F;
   cudaStream_t st;
   int CH = 8, ntasks = 0, nslots = 0;
-  bool clustered = false;
+  bool clustered = false, v2 = false;
   DBuf<int32_t> dtasks, counter;
   DBuf<double> ybuf;
   SchurArgs sa{};
@@ -897,14 +901,18 @@ struct StripSweeper {
     dtasks.alloc(dev, tasks.size());
     counter.alloc(dev, 1);
     SLB_CUDA_CHECK(cudaMemcpyAsync(dtasks.p, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    clustered = CH == 8 && strip_solve_fits(F->Wp, n2);
+    // cluster sweeps for small nrhs: version 2 (TMA tensor slices + st.async exchange, solve2.cu)
+    // unless SLB_SOLVE_V1=1 selects the round-1 kernel (solve.cu)
+    static const bool force_v1 = getenv("SLB_SOLVE_V1") != nullptr;
+    v2 = CH == 8 && !force_v1 && strip_solve2_fits(F->Wp, n2, std::min(4, F->Wp / 8));
+    clustered = CH == 8 && (v2 || strip_solve_fits(F->Wp, n2));
     nslots = clustered ? ntasks : std::min(sm_count(dev), ntasks);
     const int64_t sY = n2 * F->Wp * CH;
     ybuf.alloc(dev, (size_t)nslots * sY);
     sa.chunk = CH;
     sa.u13 = F->u13.p;
     sa.dsub = F->dsub.p;
-    sa.fsc = getenv("SLB_NO_FSC") ? 0 : 1;  // forward shortcut (SLB_NO_FSC=1 disables, for A/B runs)
+    sa.fsc = getenv("SLB_NO_FSC") ? 0 : getenv("SLB_SOLVE_NOTMA") ? 2 : 1;  // forward shortcut (A/B runs)
     sa.exc = F->exc.p;
     sa.excpos = F->excpos.p;
     sa.bsc = getenv("SLB_NO_BSC") ? 0 : 1;  // backward shortcut (SLB_NO_BSC=1 disables, for A/B runs)
@@ -936,7 +944,9 @@ struct StripSweeper {
     sa.mode = mode;
     sa.u_ifc = u_ifc;
     sa.out = out;
-    if (clustered) {
+    if (v2) {
+      strip_solve2(st, sa, ntasks);  // rhs pack + cluster sweep (+ contributions in reduce mode)
+    } else if (clustered) {
       strip_solve(st, sa, ntasks);  // rhs pack + cluster sweep
     } else {
       sweep(st, sa, nslots);
@@ -990,13 +1000,14 @@ struct SweepSolver {
       apply_Sinv(j, rj, Kn, uifc + j * n2, Kn, 1.0, 0.0);
     }
   }
+  // backward u_j -= S_j^{-1} super_j u_{j+1} = X_j u_{j+1} (stage_two.hpp:181-187 with the block upper
+  // factor kept by stage_two_build)
   void backward(double* uifc, int jlo, int jhi) {
     const int64_t n2 = F->n2, Kn = (int64_t)F->K * n2, bs = n2 * n2;
     for (int j = jhi - 1; j >= jlo; j--) {
       if (j + 1 >= F->K) continue;
-      dgemv_batched_rhs(F->stream, n2, n2, nrhs, 1.0, F->Tsup() + j * bs, n2, uifc + (j + 1) * n2, Kn, 0.0, tmp.p,
-                        n2, part.p);
-      apply_Sinv(j, tmp.p, n2, uifc + j * n2, Kn, -1.0, 1.0);
+      dgemv_batched_rhs(F->stream, n2, n2, nrhs, -1.0, F->Xup.p + (size_t)j * bs, n2, uifc + (j + 1) * n2, Kn, 1.0,
+                        uifc + j * n2, Kn, part.p);
     }
   }
 };
@@ -1098,12 +1109,12 @@ void shard_sweep_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
   F->ipivT.alloc(dev, (size_t)std::max(F->K, 1) * n2);
   F->permT.alloc(dev, (size_t)std::max(F->K, 1) * n2);
   F->dinvT.alloc(dev, (size_t)std::max(F->K, 1) * dinv_sz);
-  DBuf<double> X;
-  X.alloc(dev, bs);
-  auto sub_Sinv_super = [&](int j, double* target) {  // target -= sub_j S_j^{-1} super_j
-    SLB_CUDA_CHECK(cudaMemcpyAsync(X.p, F->Tsup() + j * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    dgetrs(st, n2, n2, F->Tdiag() + j * bs, F->ipivT.p + (size_t)j * n2, X.p, n2, nullptr);
-    dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + j * bs, n2, 0, X.p, n2, 0, 1.0, target, n2, 0, 1);
+  F->Xup.alloc(dev, (size_t)std::max(F->K - 1, 1) * bs);
+  auto sub_Sinv_super = [&](int j, double* target) {  // X_j = S_j^{-1} super_j; target -= sub_j X_j
+    double* X = F->Xup.p + (size_t)j * bs;
+    SLB_CUDA_CHECK(cudaMemcpyAsync(X, F->Tsup() + j * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    dgetrs(st, n2, n2, F->Tdiag() + j * bs, F->ipivT.p + (size_t)j * n2, X, n2, nullptr);
+    dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + j * bs, n2, 0, X, n2, 0, 1.0, target, n2, 0, 1);
   };
   for (int j = j0; j < j1; j++) {
     double* Sj = F->Tdiag() + j * bs;
@@ -1449,7 +1460,8 @@ slablu_gpu_status slablu_gpu_stats(const slablu_gpu_fact* F, slablu_gpu_stats_t*
     o->t_stage2 = F->t2;
     o->storage_stage1 = F->storage1;
     o->storage_stage2 = F->storage2;
-    o->device_bytes = (int64_t)(F->fac.bytes() + F->perm.bytes() + F->cpl.bytes() + F->T.bytes() + F->Tkeep.bytes());
+    o->device_bytes = (int64_t)(F->fac.bytes() + F->perm.bytes() + F->cpl.bytes() + F->T.bytes() + F->Tkeep.bytes() +
+                                F->Xup.bytes());
     o->gpu_launches = F->launches_factor;
     o->solve_launches = F->launches_solve;
     o->t_chain = F->t_chain;

@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -44,6 +45,13 @@ constexpr int C = 8;                    // RHS columns per task (DMMA n = 8)
 constexpr int NCW = 8;                  // consumer warps
 constexpr int CTHREADS = NCW * 32;
 constexpr int THREADS = CTHREADS + 64;  // + op producer warp + level producer warp
+// DFMA variants need at most 6 row-tile warps (G >= 4 at Wp <= 160): 8 warps in all, so two warps
+// per SM sub-partition and the full 255-register budget (10 warps cap threads at 168 registers)
+constexpr int NCW_DFMA = 6;
+template <int NC>
+constexpr int ncw_of() { return NC == 0 ? NCW : NCW_DFMA; }
+template <int NC>
+constexpr int threads_of() { return ncw_of<NC>() * 32 + 64; }
 constexpr int STAGES = 4;               // op ring: half-level chunks
 constexpr int LS = 3;                   // level-data ring
 constexpr int MNMAX = 8;                // row tiles per CTA (G >= 3 for Wp <= 160)
@@ -85,7 +93,9 @@ __host__ __device__ inline Lay2 lay2(int Wp, int G, int64_t n2) {
   L.lv = L.op + STAGES * L.op_slot;
   L.xb = L.lv + LS * L.lv_slot;
   L.part = L.xb + 3LL * Wp * C * 8;
-  L.flags = L.part + (int64_t)NCW * L.MNB * 32 * 16;
+  // DMMA partial sums, or (DFMA, NC <= 2) one private t_top copy per row-tile warp
+  const int64_t part_dmma = (int64_t)NCW * L.MNB * 32 * 16, part_dfma = 6LL * Wp * 2 * 8;
+  L.flags = L.part + (part_dmma > part_dfma ? part_dmma : part_dfma);
   L.bytes = L.flags + round_up(n2, 16) + 128;  // + alignment slack of the dynamic window
   return L;
 }
@@ -117,8 +127,351 @@ __device__ __forceinline__ bool bwd_full2(uint8_t f, int bsc) {
   return (f & 1) && !(bsc && !(f & 64) && ((f >> 2) & 15) <= 8);
 }
 
-// maps[0] Ainv tiles, maps[1] Fbot tiles, maps[2] H tiles (see solve2_maps)
-__global__ void __launch_bounds__(THREADS, 1)
+// acc0/acc1 += A rows (fragment order: lane (g, t) holds A[g][4 k4 + t]) times b[k4 * bstride + n],
+// two interleaved accumulator sets for ILP (explicit pairs: a runtime parity index would spill).
+template <int NC>
+__device__ __forceinline__ void gemv_rows(const double* Aop, int MNB, const double* b, int bstride, int KH,
+                                          double (&acc0)[NC], double (&acc1)[NC]) {
+  int k4 = 0;
+#pragma unroll 2
+  for (; k4 + 1 < KH; k4 += 2) {
+    const double a0 = Aop[(int64_t)k4 * MNB * 32], a1 = Aop[(int64_t)(k4 + 1) * MNB * 32];
+#pragma unroll
+    for (int n = 0; n < NC; n++) {
+      acc0[n] = fma(a0, b[k4 * bstride + n], acc0[n]);
+      acc1[n] = fma(a1, b[(k4 + 1) * bstride + n], acc1[n]);
+    }
+  }
+  if (k4 < KH) {
+    const double a0 = Aop[(int64_t)k4 * MNB * 32];
+#pragma unroll
+    for (int n = 0; n < NC; n++) acc0[n] = fma(a0, b[k4 * bstride + n], acc0[n]);
+  }
+}
+
+// Prefetched form: the right-hand-side values of a chunk sit in registers (gathered before the
+// operator slice is waited for), KMAX = 20 k4 rows unrolled with predication (KH <= 20 for Wp <= 160).
+constexpr int KMAX = 20;
+// k4 rows gathered per batch (register budget: 4 columns take two batches)
+template <int NC>
+constexpr int kbatch() { return NC >= 4 ? KMAX / 2 : KMAX; }
+template <int NC>
+__device__ __forceinline__ void gemv_pref(const double* Aop, int MNB, const double (&bv)[kbatch<NC>()][NC], int k0,
+                                          int KH, double (&acc0)[NC], double (&acc1)[NC]) {
+  constexpr int KB = kbatch<NC>();
+  double av[KB];
+#pragma unroll
+  for (int k = 0; k < KB; k++) av[k] = k0 + k < KH ? Aop[(int64_t)(k0 + k) * MNB * 32] : 0.0;
+#pragma unroll
+  for (int k = 0; k < KB; k++)
+#pragma unroll
+    for (int n = 0; n < NC; n++) {
+      if (k & 1) acc1[n] = fma(av[k], bv[k][n], acc1[n]);
+      else acc0[n] = fma(av[k], bv[k][n], acc0[n]);
+    }
+}
+
+// Fully unrolled form for a compile-time chunk height K (no predicates): all A and b loads first,
+// then two interleaved FMA chains.  Aw = this lane's element of k4 row 0, S = doubles per k4 row;
+// b rows at bw[k * BS + n].
+template <int NC, int K, int BS>
+__device__ __forceinline__ void gemv_fixed(const double* Aw, int S, const double* bw, double (&acc0)[NC],
+                                           double (&acc1)[NC]) {
+  double av[K], bv[K][NC];
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    av[k] = Aw[k * S];
+#pragma unroll
+    for (int n = 0; n < NC; n++) bv[k][n] = bw[k * BS + n];
+  }
+#pragma unroll
+  for (int k = 0; k < K; k++)
+#pragma unroll
+    for (int n = 0; n < NC; n++) {
+      if (k & 1) acc1[n] = fma(av[k], bv[k][n], acc1[n]);
+      else acc0[n] = fma(av[k], bv[k][n], acc0[n]);
+    }
+}
+// KH (k4 rows of a chunk, Wp / 8 <= 20) dispatched to its unrolled form (warp-uniform jump)
+template <int NC, int BS>
+__device__ __forceinline__ void gemv_k(int KH, const double* Aw, int S, const double* bw, double (&acc0)[NC],
+                                       double (&acc1)[NC]) {
+  switch (KH) {
+#define SLB_K(k) \
+  case k: gemv_fixed<NC, k, BS>(Aw, S, bw, acc0, acc1); break;
+    SLB_K(1) SLB_K(2) SLB_K(3) SLB_K(4) SLB_K(5) SLB_K(6) SLB_K(7) SLB_K(8) SLB_K(9) SLB_K(10)
+    SLB_K(11) SLB_K(12) SLB_K(13) SLB_K(14) SLB_K(15) SLB_K(16) SLB_K(17) SLB_K(18) SLB_K(19) SLB_K(20)
+#undef SLB_K
+    default: break;
+  }
+}
+
+// DFMA consumer (see strip_solve2_kernel): warp w < mn, row tile w of this CTA's slice.
+template <int NC>
+__device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, int rank, int m0, int mn, int w,
+                                                     int lane, int Wp, int64_t n2, const Lay2& Ly,
+                                                     unsigned char* smraw, double* xbuf, const uint8_t* sfl,
+                                                     uint64_t* full_bar, uint64_t* empty_bar, uint64_t* lfull,
+                                                     uint64_t* lempty, uint64_t* xbar, uint64_t* fwd_done,
+                                                     double* ybase, int ncols, int q0, const StripDesc& sd) {
+  const int g = lane >> 2, t = lane & 3;
+  const int KH = Ly.KH, MNB = Ly.MNB;
+  const int WC = Wp * C;
+  const int row = (m0 + w) * 8 + g;  // this lane's output row (all 4 t lanes hold the reduced sums)
+  const uint32_t xbytes = (uint32_t)(Wp * NC * 8);
+  int slot = 0, ls = 0;
+  uint32_t fph = 0, lph = 0, xq = 0;
+  auto arm = [&]() {
+    if (w == 0 && lane == 0) mbar_arrive_expect_tx(&xbar[xq & 1], xbytes);
+  };
+  auto wait_x = [&]() {
+    mbar_wait(&xbar[xq & 1], (xq >> 1) & 1u);
+    xq++;
+  };
+  auto acquire_op = [&]() -> const double* {
+    mbar_wait(&full_bar[slot], fph);
+    return reinterpret_cast<const double*>(smraw + Ly.op + (int64_t)slot * Ly.op_slot);
+  };
+  auto release_op = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[slot]);
+    if (++slot == STAGES) {
+      slot = 0;
+      fph ^= 1u;
+    }
+  };
+  auto release_lv = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&lempty[ls]);
+    if (++ls == LS) {
+      ls = 0;
+      lph ^= 1u;
+    }
+  };
+  // sum over the 4 t lanes of a row: every lane ends with the row's totals
+  auto rowsum = [&](double (&acc)[NC]) {
+#pragma unroll
+    for (int n = 0; n < NC; n++) {
+      acc[n] += __shfl_xor_sync(0xffffffffu, acc[n], 1);
+      acc[n] += __shfl_xor_sync(0xffffffffu, acc[n], 2);
+    }
+  };
+  auto pick = [&](const double (&v)[NC]) -> double {  // column t of a row vector (t < NC)
+    double r = v[0];
+#pragma unroll
+    for (int n = 1; n < NC; n++)
+      if (t == n) r = v[n];
+    return r;
+  };
+#ifdef SLB_SOLVE_PROF
+  long long P0 = clock64(), ph[24] = {0};
+#define PN(k) { const long long q_ = clock64(); ph[k] += q_ - P0; P0 = q_; }
+#else
+#define PN(k)
+#endif
+  // this lane's (row, column tc) element of a row-tile vector; the row's NC values gathered from the
+  // 4 t lanes, so that lane t can push the whole row to cluster CTA t (and t + 4): the G pushes of a
+  // row go out in parallel, one st.async per lane
+  const int tc = t < NC ? t : 0;
+  // lane t pushes to cluster CTAs t and t + 4: their window addresses, resolved once
+  const uint32_t rxa = dsmem_map(xbuf, t < G ? t : 0), rxb = dsmem_map(xbuf, t + 4 < G ? t + 4 : 0);
+  const uint32_t rb0a = dsmem_map(&xbar[0], t < G ? t : 0), rb0b = dsmem_map(&xbar[0], t + 4 < G ? t + 4 : 0);
+  const uint32_t rb1a = dsmem_map(&xbar[1], t < G ? t : 0), rb1b = dsmem_map(&xbar[1], t + 4 < G ? t + 4 : 0);
+  auto push_row = [&](int buf, double v) {
+    double vv[NC];
+#pragma unroll
+    for (int n = 0; n < NC; n++) vv[n] = __shfl_sync(0xffffffffu, v, (lane & ~3) + n);
+    const uint32_t off = (uint32_t)(((buf * Wp + row) * C) * 8);
+    const bool b = xq & 1;
+#pragma unroll
+    for (int rr = 0; rr < 8; rr += 4) {
+      if (rr + t >= G) continue;
+      const uint32_t dst = (rr ? rxb : rxa) + off, bar = b ? (rr ? rb1b : rb1a) : (rr ? rb0b : rb0a);
+      if constexpr (NC == 1) {
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(dst),
+                     "d"(vv[0]), "r"(bar)
+                     : "memory");
+      } else {
+#pragma unroll
+        for (int n = 0; n < NC; n += 2) st_async_v2(dst + n * 8, vv[n], vv[n + 1], bar);
+      }
+    }
+  };
+  // ---------------- forward ----------------
+  // t_top: NC <= 2 one private copy per warp (no CTA barrier), NC = 4 one shared copy
+  double* ttsh = xbuf + 2 * WC;
+  double* ttw = NC <= 2 ? reinterpret_cast<double*>(smraw + Ly.part) + w * Wp * NC : ttsh;
+  for (int64_t l = 0; l < n2; l++) {
+    const bool hn = l + 1 < n2;
+    const uint8_t fl = sfl[l];
+    const bool sc = fwd_shortcut(fl, a.fsc);
+    const double* z = xbuf + (int)(l & 1) * WC;
+    PN(7)
+    if (l > 0) wait_x();
+    if (hn) arm();
+    PN(0)
+    mbar_wait(&lfull[ls], lph);
+    PN(1)
+    const unsigned char* lv = smraw + Ly.lv + (int64_t)ls * Ly.lv_slot;
+    const int* sperm = reinterpret_cast<const int*>(lv + Ly.o_perm);
+    const double* bn = reinterpret_cast<const double*>(lv + Ly.o_b);
+    auto val = [&](int src, int n) -> double {  // row src, column n of [z_l ; b_{l+1}]
+      if (src < Wp) return z[src * C + n];
+      return hn ? bn[(src - Wp) * C + n] : 0.0;
+    };
+    // t_top = rows perm[0..Wp) of [z_l ; b_{l+1}], compact [k][NC].  Reuse is safe: the next
+    // level rewrites it only after its exchange wait, which needs this level's pushes.
+    if constexpr (NC <= 2) {
+      for (int idx = lane; idx < Wp * NC; idx += 32) ttw[idx] = val(sperm[idx / NC], idx % NC);
+      __syncwarp();
+    } else {
+      for (int idx = w * 32 + lane; idx < Wp * NC; idx += mn * 32) ttsh[idx] = val(sperm[idx / NC], idx % NC);
+      asm volatile("bar.sync 2, %0;\n" ::"r"(mn * 32) : "memory");
+    }
+    PN(2)
+    // epilogue operands ahead of the GEMV: t_bot, diag(Lsub), and the exceptional rows of this
+    // tile (z = t_bot + Fbot[e, :] t_top needs t_top only)
+    double tb = 0.0, d = 0.0, zexc = 0.0;
+    bool is_exc = false;
+    if (hn) {
+      tb = val(sperm[Wp + row], tc);
+      if (sc) {
+        d = reinterpret_cast<const double*>(lv + Ly.o_dsub)[row];
+        const int ncx = (fl >> 2) & 15;
+        const int* epos = reinterpret_cast<const int*>(lv + Ly.o_epos);
+        const double* exc = reinterpret_cast<const double*>(lv + Ly.o_exc);
+        for (int e = 0; e < ncx; e++) {
+          const int er = epos[e];
+          if (er < (m0 + w) * 8 || er >= (m0 + w) * 8 + 8) continue;  // warp-uniform
+          double q[NC];
+#pragma unroll
+          for (int n = 0; n < NC; n++) q[n] = 0.0;
+          for (int k = lane; k < Wp; k += 32) {
+            const double ev = exc[e * Wp + k];
+#pragma unroll
+            for (int n = 0; n < NC; n++) q[n] = fma(ev, ttw[k * NC + n], q[n]);
+          }
+#pragma unroll
+          for (int n = 0; n < NC; n++)
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) q[n] += __shfl_xor_sync(0xffffffffu, q[n], o);
+          if (row == er) {
+            is_exc = true;
+            zexc = tb + pick(q);
+          }
+        }
+      }
+    }
+    PN(14)
+    double acc[2][NC], acc2[2][NC];
+#pragma unroll
+    for (int n = 0; n < NC; n++) acc[0][n] = acc[1][n] = acc2[0][n] = acc2[1][n] = 0.0;
+    const int nch = (sc || !hn) ? 2 : 4;
+    for (int c = 0; c < nch; c++) {
+      const double* tk = ttw + ((c & 1) * KH * 4 + t) * NC;
+      const double* Aw = acquire_op() + w * 32 + lane;
+      PN(5)
+      if (c < 2) gemv_k<NC, 4 * NC>(KH, Aw, MNB * 32, tk, acc[0], acc[1]);
+      else gemv_k<NC, 4 * NC>(KH, Aw, MNB * 32, tk, acc2[0], acc2[1]);
+      release_op();
+      PN(6)
+    }
+#pragma unroll
+    for (int n = 0; n < NC; n++) acc[0][n] += acc[1][n];
+    rowsum(acc[0]);
+    const double yv = pick(acc[0]);
+    double zv = 0.0;
+    if (hn) {
+      if (sc) {
+        zv = is_exc ? zexc : fma(-d, yv, tb);
+      } else {
+#pragma unroll
+        for (int n = 0; n < NC; n++) acc2[0][n] += acc2[1][n];
+        rowsum(acc2[0]);
+        zv = tb + pick(acc2[0]);
+      }
+      push_row((int)((l + 1) & 1), zv);
+    }
+    PN(15)
+    if (t < NC) ybase[l * WC + row * C + t] = yv;  // y_l -> HBM (read back by the backward sweep)
+    PN(4)
+    release_lv();
+  }
+  fence_proxy_async_global();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(fwd_done);
+
+  // ---------------- backward ----------------
+  for (int idx = w * 32 + lane; idx < 3 * WC; idx += mn * 32) xbuf[idx] = 0.0;
+  asm volatile("barrier.cluster.arrive.release;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory");
+  for (int64_t l = n2 - 1; l >= 0; l--) {
+    const uint8_t fl = sfl[l];
+    const bool full = bwd_full2(fl, a.bsc);
+    const int nhc = ((fl & 1) && !full) ? ((fl >> 2) & 15) : 0;
+    const int b0 = (int)(l % 3);
+    const double* x1 = xbuf + (int)((l + 1) % 3) * WC;
+    const double* x2 = xbuf + (int)((l + 2) % 3) * WC;
+    PN(8)
+    if (l < n2 - 1) wait_x();
+    arm();
+    PN(9)
+    mbar_wait(&lfull[ls], lph);
+    PN(10)
+    const unsigned char* lv = smraw + Ly.lv + (int64_t)ls * Ly.lv_slot;
+    // y_l and the x_{l+2} columns of H ahead of the GEMV
+    double xv = reinterpret_cast<const double*>(lv + Ly.o_y)[(w * 8 + g) * C + tc];
+    if (nhc) {  // x_{l+2} half of H: the columns of the rows pivoted up
+      const int* hidx = reinterpret_cast<const int*>(lv + Ly.o_hidx);
+      const double* hcol = reinterpret_cast<const double*>(lv + Ly.o_hcol);
+      for (int e = 0; e < nhc; e++) xv = fma(-hcol[e * Wp + row], x2[hidx[e] * C + tc], xv);
+    }
+    PN(17)
+    double acc[2][NC];
+#pragma unroll
+    for (int n = 0; n < NC; n++) acc[0][n] = acc[1][n] = 0.0;
+    const int nch = full ? 4 : 2;
+    for (int c = 0; c < nch; c++) {
+      const double* xs = (c < 2 ? x1 : x2) + ((c & 1) * KH * 4 + t) * C;
+      const double* Aw = acquire_op() + w * 32 + lane;
+      PN(11)
+      gemv_k<NC, 4 * C>(KH, Aw, MNB * 32, xs, acc[0], acc[1]);
+      release_op();
+      PN(12)
+    }
+#pragma unroll
+    for (int n = 0; n < NC; n++) acc[0][n] += acc[1][n];
+    rowsum(acc[0]);
+    xv -= pick(acc[0]);
+    push_row(b0, xv);
+    if (t < NC) {
+      if (a.mode == SWEEP_RECOVER) {
+        if (row < sd.w && t < ncols) a.out[(int64_t)(q0 + t) * a.N + (int64_t)(sd.col0 + row) * n2 + l] = xv;
+      } else {
+        ybase[l * WC + row * C + t] = xv;  // x_l over y_l; to_X x_l in strip_contrib_kernel
+      }
+    }
+    PN(13)
+    release_lv();
+  }
+  wait_x();
+#ifdef SLB_SOLVE_PROF
+  if (blockIdx.x < G && lane == 0 && w < 2)
+    printf("SOLVE2S blk %d w %d G %d mn %d | fwd: xwait %lld lfull %lld tt %lld pre %lld acq %lld gemv %lld epi+push %lld ystore %lld | bwd: xwait %lld "
+           "lfull %lld pre %lld acq %lld gemv %lld epi %lld\n",
+           blockIdx.x, w, G, mn, ph[0], ph[1], ph[2], ph[14], ph[5], ph[6], ph[15], ph[4], ph[9], ph[10], ph[17], ph[11], ph[12], ph[13]);
+#endif
+#undef PN
+}
+
+// NC = 0: 8 columns, k-split DMMA GEMVs over all 8 consumer warps (one CTA barrier pair per level).
+// NC = 1, 2, 4: the first NC columns only, on DFMA (the FP64 tensor pipe gains nothing at 1-4
+// columns: DMMA 37.1 vs DFMA 34.1 TF/s measured): consumer warp w < mn owns row tile w for the whole
+// k range, gathers its own right-hand-side values through the pivot order, and needs no CTA
+// barrier at all - a level is one exchange wait plus a per-warp GEMV and epilogue.
+// mapA Ainv tiles, mapF Fbot tiles, mapH H tiles (make_map).
+template <int NC>
+__global__ void __launch_bounds__(threads_of<NC>(), 1)
     strip_solve2_kernel(const __grid_constant__ Solve2Args A2, const __grid_constant__ CUtensorMap mapA,
                         const __grid_constant__ CUtensorMap mapF, const __grid_constant__ CUtensorMap mapH) {
   const SchurArgs& a = A2.a;
@@ -154,42 +507,57 @@ __global__ void __launch_bounds__(THREADS, 1)
   double* ybase = a.ybuf + (int64_t)task * a.sY;  // b_l in (packed [l][Wp][C]), y_l / x_l out
   const int64_t lvl0 = (int64_t)s * n2;           // this strip's first level in the tensor maps
   // exchange bytes per vector: every CTA pushes its rows to every CTA (itself included)
-  const uint32_t xbytes = (uint32_t)(WC * 8);
+  const uint32_t xbytes = (uint32_t)(Wp * (NC == 0 ? C : NC) * 8);
+  // consumer warps that read the operator / level rings
+  const int ncw = NC == 0 ? NCW : mn;
 
-  for (int64_t i = tid; i < n2; i += THREADS) sfl[i] = a.u13[s * n2 + i];
+  constexpr int NT = threads_of<NC>();
+  constexpr int PW = ncw_of<NC>();  // first producer warp
+  for (int64_t i = tid; i < n2; i += NT) sfl[i] = a.u13[s * n2 + i];
   if (tid == 0) {
     for (int i = 0; i < STAGES; i++) {
       mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], NCW / 2);  // a chunk is consumed by one warp group
+      mbar_init(&empty_bar[i], NC == 0 ? NCW / 2 : mn);  // DMMA: a chunk is consumed by one warp group
     }
     for (int i = 0; i < LS; i++) {
       mbar_init(&lfull[i], 1);
-      mbar_init(&lempty[i], NCW);
+      mbar_init(&lempty[i], ncw);
     }
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
-    mbar_init(&fwd_done, NCW);
+    mbar_init(&fwd_done, ncw);
     fence_mbar_init();
   }
   // z_0 = b_0 (complete, local): exchange buffer 0
-  for (int idx = tid; idx < WC; idx += THREADS) xbuf[idx] = ybase[idx];
+  for (int idx = tid; idx < WC; idx += NT) xbuf[idx] = ybase[idx];
   __syncthreads();
   cluster.sync();  // peers' barriers initialised before any st.async targets them
 
-  if (warp >= NCW) {
-    // producers take part in the one cluster barrier of the consumers (forward -> backward) early
+  const bool idle = warp >= ncw;  // producers and (DFMA path) consumer warps without a row tile
+  static_assert(NC == 0 || NCW_DFMA >= 1, "");
+  if (idle) {
+    // they take part in the one cluster barrier of the consumers (forward -> backward) early
     asm volatile("barrier.cluster.arrive.relaxed;\n" ::: "memory");
   }
-  if (warp == NCW) {
+  if (warp == PW) {
     // ======================= op producer: level operator slices =======================
     if (lane == 0) {
       int slot = 0;
       uint32_t ph = 0;
       const uint32_t box = (uint32_t)Ly.op_slot;
+#ifdef SLB_SOLVE_PROF
+      const bool notma = a.fsc == 2;  // timing experiment only: operator slices not loaded
+#else
+      constexpr bool notma = false;
+#endif
       auto put = [&](const CUtensorMap* map, int kbeg, int64_t l) {
         mbar_wait(&empty_bar[slot], ph ^ 1u);
-        mbar_arrive_expect_tx(&full_bar[slot], box);
-        tma_load_4d(smraw + Ly.op + (int64_t)slot * Ly.op_slot, map, 0, m0, kbeg, (int)(lvl0 + l), &full_bar[slot]);
+        if (notma) {
+          mbar_arrive(&full_bar[slot]);
+        } else {
+          mbar_arrive_expect_tx(&full_bar[slot], box);
+          tma_load_4d(smraw + Ly.op + (int64_t)slot * Ly.op_slot, map, 0, m0, kbeg, (int)(lvl0 + l), &full_bar[slot]);
+        }
         if (++slot == STAGES) {
           slot = 0;
           ph ^= 1u;
@@ -213,7 +581,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     __syncwarp();
-  } else if (warp == NCW + 1) {
+  } else if (warp == PW + 1) {
     // ======================= level producer: per-level data =======================
     if (lane == 0) {
       int ls = 0;
@@ -265,6 +633,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     __syncwarp();
+  } else if (NC > 0) {
+    if (!idle) solve2_dfma_consumer<(NC > 0 ? NC : 1)>(a, G, rank, m0, mn, warp, lane, Wp, n2, Ly, smraw, xbuf, sfl, full_bar,
+                                        empty_bar, lfull, lempty, xbar, &fwd_done, ybase, ncols, q0, sd);
   } else {
     // ======================= consumer warps =======================
     int slot = 0, ls = 0;
@@ -350,6 +721,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     };
 
+#ifdef SLB_SOLVE_PROF
+    long long P0 = clock64(), ph[16] = {0};
+#define PM(k) { const long long q_ = clock64(); ph[k] += q_ - P0; P0 = q_; }
+#else
+#define PM(k)
+#endif
     // ---------------- forward ----------------
     double* tt = xbuf + 2 * WC;
     for (int64_t l = 0; l < n2; l++) {
@@ -357,9 +734,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint8_t fl = sfl[l];
       const bool sc = fwd_shortcut(fl, a.fsc);
       const int zo = (int)(l & 1) * WC;
+      PM(7)
       if (l > 0) wait_x();  // z_l complete (all rows, pushed by every CTA)
       if (hn) arm();        // exchange of z_{l+1}
+      PM(0)
       mbar_wait(&lfull[ls], lph);
+      PM(1)
       const unsigned char* lv = smraw + Ly.lv + (int64_t)ls * Ly.lv_slot;
       const int* sperm = reinterpret_cast<const int*>(lv + Ly.o_perm);
       const double* bn = reinterpret_cast<const double*>(lv + Ly.o_b);
@@ -378,6 +758,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       double2 tb = make_double2(0.0, 0.0);
       if (epi && hn) tb = vval2(sperm[Wp + erow], 2 * t);
       consumer_bar();
+      PM(2)
       const int ncx = (sc && hn) ? ((fl >> 2) & 15) : 0;
       if (warp < ncx) {  // exceptional bottom row e = warp: Fbot[e, :] t_top (all C columns)
         const double* er = reinterpret_cast<const double*>(lv + Ly.o_exc) + warp * Wp;
@@ -388,6 +769,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         q += __shfl_xor_sync(0xffffffffu, q, 16);
         if (kp == 0) excval[warp][n] = q;
       }
+      PM(3)
       double acc[MNMAX][2], acc2[MNMAX][2];
 #pragma unroll
       for (int mt = 0; mt < MNMAX; mt++) acc[mt][0] = acc[mt][1] = acc2[mt][0] = acc2[mt][1] = 0.0;
@@ -398,11 +780,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           continue;
         }
         const double* Aop = acquire_op();
+        PM(4)
         gemv_chunk(Aop, tt, (c & 1) * KH, c < 2 ? acc : acc2);
         release_op();
+        PM(5)
       }
       double y0, y1;
       reduce_parts(acc, y0, y1);
+      PM(6)
       double z0 = 0.0, z1 = 0.0;
       if (hn) {
         if (sc) {
@@ -453,9 +838,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool full = bwd_full2(fl, a.bsc);
       const int nhc = ((fl & 1) && !full) ? ((fl >> 2) & 15) : 0;
       const int b0 = (int)(l % 3), b1 = (int)((l + 1) % 3), b2 = (int)((l + 2) % 3);
+      PM(13)
       if (l < n2 - 1) wait_x();  // x_{l+1} complete
       arm();                     // exchange of x_l
+      PM(8)
       mbar_wait(&lfull[ls], lph);
+      PM(9)
       const unsigned char* lv = smraw + Ly.lv + (int64_t)ls * Ly.lv_slot;
       const double* x1 = xbuf + b1 * WC;
       const double* x2 = xbuf + b2 * WC;
@@ -469,11 +857,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           continue;
         }
         const double* Aop = acquire_op();
+        PM(10)
         gemv_chunk(Aop, c < 2 ? x1 : x2, (c & 1) * KH, acc);
         release_op();
+        PM(11)
       }
       double h0, h1;
       reduce_parts(acc, h0, h1);
+      PM(12)
       if (epi) {
         const double2 yv = reinterpret_cast<const double2*>(lv + Ly.o_y)[(et * 8 + g) * (C / 2) + t];
         double x0v = yv.x - h0, x1v = yv.y - h1;
@@ -506,8 +897,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     wait_x();  // x_0 complete everywhere before the cluster exits (peers push into us)
+#ifdef SLB_SOLVE_PROF
+    if (blockIdx.x < G && (tid == 0 || tid == 160))
+      printf("SOLVE2 blk %d tid %d G %d mn %d | fwd: xwait %lld lfull %lld tt %lld exc %lld opwait %lld gemv %lld red %lld epi %lld"
+             " | bwd: xwait %lld lfull %lld opwait %lld gemv %lld red %lld epi %lld\n",
+             blockIdx.x, tid, G, mn, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6], ph[7], ph[8], ph[9], ph[10], ph[11],
+             ph[12], ph[13]);
+#endif
   }
-  if (warp >= NCW) asm volatile("barrier.cluster.wait;\n" ::: "memory");
+  if (idle) asm volatile("barrier.cluster.wait;\n" ::: "memory");
   // no CTA leaves while a peer may still push into its shared memory
   __syncthreads();
   cluster.sync();
@@ -580,7 +978,8 @@ CUtensorMap make_map(const double* base, int mt, int tile_stride, int k4rows, in
 
 bool strip_solve2_fits(int Wp, int64_t n2, int G) {
   const int MTH = Wp / 8;
-  if (G < 2 || G > 8 || (MTH + G - 1) / G > MNMAX) return false;
+  if (G < 1 || G > 8 || G > MTH || (MTH + G - 1) / G > MNMAX) return false;
+  if ((MTH + G - 1) / G > NCW_DFMA) return false;  // the DFMA variants' row-tile warps
   return lay2(Wp, G, n2).bytes <= 227 * 1024 - 1024;
 }
 
@@ -590,22 +989,23 @@ int strip_solve2_cluster(int Wp, int64_t n2, int ntasks) {
   static std::mutex mu;
   static std::map<std::pair<int, int64_t>, int> cache;  // (Wp, n2 * 1024 + ntasks) -> G
   const char* e = getenv("SLB_SOLVE_G");
-  if (e) return atoi(e);
+  if (e) return std::min(atoi(e), Wp / 8);
   std::lock_guard<std::mutex> lk(mu);
   const auto key = std::make_pair(Wp, n2 * 1024 + ntasks);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  int best = 4;
+  const int MTH = Wp / 8;
+  int best = std::min(4, MTH);
   for (int G : {8, 6, 5, 4}) {
     if (!strip_solve2_fits(Wp, n2, G)) continue;
     const size_t smem = (size_t)lay2(Wp, G, n2).bytes;
-    if (cudaFuncSetAttribute(strip_solve2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    if (cudaFuncSetAttribute(strip_solve2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
       cudaGetLastError();
       continue;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(G * ntasks));
-    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3(threads_of<0>());
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -615,7 +1015,7 @@ int strip_solve2_cluster(int Wp, int64_t n2, int ntasks) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int nc = 0;
-    if (cudaOccupancyMaxActiveClusters(&nc, strip_solve2_kernel, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&nc, strip_solve2_kernel<0>, &cfg) != cudaSuccess) {
       cudaGetLastError();
       continue;
     }
@@ -642,11 +1042,19 @@ void strip_solve2(cudaStream_t st, const SchurArgs& a, int ntasks) {
   const CUtensorMap mF = make_map(a.fac + MTH * 32, MTH, 2 * MTH, Wp / 4, levels, lvl, Ly.MNB, Ly.KH);
   const CUtensorMap mH = make_map(a.fac + 2LL * Wp * Wp, MTH, MTH, Wp / 2, levels, lvl, Ly.MNB, Ly.KH);
   const size_t smem = (size_t)Ly.bytes;
-  SLB_CUDA_CHECK(cudaFuncSetAttribute(strip_solve2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // columns per task: 1, 2, 3-4 on DFMA, 5-8 on DMMA (SLB_SOLVE_DMMA=1 forces DMMA)
+  static const bool force_dmma = getenv("SLB_SOLVE_DMMA") != nullptr;
+  const int64_t cols = a.nrhs < C ? a.nrhs : C;
+  void (*kern)(Solve2Args, CUtensorMap, CUtensorMap, CUtensorMap) =
+      (force_dmma || cols > 4) ? strip_solve2_kernel<0>
+      : cols == 1             ? strip_solve2_kernel<1>
+      : cols == 2             ? strip_solve2_kernel<2>
+                              : strip_solve2_kernel<4>;
+  SLB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   Solve2Args A2{a, G};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(G * ntasks));
-  cfg.blockDim = dim3(THREADS);
+  cfg.blockDim = dim3((force_dmma || cols > 4) ? threads_of<0>() : threads_of<1>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -656,7 +1064,7 @@ void strip_solve2(cudaStream_t st, const SchurArgs& a, int ntasks) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, strip_solve2_kernel, A2, mA, mF, mH)); count_launch();
+  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, A2, mA, mF, mH)); count_launch();
   if (a.mode == SWEEP_REDUCE) {
     strip_contrib_kernel<<<dim3((unsigned)cdiv(a.n2, 8), (unsigned)ntasks), 256, 0, st>>>(a); count_launch();
     SLB_CUDA_CHECK(cudaGetLastError());
