@@ -48,8 +48,11 @@ constexpr int THREADS = CTHREADS + 64;  // + op producer warp + level producer w
 // DFMA variants need at most 6 row-tile warps (G >= 4 at Wp <= 160): 8 warps in all, so two warps
 // per SM sub-partition and the full 255-register budget (10 warps cap threads at 168 registers)
 constexpr int NCW_DFMA = 6;
+// NC <= 2: two warps per row tile (k halves), combined through shared memory and a pair barrier
 template <int NC>
-constexpr int ncw_of() { return NC == 0 ? NCW : NCW_DFMA; }
+constexpr bool pair_of() { return NC == 1 || NC == 2; }
+template <int NC>
+constexpr int ncw_of() { return NC == 0 ? NCW : pair_of<NC>() ? 2 * NCW_DFMA : NCW_DFMA; }
 template <int NC>
 constexpr int threads_of() { return ncw_of<NC>() * 32 + 64; }
 constexpr int STAGES = 4;               // op ring: half-level chunks
@@ -94,7 +97,9 @@ __host__ __device__ inline Lay2 lay2(int Wp, int G, int64_t n2) {
   L.xb = L.lv + LS * L.lv_slot;
   L.part = L.xb + 3LL * Wp * C * 8;
   // DMMA partial sums, or (DFMA, NC <= 2) one private t_top copy per row-tile warp
-  const int64_t part_dmma = (int64_t)NCW * L.MNB * 32 * 16, part_dfma = 6LL * Wp * 2 * 8;
+  // DFMA pair variant: a half t_top per warp (12 warps x KMAX*4 rows x 2 columns) + per tile pair
+  // partial sums (6 tiles x (32 + 8) x 2)
+  const int64_t part_dmma = (int64_t)NCW * L.MNB * 32 * 16, part_dfma = (12LL * 80 * 2 + 6LL * 40 * 2) * 8;
   L.flags = L.part + (part_dmma > part_dfma ? part_dmma : part_dfma);
   L.bytes = L.flags + round_up(n2, 16) + 128;  // + alignment slack of the dynamic window
   return L;
@@ -206,7 +211,10 @@ __device__ __forceinline__ void gemv_k(int KH, const double* Aw, int S, const do
   }
 }
 
-// DFMA consumer (see strip_solve2_kernel): warp w < mn, row tile w of this CTA's slice.
+// DFMA consumer (see strip_solve2_kernel).  Single form (NC = 4): warp w < mn owns row tile w for
+// the whole k range.  Pair form (NC <= 2): warps w and w + mn share tile w, each taking one half of
+// the k range (the two half-level chunks); the upper warp hands its partial sums to the lower one
+// through shared memory and a pair barrier, which halves the GEMV chain of a level.
 template <int NC>
 __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, int rank, int m0, int mn, int w,
                                                      int lane, int Wp, int64_t n2, const Lay2& Ly,
@@ -214,11 +222,20 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
                                                      uint64_t* full_bar, uint64_t* empty_bar, uint64_t* lfull,
                                                      uint64_t* lempty, uint64_t* xbar, uint64_t* fwd_done,
                                                      double* ybase, int ncols, int q0, const StripDesc& sd) {
+  constexpr bool PAIR = pair_of<NC>();
   const int g = lane >> 2, t = lane & 3;
   const int KH = Ly.KH, MNB = Ly.MNB;
-  const int WC = Wp * C;
-  const int row = (m0 + w) * 8 + g;  // this lane's output row (all 4 t lanes hold the reduced sums)
+  const int WC = Wp * C;    // packed level-major layout of b / y / x in HBM and the level ring
+  const int XW = Wp * NC;   // one exchange vector: [row][NC] (compact: row gathers stay bank-conflict-free)
+  const int tile = PAIR ? w % mn : w;  // row tile of this warp
+  const int h = PAIR ? w / mn : 0;     // pair form: k half (0 also owns the epilogue)
+  const bool lead = h == 0;
+  const int nact = PAIR ? 2 * mn : mn;  // active consumer warps
+  const int row = (m0 + tile) * 8 + g;  // this lane's output row (all 4 t lanes hold the reduced sums)
   const uint32_t xbytes = (uint32_t)(Wp * NC * 8);
+  // pair form: half t_top per warp and the pair's partial sums
+  double* ttw_pair = reinterpret_cast<double*>(smraw + Ly.part) + w * (KMAX * 4 * NC);
+  double* pbuf = reinterpret_cast<double*>(smraw + Ly.part) + 12 * (KMAX * 4 * NC) + tile * (40 * NC);
   int slot = 0, ls = 0;
   uint32_t fph = 0, lph = 0, xq = 0;
   auto arm = [&]() {
@@ -232,13 +249,16 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     mbar_wait(&full_bar[slot], fph);
     return reinterpret_cast<const double*>(smraw + Ly.op + (int64_t)slot * Ly.op_slot);
   };
-  auto release_op = [&]() {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[slot]);
+  auto next_slot = [&]() {
     if (++slot == STAGES) {
       slot = 0;
       fph ^= 1u;
     }
+  };
+  auto release_op = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[slot]);
+    next_slot();
   };
   auto release_lv = [&]() {
     __syncwarp();
@@ -248,6 +268,7 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
       lph ^= 1u;
     }
   };
+  auto pair_bar = [&]() { asm volatile("bar.sync %0, 64;\n" ::"r"(3 + tile) : "memory"); };
   // sum over the 4 t lanes of a row: every lane ends with the row's totals
   auto rowsum = [&](double (&acc)[NC]) {
 #pragma unroll
@@ -263,17 +284,36 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
       if (t == n) r = v[n];
     return r;
   };
+  // pair form: the upper warp's per-lane partial sums (and exceptional-row halves) join the lower's
+  // (exq: this lane's exceptional-row dot when its row is one, pbuf slot 32 NC + g NC per row)
+  auto pair_combine = [&](double (&acc)[NC], double (&exq)[NC], bool has_exq) {
+    if constexpr (PAIR) {
+      if (!lead) {
+#pragma unroll
+        for (int n = 0; n < NC; n++) pbuf[lane * NC + n] = acc[n];
+        if (has_exq)
+#pragma unroll
+          for (int n = 0; n < NC; n++) pbuf[32 * NC + g * NC + n] = exq[n];
+      }
+      pair_bar();
+      if (lead) {
+#pragma unroll
+        for (int n = 0; n < NC; n++) acc[n] += pbuf[lane * NC + n];
+        if (has_exq)
+#pragma unroll
+          for (int n = 0; n < NC; n++) exq[n] += pbuf[32 * NC + g * NC + n];
+      }
+    }
+  };
 #ifdef SLB_SOLVE_PROF
   long long P0 = clock64(), ph[24] = {0};
 #define PN(k) { const long long q_ = clock64(); ph[k] += q_ - P0; P0 = q_; }
 #else
 #define PN(k)
 #endif
-  // this lane's (row, column tc) element of a row-tile vector; the row's NC values gathered from the
-  // 4 t lanes, so that lane t can push the whole row to cluster CTA t (and t + 4): the G pushes of a
-  // row go out in parallel, one st.async per lane
+  // lane t pushes the row's NC values (gathered from the 4 t lanes) to cluster CTAs t and t + 4: the
+  // G pushes of a row go out in parallel, one st.async per lane
   const int tc = t < NC ? t : 0;
-  // lane t pushes to cluster CTAs t and t + 4: their window addresses, resolved once
   const uint32_t rxa = dsmem_map(xbuf, t < G ? t : 0), rxb = dsmem_map(xbuf, t + 4 < G ? t + 4 : 0);
   const uint32_t rb0a = dsmem_map(&xbar[0], t < G ? t : 0), rb0b = dsmem_map(&xbar[0], t + 4 < G ? t + 4 : 0);
   const uint32_t rb1a = dsmem_map(&xbar[1], t < G ? t : 0), rb1b = dsmem_map(&xbar[1], t + 4 < G ? t + 4 : 0);
@@ -281,7 +321,7 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     double vv[NC];
 #pragma unroll
     for (int n = 0; n < NC; n++) vv[n] = __shfl_sync(0xffffffffu, v, (lane & ~3) + n);
-    const uint32_t off = (uint32_t)(((buf * Wp + row) * C) * 8);
+    const uint32_t off = (uint32_t)(((buf * Wp + row) * NC) * 8);
     const bool b = xq & 1;
 #pragma unroll
     for (int rr = 0; rr < 8; rr += 4) {
@@ -298,14 +338,15 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     }
   };
   // ---------------- forward ----------------
-  // t_top: NC <= 2 one private copy per warp (no CTA barrier), NC = 4 one shared copy
-  double* ttsh = xbuf + 2 * WC;
-  double* ttw = NC <= 2 ? reinterpret_cast<double*>(smraw + Ly.part) + w * Wp * NC : ttsh;
+  // t_top: pair form one private half per warp (k rows of its chunk, local index k - h KH 4),
+  // single form (NC = 4) one shared copy built by all active warps
+  double* ttsh = xbuf + 2 * XW;
+  const int kofs = PAIR ? h * KH * 4 : 0;
   for (int64_t l = 0; l < n2; l++) {
     const bool hn = l + 1 < n2;
     const uint8_t fl = sfl[l];
     const bool sc = fwd_shortcut(fl, a.fsc);
-    const double* z = xbuf + (int)(l & 1) * WC;
+    const double* z = xbuf + (int)(l & 1) * XW;
     PN(7)
     if (l > 0) wait_x();
     if (hn) arm();
@@ -316,49 +357,57 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     const int* sperm = reinterpret_cast<const int*>(lv + Ly.o_perm);
     const double* bn = reinterpret_cast<const double*>(lv + Ly.o_b);
     auto val = [&](int src, int n) -> double {  // row src, column n of [z_l ; b_{l+1}]
-      if (src < Wp) return z[src * C + n];
+      if (src < Wp) return z[src * NC + n];
       return hn ? bn[(src - Wp) * C + n] : 0.0;
     };
     // t_top = rows perm[0..Wp) of [z_l ; b_{l+1}], compact [k][NC].  Reuse is safe: the next
     // level rewrites it only after its exchange wait, which needs this level's pushes.
-    if constexpr (NC <= 2) {
-      for (int idx = lane; idx < Wp * NC; idx += 32) ttw[idx] = val(sperm[idx / NC], idx % NC);
+    double* tt;
+    int kcnt;  // t_top rows this warp reads: [kofs, kofs + kcnt)
+    if constexpr (PAIR) {
+      tt = ttw_pair;
+      kcnt = min(KH * 4, Wp - kofs);
+      for (int idx = lane; idx < kcnt * NC; idx += 32) tt[idx] = val(sperm[kofs + idx / NC], idx % NC);
       __syncwarp();
     } else {
+      tt = ttsh;
+      kcnt = Wp;
       for (int idx = w * 32 + lane; idx < Wp * NC; idx += mn * 32) ttsh[idx] = val(sperm[idx / NC], idx % NC);
       asm volatile("bar.sync 2, %0;\n" ::"r"(mn * 32) : "memory");
     }
     PN(2)
     // epilogue operands ahead of the GEMV: t_bot, diag(Lsub), and the exceptional rows of this
-    // tile (z = t_bot + Fbot[e, :] t_top needs t_top only)
-    double tb = 0.0, d = 0.0, zexc = 0.0;
+    // tile (z = t_bot + Fbot[e, :] t_top needs t_top only; the pair form splits the dot over k)
+    double tb = 0.0, d = 0.0;
+    double exq[NC];
     bool is_exc = false;
+#pragma unroll
+    for (int n = 0; n < NC; n++) exq[n] = 0.0;
     if (hn) {
-      tb = val(sperm[Wp + row], tc);
+      if (lead) tb = val(sperm[Wp + row], tc);
       if (sc) {
-        d = reinterpret_cast<const double*>(lv + Ly.o_dsub)[row];
+        if (lead) d = reinterpret_cast<const double*>(lv + Ly.o_dsub)[row];
         const int ncx = (fl >> 2) & 15;
         const int* epos = reinterpret_cast<const int*>(lv + Ly.o_epos);
         const double* exc = reinterpret_cast<const double*>(lv + Ly.o_exc);
         for (int e = 0; e < ncx; e++) {
           const int er = epos[e];
-          if (er < (m0 + w) * 8 || er >= (m0 + w) * 8 + 8) continue;  // warp-uniform
+          if (er < (m0 + tile) * 8 || er >= (m0 + tile) * 8 + 8) continue;  // warp-uniform
           double q[NC];
 #pragma unroll
           for (int n = 0; n < NC; n++) q[n] = 0.0;
-          for (int k = lane; k < Wp; k += 32) {
-            const double ev = exc[e * Wp + k];
+          for (int k = lane; k < kcnt; k += 32) {
+            const double ev = exc[e * Wp + kofs + k];
 #pragma unroll
-            for (int n = 0; n < NC; n++) q[n] = fma(ev, ttw[k * NC + n], q[n]);
+            for (int n = 0; n < NC; n++) q[n] = fma(ev, tt[k * NC + n], q[n]);
           }
 #pragma unroll
-          for (int n = 0; n < NC; n++)
+          for (int n = 0; n < NC; n++) {
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) q[n] += __shfl_xor_sync(0xffffffffu, q[n], o);
-          if (row == er) {
-            is_exc = true;
-            zexc = tb + pick(q);
+            if (row == er) exq[n] = q[n];
           }
+          if (row == er) is_exc = true;
         }
       }
     }
@@ -368,8 +417,12 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     for (int n = 0; n < NC; n++) acc[0][n] = acc[1][n] = acc2[0][n] = acc2[1][n] = 0.0;
     const int nch = (sc || !hn) ? 2 : 4;
     for (int c = 0; c < nch; c++) {
-      const double* tk = ttw + ((c & 1) * KH * 4 + t) * NC;
-      const double* Aw = acquire_op() + w * 32 + lane;
+      if (PAIR && (c & 1) != h) {  // the other half's chunk
+        next_slot();
+        continue;
+      }
+      const double* tk = tt + ((c & 1) * KH * 4 - kofs + t) * NC;
+      const double* Aw = acquire_op() + tile * 32 + lane;
       PN(5)
       if (c < 2) gemv_k<NC, 4 * NC>(KH, Aw, MNB * 32, tk, acc[0], acc[1]);
       else gemv_k<NC, 4 * NC>(KH, Aw, MNB * 32, tk, acc2[0], acc2[1]);
@@ -377,23 +430,32 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
       PN(6)
     }
 #pragma unroll
-    for (int n = 0; n < NC; n++) acc[0][n] += acc[1][n];
-    rowsum(acc[0]);
-    const double yv = pick(acc[0]);
-    double zv = 0.0;
-    if (hn) {
-      if (sc) {
-        zv = is_exc ? zexc : fma(-d, yv, tb);
-      } else {
-#pragma unroll
-        for (int n = 0; n < NC; n++) acc2[0][n] += acc2[1][n];
-        rowsum(acc2[0]);
-        zv = tb + pick(acc2[0]);
-      }
-      push_row((int)((l + 1) & 1), zv);
+    for (int n = 0; n < NC; n++) {
+      acc[0][n] += acc[1][n];
+      acc2[0][n] += acc2[1][n];
     }
-    PN(15)
-    if (t < NC) ybase[l * WC + row * C + t] = yv;  // y_l -> HBM (read back by the backward sweep)
+    pair_combine(acc[0], exq, is_exc);
+    if (hn && !sc) {  // full Fbot GEMV (rare): its partials take a second pair exchange
+      if constexpr (PAIR) pair_bar();  // the lead has read the first partials
+      double none[NC];
+      pair_combine(acc2[0], none, false);
+    }
+    if (lead) {
+      rowsum(acc[0]);
+      const double yv = pick(acc[0]);
+      if (hn) {
+        double zv;
+        if (sc) {
+          zv = is_exc ? tb + pick(exq) : fma(-d, yv, tb);
+        } else {
+          rowsum(acc2[0]);
+          zv = tb + pick(acc2[0]);
+        }
+        push_row((int)((l + 1) & 1), zv);
+      }
+      PN(15)
+      if (t < NC) ybase[l * WC + row * C + t] = yv;  // y_l -> HBM (read back by the backward sweep)
+    }
     PN(4)
     release_lv();
   }
@@ -402,7 +464,7 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
   if (lane == 0) mbar_arrive(fwd_done);
 
   // ---------------- backward ----------------
-  for (int idx = w * 32 + lane; idx < 3 * WC; idx += mn * 32) xbuf[idx] = 0.0;
+  for (int idx = w * 32 + lane; idx < 3 * XW; idx += nact * 32) xbuf[idx] = 0.0;
   asm volatile("barrier.cluster.arrive.release;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory");
   for (int64_t l = n2 - 1; l >= 0; l--) {
@@ -410,8 +472,8 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     const bool full = bwd_full2(fl, a.bsc);
     const int nhc = ((fl & 1) && !full) ? ((fl >> 2) & 15) : 0;
     const int b0 = (int)(l % 3);
-    const double* x1 = xbuf + (int)((l + 1) % 3) * WC;
-    const double* x2 = xbuf + (int)((l + 2) % 3) * WC;
+    const double* x1 = xbuf + (int)((l + 1) % 3) * XW;
+    const double* x2 = xbuf + (int)((l + 2) % 3) * XW;
     PN(8)
     if (l < n2 - 1) wait_x();
     arm();
@@ -419,12 +481,15 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     mbar_wait(&lfull[ls], lph);
     PN(10)
     const unsigned char* lv = smraw + Ly.lv + (int64_t)ls * Ly.lv_slot;
-    // y_l and the x_{l+2} columns of H ahead of the GEMV
-    double xv = reinterpret_cast<const double*>(lv + Ly.o_y)[(w * 8 + g) * C + tc];
-    if (nhc) {  // x_{l+2} half of H: the columns of the rows pivoted up
-      const int* hidx = reinterpret_cast<const int*>(lv + Ly.o_hidx);
-      const double* hcol = reinterpret_cast<const double*>(lv + Ly.o_hcol);
-      for (int e = 0; e < nhc; e++) xv = fma(-hcol[e * Wp + row], x2[hidx[e] * C + tc], xv);
+    // y_l and the x_{l+2} columns of H ahead of the GEMV (lead warp)
+    double xv = 0.0;
+    if (lead) {
+      xv = reinterpret_cast<const double*>(lv + Ly.o_y)[(tile * 8 + g) * C + tc];
+      if (nhc) {  // x_{l+2} half of H: the columns of the rows pivoted up
+        const int* hidx = reinterpret_cast<const int*>(lv + Ly.o_hidx);
+        const double* hcol = reinterpret_cast<const double*>(lv + Ly.o_hcol);
+        for (int e = 0; e < nhc; e++) xv = fma(-hcol[e * Wp + row], x2[hidx[e] * NC + tc], xv);
+      }
     }
     PN(17)
     double acc[2][NC];
@@ -432,23 +497,33 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     for (int n = 0; n < NC; n++) acc[0][n] = acc[1][n] = 0.0;
     const int nch = full ? 4 : 2;
     for (int c = 0; c < nch; c++) {
-      const double* xs = (c < 2 ? x1 : x2) + ((c & 1) * KH * 4 + t) * C;
-      const double* Aw = acquire_op() + w * 32 + lane;
+      if (PAIR && (c & 1) != h) {
+        next_slot();
+        continue;
+      }
+      const double* xs = (c < 2 ? x1 : x2) + ((c & 1) * KH * 4 + t) * NC;
+      const double* Aw = acquire_op() + tile * 32 + lane;
       PN(11)
-      gemv_k<NC, 4 * C>(KH, Aw, MNB * 32, xs, acc[0], acc[1]);
+      gemv_k<NC, 4 * NC>(KH, Aw, MNB * 32, xs, acc[0], acc[1]);
       release_op();
       PN(12)
     }
 #pragma unroll
     for (int n = 0; n < NC; n++) acc[0][n] += acc[1][n];
-    rowsum(acc[0]);
-    xv -= pick(acc[0]);
-    push_row(b0, xv);
-    if (t < NC) {
-      if (a.mode == SWEEP_RECOVER) {
-        if (row < sd.w && t < ncols) a.out[(int64_t)(q0 + t) * a.N + (int64_t)(sd.col0 + row) * n2 + l] = xv;
-      } else {
-        ybase[l * WC + row * C + t] = xv;  // x_l over y_l; to_X x_l in strip_contrib_kernel
+    {
+      double none[NC];
+      pair_combine(acc[0], none, false);
+    }
+    if (lead) {
+      rowsum(acc[0]);
+      xv -= pick(acc[0]);
+      push_row(b0, xv);
+      if (t < NC) {
+        if (a.mode == SWEEP_RECOVER) {
+          if (row < sd.w && t < ncols) a.out[(int64_t)(q0 + t) * a.N + (int64_t)(sd.col0 + row) * n2 + l] = xv;
+        } else {
+          ybase[l * WC + row * C + t] = xv;  // x_l over y_l; to_X x_l in strip_contrib_kernel
+        }
       }
     }
     PN(13)
@@ -509,7 +584,7 @@ __global__ void __launch_bounds__(threads_of<NC>(), 1)
   // exchange bytes per vector: every CTA pushes its rows to every CTA (itself included)
   const uint32_t xbytes = (uint32_t)(Wp * (NC == 0 ? C : NC) * 8);
   // consumer warps that read the operator / level rings
-  const int ncw = NC == 0 ? NCW : mn;
+  const int ncw = NC == 0 ? NCW : pair_of<NC>() ? 2 * mn : mn;
 
   constexpr int NT = threads_of<NC>();
   constexpr int PW = ncw_of<NC>();  // first producer warp
@@ -517,7 +592,7 @@ __global__ void __launch_bounds__(threads_of<NC>(), 1)
   if (tid == 0) {
     for (int i = 0; i < STAGES; i++) {
       mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], NC == 0 ? NCW / 2 : mn);  // DMMA: a chunk is consumed by one warp group
+      mbar_init(&empty_bar[i], NC == 0 ? NCW / 2 : mn);  // a chunk is consumed by one warp group (DMMA) / tile set
     }
     for (int i = 0; i < LS; i++) {
       mbar_init(&lfull[i], 1);
@@ -528,8 +603,12 @@ __global__ void __launch_bounds__(threads_of<NC>(), 1)
     mbar_init(&fwd_done, ncw);
     fence_mbar_init();
   }
-  // z_0 = b_0 (complete, local): exchange buffer 0
-  for (int idx = tid; idx < WC; idx += NT) xbuf[idx] = ybase[idx];
+  // z_0 = b_0 (complete, local): exchange buffer 0 ([row][C] DMMA, [row][NC] DFMA)
+  if constexpr (NC == 0) {
+    for (int idx = tid; idx < WC; idx += NT) xbuf[idx] = ybase[idx];
+  } else {
+    for (int idx = tid; idx < Wp * NC; idx += NT) xbuf[idx] = ybase[(idx / NC) * C + idx % NC];
+  }
   __syncthreads();
   cluster.sync();  // peers' barriers initialised before any st.async targets them
 
@@ -1054,7 +1133,10 @@ void strip_solve2(cudaStream_t st, const SchurArgs& a, int ntasks) {
   Solve2Args A2{a, G};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(G * ntasks));
-  cfg.blockDim = dim3((force_dmma || cols > 4) ? threads_of<0>() : threads_of<1>());
+  cfg.blockDim = dim3((force_dmma || cols > 4) ? threads_of<0>()
+                      : cols == 1             ? threads_of<1>()
+                      : cols == 2             ? threads_of<2>()
+                                              : threads_of<4>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
