@@ -143,6 +143,9 @@ slablu_gpu_status slablu_gpu_solve(const slablu_gpu_fact* fact, const double* f,
 slablu_gpu_status slablu_gpu_solve_device(const slablu_gpu_fact* fact, const double* d_f,
                                           int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu);
 slablu_gpu_status slablu_gpu_stats(const slablu_gpu_fact* fact, slablu_gpu_stats_t* out);
+/* Refinement steps of later solves (SolverConfig.refine); raising it above 0 needs a factorization
+ * made with refine > 0 (the original operator is kept only then). */
+slablu_gpu_status slablu_gpu_set_refine(slablu_gpu_fact* fact, int refine);
 /* Reduced block before stage two (needs config.keep_T): which 0 diag[j], 1 super[j], 2 sub[j]. */
 slablu_gpu_status slablu_gpu_T_block(const slablu_gpu_fact* fact, int which, int64_t j, double* out);
 /* Staged reduce_rhs: out (k*n2 x nrhs) from host f (n x nrhs, ld n). */

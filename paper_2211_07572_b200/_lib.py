@@ -51,7 +51,7 @@ EXPORTS = [
     "slablu_gpu_device_count", "slablu_gpu_shard_plan", "slablu_gpu_shard_factorize_device",
     "slablu_gpu_shard_sweep", "slablu_gpu_shard_solve_forward", "slablu_gpu_shard_solve_backward",
     "slablu_gpu_residual", "slablu_gpu_sweep_solve", "slablu_gpu_recover",
-    "slablu_gpu_sweep_build",
+    "slablu_gpu_sweep_build", "slablu_gpu_set_refine",
 ]
 
 _lib = None
@@ -115,6 +115,8 @@ def lib():
     L.slablu_gpu_recover.argtypes = [P, P, P, I64, P]
     L.slablu_gpu_sweep_build.restype = St
     L.slablu_gpu_sweep_build.argtypes = [I64, I64, P, I, P]
+    L.slablu_gpu_set_refine.restype = St
+    L.slablu_gpu_set_refine.argtypes = [P, I]
     L.slablu_gpu_destroy.restype = None
     L.slablu_gpu_destroy.argtypes = [P]
     L.slablu_gpu_device_count.restype = I

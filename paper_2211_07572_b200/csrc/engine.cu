@@ -1472,6 +1472,17 @@ slablu_gpu_status slablu_gpu_stats(const slablu_gpu_fact* F, slablu_gpu_stats_t*
   })
 }
 
+slablu_gpu_status slablu_gpu_set_refine(slablu_gpu_fact* F, int refine) {
+  ABI_TRY({
+    if (!F) throw HostError(SLABLU_ERR_GENERIC, "set_refine: null factorization");
+    if (refine < 0) throw HostError(SLABLU_ERR_CONFIG, "set_refine: refine must be nonnegative");
+    if (refine > 0 && !F->a_rp.p)
+      throw HostError(SLABLU_ERR_CONFIG, "set_refine: factorize with config.refine > 0 to keep the operator");
+    std::lock_guard<std::mutex> guard(F->solve_mu);
+    F->refine = refine;
+  })
+}
+
 slablu_gpu_status slablu_gpu_T_block(const slablu_gpu_fact* F, int which, int64_t j, double* out) {
   ABI_TRY({
     if (!F || !F->Tkeep.p) throw HostError(SLABLU_ERR_GENERIC, "T_block: factorization was not built with keep_T");

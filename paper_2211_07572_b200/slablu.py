@@ -358,6 +358,12 @@ class Factorization:
         self.stats = st
         return st
 
+    def set_refine(self, refine):
+        """Iterative-refinement steps of later solves (needs the operator kept: factorize with
+        refine > 0 to be able to raise it again)."""
+        _check(lib().slablu_gpu_set_refine(self._h, int(refine)))
+        self.config.refine = int(refine)
+
     def T_block(self, which, j):
         n2 = self.n2
         out = np.empty((n2, n2), order="F")
