@@ -5,6 +5,9 @@
  * (arxiv/paper_2211_07572, /root/reference/proj/include/slablu/):
  *
  *   slablu_gpu_assemble_fd5*   <- assemble_fd5            (problem.hpp:78-132)
+ *   slablu_gpu_assemble_canned_device, _sample_solution_device, _error_report(_device)
+ *                              <- assemble_fd5 / sample_field / error_report on the device
+ *                                                         (problem.hpp:78-132, 160-206; §8(f)2)
  *   slablu_gpu_choose_b        <- choose_b                (driver.hpp:55-66)
  *   slablu_gpu_partition       <- partition               (partition.hpp:70-91)
  *   slablu_gpu_factorize       <- factorize               (driver.hpp:115-167)
@@ -114,6 +117,24 @@ slablu_gpu_status slablu_gpu_assemble_canned(int kind, int64_t n1, int64_t n2, d
 /* Manufactured solution of a canned problem sampled on the grid (problem.hpp:199-206). */
 slablu_gpu_status slablu_gpu_sample_solution(int kind, int64_t n1, int64_t n2, double kappa,
                                              double* out);
+/* On-device assembly of a canned problem: CSR + rhs written to device memory of
+ * `device` (d_rp[n+1], d_ci[5n], d_v[5n], d_rhs[n]).  Index arrays equal slablu_gpu_assemble_canned's;
+ * values follow the same operation order (bit-identical except libm-level differences in exp, and in
+ * the log / J0 Dirichlet data of the boundary rhs entries: ~1e-15 / ~1e-12 relative). */
+slablu_gpu_status slablu_gpu_assemble_canned_device(int kind, int64_t n1, int64_t n2, double kappa, int device,
+                                                    int32_t* d_rp, int32_t* d_ci, double* d_v, double* d_rhs,
+                                                    int64_t* nnz);
+slablu_gpu_status slablu_gpu_sample_solution_device(int kind, int64_t n1, int64_t n2, double kappa, int device,
+                                                    double* d_out);
+/* error_report (problem.hpp:160-196): out[0] relerr_res = ||A u - f|| / ||f||, out[1] relerr_true =
+ * ||u - u_true|| / ||u_true|| (Frobenius over the nrhs columns; absolute if the norm vanishes, flagged
+ * in out[2] / out[3]; u_true NULL gives NaN), vectors n x nrhs with ld n.  _device: device pointers. */
+slablu_gpu_status slablu_gpu_error_report(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
+                                          const double* val, const double* f, const double* u,
+                                          const double* u_true, int64_t nrhs, int device, double* out);
+slablu_gpu_status slablu_gpu_error_report_device(int64_t n, const int32_t* d_row_ptr, const int32_t* d_col_idx,
+                                                 const double* d_val, const double* d_f, const double* d_u,
+                                                 const double* d_u_true, int64_t nrhs, int device, double* out);
 double slablu_gpu_kappa_from_ppw(double ppw, int64_t n2);
 double slablu_gpu_bessel_j0(double t);
 /* gaussian_matrix (common.hpp:72-79): mt19937_64(seed) + normal_distribution. */

@@ -51,7 +51,8 @@ EXPORTS = [
     "slablu_gpu_device_count", "slablu_gpu_shard_plan", "slablu_gpu_shard_factorize_device",
     "slablu_gpu_shard_sweep", "slablu_gpu_shard_solve_forward", "slablu_gpu_shard_solve_backward",
     "slablu_gpu_residual", "slablu_gpu_sweep_solve", "slablu_gpu_recover",
-    "slablu_gpu_sweep_build", "slablu_gpu_set_refine",
+    "slablu_gpu_sweep_build", "slablu_gpu_set_refine", "slablu_gpu_assemble_canned_device",
+    "slablu_gpu_sample_solution_device", "slablu_gpu_error_report", "slablu_gpu_error_report_device",
 ]
 
 _lib = None
@@ -117,6 +118,14 @@ def lib():
     L.slablu_gpu_sweep_build.argtypes = [I64, I64, P, I, P]
     L.slablu_gpu_set_refine.restype = St
     L.slablu_gpu_set_refine.argtypes = [P, I]
+    L.slablu_gpu_assemble_canned_device.restype = St
+    L.slablu_gpu_assemble_canned_device.argtypes = [I, I64, I64, D, I, P, P, P, P, P]
+    L.slablu_gpu_sample_solution_device.restype = St
+    L.slablu_gpu_sample_solution_device.argtypes = [I, I64, I64, D, I, P]
+    L.slablu_gpu_error_report.restype = St
+    L.slablu_gpu_error_report.argtypes = [I64, P, P, P, P, P, P, I64, I, P]
+    L.slablu_gpu_error_report_device.restype = St
+    L.slablu_gpu_error_report_device.argtypes = [I64, P, P, P, P, P, P, I64, I, P]
     L.slablu_gpu_destroy.restype = None
     L.slablu_gpu_destroy.argtypes = [P]
     L.slablu_gpu_device_count.restype = I

@@ -220,28 +220,63 @@ class ErrorReport:
     solution_norm_is_absolute: bool = False
 
 
-def error_report(system, u_calc, u_true, f=None) -> ErrorReport:
-    """problem.hpp:160-190."""
+def error_report(system, u_calc, u_true, f=None, device=0) -> ErrorReport:
+    """problem.hpp:160-196, computed on the GPU (slablu_gpu_error_report: CSR SpMV residual and
+    norms with a fixed-order reduction)."""
     n = system.dim()
-    u_calc = np.asarray(u_calc).reshape(n, -1)
-    u_true = np.asarray(u_true).reshape(n, -1)
-    f = system.rhs.reshape(n, -1) if f is None else np.asarray(f).reshape(n, -1)
+    if np.shape(u_calc)[0] != n or np.shape(u_true)[0] != n or (f is not None and np.shape(f)[0] != n):
+        raise Error("error_report: vector length must equal system dimension")
+    u_calc = np.asfortranarray(np.asarray(u_calc, np.float64).reshape(n, -1))
+    u_true = np.asfortranarray(np.asarray(u_true, np.float64).reshape(n, -1))
+    f = system.rhs.reshape(n, -1) if f is None else np.asarray(f, np.float64).reshape(n, -1)
+    f = np.asfortranarray(f)
     if u_calc.shape != u_true.shape or u_calc.shape[1] != f.shape[1] or u_calc.shape[1] < 1:
         raise Error("error_report: column counts must agree")
-    rep = ErrorReport(n_rhs=u_calc.shape[1])
-    res = np.linalg.norm(system.matvec(u_calc) - f)
-    fn = np.linalg.norm(f)
-    if fn > 0:
-        rep.relerr_res = res / fn
-    else:
-        rep.relerr_res, rep.residual_norm_is_absolute = res, True
-    err = np.linalg.norm(u_calc - u_true)
-    un = np.linalg.norm(u_true)
-    if un > 0:
-        rep.relerr_true = err / un
-    else:
-        rep.relerr_true, rep.solution_norm_is_absolute = err, True
-    return rep
+    out = np.zeros(4)
+    rp = np.ascontiguousarray(system.row_ptr, np.int32)
+    ci = np.ascontiguousarray(system.col_idx, np.int32)
+    v = np.ascontiguousarray(system.values, np.float64)
+    _check(lib().slablu_gpu_error_report(n, _p(rp), _p(ci), _p(v), _p(f), _p(u_calc), _p(u_true), u_calc.shape[1],
+                                         int(device), _p(out)))
+    return ErrorReport(relerr_res=float(out[0]), relerr_true=float(out[1]), n_rhs=u_calc.shape[1],
+                       residual_norm_is_absolute=bool(out[2]), solution_norm_is_absolute=bool(out[3]))
+
+
+def assemble_canned_device(kind, n1, n2, kappa=0.0, device=0):
+    """On-device assembly of a canned problem (problem.hpp:210-261 through assemble_fd5 :78-132):
+    returns torch CUDA tensors (row_ptr, col_idx, values, rhs)."""
+    import torch
+    dev = torch.device("cuda", device)
+    n = int(n1) * int(n2)
+    rp = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    ci = torch.empty(5 * n, dtype=torch.int32, device=dev)
+    v = torch.empty(5 * n, dtype=torch.float64, device=dev)
+    rhs = torch.empty(n, dtype=torch.float64, device=dev)
+    nnz = ctypes.c_int64()
+    torch.cuda.current_stream(dev).synchronize()
+    _check(lib().slablu_gpu_assemble_canned_device(int(kind), int(n1), int(n2), float(kappa), int(device), rp.data_ptr(),
+                                                   ci.data_ptr(), v.data_ptr(), rhs.data_ptr(), ctypes.byref(nnz)))
+    return rp, ci[:nnz.value], v[:nnz.value], rhs
+
+
+def sample_solution_device(kind, n1, n2, kappa=0.0, device=0):
+    import torch
+    out = torch.empty(int(n1) * int(n2), dtype=torch.float64, device=torch.device("cuda", device))
+    _check(lib().slablu_gpu_sample_solution_device(int(kind), int(n1), int(n2), float(kappa), int(device),
+                                                   out.data_ptr()))
+    return out
+
+
+def error_report_device(n, row_ptr, col_idx, values, f, u, u_true=None, device=0) -> ErrorReport:
+    """error_report on device tensors (f, u, u_true: (nrhs, n) or (n,) CUDA float64)."""
+    nrhs = u.shape[0] if u.dim() == 2 else 1
+    _torch_sync(u)
+    out = np.zeros(4)
+    _check(lib().slablu_gpu_error_report_device(int(n), row_ptr.data_ptr(), col_idx.data_ptr(), values.data_ptr(),
+                                                f.data_ptr(), u.data_ptr(), None if u_true is None else u_true.data_ptr(),
+                                                nrhs, int(device), _p(out)))
+    return ErrorReport(relerr_res=float(out[0]), relerr_true=float(out[1]), n_rhs=nrhs,
+                       residual_norm_is_absolute=bool(out[2]), solution_norm_is_absolute=bool(out[3]))
 
 
 # ---------------------------------------------------------------------------
