@@ -20,6 +20,8 @@
  *   slablu_gpu_sweep_build     <- sweep_build / SweepFactorization(BlockTridiagonal)
  *                                                         (stage_two.hpp:41-56, 131-150, 241-243)
  *   slablu_gpu_destroy         <- ~Factorization
+ *   slablu_gpu_save / _load / _export_sweep / _import_sweep
+ *                              <- serialize / deserialize (stage_two.hpp:95-120, 200-232; dense.hpp:71-87)
  *   slablu_gpu_shard_*         <- (no reference counterpart: the multi-GPU split of
  *                                 factorize/solve designed in SURVEY.md §8(e))
  *
@@ -186,6 +188,17 @@ slablu_gpu_status slablu_gpu_sweep_build(int64_t m, int64_t k, const double* blo
 slablu_gpu_status slablu_gpu_recover(const slablu_gpu_fact* fact, const double* f, const double* u_ifc,
                                      int64_t nrhs, double* u);
 void slablu_gpu_destroy(slablu_gpu_fact* fact);
+
+/* ---- factor caching ---------------------------------------
+ * save / load: the whole GPU factorization in a versioned file (magic SLBGPU01, named sections),
+ * factor once, solve in another process.  export_sweep / import_sweep: stage two in the
+ * reference's SweepFactorization layout (magic SLBSWP01, stage_two.hpp:200-232 with DenseLU
+ * dense.hpp:71-87: write_dense blocks, int64 1-based pivots), so stage-two factors move between
+ * the reference and the GPU engine; an imported handle serves slablu_gpu_sweep_solve. */
+slablu_gpu_status slablu_gpu_save(const slablu_gpu_fact* fact, const char* path);
+slablu_gpu_status slablu_gpu_load(const char* path, int device, slablu_gpu_fact** out);
+slablu_gpu_status slablu_gpu_export_sweep(const slablu_gpu_fact* fact, const char* path);
+slablu_gpu_status slablu_gpu_import_sweep(const char* path, int device, slablu_gpu_fact** out);
 
 /* ---- multi-GPU: strip-sharded factorization and solve ----------------------
  * One process per GPU.  Rank r of G owns the contiguous global strips

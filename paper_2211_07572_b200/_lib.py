@@ -53,6 +53,7 @@ EXPORTS = [
     "slablu_gpu_residual", "slablu_gpu_sweep_solve", "slablu_gpu_recover",
     "slablu_gpu_sweep_build", "slablu_gpu_set_refine", "slablu_gpu_assemble_canned_device",
     "slablu_gpu_sample_solution_device", "slablu_gpu_error_report", "slablu_gpu_error_report_device",
+    "slablu_gpu_save", "slablu_gpu_load", "slablu_gpu_export_sweep", "slablu_gpu_import_sweep",
 ]
 
 _lib = None
@@ -126,6 +127,14 @@ def lib():
     L.slablu_gpu_error_report.argtypes = [I64, P, P, P, P, P, P, I64, I, P]
     L.slablu_gpu_error_report_device.restype = St
     L.slablu_gpu_error_report_device.argtypes = [I64, P, P, P, P, P, P, I64, I, P]
+    L.slablu_gpu_save.restype = St
+    L.slablu_gpu_save.argtypes = [P, ctypes.c_char_p]
+    L.slablu_gpu_load.restype = St
+    L.slablu_gpu_load.argtypes = [ctypes.c_char_p, I, P]
+    L.slablu_gpu_export_sweep.restype = St
+    L.slablu_gpu_export_sweep.argtypes = [P, ctypes.c_char_p]
+    L.slablu_gpu_import_sweep.restype = St
+    L.slablu_gpu_import_sweep.argtypes = [ctypes.c_char_p, I, P]
     L.slablu_gpu_destroy.restype = None
     L.slablu_gpu_destroy.argtypes = [P]
     L.slablu_gpu_device_count.restype = I

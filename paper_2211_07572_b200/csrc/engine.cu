@@ -19,6 +19,7 @@
 #include <cstring>
 #include <map>
 #include <cstdlib>
+#include <fstream>
 #include <mutex>
 #include <vector>
 
@@ -1731,6 +1732,325 @@ void slablu_gpu_destroy(slablu_gpu_fact* fact) {
     delete fact;
   } catch (...) {
   }
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Factor caching (the reference serializes each factor object in a versioned
+// binary layout: stage_two.hpp:95-120, 200-232, dense.hpp:71-87, banded.hpp:133-163).
+//   SLBGPU01  the whole GPU factorization (level operators, couplings, reduced blocks in LU form,
+//             the block upper factor, optional operator copy), for factor-once-solve-many across
+//             processes: named sections, each u64 name length, name, u64 bytes, raw bytes.
+//   SLBSWP01  stage two in the reference's own SweepFactorization layout (k DenseLU blocks as
+//             write_dense + int64 1-based pivots, then sub and super blocks), so a factorization
+//             made on the GPU loads into the reference and vice versa.
+namespace {
+
+constexpr size_t kStage = 64u << 20;  // pinned staging bytes per copy step
+
+struct Pinned {
+  void* p = nullptr;
+  explicit Pinned(size_t bytes) { SLB_CUDA_CHECK(cudaMallocHost(&p, bytes)); }
+  ~Pinned() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+void write_u64(std::ostream& os, uint64_t v) { os.write(reinterpret_cast<const char*>(&v), sizeof(v)); }
+uint64_t read_u64(std::istream& is) {
+  uint64_t v = 0;
+  is.read(reinterpret_cast<char*>(&v), sizeof(v));
+  if (!is) throw HostError(SLABLU_ERR_GENERIC, "deserialize: truncated stream");
+  return v;
+}
+void write_dev(std::ostream& os, const void* d, size_t bytes, Pinned& stage) {
+  for (size_t o = 0; o < bytes; o += kStage) {
+    const size_t n = std::min(kStage, bytes - o);
+    SLB_CUDA_CHECK(cudaMemcpy(stage.p, static_cast<const char*>(d) + o, n, cudaMemcpyDeviceToHost));
+    os.write(static_cast<const char*>(stage.p), (std::streamsize)n);
+  }
+}
+void read_dev(std::istream& is, void* d, size_t bytes, Pinned& stage) {
+  for (size_t o = 0; o < bytes; o += kStage) {
+    const size_t n = std::min(kStage, bytes - o);
+    is.read(static_cast<char*>(stage.p), (std::streamsize)n);
+    if (!is) throw HostError(SLABLU_ERR_GENERIC, "deserialize: truncated stream");
+    SLB_CUDA_CHECK(cudaMemcpy(static_cast<char*>(d) + o, stage.p, n, cudaMemcpyHostToDevice));
+  }
+}
+void write_section(std::ostream& os, const char* name, const void* data, size_t bytes, bool device, Pinned& stage) {
+  const size_t ln = strlen(name);
+  write_u64(os, ln);
+  os.write(name, (std::streamsize)ln);
+  write_u64(os, bytes);
+  if (device) write_dev(os, data, bytes, stage);
+  else os.write(static_cast<const char*>(data), (std::streamsize)bytes);
+}
+// reads the next section, which must be `name`; returns its byte count (payload left unread)
+uint64_t open_section(std::istream& is, const char* name) {
+  const uint64_t ln = read_u64(is);
+  if (ln > 64) throw HostError(SLABLU_ERR_GENERIC, "deserialize: corrupt section header");
+  std::string got(ln, '\0');
+  is.read(&got[0], (std::streamsize)ln);
+  if (!is || got != name) throw HostError(SLABLU_ERR_GENERIC, std::string("deserialize: expected section ") + name);
+  return read_u64(is);
+}
+template <class T>
+void read_section_dev(std::istream& is, const char* name, DBuf<T>& buf, int dev, Pinned& stage) {
+  const uint64_t bytes = open_section(is, name);
+  if (bytes % sizeof(T)) throw HostError(SLABLU_ERR_GENERIC, "deserialize: section size");
+  buf.release();
+  if (bytes) {
+    buf.alloc(dev, bytes / sizeof(T));
+    read_dev(is, buf.p, bytes, stage);
+  }
+}
+template <class T>
+void read_section_host(std::istream& is, const char* name, std::vector<T>& v) {
+  const uint64_t bytes = open_section(is, name);
+  if (bytes % sizeof(T)) throw HostError(SLABLU_ERR_GENERIC, "deserialize: section size");
+  v.resize(bytes / sizeof(T));
+  is.read(reinterpret_cast<char*>(v.data()), (std::streamsize)bytes);
+  if (!is) throw HostError(SLABLU_ERR_GENERIC, "deserialize: truncated stream");
+}
+
+const char kMagicGpu[9] = "SLBGPU01";
+const char kMagicSwp[9] = "SLBSWP01";
+
+void save_impl(const slablu_gpu_fact* F, const char* path) {
+  if (F->sharded) throw HostError(SLABLU_ERR_CONFIG, "save: sharded factorizations are saved per rank (not supported)");
+  std::lock_guard<std::mutex> guard(F->solve_mu);
+  DeviceGuard dg(F->device);
+  SLB_CUDA_CHECK(cudaStreamSynchronize(F->stream));
+  std::ofstream os(path, std::ios::binary | std::ios::trunc);
+  if (!os) throw HostError(SLABLU_ERR_GENERIC, std::string("save: cannot open ") + path);
+  Pinned stage(kStage);
+  os.write(kMagicGpu, 8);
+  const int64_t hdr[12] = {F->n1, F->n2, F->b, F->S, F->K, F->Wp, F->single ? 1 : 0, F->stage2_only ? 1 : 0,
+                           F->refine, F->storage1, F->storage2, F->sF};
+  write_section(os, "header", hdr, sizeof(hdr), false, stage);
+  const double times[5] = {F->t1, F->t2, F->t_chain, F->t_schur, F->t_asm};
+  write_section(os, "times", times, sizeof(times), false, stage);
+  write_section(os, "strips_h", F->strips_h.data(), F->strips_h.size() * sizeof(StripDesc), false, stage);
+  write_section(os, "ifc_off_h", F->ifc_off_h.data(), F->ifc_off_h.size() * sizeof(int64_t), false, stage);
+  write_section(os, "sym_h", F->sym_h.data(), F->sym_h.size() * sizeof(int32_t), false, stage);
+#define SLB_SEC(buf) write_section(os, #buf, F->buf.p, F->buf.bytes(), true, stage)
+  SLB_SEC(fac); SLB_SEC(perm); SLB_SEC(cpl); SLB_SEC(sym); SLB_SEC(u13); SLB_SEC(lnd); SLB_SEC(dsub); SLB_SEC(exc);
+  SLB_SEC(excpos); SLB_SEC(hcol); SLB_SEC(hidx); SLB_SEC(T); SLB_SEC(ipivT); SLB_SEC(permT); SLB_SEC(dinvT);
+  SLB_SEC(Xup); SLB_SEC(a_rp); SLB_SEC(a_ci); SLB_SEC(a_v);
+#undef SLB_SEC
+  os.flush();
+  if (!os) throw HostError(SLABLU_ERR_GENERIC, std::string("save: write failed: ") + path);
+}
+
+slablu_gpu_fact* load_impl(const char* path, int device) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw HostError(SLABLU_ERR_GENERIC, std::string("load: cannot open ") + path);
+  char magic[8];
+  is.read(magic, 8);
+  if (!is || memcmp(magic, kMagicGpu, 8) != 0)
+    throw HostError(SLABLU_ERR_GENERIC, "load: bad magic or version (expected SLBGPU01)");
+  auto F = std::make_unique<slablu_gpu_fact>();
+  F->device = device;
+  DeviceGuard dg(device);
+  int least = 0, greatest = 0;
+  SLB_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  SLB_CUDA_CHECK(cudaStreamCreateWithPriority(&F->stream, cudaStreamNonBlocking, greatest));
+  StreamScope scope(F->stream);
+  std::vector<int64_t> hdr;
+  read_section_host(is, "header", hdr);
+  if (hdr.size() != 12) throw HostError(SLABLU_ERR_GENERIC, "load: bad header");
+  F->n1 = hdr[0];
+  F->n2 = hdr[1];
+  F->N = F->n1 * F->n2;
+  F->b = hdr[2];
+  F->S = (int)hdr[3];
+  F->Sg = F->S;
+  F->s1 = F->S;
+  F->K = (int)hdr[4];
+  F->j1 = F->K;
+  F->Wp = (int)hdr[5];
+  F->single = hdr[6] != 0;
+  F->stage2_only = hdr[7] != 0;
+  F->refine = (int)hdr[8];
+  F->storage1 = hdr[9];
+  F->storage2 = hdr[10];
+  F->sF = hdr[11];
+  F->sP = F->n2 * 2 * F->Wp;
+  F->sCPL = 4 * F->n2 * F->Wp;
+  std::vector<double> times;
+  read_section_host(is, "times", times);
+  if (times.size() == 5) {
+    F->t1 = times[0];
+    F->t2 = times[1];
+    F->t_chain = times[2];
+    F->t_schur = times[3];
+    F->t_asm = times[4];
+  }
+  read_section_host(is, "strips_h", F->strips_h);
+  read_section_host(is, "ifc_off_h", F->ifc_off_h);
+  read_section_host(is, "sym_h", F->sym_h);
+  if ((int)F->strips_h.size() != F->S || (int)F->ifc_off_h.size() != F->K)
+    throw HostError(SLABLU_ERR_GENERIC, "load: inconsistent geometry");
+  Pinned stage(kStage);
+#define SLB_SEC(buf) read_section_dev(is, #buf, F->buf, device, stage)
+  SLB_SEC(fac); SLB_SEC(perm); SLB_SEC(cpl); SLB_SEC(sym); SLB_SEC(u13); SLB_SEC(lnd); SLB_SEC(dsub); SLB_SEC(exc);
+  SLB_SEC(excpos); SLB_SEC(hcol); SLB_SEC(hidx); SLB_SEC(T); SLB_SEC(ipivT); SLB_SEC(permT); SLB_SEC(dinvT);
+  SLB_SEC(Xup); SLB_SEC(a_rp); SLB_SEC(a_ci); SLB_SEC(a_v);
+#undef SLB_SEC
+  if (F->S > 0) {
+    F->strips.alloc(device, F->S);
+    SLB_CUDA_CHECK(cudaMemcpy(F->strips.p, F->strips_h.data(), F->S * sizeof(StripDesc), cudaMemcpyHostToDevice));
+  }
+  if (F->K > 0) {
+    F->ifc_off.alloc(device, F->K);
+    SLB_CUDA_CHECK(cudaMemcpy(F->ifc_off.p, F->ifc_off_h.data(), F->K * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  static const DevStatus st0{0, INT_MAX, INT_MAX, INT_MAX};
+  F->status.alloc(device, 1);
+  F->sstatus.alloc(device, 1);
+  SLB_CUDA_CHECK(cudaMemcpy(F->status.p, &st0, sizeof(st0), cudaMemcpyHostToDevice));
+  SLB_CUDA_CHECK(cudaMemcpy(F->sstatus.p, &st0, sizeof(st0), cudaMemcpyHostToDevice));
+  return F.release();
+}
+
+// stage two in the reference's SweepFactorization layout (stage_two.hpp:200-207, dense.hpp:71-76)
+void export_sweep_impl(const slablu_gpu_fact* F, const char* path) {
+  if (F->single || F->sharded || F->K < 1) throw HostError(SLABLU_ERR_CONFIG, "export_sweep: no stage two");
+  std::lock_guard<std::mutex> guard(F->solve_mu);
+  DeviceGuard dg(F->device);
+  SLB_CUDA_CHECK(cudaStreamSynchronize(F->stream));
+  std::ofstream os(path, std::ios::binary | std::ios::trunc);
+  if (!os) throw HostError(SLABLU_ERR_GENERIC, std::string("export_sweep: cannot open ") + path);
+  Pinned stage(kStage);
+  const int64_t n2 = F->n2, bs = n2 * n2;
+  os.write(kMagicSwp, 8);
+  write_u64(os, (uint64_t)F->K);
+  std::vector<int32_t> piv32(n2);
+  std::vector<int64_t> piv64(n2);
+  for (int j = 0; j < F->K; j++) {  // DenseLU: write_dense(lu), then int64 1-based pivots
+    write_u64(os, (uint64_t)n2);
+    write_u64(os, (uint64_t)n2);
+    write_dev(os, F->Tdiag() + j * bs, bs * sizeof(double), stage);
+    SLB_CUDA_CHECK(cudaMemcpy(piv32.data(), F->ipivT.p + (size_t)j * n2, n2 * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n2; i++) piv64[i] = (int64_t)piv32[i] + 1;
+    os.write(reinterpret_cast<const char*>(piv64.data()), (std::streamsize)(n2 * sizeof(int64_t)));
+  }
+  for (int which = 0; which < 2; which++)  // sub blocks, then super blocks
+    for (int j = 0; j + 1 < F->K; j++) {
+      write_u64(os, (uint64_t)n2);
+      write_u64(os, (uint64_t)n2);
+      write_dev(os, (which == 0 ? F->Tsub() : F->Tsup()) + j * bs, bs * sizeof(double), stage);
+    }
+  os.flush();
+  if (!os) throw HostError(SLABLU_ERR_GENERIC, std::string("export_sweep: write failed: ") + path);
+}
+
+// SLBSWP01 -> a stage-two-only handle (slablu_gpu_sweep_solve); the solve-side data (row
+// permutation, diagonal-block inverses, X_j = S_j^{-1} super_j) is rebuilt from the LU factors
+slablu_gpu_fact* import_sweep_impl(const char* path, int device) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw HostError(SLABLU_ERR_GENERIC, std::string("import_sweep: cannot open ") + path);
+  char magic[8];
+  is.read(magic, 8);
+  if (!is || memcmp(magic, kMagicSwp, 8) != 0)
+    throw HostError(SLABLU_ERR_GENERIC, "SweepFactorization::deserialize: bad magic or version");
+  const int64_t k = (int64_t)read_u64(is);
+  if (k < 1 || k > (1 << 20)) throw HostError(SLABLU_ERR_GENERIC, "import_sweep: bad block count");
+  auto F = std::make_unique<slablu_gpu_fact>();
+  F->device = device;
+  DeviceGuard dg(device);
+  SLB_CUDA_CHECK(cudaStreamCreateWithFlags(&F->stream, cudaStreamNonBlocking));
+  StreamScope scope(F->stream);
+  Pinned stage(kStage);
+  int64_t m = -1;
+  auto dense_header = [&]() {
+    const int64_t r = (int64_t)read_u64(is), c = (int64_t)read_u64(is);
+    if (r != c || (m >= 0 && r != m) || r < 1 || r > kMaxIfc)
+      throw HostError(SLABLU_ERR_GENERIC, "import_sweep: blocks must be square, equal-sized, <= 4096");
+    m = r;
+  };
+  std::vector<std::vector<int64_t>> pivs;
+  for (int64_t j = 0; j < k; j++) {
+    dense_header();
+    if (j == 0) {
+      F->K = (int)k;
+      F->n1 = k;
+      F->n2 = m;
+      F->N = k * m;
+      F->T.alloc(device, (size_t)(3 * k - 2) * m * m);
+      F->ipivT.alloc(device, (size_t)k * m);
+    }
+    read_dev(is, F->Tdiag() + j * m * m, (size_t)m * m * sizeof(double), stage);
+    std::vector<int64_t> p64(m);
+    is.read(reinterpret_cast<char*>(p64.data()), (std::streamsize)(m * sizeof(int64_t)));
+    if (!is) throw HostError(SLABLU_ERR_GENERIC, "DenseLU::deserialize: truncated stream");
+    std::vector<int32_t> p32(m);
+    for (int64_t i = 0; i < m; i++) {
+      if (p64[i] < 1 || p64[i] > m) throw HostError(SLABLU_ERR_GENERIC, "import_sweep: pivot out of range");
+      p32[i] = (int32_t)(p64[i] - 1);
+    }
+    SLB_CUDA_CHECK(cudaMemcpy(F->ipivT.p + (size_t)j * m, p32.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  for (int which = 0; which < 2; which++)
+    for (int64_t j = 0; j + 1 < k; j++) {
+      dense_header();
+      read_dev(is, (which == 0 ? F->Tsub() : F->Tsup()) + j * m * m, (size_t)m * m * sizeof(double), stage);
+    }
+  F->stage2_only = true;
+  F->status.alloc(device, 1);
+  F->sstatus.alloc(device, 1);
+  static const DevStatus st0{0, INT_MAX, INT_MAX, INT_MAX};
+  SLB_CUDA_CHECK(cudaMemcpy(F->status.p, &st0, sizeof(st0), cudaMemcpyHostToDevice));
+  SLB_CUDA_CHECK(cudaMemcpy(F->sstatus.p, &st0, sizeof(st0), cudaMemcpyHostToDevice));
+  const int64_t dinv_sz = cdiv(m, 64) * 2 * 64 * 64, bs = m * m;
+  F->permT.alloc(device, (size_t)k * m);
+  F->dinvT.alloc(device, (size_t)k * dinv_sz);
+  F->Xup.alloc(device, (size_t)std::max<int64_t>(k - 1, 1) * bs);
+  for (int64_t j = 0; j < k; j++)
+    getrs_prepare(F->stream, m, F->Tdiag() + j * bs, F->ipivT.p + j * m, F->permT.p + j * m, F->dinvT.p + j * dinv_sz);
+  for (int64_t j = 0; j + 1 < k; j++) {
+    double* X = F->Xup.p + j * bs;
+    SLB_CUDA_CHECK(cudaMemcpyAsync(X, F->Tsup() + j * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, F->stream));
+    dgetrs(F->stream, m, m, F->Tdiag() + j * bs, F->ipivT.p + j * m, X, m, nullptr);
+  }
+  SLB_CUDA_CHECK(cudaStreamSynchronize(F->stream));
+  F->storage2 = (k + 2 * (k - 1)) * m * m;
+  return F.release();
+}
+
+}  // namespace
+
+extern "C" {
+
+slablu_gpu_status slablu_gpu_save(const slablu_gpu_fact* fact, const char* path) {
+  ABI_TRY({
+    if (!fact || !path) throw HostError(SLABLU_ERR_GENERIC, "save: null argument");
+    save_impl(fact, path);
+  })
+}
+slablu_gpu_status slablu_gpu_load(const char* path, int device, slablu_gpu_fact** out) {
+  ABI_TRY({
+    require_device();
+    *out = nullptr;
+    if (!path) throw HostError(SLABLU_ERR_GENERIC, "load: null path");
+    *out = load_impl(path, device);
+  })
+}
+slablu_gpu_status slablu_gpu_export_sweep(const slablu_gpu_fact* fact, const char* path) {
+  ABI_TRY({
+    if (!fact || !path) throw HostError(SLABLU_ERR_GENERIC, "export_sweep: null argument");
+    export_sweep_impl(fact, path);
+  })
+}
+slablu_gpu_status slablu_gpu_import_sweep(const char* path, int device, slablu_gpu_fact** out) {
+  ABI_TRY({
+    require_device();
+    *out = nullptr;
+    if (!path) throw HostError(SLABLU_ERR_GENERIC, "import_sweep: null path");
+    *out = import_sweep_impl(path, device);
+  })
 }
 
 }  // extern "C"

@@ -393,6 +393,14 @@ class Factorization:
         self.stats = st
         return st
 
+    def save(self, path):
+        """Versioned binary file (SLBGPU01) of the whole factorization; see load()."""
+        _check(lib().slablu_gpu_save(self._h, str(path).encode()))
+
+    def export_sweep(self, path):
+        """Stage two in the reference's SweepFactorization layout (SLBSWP01, stage_two.hpp:200-232)."""
+        _check(lib().slablu_gpu_export_sweep(self._h, str(path).encode()))
+
     def set_refine(self, refine):
         """Iterative-refinement steps of later solves (needs the operator kept: factorize with
         refine > 0 to be able to raise it again)."""
@@ -520,6 +528,28 @@ class SweepFactorization:
             self.close()
         except Exception:
             pass
+
+
+def load(path, device=0, config: Optional[SolverConfig] = None) -> Factorization:
+    """A factorization saved by Factorization.save (another process, same or another GPU)."""
+    h = ctypes.c_void_p()
+    _check(lib().slablu_gpu_load(str(path).encode(), int(device), ctypes.byref(h)))
+    st = _lib.Stats()
+    _check(lib().slablu_gpu_stats(h, ctypes.byref(st)))
+    cfg = config or SolverConfig(b=int(st.b), device=int(device))
+    return Factorization(h.value, cfg)
+
+
+def import_sweep(path, device=0) -> "SweepFactorization":
+    """SweepFactorization::deserialize (SLBSWP01) onto the GPU; solve with .solve(f)."""
+    h = ctypes.c_void_p()
+    _check(lib().slablu_gpu_import_sweep(str(path).encode(), int(device), ctypes.byref(h)))
+    obj = SweepFactorization.__new__(SweepFactorization)
+    obj._h = h
+    st = _lib.Stats()
+    _check(lib().slablu_gpu_stats(h, ctypes.byref(st)))
+    obj.stats, obj.k, obj.m = st, int(st.interfaces), int(st.n2)
+    return obj
 
 
 def sweep_build(t: BlockTridiagonal, device=0) -> SweepFactorization:
