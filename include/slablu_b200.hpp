@@ -9,6 +9,9 @@
 //   SolverConfig, CompressionChoice, choose_b      driver.hpp:37-66
 //   GridStrip, SlabPartition, partition            partition.hpp:27-91
 //   Factorization, factorize, solve                driver.hpp:72-179
+//   ErrorReport, error_report, sample_field        problem.hpp:160-206
+//   SolveReport, csv_row, json_row, run_problem,
+//   benchmark                                      driver.hpp:182-322
 //   Shard (multi-GPU split, engine extension)      include/slablu_gpu.h slablu_gpu_shard_*
 //
 // Matrices are column major std::vector<double> (the reference uses
@@ -16,9 +19,12 @@
 #ifndef SLABLU_B200_HPP
 #define SLABLU_B200_HPP
 
+#include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <functional>
+#include <ostream>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -257,6 +263,153 @@ inline std::vector<double> solve(const Factorization& fact, const std::vector<do
   std::vector<double> u(f.size());
   detail::check(slablu_gpu_solve(fact.handle(), f.data(), n, nrhs, u.data(), n));
   return u;
+}
+
+// ---- validation and reports (problem.hpp:160-206, driver.hpp:182-322) ---------------
+struct ErrorReport {
+  double relerr_res = 0.0, relerr_true = 0.0;
+  int64_t n_rhs = 0;
+  bool residual_norm_is_absolute = false, solution_norm_is_absolute = false;
+};
+// error_report on the GPU (slablu_gpu_error_report): Frobenius norms over the nrhs columns.
+inline ErrorReport error_report(const SparseSystem& system, const std::vector<double>& u_calc,
+                                const std::vector<double>& u_true, const std::vector<double>& f, int64_t nrhs = 1,
+                                int device = 0) {
+  const int64_t n = system.dim();
+  if (nrhs < 1 || static_cast<int64_t>(u_calc.size()) != n * nrhs ||
+      static_cast<int64_t>(u_true.size()) != n * nrhs || static_cast<int64_t>(f.size()) != n * nrhs)
+    throw Error("error_report: vector length must equal system dimension");
+  double out[4] = {0, 0, 0, 0};
+  detail::check(slablu_gpu_error_report(n, system.row_ptr.data(), system.col_idx.data(), system.values.data(),
+                                        f.data(), u_calc.data(), u_true.data(), nrhs, device, out));
+  ErrorReport r;
+  r.relerr_res = out[0];
+  r.relerr_true = out[1];
+  r.n_rhs = nrhs;
+  r.residual_norm_is_absolute = out[2] != 0.0;
+  r.solution_norm_is_absolute = out[3] != 0.0;
+  return r;
+}
+inline ErrorReport error_report(const SparseSystem& system, const std::vector<double>& u_calc,
+                                const std::vector<double>& u_true) {
+  return error_report(system, u_calc, u_true, system.rhs, 1);
+}
+// sample_field (problem.hpp:199-206): node (i, j) at ((i+1) h, (j+1) h), index i * n2 + j
+inline std::vector<double> sample_field(const SparseSystem& system, const ScalarField& field) {
+  std::vector<double> v(system.dim());
+  for (int64_t i = 0; i < system.n1; i++)
+    for (int64_t j = 0; j < system.n2; j++) v[i * system.n2 + j] = field(double(i + 1) * system.h, double(j + 1) * system.h);
+  return v;
+}
+
+struct SolveReport {
+  int64_t n = 0, n1 = 0, n2 = 0, b = 0;
+  double kappa = 0.0;
+  double t_factor_stage1 = 0.0, t_factor_stage2 = 0.0, t_solve = 0.0;
+  std::size_t m_factor_scalars = 0;
+  ErrorReport errors{};
+  int64_t hbs_max_rank = 0;
+  uint64_t seed = 0;
+};
+
+inline const char* kCsvHeader =
+    "N,n1,n2,b,kappa,T_factor_stage1_s,T_factor_stage2_s,T_solve_s,"
+    "M_factor_scalars,relerr_res,relerr_true,hbs_max_rank,seed";
+
+namespace detail {
+inline std::string format_double(double v) {
+  char buf[40];
+  std::snprintf(buf, sizeof(buf), "%.17g", v);
+  return buf;
+}
+inline std::string format_time(double v) {
+  char buf[40];
+  std::snprintf(buf, sizeof(buf), "%.6e", v);
+  return buf;
+}
+}  // namespace detail
+
+// driver.hpp:218-236 column order; `status` appends the benchmark status column
+inline std::string csv_row(const SolveReport& r, const char* status = nullptr) {
+  std::string row = std::to_string(r.n) + "," + std::to_string(r.n1) + "," + std::to_string(r.n2) + "," +
+                    std::to_string(r.b) + "," + detail::format_double(r.kappa) + "," +
+                    detail::format_time(r.t_factor_stage1) + "," + detail::format_time(r.t_factor_stage2) + "," +
+                    detail::format_time(r.t_solve) + "," + std::to_string(r.m_factor_scalars) + "," +
+                    detail::format_double(r.errors.relerr_res) + "," + detail::format_double(r.errors.relerr_true) +
+                    "," + std::to_string(r.hbs_max_rank) + "," + std::to_string(r.seed);
+  if (status) row += std::string(",") + status;
+  return row;
+}
+// driver.hpp:239-262: the CSV fields under identical names
+inline std::string json_row(const SolveReport& r, const char* status = nullptr) {
+  std::string out = "{";
+  out += "\"N\": " + std::to_string(r.n) + ", ";
+  out += "\"n1\": " + std::to_string(r.n1) + ", ";
+  out += "\"n2\": " + std::to_string(r.n2) + ", ";
+  out += "\"b\": " + std::to_string(r.b) + ", ";
+  out += "\"kappa\": " + detail::format_double(r.kappa) + ", ";
+  out += "\"T_factor_stage1_s\": " + detail::format_time(r.t_factor_stage1) + ", ";
+  out += "\"T_factor_stage2_s\": " + detail::format_time(r.t_factor_stage2) + ", ";
+  out += "\"T_solve_s\": " + detail::format_time(r.t_solve) + ", ";
+  out += "\"M_factor_scalars\": " + std::to_string(r.m_factor_scalars) + ", ";
+  out += "\"relerr_res\": " + detail::format_double(r.errors.relerr_res) + ", ";
+  out += "\"relerr_true\": " + detail::format_double(r.errors.relerr_true) + ", ";
+  out += "\"hbs_max_rank\": " + std::to_string(r.hbs_max_rank) + ", ";
+  out += "\"seed\": " + std::to_string(r.seed);
+  if (status) out += std::string(", \"status\": \"") + status + "\"";
+  out += "}";
+  return out;
+}
+
+// run_problem (driver.hpp:268-292): assemble, factorize (device-timed stages), solve (wall clock
+// around the call, as the reference), error report against the Dirichlet field
+inline SolveReport run_problem(const ProblemSpec& spec, const SolverConfig& config) {
+  const SparseSystem system = assemble_fd5(spec);
+  SolveReport report;
+  report.n = system.dim();
+  report.n1 = system.n1;
+  report.n2 = system.n2;
+  report.kappa = spec.kappa;
+  report.seed = config.seed;
+  const Factorization fact = factorize(system, config);
+  report.b = fact.b;
+  report.hbs_max_rank = fact.hbs_max_rank;
+  report.t_factor_stage1 = fact.t_stage1;
+  report.t_factor_stage2 = fact.t_stage2;
+  report.m_factor_scalars = fact.storage_scalars();
+  const auto t0 = std::chrono::steady_clock::now();
+  const std::vector<double> u = solve(fact, system.rhs);
+  report.t_solve = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  const std::vector<double> u_true = sample_field(system, spec.dirichlet_data);
+  report.errors = error_report(system, u, u_true);
+  return report;
+}
+
+// benchmark (driver.hpp:298-322): one report per problem, rows appended as they complete; a
+// failed run keeps its row with the error in the status column and the sweep continues
+inline std::vector<SolveReport> benchmark(const std::vector<ProblemSpec>& sweep, const SolverConfig& config,
+                                          std::ostream* csv = nullptr) {
+  std::vector<SolveReport> reports;
+  if (csv) *csv << kCsvHeader << ",status\n" << std::flush;
+  for (const ProblemSpec& spec : sweep) {
+    SolveReport report;
+    std::string status = "ok";
+    try {
+      report = run_problem(spec, config);
+    } catch (const Error& e) {
+      report.n1 = spec.n1;
+      report.n2 = spec.n2;
+      report.n = spec.n1 * spec.n2;
+      report.kappa = spec.kappa;
+      report.seed = config.seed;
+      status = std::string("error: ") + e.what();
+      for (char& ch : status)
+        if (ch == ',' || ch == '\n') ch = ';';
+    }
+    reports.push_back(report);
+    if (csv) *csv << csv_row(report, status.c_str()) << "\n" << std::flush;
+  }
+  return reports;
 }
 
 // ---- multi-GPU shards (no reference counterpart) -------------------
