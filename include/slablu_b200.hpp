@@ -415,8 +415,9 @@ inline std::vector<SolveReport> benchmark(const std::vector<ProblemSpec>& sweep,
 // ---- multi-GPU shards (no reference counterpart) -------------------
 // One process per GPU.  All pointers are device memory of the shard's device; the caller moves
 // the n2 x n2 (sweep) and n2 x nrhs (solve) messages between neighbouring ranks, e.g. with
-// ncclSend/ncclRecv, in the order: sweep (r-1 -> r), solve_forward (r-1 -> r),
-// solve_backward (r+1 -> r).
+// ncclSend/ncclRecv.  Factorize: eliminate() (no communication), then sweep() in rank order
+// (r-1 -> r).  Solve: solve_local() (no communication), solve_forward() in rank order (r-1 -> r),
+// solve_backward() in reverse order (r+1 -> r).
 class Shard {
  public:
   Shard(int64_t n1, int64_t n2, int64_t nnz, const int32_t* d_row_ptr, const int32_t* d_col_idx,
@@ -430,9 +431,13 @@ class Shard {
     detail::check(slablu_gpu_shard_plan(n1, n2, st.b, rank, nranks, &plan_));
   }
   const slablu_gpu_shard_t& plan() const { return plan_; }
+  void eliminate() { detail::check(slablu_gpu_shard_eliminate(h_.get())); }
   void sweep(const double* d_in, double* d_out) { detail::check(slablu_gpu_shard_sweep(h_.get(), d_in, d_out)); }
-  void solve_forward(const double* d_f, int64_t ldf, int64_t nrhs, const double* d_in, double* d_out) {
-    detail::check(slablu_gpu_shard_solve_forward(h_.get(), d_f, ldf, nrhs, d_in, d_out));
+  void solve_local(const double* d_f, int64_t ldf, int64_t nrhs) {
+    detail::check(slablu_gpu_shard_solve_local(h_.get(), d_f, ldf, nrhs));
+  }
+  void solve_forward(const double* d_in, double* d_out) {
+    detail::check(slablu_gpu_shard_solve_forward(h_.get(), d_in, d_out));
   }
   void solve_backward(const double* d_in, double* d_out, double* d_u, int64_t ldu) {
     detail::check(slablu_gpu_shard_solve_backward(h_.get(), d_in, d_out, d_u, ldu));

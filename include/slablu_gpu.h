@@ -201,21 +201,22 @@ slablu_gpu_status slablu_gpu_export_sweep(const slablu_gpu_fact* fact, const cha
 slablu_gpu_status slablu_gpu_import_sweep(const char* path, int device, slablu_gpu_fact** out);
 
 /* ---- multi-GPU: strip-sharded factorization and solve ----------------------
- * One process per GPU.  Rank r of G owns the contiguous global strips
- * [s_begin, s_end) (s_begin = r*S/G) and the interfaces [j_begin, j_end) whose
- * right strip it owns (the last rank also owns a trailing interface).  Stage
- * one (band LU, Schur blocks) is local.  Stage two and the interface solves
- * are pipelined over the ranks with ONE message per rank boundary and phase;
- * the caller moves it (ncclSend/ncclRecv over NVLink between processes, or a
- * device copy between logical shards on one GPU):
- *   factorize : shard_factorize_device, then shard_sweep(in from r-1, out to r+1),
- *               messages n2 x n2 (ld n2)
- *   solve     : shard_solve_forward(in from r-1, out to r+1), then
+ * One process per GPU.  Rank r of G owns the contiguous global strips [s_begin, s_end)
+ * (s_begin = r*S/G) and the interfaces [j_begin, j_end) (j_begin = s_begin - 1 for r > 0; the last
+ * rank also owns a trailing interface).  For r > 0 interface j_begin is the rank's SEPARATOR; the
+ * rest is its interior chain.  Stage one (band LU, Schur blocks) is local.  Stage two is a
+ * partitioned (SPIKE-style) elimination: every rank eliminates its interior chain on its own, then
+ * the G - 1 separators are swept in rank order with ONE message per rank boundary (the caller moves
+ * it: ncclSend/ncclRecv over NVLink between processes, or a device copy between logical shards):
+ *   factorize : shard_factorize_device; shard_eliminate (no communication);
+ *               shard_sweep(in from r-1, out to r+1), messages n2 x n2 (ld n2)
+ *   solve     : shard_solve_local (no communication);
+ *               shard_solve_forward(in from r-1, out to r+1);
  *               shard_solve_backward(in from r+1, out to r-1), messages n2 x nrhs (ld n2)
- * NULL message pointers on the ends (rank 0 has no "from r-1" etc.).  All
- * buffers are device memory of the shard's device.  A sharded factorization
- * is not usable with slablu_gpu_solve; the sharded solve keeps per-solve state
- * in the factorization (one solve at a time) and does no refinement. */
+ * NULL message pointers on the ends (rank 0 has no "from r-1" etc.).  All buffers are device
+ * memory of the shard's device.  A sharded factorization is not usable with slablu_gpu_solve; the
+ * sharded solve keeps per-solve state in the factorization (one solve at a time) and does no
+ * refinement (slablu_gpu_residual serves a host-driven one). */
 typedef struct {
   int rank, nranks;
   int64_t s_begin, s_end;     /* local strips (global indices) */
@@ -228,10 +229,11 @@ slablu_gpu_status slablu_gpu_shard_factorize_device(int64_t n1, int64_t n2, int6
                                                     const int32_t* d_row_ptr, const int32_t* d_col_idx,
                                                     const double* d_val, const slablu_gpu_config* config,
                                                     int rank, int nranks, slablu_gpu_fact** out);
+slablu_gpu_status slablu_gpu_shard_eliminate(slablu_gpu_fact* fact);
 slablu_gpu_status slablu_gpu_shard_sweep(slablu_gpu_fact* fact, const double* d_in, double* d_out);
 /* d_f: n x nrhs (ld ldf >= n) device; kept (copied) until the backward phase. */
-slablu_gpu_status slablu_gpu_shard_solve_forward(slablu_gpu_fact* fact, const double* d_f, int64_t ldf,
-                                                 int64_t nrhs, const double* d_in, double* d_out);
+slablu_gpu_status slablu_gpu_shard_solve_local(slablu_gpu_fact* fact, const double* d_f, int64_t ldf, int64_t nrhs);
+slablu_gpu_status slablu_gpu_shard_solve_forward(slablu_gpu_fact* fact, const double* d_in, double* d_out);
 /* d_u: n x nrhs with ldu == n; receives the shard's unknowns, other entries untouched. */
 slablu_gpu_status slablu_gpu_shard_solve_backward(slablu_gpu_fact* fact, const double* d_in, double* d_out,
                                                   double* d_u, int64_t ldu);

@@ -50,6 +50,7 @@ EXPORTS = [
     "slablu_gpu_stats", "slablu_gpu_T_block", "slablu_gpu_reduce_rhs", "slablu_gpu_destroy",
     "slablu_gpu_device_count", "slablu_gpu_shard_plan", "slablu_gpu_shard_factorize_device",
     "slablu_gpu_shard_sweep", "slablu_gpu_shard_solve_forward", "slablu_gpu_shard_solve_backward",
+    "slablu_gpu_shard_eliminate", "slablu_gpu_shard_solve_local",
     "slablu_gpu_residual", "slablu_gpu_sweep_solve", "slablu_gpu_recover",
     "slablu_gpu_sweep_build", "slablu_gpu_set_refine", "slablu_gpu_assemble_canned_device",
     "slablu_gpu_sample_solution_device", "slablu_gpu_error_report", "slablu_gpu_error_report_device",
@@ -96,7 +97,11 @@ def lib():
     L.slablu_gpu_shard_sweep.restype = St
     L.slablu_gpu_shard_sweep.argtypes = [P, P, P]
     L.slablu_gpu_shard_solve_forward.restype = St
-    L.slablu_gpu_shard_solve_forward.argtypes = [P, P, I64, I64, P, P]
+    L.slablu_gpu_shard_solve_forward.argtypes = [P, P, P]
+    L.slablu_gpu_shard_eliminate.restype = St
+    L.slablu_gpu_shard_eliminate.argtypes = [P]
+    L.slablu_gpu_shard_solve_local.restype = St
+    L.slablu_gpu_shard_solve_local.argtypes = [P, P, I64, I64]
     L.slablu_gpu_shard_solve_backward.restype = St
     L.slablu_gpu_shard_solve_backward.argtypes = [P, P, P, P, I64]
     L.slablu_gpu_factorize_device.restype = St

@@ -350,9 +350,17 @@ struct slablu_gpu_fact {
   int rank = 0, nranks = 1, Sg = 0, s0 = 0, s1 = 0, j0 = 0, j1 = 0;
   bool sharded = false, swept = false;
   bool stage2_only = false;  // slablu_gpu_sweep_build: a block-tridiagonal system only
-  // shard solve state between the forward and backward phases
-  DBuf<double> sh_f, sh_red, sh_uifc;
+  // partitioned stage two (SPIKE-style): the rank's interior chain [ia, ib) and the
+  // spike ends on its separators: sh_a = super_{j0} (A_I^{-1} E_L)_first, sh_b = super_{j0}
+  // (A_I^{-1} E_R)_first, sh_c = sub_{ib-1} (A_I^{-1} E_L)_last, sh_d = sub_{ib-1} (A_I^{-1} E_R)_last,
+  // sh_yl = (A_I^{-1} E_L)_last, sh_xhat = S^_r^{-1} sh_b (all n2 x n2)
+  int ia = 0, ib = 0;
+  bool has_left = false, has_right = false, eliminated = false;
+  DBuf<double> sh_a, sh_b, sh_c, sh_d, sh_yl, sh_xhat;
+  // shard solve state between its phases
+  DBuf<double> sh_f, sh_red, sh_red0, sh_uifc, sh_v;
   int64_t sh_nrhs = 0;
+  int sh_phase = 0;  // 0 idle, 1 local done, 2 forward done
   std::vector<StripDesc> strips_h;
   std::vector<int64_t> ifc_off_h;
   std::vector<int32_t> sym_h;
@@ -428,8 +436,7 @@ void shard_ranges(int Sg, int K, int rank, int nranks, int* s0, int* s1, int* j0
 // S_j stays in LU form (as DenseLU in the reference): X = S_{j-1}^{-1} super_{j-1} by getrs, the
 // solve applies S_j^{-1} by the chained getrs (stage_two.hpp:138-147, 176-186).  Singular S_j raise
 // ERR_SINGULAR with the block index in F->status (checked by the caller).
-void stage_two_build(slablu_gpu_fact* F) {
-  cudaStream_t st = F->stream;
+void stage_two_alloc(slablu_gpu_fact* F) {
   const int dev = F->device, K = F->K;
   const int64_t n2 = F->n2, bs = n2 * n2;
   const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
@@ -440,17 +447,37 @@ void stage_two_build(slablu_gpu_fact* F) {
   // the recurrence computes them anyway (stage_two.hpp:138-140), and the backward sweep of the
   // solve is then u_j -= X_j u_{j+1}, one GEMV instead of a GEMV plus a triangular-solve chain.
   F->Xup.alloc(dev, (size_t)std::max(K - 1, 1) * bs);
-  for (int j = 0; j < K; j++) {
-    double* Sj = F->Tdiag() + j * bs;
-    if (j > 0) {
+}
+
+// LU form of S_j in place (Tdiag[j]) plus the chained-getrs data of the solve
+void factor_S(slablu_gpu_fact* F, int j) {
+  const int64_t n2 = F->n2, bs = n2 * n2, dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
+  double* Sj = F->Tdiag() + j * bs;
+  dgetrf(F->stream, n2, Sj, F->ipivT.p + (size_t)j * n2, nullptr, F->status.p, j);
+  getrs_prepare(F->stream, n2, Sj, F->ipivT.p + (size_t)j * n2, F->permT.p + (size_t)j * n2,
+                F->dinvT.p + (size_t)j * dinv_sz);
+}
+
+// The sweep over the interfaces [ia, ib) started fresh at ia: S_ia = T_{ia ia},
+// X_{j-1} = S_{j-1}^{-1} super_{j-1}, S_j = T_jj - sub_{j-1} X_{j-1}.
+void stage_two_range(slablu_gpu_fact* F, int ia, int ib) {
+  cudaStream_t st = F->stream;
+  const int64_t n2 = F->n2, bs = n2 * n2;
+  for (int j = ia; j < ib; j++) {
+    if (j > ia) {
       double* X = F->Xup.p + (size_t)(j - 1) * bs;
       SLB_CUDA_CHECK(cudaMemcpyAsync(X, F->Tsup() + (j - 1) * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
       dgetrs(st, n2, n2, F->Tdiag() + (j - 1) * bs, F->ipivT.p + (size_t)(j - 1) * n2, X, n2, nullptr);
-      dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X, n2, 0, 1.0, Sj, n2, 0, 1);
+      dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X, n2, 0, 1.0, F->Tdiag() + j * bs, n2, 0,
+                    1);
     }
-    dgetrf(st, n2, Sj, F->ipivT.p + (size_t)j * n2, nullptr, F->status.p, j);
-    getrs_prepare(st, n2, Sj, F->ipivT.p + (size_t)j * n2, F->permT.p + (size_t)j * n2, F->dinvT.p + (size_t)j * dinv_sz);
+    factor_S(F, j);
   }
+}
+
+void stage_two_build(slablu_gpu_fact* F) {
+  stage_two_alloc(F);
+  stage_two_range(F, 0, F->K);
 }
 
 slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32_t* rp, const int32_t* ci,
@@ -1003,10 +1030,11 @@ struct SweepSolver {
   }
   // backward u_j -= S_j^{-1} super_j u_{j+1} = X_j u_{j+1} (stage_two.hpp:181-187 with the block upper
   // factor kept by stage_two_build)
-  void backward(double* uifc, int jlo, int jhi) {
+  // open_end: [jlo, jhi) is a chain of its own (u_{jhi} is not part of it: no X_{jhi-1} term)
+  void backward(double* uifc, int jlo, int jhi, bool open_end = false) {
     const int64_t n2 = F->n2, Kn = (int64_t)F->K * n2, bs = n2 * n2;
     for (int j = jhi - 1; j >= jlo; j--) {
-      if (j + 1 >= F->K) continue;
+      if (j + 1 >= F->K || (open_end && j == jhi - 1)) continue;
       dgemv_batched_rhs(F->stream, n2, n2, nrhs, -1.0, F->Xup.p + (size_t)j * bs, n2, uifc + (j + 1) * n2, Kn, 1.0,
                         uifc + j * n2, Kn, part.p);
     }
@@ -1085,48 +1113,102 @@ void require_shard(const slablu_gpu_fact* F, const char* who) {
   if (!F->sharded) throw HostError(SLABLU_ERR_CONFIG, std::string(who) + ": not a sharded factorization");
 }
 
-// Stage two of a shard (stage_two.hpp:131-150 restricted to the owned interfaces [j0, j1)):
-// T_{j0 j0} += M_in (rank r-1's strip term and its sweep correction); S_j as usual;
-// M_out = (strip s1-1's term on interface j1) - sub_{j1-1} S_{j1-1}^{-1} super_{j1-1}.
-void shard_sweep_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
-  require_shard(F, "shard_sweep");
-  if (F->rank > 0 && !d_in) throw HostError(SLABLU_ERR_CONFIG, "shard_sweep: rank > 0 needs the message of rank - 1");
-  if (F->rank < F->nranks - 1 && !d_out)
-    throw HostError(SLABLU_ERR_CONFIG, "shard_sweep: rank < nranks - 1 needs an output message buffer");
+// ---------------------------------------------------------------------------
+// Partitioned stage two over the ranks.  Rank r owns the
+// interfaces [j0, j1): for r > 0 the first, j0, is its separator s_r; the others form its interior
+// chain [ia, ib) (ia = j0 + 1, or 0 on rank 0; ib = j1).  Every rank eliminates its interior on its
+// own (shard_eliminate, no communication), leaving a block-tridiagonal system on the G - 1
+// separators whose blocks are, with E_L = [sub_{j0}; 0 ..] and E_R = [.. 0; super_{ib-1}]:
+//   D^_r = T_{s_r s_r} - super_{j0} (A_I^{-1} E_L)_first - sub_{ib'-1} (A_I'^{-1} E_R)_last   (I' of r-1)
+//   U^_r = -super_{j0} (A_I^{-1} E_R)_first,   L^_r = -sub_{ib-1} (A_I^{-1} E_L)_last
+// (direct couplings super_{j0} / sub_{j0} when the interior is empty).  The separator sweep is a
+// pipeline with ONE n2 x n2 message per rank boundary (shard_sweep):
+//   S^_r = T_{j0 j0}[own terms] - a_r + M_in,  X^_r = S^_r^{-1} b_r,
+//   M_out = T_{j1 j1}[own strip term] - d_r - c_r X^_r          (c X^ = L^ S^^{-1} U^).
+// The solve: every rank reduces its right-hand side and solves its interior (shard_solve_local);
+// the separator values go forward and back through the pipeline with one n2 x nrhs message per
+// boundary and direction; every rank then re-solves its interior with the separator couplings
+// moved to the right-hand side and recovers its slab interiors.
+
+void shard_eliminate_impl(slablu_gpu_fact* F) {
+  require_shard(F, "shard_eliminate");
   DeviceGuard dg(F->device);
   cudaStream_t st = F->stream;
   StreamScope scope(st);
   const int dev = F->device;
   const int64_t n2 = F->n2, bs = n2 * n2;
-  const int j0 = F->j0, j1 = F->j1;
   const int64_t l0 = slb::g_kernel_count.load();
   cudaEvent_t e0, e1;
   SLB_CUDA_CHECK(cudaEventCreate(&e0));
   SLB_CUDA_CHECK(cudaEventCreate(&e1));
   SLB_CUDA_CHECK(cudaEventRecord(e0, st));
-  if (F->rank > 0) add2d(st, d_in, n2, F->Tdiag() + j0 * bs, n2, n2, n2);
-  // S_j in LU form as in the unsharded sweep (DenseLU, stage_two.hpp:138-147)
-  const int64_t dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
-  F->ipivT.alloc(dev, (size_t)std::max(F->K, 1) * n2);
-  F->permT.alloc(dev, (size_t)std::max(F->K, 1) * n2);
-  F->dinvT.alloc(dev, (size_t)std::max(F->K, 1) * dinv_sz);
-  F->Xup.alloc(dev, (size_t)std::max(F->K - 1, 1) * bs);
-  auto sub_Sinv_super = [&](int j, double* target) {  // X_j = S_j^{-1} super_j; target -= sub_j X_j
-    double* X = F->Xup.p + (size_t)j * bs;
-    SLB_CUDA_CHECK(cudaMemcpyAsync(X, F->Tsup() + j * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    dgetrs(st, n2, n2, F->Tdiag() + j * bs, F->ipivT.p + (size_t)j * n2, X, n2, nullptr);
-    dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + j * bs, n2, 0, X, n2, 0, 1.0, target, n2, 0, 1);
-  };
-  for (int j = j0; j < j1; j++) {
-    double* Sj = F->Tdiag() + j * bs;
-    if (j > j0) sub_Sinv_super(j - 1, Sj);
-    dgetrf(st, n2, Sj, F->ipivT.p + (size_t)j * n2, nullptr, F->status.p, j);
-    getrs_prepare(st, n2, Sj, F->ipivT.p + (size_t)j * n2, F->permT.p + (size_t)j * n2,
-                  F->dinvT.p + (size_t)j * dinv_sz);
+  F->has_left = F->rank > 0;
+  F->has_right = F->rank < F->nranks - 1;
+  F->ia = F->has_left ? F->j0 + 1 : 0;
+  F->ib = F->j1;
+  const int ia = F->ia, ib = F->ib, m = ib - ia, j0 = F->j0;
+  stage_two_alloc(F);
+  stage_two_range(F, ia, ib);  // the interior chain: LU(S_j), X_j for j in [ia, ib - 1)
+  for (DBuf<double>* b : {&F->sh_a, &F->sh_b, &F->sh_c, &F->sh_d, &F->sh_yl, &F->sh_xhat}) {
+    b->alloc(dev, bs);
+    SLB_CUDA_CHECK(cudaMemsetAsync(b->p, 0, b->bytes(), st));
   }
-  if (F->rank < F->nranks - 1) {
-    SLB_CUDA_CHECK(cudaMemcpyAsync(d_out, F->Tdiag() + j1 * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    if (j1 > j0) sub_Sinv_super(j1 - 1, d_out);
+  auto gemm = [&](double* C, const double* A, const double* B, double alpha, double beta) {
+    dgemm_batched(st, n2, n2, n2, alpha, A, n2, 0, B, n2, 0, beta, C, n2, 0, 1);
+  };
+  auto getrs = [&](int j, double* B) {  // B = S_j^{-1} B
+    dgetrs(st, n2, n2, F->Tdiag() + (size_t)j * bs, F->ipivT.p + (size_t)j * n2, B, n2, nullptr);
+  };
+  auto copy = [&](double* dst, const double* src) {
+    SLB_CUDA_CHECK(cudaMemcpyAsync(dst, src, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  };
+  if (m == 0) {  // adjacent separators couple directly: U^ = super_{j0}, L^ = sub_{j0}
+    if (F->has_left && F->has_right) {
+      add2d(st, F->Tsup() + (size_t)j0 * bs, n2, F->sh_b.p, n2, n2, n2, -1.0);
+      add2d(st, F->Tsub() + (size_t)j0 * bs, n2, F->sh_c.p, n2, n2, n2, -1.0);
+    }
+  } else {
+    DBuf<double> Y, t0;
+    t0.alloc(dev, bs);
+    if (F->has_left) {
+      // A_I^{-1} E_L: forward y_ia = S_ia^{-1} sub_{j0}, y_j = -S_j^{-1} sub_{j-1} y_{j-1};
+      // backward x_j = y_j - X_j x_{j+1} (all m blocks kept: the first and the last are needed)
+      Y.alloc(dev, (size_t)m * bs);
+      copy(Y.p, F->Tsub() + (size_t)j0 * bs);
+      getrs(ia, Y.p);
+      for (int j = ia + 1; j < ib; j++) {
+        double* y = Y.p + (size_t)(j - ia) * bs;
+        gemm(y, F->Tsub() + (size_t)(j - 1) * bs, y - bs, -1.0, 0.0);
+        getrs(j, y);
+      }
+      for (int j = ib - 2; j >= ia; j--) {
+        double* y = Y.p + (size_t)(j - ia) * bs;
+        gemm(y, F->Xup.p + (size_t)j * bs, y + bs, -1.0, 1.0);
+      }
+      gemm(F->sh_a.p, F->Tsup() + (size_t)j0 * bs, Y.p, 1.0, 0.0);
+      if (F->has_right) {
+        copy(F->sh_yl.p, Y.p + (size_t)(m - 1) * bs);
+        gemm(F->sh_c.p, F->Tsub() + (size_t)(ib - 1) * bs, F->sh_yl.p, 1.0, 0.0);
+      }
+      Y.release();
+    }
+    if (F->has_right) {
+      // A_I^{-1} E_R: x_{ib-1} = S_{ib-1}^{-1} super_{ib-1}, x_j = -X_j x_{j+1}
+      copy(t0.p, F->Tsup() + (size_t)(ib - 1) * bs);
+      getrs(ib - 1, t0.p);
+      gemm(F->sh_d.p, F->Tsub() + (size_t)(ib - 1) * bs, t0.p, 1.0, 0.0);
+      if (F->has_left) {
+        DBuf<double> t1;
+        t1.alloc(dev, bs);
+        double* cur = t0.p;
+        double* nxt = t1.p;
+        for (int j = ib - 2; j >= ia; j--) {
+          gemm(nxt, F->Xup.p + (size_t)j * bs, cur, -1.0, 0.0);
+          std::swap(cur, nxt);
+        }
+        gemm(F->sh_b.p, F->Tsup() + (size_t)j0 * bs, cur, 1.0, 0.0);
+      }
+    }
   }
   SLB_CUDA_CHECK(cudaEventRecord(e1, st));
   SLB_CUDA_CHECK(cudaEventSynchronize(e1));
@@ -1142,84 +1224,188 @@ void shard_sweep_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
   cudaEventDestroy(e1);
   F->t2 = ms * 1e-3;
   F->launches_factor += slb::g_kernel_count.load() - l0;
+  F->eliminated = true;
+}
+
+// One step of the separator sweep (rank order): M_in from r - 1, M_out to r + 1 (n2 x n2, ld n2).
+void shard_sweep_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
+  require_shard(F, "shard_sweep");
+  if (!F->eliminated) throw HostError(SLABLU_ERR_CONFIG, "shard_sweep: call slablu_gpu_shard_eliminate first");
+  if (F->has_left && !d_in) throw HostError(SLABLU_ERR_CONFIG, "shard_sweep: rank > 0 needs the message of rank - 1");
+  if (F->has_right && !d_out)
+    throw HostError(SLABLU_ERR_CONFIG, "shard_sweep: rank < nranks - 1 needs an output message buffer");
+  DeviceGuard dg(F->device);
+  cudaStream_t st = F->stream;
+  StreamScope scope(st);
+  const int64_t n2 = F->n2, bs = n2 * n2;
+  const int j0 = F->j0, j1 = F->j1;
+  const int64_t l0 = slb::g_kernel_count.load();
+  cudaEvent_t e0, e1;
+  SLB_CUDA_CHECK(cudaEventCreate(&e0));
+  SLB_CUDA_CHECK(cudaEventCreate(&e1));
+  SLB_CUDA_CHECK(cudaEventRecord(e0, st));
+  if (F->has_left) {  // S^_r = T_{j0 j0} - a_r + M_in, in place; X^_r = S^_r^{-1} b_r
+    double* Sh = F->Tdiag() + (size_t)j0 * bs;
+    add2d(st, F->sh_a.p, n2, Sh, n2, n2, n2, -1.0);
+    add2d(st, d_in, n2, Sh, n2, n2, n2, 1.0);
+    factor_S(F, j0);
+    if (F->has_right) {
+      SLB_CUDA_CHECK(cudaMemcpyAsync(F->sh_xhat.p, F->sh_b.p, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      dgetrs(st, n2, n2, Sh, F->ipivT.p + (size_t)j0 * n2, F->sh_xhat.p, n2, nullptr);
+    }
+  }
+  if (F->has_right) {  // M_out = T_{j1 j1}[own strip term] - d_r - c_r X^_r
+    SLB_CUDA_CHECK(cudaMemcpyAsync(d_out, F->Tdiag() + (size_t)j1 * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    add2d(st, F->sh_d.p, n2, d_out, n2, n2, n2, -1.0);
+    if (F->has_left) dgemm_batched(st, n2, n2, n2, -1.0, F->sh_c.p, n2, 0, F->sh_xhat.p, n2, 0, 1.0, d_out, n2, 0, 1);
+  }
+  SLB_CUDA_CHECK(cudaEventRecord(e1, st));
+  SLB_CUDA_CHECK(cudaEventSynchronize(e1));
+  {
+    DevStatus hs;
+    SLB_CUDA_CHECK(cudaMemcpy(&hs, F->status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost));
+    if (hs.flags & ERR_SINGULAR)
+      throw HostError(SLABLU_ERR_SINGULAR, "sweep_build: singular Schur complement block", hs.singular_block);
+  }
+  float ms = 0;
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  F->t2 += ms * 1e-3;
+  F->launches_factor += slb::g_kernel_count.load() - l0;
   F->swept = true;
 }
 
-// Solve, forward half (shard): reduce_rhs on the local strips (stage_one.hpp:415-433) and the
-// forward block sweep over the owned interfaces (stage_two.hpp:170-180).  Messages are
-// n2 x nrhs (ld n2): d_in = strip s0-1's reduction term on interface j0 minus sub u from rank-1.
-void shard_solve_fwd_impl(slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, const double* d_in,
-                          double* d_out) {
+// Solve, local phase: reduce_rhs on the local strips (stage_one.hpp:415-433) and the interior
+// chain solve z = A_I^{-1} red_I (no communication).
+void shard_solve_local_impl(slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs) {
+  require_shard(F, "shard_solve_local");
+  if (!F->swept) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_local: factor with shard_eliminate + shard_sweep first");
+  DeviceGuard dg(F->device);
+  cudaStream_t st = F->stream;
+  StreamScope scope(st);
+  const int dev = F->device;
+  const int64_t n2 = F->n2, N = F->N, Kn = (int64_t)F->K * n2;
+  F->sh_nrhs = nrhs;
+  F->sh_f.alloc(dev, (size_t)N * nrhs);
+  copy2d(st, d_f, ldf, F->sh_f.p, N, N, nrhs);
+  F->sh_red.alloc(dev, (size_t)std::max<int64_t>(Kn, 1) * nrhs);
+  F->sh_red0.alloc(dev, (size_t)std::max<int64_t>(Kn, 1) * nrhs);
+  F->sh_uifc.alloc(dev, (size_t)std::max<int64_t>(Kn, 1) * nrhs);
+  F->sh_v.alloc(dev, (size_t)n2 * nrhs);
+  SLB_CUDA_CHECK(cudaMemsetAsync(F->sh_uifc.p, 0, F->sh_uifc.bytes(), st));
+  SLB_CUDA_CHECK(cudaMemsetAsync(F->sh_v.p, 0, F->sh_v.bytes(), st));
+  {
+    StripSweeper sw(F, F->sh_f.p, nrhs);
+    reduce_phase(F, sw, F->sh_f.p, nrhs, F->sh_red.p, F->j0, F->j1);
+  }
+  copy2d(st, F->sh_red.p, Kn, F->sh_red0.p, Kn, Kn, nrhs);
+  if (F->ib > F->ia) {  // z = A_I^{-1} red_I into uifc[ia, ib)
+    SweepSolver ss(F, nrhs);
+    ss.forward(F->sh_red.p, F->sh_uifc.p, F->ia, F->ib);
+    ss.backward(F->sh_uifc.p, F->ia, F->ib, true);
+  }
+  SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+  F->sh_phase = 1;
+}
+
+// Separator forward step (rank order): q_in from r - 1, q_out to r + 1 (n2 x nrhs, ld n2):
+//   v_r = S^_r^{-1} (red[j0] - super_{j0} z_ia + q_in),
+//   q_out = red[j1] - sub_{ib-1} (z_{ib-1} - (A_I^{-1} E_L)_last v_r)     (L^ v folded in).
+void shard_solve_fwd_impl(slablu_gpu_fact* F, const double* d_in, double* d_out) {
   require_shard(F, "shard_solve_forward");
-  if (!F->swept) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_forward: call slablu_gpu_shard_sweep first");
-  if (F->rank > 0 && !d_in) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_forward: rank > 0 needs the message of rank - 1");
-  if (F->rank < F->nranks - 1 && !d_out)
+  if (F->sh_phase != 1) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_forward: call slablu_gpu_shard_solve_local first");
+  if (F->has_left && !d_in) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_forward: rank > 0 needs the message of rank - 1");
+  if (F->has_right && !d_out)
     throw HostError(SLABLU_ERR_CONFIG, "shard_solve_forward: rank < nranks - 1 needs an output message buffer");
   DeviceGuard dg(F->device);
   cudaStream_t st = F->stream;
   StreamScope scope(st);
   const int dev = F->device;
-  const int64_t n2 = F->n2, N = F->N, Kn = (int64_t)F->K * n2, bs = n2 * n2;
-  const int j0 = F->j0, j1 = F->j1;
-  F->sh_nrhs = nrhs;
-  F->sh_f.alloc(dev, (size_t)N * nrhs);
-  copy2d(st, d_f, ldf, F->sh_f.p, N, N, nrhs);
-  F->sh_red.alloc(dev, (size_t)std::max<int64_t>(Kn, 1) * nrhs);
-  F->sh_uifc.alloc(dev, (size_t)std::max<int64_t>(Kn, 1) * nrhs);
-  SLB_CUDA_CHECK(cudaMemsetAsync(F->sh_uifc.p, 0, F->sh_uifc.bytes(), st));
-  double* red = F->sh_red.p;
-  double* uifc = F->sh_uifc.p;
-  {
-    StripSweeper sw(F, F->sh_f.p, nrhs);
-    reduce_phase(F, sw, F->sh_f.p, nrhs, red, j0, j1);
+  const int64_t n2 = F->n2, Kn = (int64_t)F->K * n2, bs = n2 * n2, nrhs = F->sh_nrhs;
+  const int j0 = F->j0, j1 = F->j1, ia = F->ia, ib = F->ib;
+  const bool interior = ib > ia;
+  DBuf<double> part, t;
+  part.alloc(dev, (size_t)8 * n2 * nrhs);
+  t.alloc(dev, (size_t)n2 * nrhs);
+  const double* red0 = F->sh_red0.p;
+  const double* z = F->sh_uifc.p;
+  if (F->has_left) {
+    copy2d(st, red0 + (size_t)j0 * n2, Kn, t.p, n2, n2, nrhs);
+    if (interior)
+      dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsup() + (size_t)j0 * bs, n2, z + (size_t)ia * n2, Kn, 1.0, t.p, n2,
+                        part.p);
+    add2d(st, d_in, n2, t.p, n2, n2, nrhs, 1.0);
+    SweepSolver ss(F, nrhs);
+    ss.apply_Sinv(j0, t.p, n2, F->sh_v.p, n2, 1.0, 0.0);
   }
-  if (F->rank > 0) add2d(st, d_in, n2, red + j0 * n2, Kn, n2, nrhs);
-  SweepSolver ss(F, nrhs);
-  ss.forward(red, uifc, j0, j1);
-  if (F->rank < F->nranks - 1) {
-    copy2d(st, red + j1 * n2, Kn, d_out, n2, n2, nrhs);
-    if (j1 > j0) {
-      dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (j1 - 1) * bs, n2, uifc + (j1 - 1) * n2, Kn, 1.0, d_out,
-                        n2, ss.part.p);
+  if (F->has_right) {
+    copy2d(st, red0 + (size_t)j1 * n2, Kn, d_out, n2, n2, nrhs);
+    if (interior) {
+      copy2d(st, z + (size_t)(ib - 1) * n2, Kn, t.p, n2, n2, nrhs);
+      if (F->has_left)
+        dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->sh_yl.p, n2, F->sh_v.p, n2, 1.0, t.p, n2, part.p);
+      dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (size_t)(ib - 1) * bs, n2, t.p, n2, 1.0, d_out, n2,
+                        part.p);
+    } else if (F->has_left) {  // adjacent separators: q = red[j1] - sub_{j0} v
+      dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (size_t)j0 * bs, n2, F->sh_v.p, n2, 1.0, d_out, n2,
+                        part.p);
     }
   }
   SLB_CUDA_CHECK(cudaGetLastError());
   SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+  F->sh_phase = 2;
 }
 
-// Solve, backward half (shard): backward block sweep (stage_two.hpp:181-187) with u_{j1} from
-// rank+1, recover_interiors on the local strips (stage_one.hpp:438-462).  d_u (ld N) receives the
-// shard's unknowns (local strips and owned interfaces); every other entry is left untouched.
+// Separator backward step (reverse rank order) and the local finish: u_{s_r} = v_r + X^_r u_{s_{r+1}}
+// (d_in = u_{s_{r+1}} from r + 1, d_out = u_{s_r} to r - 1), then the interior re-solved with the
+// separator couplings on the right-hand side, recover_interiors (stage_one.hpp:438-462) on the local
+// strips.  d_u (ld N) receives the shard's unknowns; every other entry is left untouched.
 void shard_solve_bwd_impl(slablu_gpu_fact* F, const double* d_in, double* d_out, double* d_u, int64_t ldu) {
   require_shard(F, "shard_solve_backward");
-  if (F->sh_nrhs <= 0 || !F->sh_red.p)
-    throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: call slablu_gpu_shard_solve_forward first");
+  if (F->sh_phase != 2) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: call slablu_gpu_shard_solve_forward first");
   if (ldu != F->N) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: ldu must equal n1*n2");
-  if (F->rank < F->nranks - 1 && !d_in)
+  if (F->has_right && !d_in)
     throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: rank < nranks - 1 needs u of interface j_end");
-  if (F->rank > 0 && !d_out) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: rank > 0 needs an output buffer");
+  if (F->has_left && !d_out) throw HostError(SLABLU_ERR_CONFIG, "shard_solve_backward: rank > 0 needs an output buffer");
   DeviceGuard dg(F->device);
   cudaStream_t st = F->stream;
   StreamScope scope(st);
-  const int64_t n2 = F->n2, Kn = (int64_t)F->K * n2, nrhs = F->sh_nrhs;
-  const int j0 = F->j0, j1 = F->j1;
+  const int dev = F->device;
+  const int64_t n2 = F->n2, Kn = (int64_t)F->K * n2, bs = n2 * n2, nrhs = F->sh_nrhs;
+  const int j0 = F->j0, j1 = F->j1, ia = F->ia, ib = F->ib;
   double* uifc = F->sh_uifc.p;
-  if (F->rank < F->nranks - 1) copy2d(st, d_in, n2, uifc + j1 * n2, Kn, n2, nrhs);
-  {
-    SweepSolver ss(F, nrhs);
-    ss.backward(uifc, j0, j1);
+  double* red = F->sh_red.p;
+  DBuf<double> part;
+  part.alloc(dev, (size_t)8 * n2 * nrhs);
+  if (F->has_right) copy2d(st, d_in, n2, uifc + (size_t)j1 * n2, Kn, n2, nrhs);
+  if (F->has_left) {
+    copy2d(st, F->sh_v.p, n2, uifc + (size_t)j0 * n2, Kn, n2, nrhs);
+    if (F->has_right)
+      dgemv_batched_rhs(st, n2, n2, nrhs, 1.0, F->sh_xhat.p, n2, d_in, n2, 1.0, uifc + (size_t)j0 * n2, Kn, part.p);
+    copy2d(st, uifc + (size_t)j0 * n2, Kn, d_out, n2, n2, nrhs);
   }
-  if (F->rank > 0) copy2d(st, uifc + j0 * n2, Kn, d_out, n2, n2, nrhs);
+  if (ib > ia) {  // u_I = A_I^{-1} (red_I - E_L u_{s_r} - E_R u_{s_{r+1}})
+    copy2d(st, F->sh_red0.p, Kn, red, Kn, Kn, nrhs);
+    if (F->has_left)
+      dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsub() + (size_t)j0 * bs, n2, uifc + (size_t)j0 * n2, Kn, 1.0,
+                        red + (size_t)ia * n2, Kn, part.p);
+    if (F->has_right)
+      dgemv_batched_rhs(st, n2, n2, nrhs, -1.0, F->Tsup() + (size_t)(ib - 1) * bs, n2, uifc + (size_t)j1 * n2, Kn, 1.0,
+                        red + (size_t)(ib - 1) * n2, Kn, part.p);
+    SweepSolver ss(F, nrhs);
+    ss.forward(red, uifc, ia, ib);
+    ss.backward(uifc, ia, ib, true);
+  }
   {
     StripSweeper sw(F, F->sh_f.p, nrhs);
     recover_phase(F, sw, uifc, nrhs, d_u, j0, j1);
   }
   SLB_CUDA_CHECK(cudaStreamSynchronize(st));
   check_solve_status(F);
-  F->sh_f.release();
-  F->sh_red.release();
-  F->sh_uifc.release();
+  for (DBuf<double>* b : {&F->sh_f, &F->sh_red, &F->sh_red0, &F->sh_uifc, &F->sh_v}) b->release();
   F->sh_nrhs = 0;
+  F->sh_phase = 0;
 }
 
 void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_t nrhs, double* d_u, int64_t ldu) {
@@ -1389,6 +1575,21 @@ slablu_gpu_status slablu_gpu_residual(const slablu_gpu_fact* fact, const double*
   })
 }
 
+slablu_gpu_status slablu_gpu_shard_eliminate(slablu_gpu_fact* fact) {
+  ABI_TRY({
+    if (!fact) throw HostError(SLABLU_ERR_GENERIC, "shard_eliminate: null factorization");
+    shard_eliminate_impl(fact);
+  })
+}
+
+slablu_gpu_status slablu_gpu_shard_solve_local(slablu_gpu_fact* fact, const double* d_f, int64_t ldf, int64_t nrhs) {
+  ABI_TRY({
+    if (!fact) throw HostError(SLABLU_ERR_GENERIC, "shard_solve_local: null factorization");
+    if (nrhs < 1 || ldf < fact->N) throw HostError(SLABLU_ERR_GENERIC, "shard_solve_local: bad rhs shape");
+    shard_solve_local_impl(fact, d_f, ldf, nrhs);
+  })
+}
+
 slablu_gpu_status slablu_gpu_shard_sweep(slablu_gpu_fact* fact, const double* d_in, double* d_out) {
   ABI_TRY({
     if (!fact) throw HostError(SLABLU_ERR_GENERIC, "shard_sweep: null factorization");
@@ -1396,12 +1597,10 @@ slablu_gpu_status slablu_gpu_shard_sweep(slablu_gpu_fact* fact, const double* d_
   })
 }
 
-slablu_gpu_status slablu_gpu_shard_solve_forward(slablu_gpu_fact* fact, const double* d_f, int64_t ldf, int64_t nrhs,
-                                                 const double* d_in, double* d_out) {
+slablu_gpu_status slablu_gpu_shard_solve_forward(slablu_gpu_fact* fact, const double* d_in, double* d_out) {
   ABI_TRY({
     if (!fact) throw HostError(SLABLU_ERR_GENERIC, "shard_solve_forward: null factorization");
-    if (nrhs < 1 || ldf < fact->N) throw HostError(SLABLU_ERR_GENERIC, "shard_solve_forward: bad rhs shape");
-    shard_solve_fwd_impl(fact, d_f, ldf, nrhs, d_in, d_out);
+    shard_solve_fwd_impl(fact, d_in, d_out);
   })
 }
 

@@ -3,21 +3,22 @@
 The reference has no multi-GPU path; this is the engine's.  Stage one of
 SlabLU is independent per strip, so rank r of G owns the contiguous global
 strips [s_begin, s_end) and runs their band LU and Schur sweeps alone.  The
-block-tridiagonal stage two (stage_two.hpp:131-188) is a recurrence over the
-interfaces, so it is pipelined over the ranks: rank r owns the interfaces whose
-right strip it holds and exchanges ONE message with each neighbour per phase:
+block-tridiagonal stage two (stage_two.hpp:131-188) is eliminated in a
+partitioned (SPIKE-style) way: for r > 0 the first interface the rank owns is
+its separator, the others form its interior chain, which every rank eliminates
+on its own; the G - 1 separators then form a small block-tridiagonal system
+swept in rank order with ONE message per rank boundary and phase:
 
-  factorize  r-1 -> r : M = (strip s_begin-1's Schur term on interface j_begin)
-                            - sub S^{-1} super of r-1's last interface        (n2 x n2)
-  solve fwd  r-1 -> r : strip s_begin-1's reduce_rhs term - sub u             (n2 x nrhs)
-  solve bwd  r+1 -> r : u of interface j_end                                  (n2 x nrhs)
+  factorize  eliminate (local)  ;  r-1 -> r : M (n2 x n2)   the separator sweep
+  solve      solve_local (local);  r-1 -> r : q (n2 x nrhs) separator forward
+                                   r+1 -> r : u of the next separator (n2 x nrhs)
 
 Messages are device tensors moved with torch.distributed send/recv (NCCL over
-NVLink between processes), or plain device copies between logical shards of
-one process (``factorize_logical`` / ``solve_logical``), which is how the
-single-GPU tests exercise the engine's shard code.  Any backend with the
-``Shard`` method set can be driven by the same orchestration, which is how the
-CPU tests (gloo, world_size 2) check the protocol.
+NVLink between processes; gloo through host staging), or plain device copies
+between logical shards of one process (``factorize_logical`` /
+``solve_logical``), which is how the single-GPU tests exercise the engine's
+shard code.  Any backend with the ``Shard`` method set can be driven by the
+same orchestration, which is how the CPU tests (gloo) check the protocol.
 """
 import ctypes
 from dataclasses import dataclass
@@ -95,15 +96,26 @@ class Shard:
         """An n2 x cols column-major message buffer (torch shape (cols, n2))."""
         return self.torch.empty((cols, self.n2), dtype=self.torch.float64, device=self.device)
 
+    def eliminate(self):
+        """Local elimination of the interior chain and its separator spikes (no communication)."""
+        self._sync()
+        _check(lib().slablu_gpu_shard_eliminate(self._h))
+
     def sweep(self, m_in, m_out):
+        """Separator sweep step: M_in from rank - 1, M_out to rank + 1 (n2 x n2)."""
         self._sync()
         _check(lib().slablu_gpu_shard_sweep(self._h, _ptr(m_in), _ptr(m_out)))
 
-    def solve_forward(self, f, m_in, m_out):
-        """f: (nrhs, N) CUDA tensor (column-major N x nrhs)."""
+    def solve_local(self, f):
+        """f: (nrhs, N) CUDA tensor (column-major N x nrhs); local reduce + interior solve."""
         nrhs = f.shape[0] if f.dim() == 2 else 1
         self._sync()
-        _check(lib().slablu_gpu_shard_solve_forward(self._h, f.data_ptr(), self.N, nrhs, _ptr(m_in), _ptr(m_out)))
+        _check(lib().slablu_gpu_shard_solve_local(self._h, f.data_ptr(), self.N, nrhs))
+
+    def solve_forward(self, m_in, m_out):
+        """Separator forward step: q from rank - 1, q to rank + 1 (n2 x nrhs)."""
+        self._sync()
+        _check(lib().slablu_gpu_shard_solve_forward(self._h, _ptr(m_in), _ptr(m_out)))
 
     def solve_backward(self, m_in, m_out, u):
         """u: (nrhs, N) CUDA tensor; receives this shard's unknowns (others untouched)."""
@@ -135,29 +147,47 @@ class Shard:
 
 
 class TorchExchange:
-    """Neighbour messages over torch.distributed (NCCL for CUDA tensors, gloo for CPU)."""
+    """Neighbour messages over torch.distributed (NCCL for CUDA tensors, gloo for CPU).
 
-    def __init__(self, group=None):
+    staged=True moves CUDA messages through host memory (gloo between processes that share
+    one GPU, as the single-GPU multi-process tests do)."""
+
+    def __init__(self, group=None, staged=False):
         import torch.distributed as dist
-        self.dist, self.group = dist, group
+        self.dist, self.group, self.staged = dist, group, staged
         self.rank = dist.get_rank(group)
 
+    def _send(self, t, peer):
+        if self.staged and t.is_cuda:
+            t = t.cpu()
+        self.dist.send(t, peer, group=self.group)
+
+    def _recv(self, t, peer):
+        if self.staged and t.is_cuda:
+            h = t.new_empty(t.shape, device="cpu")
+            self.dist.recv(h, peer, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.recv(t, peer, group=self.group)
+
     def send_next(self, t):
-        self.dist.send(t, self.rank + 1, group=self.group)
+        self._send(t, self.rank + 1)
 
     def send_prev(self, t):
-        self.dist.send(t, self.rank - 1, group=self.group)
+        self._send(t, self.rank - 1)
 
     def recv_prev(self, t):
-        self.dist.recv(t, self.rank - 1, group=self.group)
+        self._recv(t, self.rank - 1)
 
     def recv_next(self, t):
-        self.dist.recv(t, self.rank + 1, group=self.group)
+        self._recv(t, self.rank + 1)
 
 
 def factorize_dist(shard, ex):
-    """Stage two of a sharded factorization across processes (call after stage one)."""
+    """Stage two of a sharded factorization across processes (call after stage one): local
+    elimination on every rank at once, then the separator sweep in rank order."""
     last = shard.rank == shard.nranks - 1
+    shard.eliminate()
     m_in = None
     if shard.rank > 0:
         m_in = shard.new_message(shard.n2)
@@ -172,12 +202,13 @@ def solve_dist(shard, f, u, ex):
     """u (nrhs, N), zero-initialised by the caller, receives this rank's unknowns."""
     nrhs = f.shape[0] if f.dim() == 2 else 1
     last = shard.rank == shard.nranks - 1
+    shard.solve_local(f)  # every rank at once
     m_in = None
     if shard.rank > 0:
         m_in = shard.new_message(nrhs)
         ex.recv_prev(m_in)
     m_out = None if last else shard.new_message(nrhs)
-    shard.solve_forward(f, m_in, m_out)
+    shard.solve_forward(m_in, m_out)
     if not last:
         ex.send_next(m_out)
     b_in = None
@@ -211,6 +242,8 @@ def solve_dist_refined(shard, f, ex, refine=1, group=None):
 
 def factorize_logical(shards):
     """Stage two for G shards held by one process (messages are device copies)."""
+    for sh in shards:
+        sh.eliminate()
     m = None
     for r, sh in enumerate(shards):
         out = sh.new_message(sh.n2) if r < len(shards) - 1 else None
@@ -232,10 +265,12 @@ def solve_logical_refined(shards, f, refine=1):
 def solve_logical(shards, f, u_parts):
     """Pipelined solve over logical shards; u_parts[r] (zeroed) receives shard r's unknowns."""
     nrhs = f.shape[0] if f.dim() == 2 else 1
+    for sh in shards:
+        sh.solve_local(f)
     m = None
     for r, sh in enumerate(shards):
         out = sh.new_message(nrhs) if r < len(shards) - 1 else None
-        sh.solve_forward(f, m, out)
+        sh.solve_forward(m, out)
         m = out
     m = None
     for r in range(len(shards) - 1, -1, -1):

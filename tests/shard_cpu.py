@@ -1,12 +1,14 @@
 """CPU (numpy) backend with the method set of paper_2211_07572_b200.distributed.Shard.
 
 Test infrastructure only: it restates, densely and for small grids, what the
-engine's shard entry points compute (engine.cu shard_sweep_impl /
-shard_solve_fwd_impl / shard_solve_bwd_impl) so that the multi-process
-orchestration (distributed.factorize_dist / solve_dist over gloo) can be
-checked on CPU against the oracle's unsharded solve.  Block definitions follow
-stage_one.hpp:284-297 (T blocks), :415-462 (reduce / recover) and
-stage_two.hpp:131-188 (sweep)."""
+engine's shard entry points compute (engine.cu shard_eliminate_impl /
+shard_sweep_impl / shard_solve_local_impl / shard_solve_fwd_impl /
+shard_solve_bwd_impl: partitioned elimination with the separator sweep) so that
+the multi-process orchestration (distributed.factorize_dist / solve_dist over
+gloo) can be checked on CPU against the oracle's unsharded solve.  The interior
+chain and its spikes are formed as dense matrices here (the engine sweeps them
+block by block).  Block definitions follow stage_one.hpp:284-297 (T blocks),
+:415-462 (reduce / recover) and stage_two.hpp:131-188 (sweep)."""
 import numpy as np
 import scipy.sparse as sp
 import torch
@@ -55,22 +57,55 @@ class CpuShard:
     def new_message(self, cols):
         return torch.zeros((cols, self.n2), dtype=torch.float64)
 
+    # ---- partitioned stage two ------------------------------------------------
+    def eliminate(self):
+        n2, j0, j1 = self.n2, self.j0, self.j1
+        self.has_left, self.has_right = self.rank > 0, self.rank < self.nranks - 1
+        self.ia, self.ib = (j0 + 1 if self.has_left else 0), j1
+        ia, ib = self.ia, self.ib
+        m = ib - ia
+        Z = np.zeros((n2, n2))
+        self.a = self.b = self.c = self.d = self.yl = Z
+        if m == 0:
+            if self.has_left and self.has_right:
+                self.b, self.c = -self.Tsup[j0], -self.Tsub[j0]
+            return
+        AI = np.zeros((m * n2, m * n2))
+        for k, j in enumerate(range(ia, ib)):
+            AI[k * n2:(k + 1) * n2, k * n2:(k + 1) * n2] = self.Tdiag[j]
+            if j + 1 < ib:
+                AI[k * n2:(k + 1) * n2, (k + 1) * n2:(k + 2) * n2] = self.Tsup[j]
+                AI[(k + 1) * n2:(k + 2) * n2, k * n2:(k + 1) * n2] = self.Tsub[j]
+        self.AI = AI
+        if self.has_left:
+            EL = np.zeros((m * n2, n2))
+            EL[:n2] = self.Tsub[j0]
+            YL = np.linalg.solve(AI, EL)
+            self.a = self.Tsup[j0] @ YL[:n2]
+            if self.has_right:
+                self.yl = YL[-n2:]
+                self.c = self.Tsub[ib - 1] @ self.yl
+        if self.has_right:
+            ER = np.zeros((m * n2, n2))
+            ER[-n2:] = self.Tsup[ib - 1]
+            YR = np.linalg.solve(AI, ER)
+            self.d = self.Tsub[ib - 1] @ YR[-n2:]
+            if self.has_left:
+                self.b = self.Tsup[j0] @ YR[:n2]
+
     def sweep(self, m_in, m_out):
         j0, j1 = self.j0, self.j1
-        for j in range(j0, j1):
-            Sj = self.Tdiag[j].copy()
-            if j == j0 and self.rank > 0:
-                Sj += m_in.numpy().T
-            if j > j0:
-                Sj -= self.Tsub[j - 1] @ self.Sinv[j - 1] @ self.Tsup[j - 1]
-            self.Sinv[j] = np.linalg.inv(Sj)
-        if self.rank < self.nranks - 1:
-            M = self.Tdiag[j1].copy()
-            if j1 > j0:
-                M -= self.Tsub[j1 - 1] @ self.Sinv[j1 - 1] @ self.Tsup[j1 - 1]
+        if self.has_left:
+            self.Shat = self.Tdiag[j0] - self.a + m_in.numpy().T
+            if self.has_right:
+                self.xhat = np.linalg.solve(self.Shat, self.b)
+        if self.has_right:
+            M = self.Tdiag[j1] - self.d
+            if self.has_left:
+                M = M - self.c @ self.xhat
             m_out.copy_(torch.from_numpy(np.ascontiguousarray(M.T)))
 
-    def solve_forward(self, f, m_in, m_out):
+    def solve_local(self, f):
         F = f.numpy().reshape(-1, self.N).T.copy()
         self.F = F
         red = {j: (F[self.iidx[j]].copy() if self.j0 <= j < self.j1 else np.zeros((self.n2, F.shape[1])))
@@ -80,26 +115,46 @@ class CpuShard:
             for j in (s - 1, s):
                 if 0 <= j < self.K:
                     red[j] -= self.A[np.ix_(self.iidx[j], self.sidx[s])] @ xs
-        if self.rank > 0:
-            red[self.j0] += m_in.numpy().T
-        u = {}
-        for j in range(self.j0, self.j1):
-            r = red[j] - (self.Tsub[j - 1] @ u[j - 1] if j > self.j0 else 0.0)
-            u[j] = self.Sinv[j] @ r
-        if self.rank < self.nranks - 1:
-            out = red[self.j1] - (self.Tsub[self.j1 - 1] @ u[self.j1 - 1] if self.j1 > self.j0 else 0.0)
-            m_out.copy_(torch.from_numpy(np.ascontiguousarray(out.T)))
-        self.u = u
+        self.red = red
+        ia, ib, n2 = self.ia, self.ib, self.n2
+        if ib > ia:
+            z = np.linalg.solve(self.AI, np.vstack([red[j] for j in range(ia, ib)]))
+            self.z = {j: z[(j - ia) * n2:(j - ia + 1) * n2] for j in range(ia, ib)}
+
+    def solve_forward(self, m_in, m_out):
+        j0, j1, ia, ib = self.j0, self.j1, self.ia, self.ib
+        interior = ib > ia
+        if self.has_left:
+            rhs = self.red[j0] + m_in.numpy().T
+            if interior:
+                rhs = rhs - self.Tsup[j0] @ self.z[ia]
+            self.v = np.linalg.solve(self.Shat, rhs)
+        if self.has_right:
+            q = self.red[j1].copy()
+            if interior:
+                t = self.z[ib - 1] - (self.yl @ self.v if self.has_left else 0.0)
+                q = q - self.Tsub[ib - 1] @ t
+            elif self.has_left:
+                q = q - self.Tsub[j0] @ self.v
+            m_out.copy_(torch.from_numpy(np.ascontiguousarray(q.T)))
 
     def solve_backward(self, m_in, m_out, u_t):
-        u = self.u
-        if self.rank < self.nranks - 1:
-            u[self.j1] = m_in.numpy().T.copy()
-        for j in range(self.j1 - 1, self.j0 - 1, -1):
-            if j + 1 < self.K:
-                u[j] = u[j] - self.Sinv[j] @ (self.Tsup[j] @ u[j + 1])
-        if self.rank > 0:
-            m_out.copy_(torch.from_numpy(np.ascontiguousarray(u[self.j0].T)))
+        j0, j1, ia, ib, n2 = self.j0, self.j1, self.ia, self.ib, self.n2
+        u = {}
+        if self.has_right:
+            u[j1] = m_in.numpy().T.copy()
+        if self.has_left:
+            u[j0] = self.v + (self.xhat @ u[j1] if self.has_right else 0.0)
+            m_out.copy_(torch.from_numpy(np.ascontiguousarray(u[j0].T)))
+        if ib > ia:
+            rhs = np.vstack([self.red[j] for j in range(ia, ib)])
+            if self.has_left:
+                rhs[:n2] -= self.Tsub[j0] @ u[j0]
+            if self.has_right:
+                rhs[-n2:] -= self.Tsup[ib - 1] @ u[j1]
+            uI = np.linalg.solve(self.AI, rhs)
+            for j in range(ia, ib):
+                u[j] = uI[(j - ia) * n2:(j - ia + 1) * n2]
         U = u_t.numpy().reshape(-1, self.N).T  # view (N x nrhs)
         for s in range(self.s0, self.s1):
             rhs = self.F[self.sidx[s]].copy()

@@ -1,7 +1,8 @@
-"""Multi-GPU host logic on CPU: shard ranges (Python == C ABI) and the pipelined
-factorize/solve protocol over torch.distributed gloo, world_size 2 and 3, with
-the numpy shard backend (tests/shard_cpu.py), checked against the oracle's
-unsharded solve."""
+"""Multi-GPU host logic on CPU: shard ranges (Python == C ABI) and the partitioned
+factorize/solve protocol (local elimination + separator sweep) over
+torch.distributed gloo, world_size 2 to 4, with the numpy shard backend
+(tests/shard_cpu.py), checked against the oracle's unsharded solve
+(SURVEY.md §8(e))."""
 import os
 import socket
 
@@ -67,8 +68,9 @@ def _worker(rank, world, port, n1, n2, b, kappa, nrhs, outdir):
 
 
 @pytest.mark.parametrize("world,n1,n2,b,kappa,nrhs", [(2, 40, 10, 3, 0.0, 1), (3, 40, 10, 3, 12.0, 2),
-                                                      (2, 39, 8, 4, 0.0, 1)])
-def test_pipelined_protocol_gloo(tmp_path, world, n1, n2, b, kappa, nrhs):
+                                                      (2, 39, 8, 4, 0.0, 1), (4, 40, 10, 3, 9.0, 1),
+                                                      (4, 31, 8, 6, 0.0, 2)])
+def test_partitioned_protocol_gloo(tmp_path, world, n1, n2, b, kappa, nrhs):
     here = os.path.dirname(os.path.abspath(__file__))
     os.environ["PYTHONPATH"] = here + os.pathsep + os.environ.get("PYTHONPATH", "")
     mp.spawn(_worker, args=(world, _free_port(), n1, n2, b, kappa, nrhs, str(tmp_path)), nprocs=world, join=True)
