@@ -48,11 +48,8 @@ constexpr int THREADS = CTHREADS + 64;  // + op producer warp + level producer w
 // DFMA variants need at most 6 row-tile warps (G >= 4 at Wp <= 160): 8 warps in all, so two warps
 // per SM sub-partition and the full 255-register budget (10 warps cap threads at 168 registers)
 constexpr int NCW_DFMA = 6;
-// NC <= 2: two warps per row tile (k halves), combined through shared memory and a pair barrier
 template <int NC>
-constexpr bool pair_of() { return NC == 1 || NC == 2; }
-template <int NC>
-constexpr int ncw_of() { return NC == 0 ? NCW : pair_of<NC>() ? 2 * NCW_DFMA : NCW_DFMA; }
+constexpr int ncw_of() { return NC == 0 ? NCW : NCW_DFMA; }
 template <int NC>
 constexpr int threads_of() { return ncw_of<NC>() * 32 + 64; }
 constexpr int STAGES = 4;               // op ring: half-level chunks
@@ -97,10 +94,7 @@ __host__ __device__ inline Lay2 lay2(int Wp, int G, int64_t n2) {
   L.xb = L.lv + LS * L.lv_slot;
   L.part = L.xb + 3LL * Wp * C * 8;
   // DMMA partial sums, or (DFMA, NC <= 2) one private t_top copy per row-tile warp
-  // DFMA pair variant: a half t_top per warp (12 warps x KMAX*4 rows x 2 columns) + per tile pair
-  // partial sums (6 tiles x (32 + 8) x 2)
-  const int64_t part_dmma = (int64_t)NCW * L.MNB * 32 * 16, part_dfma = (12LL * 80 * 2 + 6LL * 40 * 2) * 8;
-  L.flags = L.part + (part_dmma > part_dfma ? part_dmma : part_dfma);
+  L.flags = L.part + (int64_t)NCW * L.MNB * 32 * 16;  // DMMA partial sums
   L.bytes = L.flags + round_up(n2, 16) + 128;  // + alignment slack of the dynamic window
   return L;
 }
@@ -211,10 +205,9 @@ __device__ __forceinline__ void gemv_k(int KH, const double* Aw, int S, const do
   }
 }
 
-// DFMA consumer (see strip_solve2_kernel).  Single form (NC = 4): warp w < mn owns row tile w for
-// the whole k range.  Pair form (NC <= 2): warps w and w + mn share tile w, each taking one half of
-// the k range (the two half-level chunks); the upper warp hands its partial sums to the lower one
-// through shared memory and a pair barrier, which halves the GEMV chain of a level.
+// DFMA consumer (see strip_solve2_kernel): warp w < mn owns row tile w for the whole k range.
+// (Splitting a tile's k range over two warps combined through shared memory measured the same
+// time at cfg3 and was dropped.)
 template <int NC>
 __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, int rank, int m0, int mn, int w,
                                                      int lane, int Wp, int64_t n2, const Lay2& Ly,
@@ -222,20 +215,13 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
                                                      uint64_t* full_bar, uint64_t* empty_bar, uint64_t* lfull,
                                                      uint64_t* lempty, uint64_t* xbar, uint64_t* fwd_done,
                                                      double* ybase, int ncols, int q0, const StripDesc& sd) {
-  constexpr bool PAIR = pair_of<NC>();
   const int g = lane >> 2, t = lane & 3;
   const int KH = Ly.KH, MNB = Ly.MNB;
   const int WC = Wp * C;    // packed level-major layout of b / y / x in HBM and the level ring
   const int XW = Wp * NC;   // one exchange vector: [row][NC] (compact: row gathers stay bank-conflict-free)
-  const int tile = PAIR ? w % mn : w;  // row tile of this warp
-  const int h = PAIR ? w / mn : 0;     // pair form: k half (0 also owns the epilogue)
-  const bool lead = h == 0;
-  const int nact = PAIR ? 2 * mn : mn;  // active consumer warps
+  const int tile = w;                   // row tile of this warp
   const int row = (m0 + tile) * 8 + g;  // this lane's output row (all 4 t lanes hold the reduced sums)
   const uint32_t xbytes = (uint32_t)(Wp * NC * 8);
-  // pair form: half t_top per warp and the pair's partial sums
-  double* ttw_pair = reinterpret_cast<double*>(smraw + Ly.part) + w * (KMAX * 4 * NC);
-  double* pbuf = reinterpret_cast<double*>(smraw + Ly.part) + 12 * (KMAX * 4 * NC) + tile * (40 * NC);
   int slot = 0, ls = 0;
   uint32_t fph = 0, lph = 0, xq = 0;
   auto arm = [&]() {
@@ -268,7 +254,6 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
       lph ^= 1u;
     }
   };
-  auto pair_bar = [&]() { asm volatile("bar.sync %0, 64;\n" ::"r"(3 + tile) : "memory"); };
   // sum over the 4 t lanes of a row: every lane ends with the row's totals
   auto rowsum = [&](double (&acc)[NC]) {
 #pragma unroll
@@ -283,27 +268,6 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     for (int n = 1; n < NC; n++)
       if (t == n) r = v[n];
     return r;
-  };
-  // pair form: the upper warp's per-lane partial sums (and exceptional-row halves) join the lower's
-  // (exq: this lane's exceptional-row dot when its row is one, pbuf slot 32 NC + g NC per row)
-  auto pair_combine = [&](double (&acc)[NC], double (&exq)[NC], bool has_exq) {
-    if constexpr (PAIR) {
-      if (!lead) {
-#pragma unroll
-        for (int n = 0; n < NC; n++) pbuf[lane * NC + n] = acc[n];
-        if (has_exq)
-#pragma unroll
-          for (int n = 0; n < NC; n++) pbuf[32 * NC + g * NC + n] = exq[n];
-      }
-      pair_bar();
-      if (lead) {
-#pragma unroll
-        for (int n = 0; n < NC; n++) acc[n] += pbuf[lane * NC + n];
-        if (has_exq)
-#pragma unroll
-          for (int n = 0; n < NC; n++) exq[n] += pbuf[32 * NC + g * NC + n];
-      }
-    }
   };
 #ifdef SLB_SOLVE_PROF
   long long P0 = clock64(), ph[24] = {0};
@@ -332,16 +296,21 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
                      "d"(vv[0]), "r"(bar)
                      : "memory");
       } else {
+#ifdef SLB_NC2_SCALAR
+#pragma unroll
+        for (int n = 0; n < NC; n++)
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(dst + n * 8),
+                       "d"(vv[n]), "r"(bar)
+                       : "memory");
+#else
 #pragma unroll
         for (int n = 0; n < NC; n += 2) st_async_v2(dst + n * 8, vv[n], vv[n + 1], bar);
+#endif
       }
     }
   };
   // ---------------- forward ----------------
-  // t_top: pair form one private half per warp (k rows of its chunk, local index k - h KH 4),
-  // single form (NC = 4) one shared copy built by all active warps
-  double* ttsh = xbuf + 2 * XW;
-  const int kofs = PAIR ? h * KH * 4 : 0;
+  double* tt = xbuf + 2 * XW;  // t_top, one shared copy built by all active warps
   for (int64_t l = 0; l < n2; l++) {
     const bool hn = l + 1 < n2;
     const uint8_t fl = sfl[l];
@@ -362,31 +331,20 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     };
     // t_top = rows perm[0..Wp) of [z_l ; b_{l+1}], compact [k][NC].  Reuse is safe: the next
     // level rewrites it only after its exchange wait, which needs this level's pushes.
-    double* tt;
-    int kcnt;  // t_top rows this warp reads: [kofs, kofs + kcnt)
-    if constexpr (PAIR) {
-      tt = ttw_pair;
-      kcnt = min(KH * 4, Wp - kofs);
-      for (int idx = lane; idx < kcnt * NC; idx += 32) tt[idx] = val(sperm[kofs + idx / NC], idx % NC);
-      __syncwarp();
-    } else {
-      tt = ttsh;
-      kcnt = Wp;
-      for (int idx = w * 32 + lane; idx < Wp * NC; idx += mn * 32) ttsh[idx] = val(sperm[idx / NC], idx % NC);
-      asm volatile("bar.sync 2, %0;\n" ::"r"(mn * 32) : "memory");
-    }
+    for (int idx = w * 32 + lane; idx < Wp * NC; idx += mn * 32) tt[idx] = val(sperm[idx / NC], idx % NC);
+    asm volatile("bar.sync 2, %0;\n" ::"r"(mn * 32) : "memory");
     PN(2)
     // epilogue operands ahead of the GEMV: t_bot, diag(Lsub), and the exceptional rows of this
-    // tile (z = t_bot + Fbot[e, :] t_top needs t_top only; the pair form splits the dot over k)
+    // tile (z = t_bot + Fbot[e, :] t_top needs t_top only)
     double tb = 0.0, d = 0.0;
     double exq[NC];
     bool is_exc = false;
 #pragma unroll
     for (int n = 0; n < NC; n++) exq[n] = 0.0;
     if (hn) {
-      if (lead) tb = val(sperm[Wp + row], tc);
+      tb = val(sperm[Wp + row], tc);
       if (sc) {
-        if (lead) d = reinterpret_cast<const double*>(lv + Ly.o_dsub)[row];
+        d = reinterpret_cast<const double*>(lv + Ly.o_dsub)[row];
         const int ncx = (fl >> 2) & 15;
         const int* epos = reinterpret_cast<const int*>(lv + Ly.o_epos);
         const double* exc = reinterpret_cast<const double*>(lv + Ly.o_exc);
@@ -396,8 +354,8 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
           double q[NC];
 #pragma unroll
           for (int n = 0; n < NC; n++) q[n] = 0.0;
-          for (int k = lane; k < kcnt; k += 32) {
-            const double ev = exc[e * Wp + kofs + k];
+          for (int k = lane; k < Wp; k += 32) {
+            const double ev = exc[e * Wp + k];
 #pragma unroll
             for (int n = 0; n < NC; n++) q[n] = fma(ev, tt[k * NC + n], q[n]);
           }
@@ -417,11 +375,7 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     for (int n = 0; n < NC; n++) acc[0][n] = acc[1][n] = acc2[0][n] = acc2[1][n] = 0.0;
     const int nch = (sc || !hn) ? 2 : 4;
     for (int c = 0; c < nch; c++) {
-      if (PAIR && (c & 1) != h) {  // the other half's chunk
-        next_slot();
-        continue;
-      }
-      const double* tk = tt + ((c & 1) * KH * 4 - kofs + t) * NC;
+      const double* tk = tt + ((c & 1) * KH * 4 + t) * NC;
       const double* Aw = acquire_op() + tile * 32 + lane;
       PN(5)
       if (c < 2) gemv_k<NC, 4 * NC>(KH, Aw, MNB * 32, tk, acc[0], acc[1]);
@@ -434,13 +388,7 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
       acc[0][n] += acc[1][n];
       acc2[0][n] += acc2[1][n];
     }
-    pair_combine(acc[0], exq, is_exc);
-    if (hn && !sc) {  // full Fbot GEMV (rare): its partials take a second pair exchange
-      if constexpr (PAIR) pair_bar();  // the lead has read the first partials
-      double none[NC];
-      pair_combine(acc2[0], none, false);
-    }
-    if (lead) {
+    {
       rowsum(acc[0]);
       const double yv = pick(acc[0]);
       if (hn) {
@@ -464,7 +412,7 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
   if (lane == 0) mbar_arrive(fwd_done);
 
   // ---------------- backward ----------------
-  for (int idx = w * 32 + lane; idx < 3 * XW; idx += nact * 32) xbuf[idx] = 0.0;
+  for (int idx = w * 32 + lane; idx < 3 * XW; idx += mn * 32) xbuf[idx] = 0.0;
   asm volatile("barrier.cluster.arrive.release;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory");
   for (int64_t l = n2 - 1; l >= 0; l--) {
@@ -481,9 +429,9 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     mbar_wait(&lfull[ls], lph);
     PN(10)
     const unsigned char* lv = smraw + Ly.lv + (int64_t)ls * Ly.lv_slot;
-    // y_l and the x_{l+2} columns of H ahead of the GEMV (lead warp)
+    // y_l and the x_{l+2} columns of H ahead of the GEMV
     double xv = 0.0;
-    if (lead) {
+    {
       xv = reinterpret_cast<const double*>(lv + Ly.o_y)[(tile * 8 + g) * C + tc];
       if (nhc) {  // x_{l+2} half of H: the columns of the rows pivoted up
         const int* hidx = reinterpret_cast<const int*>(lv + Ly.o_hidx);
@@ -497,10 +445,6 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
     for (int n = 0; n < NC; n++) acc[0][n] = acc[1][n] = 0.0;
     const int nch = full ? 4 : 2;
     for (int c = 0; c < nch; c++) {
-      if (PAIR && (c & 1) != h) {
-        next_slot();
-        continue;
-      }
       const double* xs = (c < 2 ? x1 : x2) + ((c & 1) * KH * 4 + t) * NC;
       const double* Aw = acquire_op() + tile * 32 + lane;
       PN(11)
@@ -511,10 +455,6 @@ __device__ __forceinline__ void solve2_dfma_consumer(const SchurArgs& a, int G, 
 #pragma unroll
     for (int n = 0; n < NC; n++) acc[0][n] += acc[1][n];
     {
-      double none[NC];
-      pair_combine(acc[0], none, false);
-    }
-    if (lead) {
       rowsum(acc[0]);
       xv -= pick(acc[0]);
       push_row(b0, xv);
@@ -584,7 +524,7 @@ __global__ void __launch_bounds__(threads_of<NC>(), 1)
   // exchange bytes per vector: every CTA pushes its rows to every CTA (itself included)
   const uint32_t xbytes = (uint32_t)(Wp * (NC == 0 ? C : NC) * 8);
   // consumer warps that read the operator / level rings
-  const int ncw = NC == 0 ? NCW : pair_of<NC>() ? 2 * mn : mn;
+  const int ncw = NC == 0 ? NCW : mn;
 
   constexpr int NT = threads_of<NC>();
   constexpr int PW = ncw_of<NC>();  // first producer warp
