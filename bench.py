@@ -136,20 +136,33 @@ def problem(cfg):
     return spec, kappa
 
 
-def cpu_sample(cfg, threads, budget_s=20.0):
-    """Bounded CPU-baseline sample of the reference path (oracle port), extrapolated to T_factor."""
+_CPU_CACHE = {}
+
+
+def cpu_sample(cfg, threads):
+    """Bounded CPU-baseline sample of the reference path (oracle port), extrapolated to T_factor.
+    The system is assembled once per process and the dgbtrs sample size calibrated once, so a step
+    is one full-strip dgbtrf, one dgbtrs sample and one stage-two step (a few seconds)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     kind, n1, n2, b, ppw, _ = CONFIGS[cfg]
-    kappa = 0.0 if ppw is None else O.kappa_from_ppw(ppw, n2)
     O.set_blas_threads(threads)
-    sysm = O.assemble_canned(kind, n1, n2, kappa)
+    if cfg not in _CPU_CACHE:
+        kappa = 0.0 if ppw is None else O.kappa_from_ppw(ppw, n2)
+        _CPU_CACHE[cfg] = {"sys": O.assemble_canned(kind, n1, n2, kappa), "nrhs": None}
+    cache = _CPU_CACHE[cfg]
+    sysm = cache["sys"]
     widths, k = geometry(n1, n2, b)
     full = max(range(len(widths)), key=lambda s: widths[s] if 0 < s < k else -1)
-    nrhs = 8
-    t_trf, t_trs = O.time_slab_sample(sysm, b, full, nrhs)
-    while t_trs < 0.5 and nrhs < n2:  # grow the RHS sample to a measurable size
-        nrhs = min(n2, nrhs * 4)
+    if cache["nrhs"] is None:  # calibrate once: a dgbtrs sample of >= 0.5 s
+        nrhs = 8
+        t_trf, t_trs = O.time_slab_sample(sysm, b, full, nrhs)
+        while t_trs < 0.5 and nrhs < n2:
+            nrhs = min(n2, nrhs * 4)
+            t_trf, t_trs = O.time_slab_sample(sysm, b, full, nrhs)
+        cache["nrhs"] = nrhs
+    else:
+        nrhs = cache["nrhs"]
         t_trf, t_trs = O.time_slab_sample(sysm, b, full, nrhs)
     per_col = t_trs / nrhs
     w_full = widths[full]
@@ -180,12 +193,12 @@ def run_reference(args):
         r = cpu_sample(args.config, threads)
         if step >= args.warmup:
             vals.append(r["dof_s"])
-        if time.perf_counter() - t0 > 240:
+        if time.perf_counter() - t0 > 900:  # safety cap; a step is a few seconds (assembly cached)
             break
     v = float(np.median(vals)) if vals else r["dof_s"]
     line = {"metric": "factorization DOF/s (dense SlabLU, N=16M FD bump Helmholtz)" if args.config == "cfg3" else
             f"factorization DOF/s ({desc})", "value": v, "unit": "DOF/s", "n_gpus": args.gpus, "steps": len(vals),
-            "warmup": args.warmup, "ms_per_step": n1 * n2 / v * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": n1 * n2 / v * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic canned problem)",
             "config": {"workload": desc, "n1": n1, "n2": n2, "b": b, "N": n1 * n2}, "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "DOF/s", "cores": threads, "kind": "port", "sample": r["sample"]},
@@ -313,7 +326,7 @@ def run_ours(args):
         "metric": "factorization DOF/s (dense SlabLU, N=16M FD bump Helmholtz)" if args.config == "cfg3"
         else f"factorization DOF/s ({desc})",
         "value": world * N / T, "unit": "DOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": T * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": T * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (deterministic canned problem, inputs resident in HBM; factors > L2 so no flush needed)",
         "config": {"workload": desc, "n1": n1, "n2": n2, "b": b, "kappa": kappa, "N": N,
                    "parallelism": "single-gpu",
