@@ -1,6 +1,7 @@
 // Internal launcher declarations for the SlabLU B200 engine.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace slb {
@@ -131,6 +132,10 @@ struct SchurArgs {
   double* out;            // reduce: contrib[s][X][nrhs][n2]; recover: u (N x nrhs)
 };
 enum SweepMode { SWEEP_SCHUR = 0, SWEEP_REDUCE = 1, SWEEP_RECOVER = 2 };
+// 4-D TMA map {32 doubles, m tiles, k4 rows, level} over per-level operator blocks in DMMA fragment
+// order [k4][m8][lane] (solve2.cu): base = first tile, tile_stride tiles per k4 row, box_mt x box_k.
+CUtensorMap make_map(const double* base, int mt, int tile_stride, int k4rows, int64_t levels, int64_t lvl_doubles,
+                     int box_mt, int box_k);
 constexpr int kSweepChunk = 64;
 void sweep(cudaStream_t st, const SchurArgs& a, int nslots);
 // Solve-phase slab sweeps (8 RHS columns per task) on clusters of 4 CTAs (solve.cu);

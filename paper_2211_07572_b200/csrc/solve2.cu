@@ -957,6 +957,8 @@ __global__ void __launch_bounds__(256) strip_contrib_kernel(SchurArgs a) {
   }
 }
 
+}  // namespace
+
 // ---- tensor maps over the factor storage (driver API entry point resolved at run time) ----
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -993,7 +995,6 @@ CUtensorMap make_map(const double* base, int mt, int tile_stride, int k4rows, in
   return m;
 }
 
-}  // namespace
 
 bool strip_solve2_fits(int Wp, int64_t n2, int G) {
   const int MTH = Wp / 8;
