@@ -216,6 +216,307 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
       if (c < nb) A[(j + c) * lda + j + i] = r[c];
 }
 
+// Panel of nb <= PNB columns with the register row SHIFTED one column per step: at step k
+// a thread's r[c] holds column k + c of its row, so the pivot column is always r[0] and every
+// register index is static inside a rolled loop (no select trees, small code).  L entries are
+// stored as they are computed (coalesced across threads); a row retires as U when it becomes
+// row k.  The per-column exchange is data driven: every CTA pushes its candidate (|a|, row
+// index, row) and CTA 0 row k into every CTA of the cluster (itself included) with st.async,
+// counted on the receiver's mbarrier; two barriers and buffers alternate by column parity.  A
+// CTA pushes column k+1 only after its own column-k resolve and update (the CTA barrier of k+1
+// orders them), and a peer can push column k+2 into buffer k&1 only after it received column
+// k+1 from this CTA, so no cluster barrier per column is needed.  The panel's interchanges are
+// replayed at the end into a swap list (row pos[s] <- original row org[s]) for
+// panel_swaps_list_kernel.
+constexpr int PNW = PTHREADS / 32;
+__global__ void __launch_bounds__(PTHREADS) panel32_kernel(double* A, int64_t lda, int64_t n, int64_t j, int nb,
+                                                           int32_t* ipiv, DevStatus* status, int block_index,
+                                                           int32_t* swl) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int ncta = (int)cluster.num_blocks();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t m = n - j;
+  const int64_t i = (int64_t)rank * PTHREADS + tid;
+  const bool own = i < m;
+  __shared__ __align__(16) double s_row[2][16][PNB];  // candidate rows of all CTAs (pushed)
+  __shared__ __align__(16) double s_rec[2][16][2];    // {|a|, row index} of all CTAs (pushed)
+  __shared__ __align__(16) double s_krow[2][PNB];     // row k (pushed by CTA 0)
+  __shared__ __align__(16) double s_wrow[2][PNW][PNB];  // per-warp candidate rows (local staging)
+  __shared__ __align__(16) double s_kst[2][PNB];        // row k (local staging, CTA 0)
+  __shared__ double s_wv[2][PNW];
+  __shared__ int s_wi[2][PNW];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ int s_piv[PNB];
+  __shared__ int s_pos[2 * PNB], s_org[2 * PNB];
+  __shared__ double s_urow[PNB][PNB + 1];  // retired U rows (CTA 0), shifted: [k][c] = U(k, k + c)
+
+  double r[PNB];
+#pragma unroll
+  for (int c = 0; c < PNB; c++) r[c] = (own && c < nb) ? A[(j + c) * lda + j + i] : 0.0;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  cluster.sync();  // every CTA's barriers initialised before any push targets them
+  // warp w pushes to CTAs w and w + PNW
+  uint32_t rrow[2], rrec[2], rkrow[2], rbar[2];
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    const int d = warp + q * PNW < ncta ? warp + q * PNW : 0;
+    rrow[q] = dsmem_map(&s_row[0][rank][0], d);
+    rrec[q] = dsmem_map(&s_rec[0][rank][0], d);
+    rkrow[q] = dsmem_map(&s_krow[0][0], d);
+    rbar[q] = dsmem_map(&s_bar[0], d);
+  }
+  const uint32_t xbytes = (uint32_t)(ncta * (PNB * 8 + 16) + PNB * 8);
+#ifdef SLB_PANEL_PROF
+  long long P0 = clock64(), ph[5] = {0, 0, 0, 0, 0};
+#endif
+
+#pragma unroll 1
+  for (int k = 0; k < nb; k++) {
+    const int pb = k & 1;
+    const bool live = own && i >= k;  // rows above k have retired
+    if (tid == 0) mbar_arrive_expect_tx(&s_bar[pb], xbytes);
+    // (1) warp argmax (first max by row index); the warp winner stages its row
+    double v = live ? fabs(r[0]) : -1.0;
+    int vi = live ? (int)i : INT_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) better(v, vi, __shfl_xor_sync(0xffffffffu, v, o), __shfl_xor_sync(0xffffffffu, vi, o));
+    if (live && i == vi)
+#pragma unroll
+      for (int c = 0; c < PNB; c++) s_wrow[pb][warp][c] = r[c];
+    if (live && i == k)
+#pragma unroll
+      for (int c = 0; c < PNB; c++) s_kst[pb][c] = r[c];
+    if (lane == 0) {
+      s_wv[pb][warp] = v;
+      s_wi[pb][warp] = vi;
+    }
+    __syncthreads();
+    PP(0)
+    // (2) CTA winner (every warp, redundantly), then push to this warp's two destinations
+    int wb = lane < PNW ? lane : 0;
+    v = lane < PNW ? s_wv[pb][lane] : -1.0;
+    vi = lane < PNW ? s_wi[pb][lane] : INT_MAX;
+#pragma unroll
+    for (int o = PNW / 2; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
+      const int ob = __shfl_xor_sync(0xffffffffu, wb, o);
+      if (ov > v || (ov == v && oi < vi)) {
+        v = ov;
+        vi = oi;
+        wb = ob;
+      }
+    }
+    v = __shfl_sync(0xffffffffu, v, 0);
+    vi = __shfl_sync(0xffffffffu, vi, 0);
+    wb = __shfl_sync(0xffffffffu, wb, 0);
+    {
+      const uint32_t boff = (uint32_t)(pb * 8);
+      const uint32_t roff = (uint32_t)(pb * 16 * PNB * 8);
+      const uint32_t coff = (uint32_t)(pb * 16 * 2 * 8);
+      const uint32_t koff = (uint32_t)(pb * PNB * 8);
+      const bool lo = lane < 16;
+      const int e = 2 * (lane & 15);
+      const double a0 = lo ? s_wrow[pb][wb][e] : s_kst[pb][e];
+      const double a1 = lo ? s_wrow[pb][wb][e + 1] : s_kst[pb][e + 1];
+      const uint32_t dst = (lo ? roff : koff) + (uint32_t)(lane & 15) * 16;
+      const bool go = lo || rank == 0;
+#pragma unroll
+      for (int q = 0; q < 2; q++)
+        if (warp + q * PNW < ncta) {
+          if (go) st_async_v2((lo ? rrow[q] : rkrow[q]) + dst, a0, a1, rbar[q] + boff);
+          if (lane == 0) st_async_v2(rrec[q] + coff, v, (double)vi, rbar[q] + boff);
+        }
+    }
+    PP(1)
+    // (3) wait for every CTA's candidate and row k
+    mbar_wait(&s_bar[pb], (uint32_t)((k >> 1) & 1));
+    PP(2)
+    // (4) resolve the pivot from the local copies
+    double bv = -1.0;
+    int bi = INT_MAX, bc = 0;
+    if (lane < ncta) {
+      bv = s_rec[pb][lane][0];
+      bi = (int)s_rec[pb][lane][1];
+      bc = lane;
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {  // ncta <= 16
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+        bc = oc;
+      }
+    }
+    bv = __shfl_sync(0xffffffffu, bv, 0);
+    bi = __shfl_sync(0xffffffffu, bi, 0);
+    bc = __shfl_sync(0xffffffffu, bc, 0);
+    if (!(bv > 0.0)) {  // exactly singular column: no interchange
+      bi = k;
+      bc = 0;
+      if (tid == 0 && rank == 0) {
+        atomicOr(&status->flags, ERR_SINGULAR);
+        atomicMin(&status->singular_block, block_index);
+      }
+    }
+    if (tid == 0 && rank == 0) {
+      ipiv[j + k] = (int32_t)(j + bi);
+      s_piv[k] = bi;
+    }
+    const double* prow = (bi == k) ? s_krow[pb] : s_row[pb][bc];
+    if (live) {
+      if (i == k) {  // row k retires as the U row: the pivot row (shifted: r[c] = column k + c)
+#pragma unroll
+        for (int c = 0; c < PNB; c++) s_urow[k][c] = prow[c];
+      } else {
+        if (i == bi && bi != k)
+#pragma unroll
+          for (int c = 0; c < PNB; c++) r[c] = s_krow[pb][c];
+        // (5) scale, store L, rank-1 update shifted down one column
+        const double pv = prow[0];
+        const double l = r[0] * (pv != 0.0 ? 1.0 / pv : 0.0);
+        A[(j + k) * lda + j + i] = l;
+#pragma unroll
+        for (int c = 1; c < PNB; c++) r[c - 1] = fma(-l, prow[c], r[c]);
+        r[PNB - 1] = 0.0;
+      }
+    }
+    PP(3)
+  }
+#ifdef SLB_PANEL_PROF
+  if (tid == 0 && (rank == 0 || rank == ncta - 1) && j == 0)
+    printf("PANEL32 rank %d/%d m=%lld: argmax+stage %lld push %lld wait %lld resolve+update %lld (cycles)\n", rank, ncta,
+           (long long)m, ph[0], ph[1], ph[2], ph[3]);
+#endif
+  if (rank == 0) {  // U rows, coalesced: thread (c, k) for the upper triangle
+    __syncthreads();
+    for (int e = tid; e < PNB * PNB; e += PTHREADS) {
+      const int c = e / PNB, k = e % PNB;  // column c, row k <= c
+      if (c < nb && k <= c) A[(j + c) * lda + j + k] = s_urow[k][c - k];
+    }
+  }
+  // swap list: replay the interchanges over the affected rows (slots 0..31 = panel rows,
+  // 32.. = rows below the panel that took part)
+  if (rank == 0 && warp == 0) {
+    __syncwarp();
+    s_pos[lane] = lane;
+    s_org[lane] = lane;
+    int ns = 0;
+    for (int q = 0; q < nb; q++) {
+      const int p = s_piv[q];
+      int slot = p;
+      if (p >= nb) {
+        const unsigned hit = __ballot_sync(0xffffffffu, lane < ns && s_pos[PNB + lane] == p);
+        if (hit) {
+          slot = PNB + __ffs(hit) - 1;
+        } else {
+          slot = PNB + ns;
+          if (lane == 0) {
+            s_pos[slot] = p;
+            s_org[slot] = p;
+          }
+          ns++;
+        }
+      }
+      __syncwarp();
+      if (lane == 0 && slot != q) {
+        const int t = s_org[q];
+        s_org[q] = s_org[slot];
+        s_org[slot] = t;
+      }
+      __syncwarp();
+    }
+    const int cnt = PNB + ns;
+    if (lane == 0) swl[0] = cnt;
+    for (int s2 = lane; s2 < cnt; s2 += 32) {
+      swl[1 + s2] = (int32_t)(j + s_pos[s2]);
+      swl[1 + 2 * PNB + s2] = (int32_t)(j + s_org[s2]);
+    }
+  }
+  cluster.sync();  // no CTA leaves while a peer may still push into it
+}
+
+// The panel's interchanges applied to every column outside it from the swap list: one warp
+// per column, every affected row loaded first, then stored (no dependent swap chain).
+constexpr int SWL = 1 + 4 * PNB;  // swap-list ints per panel
+// Interchanges ipiv[j + q0 + 1 .. j + nb) applied to one column (rows relative to j): one warp
+// replays them over the affected rows (ballot search of the side list), then moves the values.
+__device__ void panel_column_swaps(double* col, int64_t j, int nb, int q0, const int32_t* ipiv, int lane) {
+  int pos0 = lane, org0 = lane;  // slot `lane`: panel row `lane`
+  int pos1 = -1, org1 = -1;      // side slot `lane`: a row below the panel
+  int ns = 0;
+  for (int q = q0 + 1; q < nb; q++) {
+    const int p = (int)(ipiv[j + q] - j);
+    if (p == q) continue;
+    // slot of row p: panel row p, or the side slot holding it (appended if new)
+    int side = -1;
+    if (p >= nb) {
+      const unsigned hit = __ballot_sync(0xffffffffu, lane < ns && pos1 == p);
+      if (hit) {
+        side = __ffs(hit) - 1;
+      } else {
+        side = ns;
+        if (lane == ns) {
+          pos1 = p;
+          org1 = p;
+        }
+        ns++;
+      }
+    }
+    // swap the contents (org) of slot q and the slot of p
+    const int oq = __shfl_sync(0xffffffffu, org0, q);
+    const int op = side < 0 ? __shfl_sync(0xffffffffu, org0, p) : __shfl_sync(0xffffffffu, org1, side);
+    if (lane == q) org0 = op;
+    if (side < 0 && lane == p) org0 = oq;
+    if (side >= 0 && lane == side) org1 = oq;
+  }
+  const bool a0 = lane < nb && pos0 != org0;
+  const bool a1 = lane < ns && pos1 != org1;
+  const double v0 = a0 ? col[j + org0] : 0.0;
+  const double v1 = a1 ? col[j + org1] : 0.0;
+  __syncwarp();
+  if (a0) col[j + pos0] = v0;
+  if (a1) col[j + pos1] = v1;
+}
+
+__global__ void __launch_bounds__(256) panel_swaps_list_kernel(double* A, int64_t lda, int64_t n, int64_t j, int nb,
+                                                              const int32_t* swl, const int32_t* ipiv) {
+  __shared__ int s_cnt;
+  __shared__ int s_pos[2 * PNB], s_org[2 * PNB];
+  if (threadIdx.x == 0) s_cnt = swl[0];
+  if (threadIdx.x < 2 * PNB) {
+    s_pos[threadIdx.x] = swl[1 + threadIdx.x];
+    s_org[threadIdx.x] = swl[1 + 2 * PNB + threadIdx.x];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (c >= n) return;
+  if (c >= n - nb) {  // the panel's own column q: its L entries take the interchanges of steps > q
+    const int q0 = (int)(c - (n - nb));
+    panel_column_swaps(A + (j + q0) * lda, j, nb, q0, ipiv, lane);
+    return;
+  }
+  if (c >= j) c += nb;
+  double* col = A + c * lda;
+  const int cnt = s_cnt;
+  const bool a0 = lane < cnt && s_pos[lane] != s_org[lane];
+  const bool a1 = lane + 32 < cnt && s_pos[lane + 32] != s_org[lane + 32];
+  const double v0 = a0 ? col[s_org[lane]] : 0.0;
+  const double v1 = a1 ? col[s_org[lane + 32]] : 0.0;
+  __syncwarp();
+  if (a0) col[s_pos[lane]] = v0;
+  if (a1) col[s_pos[lane + 32]] = v1;
+}
+
 // Row interchanges ipiv[k1..k2) (LAPACK order) as one permutation of rows
 // [k1, n): idx[r - k1] = source row of row r.  One CTA, swaps replayed in
 // shared memory by one thread (n - k1 <= 8192).
@@ -321,6 +622,40 @@ void panel(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t j, int nb
   SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, A, lda, n, j, nb, ipiv, status, block_index)); count_launch();
 }
 
+bool panel_v1() {
+  static const bool v1 = [] {
+    const char* e = getenv("SLB_PANEL_V1");
+    return e && e[0] == '1';
+  }();
+  return v1;
+}
+
+void panel32(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t j, int nb, int32_t* ipiv,
+             DevStatus* status, int block_index, int32_t* swl) {
+  const int64_t m = n - j;
+  const int ncta = (int)cdiv(m, PTHREADS);
+  if (ncta > 16)
+    throw CudaFailure(cudaErrorInvalidValue, "dgetrf: block dimension > 4096 unsupported", __FILE__, __LINE__);
+  static bool attr = false;
+  if (!attr) {
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(panel32_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncta);
+  cfg.blockDim = dim3(PTHREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = ncta;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel32_kernel, A, lda, n, j, nb, ipiv, status, block_index, swl));
+  count_launch();
+}
+
 // Scratch for laswp (grown on demand, per device; stage two is stream ordered).
 struct SwapScratch {
   int32_t* idx = nullptr;
@@ -388,9 +723,17 @@ void trsm(cudaStream_t st, bool lower, const double* L, int64_t ldl, int64_t m, 
 
 // Recursive LU of columns [c0, c1) (rows c0..n) of the n x n matrix A.
 void getrf_rec(cudaStream_t st, double* A, int64_t n, int64_t c0, int64_t c1, int32_t* ipiv,
-               DevStatus* status, int block_index) {
+               DevStatus* status, int block_index, int32_t* swl) {
   const int64_t w = c1 - c0;
   if (w <= PNB) {
+    if (swl && !panel_v1()) {
+      panel32(st, A, n, n, c0, (int)w, ipiv, status, block_index, swl);
+      // interchanges on every other column now (so the recursion needs no laswp) and the later
+      // steps' interchanges on the panel's own L columns
+      panel_swaps_list_kernel<<<(unsigned)cdiv(n, 8), 256, 0, st>>>(A, n, n, c0, (int)w, swl, ipiv); count_launch();
+      SLB_CUDA_CHECK(cudaGetLastError());
+      return;
+    }
     panel(st, A, n, n, c0, (int)w, ipiv, status, block_index);
     if (n - w > 0) {  // interchanges on every other column now, so the recursion needs no laswp
       panel_swaps_kernel<<<(unsigned)cdiv(n - w, 128), 128, 0, st>>>(A, n, n, c0, (int)w, ipiv); count_launch();
@@ -400,18 +743,21 @@ void getrf_rec(cudaStream_t st, double* A, int64_t n, int64_t c0, int64_t c1, in
   }
   int64_t h = round_up(w / 2, PNB);
   if (h >= w) h = w - PNB;
-  getrf_rec(st, A, n, c0, c0 + h, ipiv, status, block_index);
+  getrf_rec(st, A, n, c0, c0 + h, ipiv, status, block_index, swl);
   trsm(st, true, A + c0 * n + c0, n, h, A + (c0 + h) * n + c0, n, w - h);
   dgemm_batched(st, n - c0 - h, w - h, h, -1.0, A + c0 * n + c0 + h, n, 0, A + (c0 + h) * n + c0, n, 0, 1.0,
                 A + (c0 + h) * n + c0 + h, n, 0, 1);
-  getrf_rec(st, A, n, c0 + h, c1, ipiv, status, block_index);
+  getrf_rec(st, A, n, c0 + h, c1, ipiv, status, block_index, swl);
 }
 
 }  // namespace
 
 void dgetrf(cudaStream_t st, int64_t n, double* a, int32_t* ipiv, double* /*work*/, DevStatus* status,
             int block_index) {
-  getrf_rec(st, a, n, 0, n, ipiv, status, block_index);
+  int32_t* swl = nullptr;  // swap list of the current panel (stream ordered, reused by every panel)
+  SLB_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&swl), SWL * sizeof(int32_t), st));
+  getrf_rec(st, a, n, 0, n, ipiv, status, block_index, swl);
+  SLB_CUDA_CHECK(cudaFreeAsync(swl, st));
 }
 
 void dgetrs(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const int32_t* ipiv, double* b,
