@@ -50,11 +50,19 @@ class SingularMatrixError : public Error {
   std::ptrdiff_t index;
 };
 
+class CompressionError : public Error {
+ public:
+  CompressionError(const std::string& what, double residual_estimate)
+      : Error(what), residual_estimate(residual_estimate) {}
+  double residual_estimate;
+};
+
 namespace detail {
 inline void check(const slablu_gpu_status& s) {
   if (s.code == SLABLU_OK) return;
   const std::string msg(s.msg);
   if (s.code == SLABLU_ERR_CONFIG) throw ConfigError(msg);
+  if (s.code == SLABLU_ERR_COMPRESSION) throw CompressionError(msg, s.residual);
   if (s.code == SLABLU_ERR_SINGULAR) throw SingularMatrixError(msg, static_cast<std::ptrdiff_t>(s.index));
   throw Error(msg);
 }
@@ -169,6 +177,9 @@ struct SolverConfig {
     g.device = device;
     g.keep_T = keep_T ? 1 : 0;
     g.refine = refine;
+    g.hbs_tol = hbs_tol;
+    g.hbs_trunc_rel = hbs_trunc_rel;
+    g.hbs_leaf_size = hbs_leaf_size;
     return g;
   }
 };
@@ -246,8 +257,9 @@ inline Factorization factorize(const SparseSystem& system, SolverConfig config) 
   f.n2 = system.n2;
   f.b = f.stats_.b;
   config.b = f.b;
-  config.compression = CompressionChoice::dense;
+  config.compression = f.stats_.compression == 2 ? CompressionChoice::hbs : CompressionChoice::dense;
   f.config = config;
+  f.hbs_max_rank = f.stats_.hbs_max_rank;
   f.t_stage1 = f.stats_.t_stage1;
   f.t_stage2 = f.stats_.t_stage2;
   f.storage_stage1 = static_cast<std::size_t>(f.stats_.storage_stage1);

@@ -56,12 +56,13 @@ enum {
   SLABLU_ERR_SINGULAR = 3,    /* SingularMatrixError; index = strip or block */
   SLABLU_ERR_CUDA = 4,        /* CUDA runtime failure or no device */
   SLABLU_ERR_OOM = 5,         /* device memory exhausted */
-  SLABLU_ERR_UNSUPPORTED = 6  /* valid input outside the engine's envelope */
+  SLABLU_ERR_UNSUPPORTED = 6, /* valid input outside the engine's envelope */
+  SLABLU_ERR_COMPRESSION = 7  /* CompressionError (common.hpp:55-60); residual estimate in .residual */
 };
 
-/* SolverConfig (driver.hpp:41-50). compression: 0 automatic, 1 dense, 2 hbs.
- * The engine implements the dense path; automatic resolves to dense and hbs
- * is rejected with SLABLU_ERR_UNSUPPORTED. */
+/* SolverConfig (driver.hpp:41-50). compression: 0 automatic, 1 dense, 2 hbs; automatic
+ * resolves to hbs when n2 >= 512 and b >= 16, else dense (driver.hpp:125-130).  The hbs_*
+ * fields follow the reference's defaults when left 0 (1e-11, 1e-13, 64). */
 typedef struct {
   int64_t b;          /* explicit slab width; 0 derives it from c */
   double c;           /* b ~ c * n2^(2/3), c in (0, 2] */
@@ -71,12 +72,16 @@ typedef struct {
   int device;         /* CUDA device ordinal */
   int keep_T;         /* keep a copy of the reduced blocks for slablu_gpu_T_block */
   int refine;         /* iterative-refinement steps per solve (residual with the original CSR) */
+  double hbs_tol;         /* per-block compression tolerance (0: 1e-11) */
+  double hbs_trunc_rel;   /* generator truncation floor (0: 1e-13) */
+  int64_t hbs_leaf_size;  /* cluster-tree leaf size (0: 64) */
 } slablu_gpu_config;
 
 typedef struct {
   int code;
   int64_t index;
   char msg[256];
+  double residual;    /* SLABLU_ERR_COMPRESSION: the probe's residual estimate */
 } slablu_gpu_status;
 
 typedef struct {
@@ -98,6 +103,9 @@ typedef struct {
   double t_assemble;      /* stage one: T assembly + validation (s) */
   double t_solve_last;    /* device time of the last solve (s) */
   double t_solve_strips;  /* ... of which the two slab sweeps (reduce + recover) */
+  int compression;        /* resolved: 1 dense, 2 hbs */
+  int64_t hbs_max_rank;   /* Factorization::hbs_max_rank (driver.hpp:84) */
+  double t_hbs;           /* stage one: HBS compression of the reduced blocks (s) */
 } slablu_gpu_stats_t;
 
 typedef struct slablu_gpu_fact slablu_gpu_fact;
@@ -150,6 +158,21 @@ slablu_gpu_status slablu_gpu_partition(int64_t n1, int64_t n2, int64_t b, int64_
                                        int64_t* interfaces, int64_t cap);
 
 /* ---- factorize / solve ------------------------------------------------------ */
+/* Randomized HBS compression of one dense n x n operator (host buffers, column major), the
+ * reference's hbs_compress (adaptive = 0, rank bound r_max) / hbs_compress_adaptive
+ * (adaptive = 1, ranks r_start doubling to r_max) with the dense sampler of test_hbs.cpp:64-68
+ * (hbs_compress.hpp:186-311).  out = the dense materialization of the compressed operator
+ * (HbsMatrix::to_dense, hbs.hpp:150-154).  CompressionError -> SLABLU_ERR_COMPRESSION. */
+typedef struct {
+  int64_t products_normal, products_adjoint;
+  int rounds;
+  int64_t final_rank;
+  double residual_estimate;
+} slablu_gpu_hbs_stats;
+slablu_gpu_status slablu_gpu_hbs_compress(int64_t n, const double* m, int64_t leaf_size, int64_t r_start,
+                                          int64_t r_max, int adaptive, double tol, double trunc_rel,
+                                          uint64_t seed, int device, double* out, slablu_gpu_hbs_stats* stats);
+
 /* Host CSR. */
 slablu_gpu_status slablu_gpu_factorize(int64_t n1, int64_t n2, const int32_t* row_ptr,
                                        const int32_t* col_idx, const double* val,

@@ -5,10 +5,10 @@ solve); compute runs in hand-written sm_100a kernels behind the C ABI in
 include/slablu_gpu.h (libslablu_gpu.so, built in-tree).
 """
 from .slablu import (  # noqa: F401
-    BlockTridiagonal, CompressionChoice, ConfigError, Error, ErrorReport, Factorization, GridStrip, ProblemSpec,
+    BlockTridiagonal, CompressionChoice, CompressionError, CompressOptions, CompressStats, ConfigError, Error, ErrorReport, Factorization, GridStrip, ProblemSpec,
     SingularMatrixError, SlabPartition, SweepFactorization, sweep_build, load, import_sweep, SolverConfig, SparseSystem, UnsupportedError, assemble_fd5,
     assemble_canned_device, bessel_j0, choose_b, device_count, error_report, error_report_device, factorize, factorize_device, gaussian_matrix,
-    helmholtz_bump_problem, helmholtz_problem, kappa_from_ppw, partition, poisson_log_problem,
+    hbs_compress, hbs_compress_adaptive, helmholtz_bump_problem, helmholtz_problem, kappa_from_ppw, partition, poisson_log_problem,
     run_problem, sample_field, sample_solution, sample_solution_device, solve, solve_device, true_solution_helmholtz,
     true_solution_poisson,
 )

@@ -17,12 +17,13 @@ I = ctypes.c_int
 
 
 class Status(ctypes.Structure):
-    _fields_ = [("code", I), ("index", I64), ("msg", ctypes.c_char * 256)]
+    _fields_ = [("code", I), ("index", I64), ("msg", ctypes.c_char * 256), ("residual", D)]
 
 
 class Config(ctypes.Structure):
     _fields_ = [("b", I64), ("c", D), ("compression", I), ("seed", ctypes.c_uint64),
-                ("threads", I), ("device", I), ("keep_T", I), ("refine", I)]
+                ("threads", I), ("device", I), ("keep_T", I), ("refine", I),
+                ("hbs_tol", D), ("hbs_trunc_rel", D), ("hbs_leaf_size", I64)]
 
 
 class Stats(ctypes.Structure):
@@ -31,7 +32,12 @@ class Stats(ctypes.Structure):
                 ("t_stage1", D), ("t_stage2", D), ("storage_stage1", I64), ("storage_stage2", I64),
                 ("device_bytes", I64), ("gpu_launches", I64), ("solve_launches", I64),
                 ("t_chain", D), ("t_schur", D), ("t_assemble", D), ("t_solve_last", D),
-                ("t_solve_strips", D)]
+                ("t_solve_strips", D), ("compression", I), ("hbs_max_rank", I64), ("t_hbs", D)]
+
+
+class HbsStatsT(ctypes.Structure):
+    _fields_ = [("products_normal", I64), ("products_adjoint", I64), ("rounds", I),
+                ("final_rank", I64), ("residual_estimate", D)]
 
 
 class ShardT(ctypes.Structure):
@@ -55,6 +61,7 @@ EXPORTS = [
     "slablu_gpu_sweep_build", "slablu_gpu_set_refine", "slablu_gpu_assemble_canned_device",
     "slablu_gpu_sample_solution_device", "slablu_gpu_error_report", "slablu_gpu_error_report_device",
     "slablu_gpu_save", "slablu_gpu_load", "slablu_gpu_export_sweep", "slablu_gpu_import_sweep",
+    "slablu_gpu_hbs_compress",
 ]
 
 _lib = None
@@ -120,6 +127,8 @@ def lib():
     L.slablu_gpu_sweep_solve.argtypes = [P, P, I64, P]
     L.slablu_gpu_recover.restype = St
     L.slablu_gpu_recover.argtypes = [P, P, P, I64, P]
+    L.slablu_gpu_hbs_compress.restype = St
+    L.slablu_gpu_hbs_compress.argtypes = [I64, P, I64, I64, I64, I, D, D, ctypes.c_uint64, I, P, P]
     L.slablu_gpu_sweep_build.restype = St
     L.slablu_gpu_sweep_build.argtypes = [I64, I64, P, I, P]
     L.slablu_gpu_set_refine.restype = St

@@ -389,7 +389,9 @@ struct slablu_gpu_fact {
   DBuf<double> a_v;
   int refine = 0;
   int64_t sF = 0, sP = 0, sCPL = 0;
-  double t1 = 0, t2 = 0, t_chain = 0, t_schur = 0, t_asm = 0;
+  double t1 = 0, t2 = 0, t_chain = 0, t_schur = 0, t_asm = 0, t_hbs = 0;
+  int compression = 1;       // resolved: 1 dense, 2 hbs (driver.hpp:125-130)
+  int64_t hbs_max_rank = 0;
   mutable double t_solve = 0, t_solve_strips = 0;
   int64_t storage1 = 0, storage2 = 0;
   int64_t launches_factor = 0;
@@ -480,6 +482,68 @@ void stage_two_build(slablu_gpu_fact* F) {
   stage_two_range(F, 0, F->K);
 }
 
+// build_reduced in hbs mode (stage_one.hpp:357-411): every reduced block compressed with the
+// adaptive randomized HBS scheme and densified in place, seeds mix_seed(seed, ordinal) with the
+// reference's ordinals (diag j: 3j, super j: 3j+1, sub j: 3j+2), leaf and rank range derived
+// as stage_one.hpp:364-370.
+void hbs_reduce(slablu_gpu_fact* F, const slablu_gpu_config& c) {
+  const int64_t n2 = F->n2, K = F->K, bs = n2 * n2;
+  HbsOptions o;
+  o.tol = c.hbs_tol > 0 ? c.hbs_tol : 1e-11;
+  o.trunc_rel = c.hbs_trunc_rel > 0 ? c.hbs_trunc_rel : 1e-13;
+  const int64_t leaf_cfg = c.hbs_leaf_size > 0 ? c.hbs_leaf_size : 64;
+  const int64_t leaf = std::min(leaf_cfg, n2);
+  int64_t r_start = std::max<int64_t>(2, (leaf - 10 + 1) / 2);
+  int64_t r_max = std::max<int64_t>(2 * F->b + 8, r_start);
+  r_max = std::min(r_max, n2);
+  r_start = std::min(r_start, r_max);
+  o.leaf = (int)leaf;
+  o.r_start = r_start;
+  o.r_max = r_max;
+  std::vector<double*> blocks;
+  std::vector<uint64_t> seeds;
+  std::vector<std::pair<int64_t, int64_t>> jk;
+  for (int64_t j = 0; j < K; j++) {
+    blocks.push_back(F->Tdiag() + j * bs);
+    seeds.push_back(mix_seed(c.seed, 3 * j));
+    jk.push_back({j, j});
+  }
+  for (int64_t j = 0; j + 1 < K; j++) {
+    blocks.push_back(F->Tsup() + j * bs);
+    seeds.push_back(mix_seed(c.seed, 3 * j + 1));
+    jk.push_back({j, j + 1});
+    blocks.push_back(F->Tsub() + j * bs);
+    seeds.push_back(mix_seed(c.seed, 3 * j + 2));
+    jk.push_back({j + 1, j});
+  }
+  std::vector<HbsStats> stats(blocks.size());
+  cudaEvent_t h0, h1;
+  SLB_CUDA_CHECK(cudaEventCreate(&h0));
+  SLB_CUDA_CHECK(cudaEventCreate(&h1));
+  SLB_CUDA_CHECK(cudaEventRecord(h0, F->stream));
+  try {
+    hbs_compress_blocks(F->stream, n2, (int)blocks.size(), blocks.data(), seeds.data(), o, stats.data());
+  } catch (const HostError& e) {
+    cudaEventDestroy(h0);
+    cudaEventDestroy(h1);
+    if (e.code != SLABLU_ERR_COMPRESSION || e.index < 0) throw;
+    const auto& p = jk[(size_t)e.index];
+    HostError w(e.code, "build_reduced: block (" + std::to_string(p.first) + ", " + std::to_string(p.second) +
+                            "): " + e.what(), -1);
+    w.residual = e.residual;
+    throw w;
+  }
+  SLB_CUDA_CHECK(cudaEventRecord(h1, F->stream));
+  SLB_CUDA_CHECK(cudaEventSynchronize(h1));
+  float ms = 0;
+  SLB_CUDA_CHECK(cudaEventElapsedTime(&ms, h0, h1));
+  F->t_hbs = ms * 1e-3;
+  cudaEventDestroy(h0);
+  cudaEventDestroy(h1);
+  F->hbs_max_rank = 0;
+  for (const HbsStats& st : stats) F->hbs_max_rank = std::max(F->hbs_max_rank, st.final_rank);
+}
+
 slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32_t* rp, const int32_t* ci,
                                 const double* v, const slablu_gpu_config* cfg, int rank = 0, int nranks = 1,
                                 bool sharded = false) {
@@ -487,8 +551,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   slablu_gpu_config c{};
   c.c = 0.6;
   if (cfg) c = *cfg;
-  if (c.compression == 2)
-    throw HostError(SLABLU_ERR_UNSUPPORTED, "factorize: hbs compression is not implemented by the GPU engine");
+  if (c.compression < 0 || c.compression > 2) throw HostError(SLABLU_ERR_CONFIG, "factorize: unknown compression choice");
   const int64_t launches0 = slb::g_kernel_count.load();
   auto F = std::make_unique<slablu_gpu_fact>();
   F->device = c.device;
@@ -507,6 +570,11 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   F->N = n1 * n2;
   F->b = c.b > 0 ? c.b : choose_b(n1, n2, 0, c.c);
   const int dev = c.device;
+  // driver.hpp:125-130: automatic compresses once the interfaces are long enough
+  const bool use_hbs = c.compression == 2 || (c.compression == 0 && n2 >= 512 && F->b >= 16 && !sharded);
+  if (use_hbs && sharded)
+    throw HostError(SLABLU_ERR_UNSUPPORTED, "shard: hbs compression needs whole reduced blocks (use dense)");
+  F->compression = use_hbs ? 2 : 1;
 
   // geometry (driver.hpp:134-139: degenerate whole-grid path)
   std::vector<GridStrip> ints;
@@ -840,6 +908,7 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
     assemble_T(st, n2, K, S, F->strips.p, F->sym.p, gbuf.p, sG, F->Tdiag(), F->Tsup(), F->Tsub(), A,
                F->ifc_off.p, F->status.p, tr);
     check_finite(st, F->T.p, (int64_t)(3 * K - 2) * n2 * n2, F->status.p);
+    if (F->compression == 2 && K > 0) hbs_reduce(F.get(), c);
     if (c.keep_T) {
       F->Tkeep.alloc(dev, F->T.n);
       SLB_CUDA_CHECK(cudaMemcpyAsync(F->Tkeep.p, F->T.p, F->T.bytes(), cudaMemcpyDeviceToDevice, st));
@@ -1458,7 +1527,7 @@ void solve_impl(const slablu_gpu_fact* F, const double* d_f, int64_t ldf, int64_
   check_solve_status(F);
 }
 
-slablu_gpu_status status_from(const HostError& e) { return make_status(e.code, e.what(), e.index); }
+slablu_gpu_status status_from(const HostError& e) { return make_status(e.code, e.what(), e.index, e.residual); }
 slablu_gpu_status status_from(const CudaFailure& e) {
   const int code = e.err == cudaErrorMemoryAllocation ? SLABLU_ERR_OOM : SLABLU_ERR_CUDA;
   return make_status(code, std::string("CUDA error: ") + cudaGetErrorString(e.err) + " at " + e.file + ":" +
@@ -1667,6 +1736,9 @@ slablu_gpu_status slablu_gpu_stats(const slablu_gpu_fact* F, slablu_gpu_stats_t*
     o->t_chain = F->t_chain;
     o->t_schur = F->t_schur;
     o->t_assemble = F->t_asm;
+    o->compression = F->compression;
+    o->hbs_max_rank = F->hbs_max_rank;
+    o->t_hbs = F->t_hbs;
     o->t_solve_last = F->t_solve;
     o->t_solve_strips = F->t_solve_strips;
   })
@@ -1739,6 +1811,58 @@ slablu_gpu_status slablu_gpu_sweep_solve(const slablu_gpu_fact* F, const double*
 
 // sweep_build (stage_two.hpp:131-150, validate :41-56) on a caller-supplied block-tridiagonal
 // system: blocks = [diag 0..k-1 | super 0..k-2 | sub 0..k-2], each m x m column major (host).
+slablu_gpu_status slablu_gpu_hbs_compress(int64_t n, const double* m, int64_t leaf_size, int64_t r_start,
+                                          int64_t r_max, int adaptive, double tol, double trunc_rel,
+                                          uint64_t seed, int device, double* out, slablu_gpu_hbs_stats* stats) {
+  ABI_TRY({
+    require_device();
+    if (n < 1 || !m || !out) throw HostError(SLABLU_ERR_CONFIG, "hbs_compress: empty operator");
+    if (leaf_size < 1 || leaf_size > n) throw HostError(SLABLU_ERR_CONFIG, "ClusterTree: need 1 <= leaf_size <= n");
+    DeviceGuard dg(device);
+    cudaStream_t st;
+    SLB_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    StreamScope scope(st);
+    HbsOptions o;
+    o.tol = tol;
+    o.trunc_rel = trunc_rel;
+    o.leaf = (int)leaf_size;
+    o.r_start = r_start;
+    o.r_max = r_max;
+    o.fixed_rank = adaptive == 0;
+    HbsStats hs;
+    double* d = nullptr;
+    try {
+      SLB_CUDA_CHECK(cudaMalloc(&d, (size_t)n * n * sizeof(double)));
+      SLB_CUDA_CHECK(cudaMemcpyAsync(d, m, (size_t)n * n * sizeof(double), cudaMemcpyHostToDevice, st));
+      hbs_compress_blocks(st, n, 1, &d, &seed, o, &hs);
+      SLB_CUDA_CHECK(cudaMemcpyAsync(out, d, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+    } catch (const HostError& e) {
+      if (stats) {
+        stats->residual_estimate = e.residual;
+      }
+      cudaFree(d);
+      cudaStreamDestroy(st);
+      HostError w(e.code, e.what(), -1);
+      w.residual = e.residual;
+      throw w;
+    } catch (...) {
+      cudaFree(d);
+      cudaStreamDestroy(st);
+      throw;
+    }
+    cudaFree(d);
+    cudaStreamDestroy(st);
+    if (stats) {
+      stats->products_normal = hs.products_normal;
+      stats->products_adjoint = hs.products_adjoint;
+      stats->rounds = hs.rounds;
+      stats->final_rank = hs.final_rank;
+      stats->residual_estimate = hs.residual;
+    }
+  });
+}
+
 slablu_gpu_status slablu_gpu_sweep_build(int64_t m, int64_t k, const double* blocks, int device,
                                          slablu_gpu_fact** out) {
   ABI_TRY({

@@ -15,10 +15,11 @@
 
 namespace slb {
 
-slablu_gpu_status make_status(int code, const std::string& msg, int64_t index) {
+slablu_gpu_status make_status(int code, const std::string& msg, int64_t index, double residual) {
   slablu_gpu_status s;
   s.code = code;
   s.index = index;
+  s.residual = residual;
   std::snprintf(s.msg, sizeof(s.msg), "%s", msg.c_str());
   return s;
 }

@@ -193,4 +193,25 @@ void dgemv_batched_rhs(cudaStream_t st, int64_t m, int64_t n, int64_t nrhs, doub
                        double* y, int64_t ldy, double* part);
 void dset_identity(cudaStream_t st, double* a, int64_t n);
 
+// ---- hbs.cu ------------------------------------------------------------------
+// Randomized HBS compression of dense blocks (hbs_compress.hpp:90-311).
+struct HbsOptions {
+  double tol = 1e-11;        // probe tolerance (SolverConfig.hbs_tol)
+  double trunc_rel = 1e-13;  // generator truncation floor (SolverConfig.hbs_trunc_rel)
+  int leaf = 64;             // cluster-tree leaf size
+  int64_t r_start = 0, r_max = 0;
+  bool fixed_rank = false;   // hbs_compress with rank bound r_max instead of the adaptive loop
+};
+struct HbsStats {
+  int64_t products_normal = 0, products_adjoint = 0;
+  int rounds = 0;
+  int64_t final_rank = 0;
+  double residual = 0.0;
+};
+// Each of the nb dense n x n blocks (device, column major, ld n) is replaced in place by the
+// dense materialization of its HBS approximation; seeds[i] = the block's CompressOptions.seed.
+// Throws HostError (SLABLU_ERR_COMPRESSION with the residual, or SLABLU_ERR_CONFIG).
+void hbs_compress_blocks(cudaStream_t st, int64_t n, int nb, double* const* blocks, const uint64_t* seeds,
+                         const HbsOptions& o, HbsStats* stats);
+
 }  // namespace slb

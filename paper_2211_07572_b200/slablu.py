@@ -47,6 +47,14 @@ class UnsupportedError(Error):
     pass
 
 
+class CompressionError(Error):
+    """common.hpp:55-60: the probe missed the tolerance; carries the residual estimate."""
+
+    def __init__(self, what, residual_estimate):
+        super().__init__(what)
+        self.residual_estimate = residual_estimate
+
+
 def _check(st):
     if st.code == 0:
         return
@@ -57,6 +65,8 @@ def _check(st):
         raise SingularMatrixError(msg, int(st.index))
     if st.code == 6:
         raise UnsupportedError(msg)
+    if st.code == 7:
+        raise CompressionError(msg, float(st.residual))
     if st.code == 5:
         raise MemoryError(msg)
     raise Error(msg)
@@ -303,7 +313,8 @@ class SolverConfig:
 
     def _c(self):
         return _lib.Config(int(self.b), float(self.c), int(self.compression), int(self.seed),
-                           int(self.threads), int(self.device), int(bool(self.keep_T)), int(self.refine))
+                           int(self.threads), int(self.device), int(bool(self.keep_T)), int(self.refine),
+                           float(self.hbs_tol), float(self.hbs_trunc_rel), int(self.hbs_leaf_size))
 
 
 def choose_b(n1, n2, config: SolverConfig = SolverConfig()):
@@ -374,10 +385,10 @@ class Factorization:
         _check(lib().slablu_gpu_stats(self._h, ctypes.byref(st)))
         self.n1, self.n2, self.b = int(st.n1), int(st.n2), int(st.b)
         self.config = SolverConfig(**{**config.__dict__, "b": int(st.b),
-                                      "compression": CompressionChoice.dense})
+                                      "compression": CompressionChoice(int(st.compression) or 1)})
         self.t_stage1, self.t_stage2 = float(st.t_stage1), float(st.t_stage2)
         self.storage_stage1, self.storage_stage2 = int(st.storage_stage1), int(st.storage_stage2)
-        self.hbs_max_rank = 0
+        self.hbs_max_rank = int(st.hbs_max_rank)
         self.stats = st
         self.part = None if st.single_slab else partition(self.n1, self.n2, self.b)
 
@@ -611,4 +622,47 @@ def run_problem(spec: ProblemSpec, config: SolverConfig = SolverConfig()):
     return {"N": system.dim(), "n1": spec.n1, "n2": spec.n2, "b": fact.b, "kappa": spec.kappa,
             "T_factor_stage1_s": fact.t_stage1, "T_factor_stage2_s": fact.t_stage2, "T_solve_s": t_solve,
             "M_factor_scalars": fact.storage_scalars(), "relerr_res": rep.relerr_res,
-            "relerr_true": rep.relerr_true, "hbs_max_rank": 0, "seed": config.seed}
+            "relerr_true": rep.relerr_true, "hbs_max_rank": fact.hbs_max_rank, "seed": config.seed}
+
+
+# ---------------------------------------------------------------------------
+# randomized HBS compression of a dense operator (hbs_compress.hpp:186-311)
+@dataclass
+class CompressOptions:
+    tol: float = 1e-10
+    trunc_rel: float = 1e-12
+    seed: int = 0
+
+
+@dataclass
+class CompressStats:
+    products_normal: int = 0
+    products_adjoint: int = 0
+    rounds: int = 0
+    final_rank: int = 0
+    residual_estimate: float = 0.0
+
+
+def _hbs(m, leaf_size, r_start, r_max, adaptive, options, device):
+    m = np.asfortranarray(np.asarray(m, dtype=np.float64))
+    n = m.shape[0]
+    if m.ndim != 2 or m.shape[1] != n:
+        raise ConfigError("hbs_compress: square operator required")
+    out = np.zeros((n, n), dtype=np.float64, order="F")
+    st = _lib.HbsStatsT()
+    _check(lib().slablu_gpu_hbs_compress(n, _p(m), int(leaf_size), int(r_start), int(r_max), int(adaptive),
+                                          float(options.tol), float(options.trunc_rel), int(options.seed),
+                                          int(device), _p(out), ctypes.byref(st)))
+    return out, CompressStats(int(st.products_normal), int(st.products_adjoint), int(st.rounds),
+                              int(st.final_rank), float(st.residual_estimate))
+
+
+def hbs_compress(m, leaf_size, rank_bound, options: CompressOptions = CompressOptions(), device=0):
+    """hbs_compress (hbs_compress.hpp:211-250) of the dense operator m with the dense sampler
+    (test_hbs.cpp:64-68), on the GPU.  Returns (to_dense of the compressed operator, stats)."""
+    return _hbs(m, leaf_size, 0, rank_bound, 0, options, device)
+
+
+def hbs_compress_adaptive(m, leaf_size, r_start, r_max, options: CompressOptions = CompressOptions(), device=0):
+    """hbs_compress_adaptive (hbs_compress.hpp:254-311) of the dense operator m, on the GPU."""
+    return _hbs(m, leaf_size, r_start, r_max, 1, options, device)

@@ -194,12 +194,14 @@ def test_cfg2_vs_oracle_fixture():
     (1, 27.12, 1e-9, 3e-4, 1e-2),     # test_driver.cpp:325-335
 ])
 def test_reference_accuracy_windows_1000(kind, kappa, res_tol, lo, hi):
-    """The reference's slow-suite accuracy windows at 1000^2, b = 60."""
+    """The reference's slow-suite accuracy windows at 1000^2, b = 60 (automatic -> hbs, as there)."""
     spec = S.poisson_log_problem(1000, 1000) if kind == 0 else S.helmholtz_problem(1000, 1000, kappa)
     rep = S.run_problem(spec, S.SolverConfig(b=60))
     print(f"1000^2 kind {kind}: relerr_res {rep['relerr_res']:.3e} relerr_true {rep['relerr_true']:.3e}")
     assert rep["relerr_res"] < res_tol
     assert lo < rep["relerr_true"] < hi
+    if kind == 0:
+        assert rep["hbs_max_rank"] > 0  # automatic -> hbs: interfaces wide enough to compress
 
 
 def test_acceptance_criteria_5_to_7():
