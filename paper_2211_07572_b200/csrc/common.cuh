@@ -87,6 +87,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// Non-blocking probe of a phase (mbarrier.test_wait): true once the phase with this parity completed.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
 // Same with a suspend-time hint: the waiting thread sleeps in hardware until the phase completes
 // (or the hint, in ns, expires) instead of re-polling; spinning warps otherwise take issue slots
 // from the warps doing the work on the same sub-partition.
