@@ -985,7 +985,13 @@ struct StripSweeper {
   StripSweeper(const slablu_gpu_fact* F_, const double* fp, int64_t nrhs) : F(F_), st(F_->stream) {
     const int dev = F->device;
     const int64_t n2 = F->n2;
-    CH = nrhs <= 8 ? 8 : kSweepChunk;
+    // 8-column tasks on the cluster kernel for any nrhs (each task streams its strip's operators
+    // once per 8 columns but keeps every SM busy); the 64-column sweep kernel (one CTA per
+    // strip and chunk) only if the cluster kernel does not fit or SLB_SOLVE_WIDE=1 (A/B runs)
+    static const bool wide = getenv("SLB_SOLVE_WIDE") != nullptr;
+    static const bool force_v1_ch = getenv("SLB_SOLVE_V1") != nullptr;
+    CH = (nrhs <= 8 || (!wide && !force_v1_ch && strip_solve2_fits(F->Wp, n2, std::min(4, F->Wp / 8)))) ? 8
+                                                                                                       : kSweepChunk;
     const int64_t nch = cdiv(nrhs, CH);
     std::vector<int32_t> tasks;
     for (int s = 0; s < F->S; s++)
