@@ -417,12 +417,14 @@ def run_ours_sharded(args):
     clocks = ClockSampler()
     clocks.start()
     ts, sh = [], None
+    log(f"[bench r{rank}] timed steps")
     for s in range(args.steps):
         if sh is not None:
             sh.close()
         sh, t = timed(step)
         ts.append(t)
     st = sh.refresh_stats()
+    log(f"[bench r{rank}] solve")
     d_f = torch.from_numpy(sysm.rhs).to(dev).reshape(1, N)
     for _ in range(2):  # second solve is the timed one (first-call allocations)
         d_u, t_solve = timed(lambda: D.solve_dist_refined(sh, d_f, ex, refine=1))
@@ -447,6 +449,7 @@ def run_ours_sharded(args):
         h_u.copy_(u.reshape(N))
         s2.close()
 
+    log(f"[bench r{rank}] e2e")
     _, te = timed(e2e)
     T = float(np.mean(ts))
     if rank == 0:
