@@ -10,6 +10,8 @@
 // bulk work is DMMA GEMM (gemm.cu) with large K from the recursion.
 // trsm: recursive, 64-row leaves solved per right-hand-side column.
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <climits>
 #include <cstdlib>
 #include <cooperative_groups.h>
@@ -488,7 +490,7 @@ __device__ void panel_column_swaps(double* col, int64_t j, int nb, int q0, const
 }
 
 __global__ void __launch_bounds__(256) panel_swaps_list_kernel(double* A, int64_t lda, int64_t n, int64_t j, int nb,
-                                                              const int32_t* swl, const int32_t* ipiv) {
+                                                              const int32_t* swl, const int32_t* ipiv, int64_t cmax) {
   __shared__ int s_cnt;
   __shared__ int s_pos[2 * PNB], s_org[2 * PNB];
   if (threadIdx.x == 0) s_cnt = swl[0];
@@ -506,6 +508,7 @@ __global__ void __launch_bounds__(256) panel_swaps_list_kernel(double* A, int64_
     return;
   }
   if (c >= j) c += nb;
+  if (c >= cmax) return;  // columns at or beyond cmax take these interchanges later (laswp)
   double* col = A + c * lda;
   const int cnt = s_cnt;
   const bool a0 = lane < cnt && s_pos[lane] != s_org[lane];
@@ -560,13 +563,14 @@ __global__ void scatter_rows_kernel(double* A, int64_t lda, int64_t c0, int64_t 
 // (LAPACK dlaswp on both sides at once): one thread per column, rows swapped in registers-free
 // place.  Applying them when the panel finishes is equivalent to the recursion's deferred laswp
 // calls (row interchanges commute with the updates of columns not yet touched).
-__global__ void panel_swaps_kernel(double* A, int64_t lda, int64_t n, int64_t j, int nb, const int32_t* ipiv) {
+__global__ void panel_swaps_kernel(double* A, int64_t lda, int64_t n, int64_t j, int nb, const int32_t* ipiv,
+                                   int64_t cmax) {
   __shared__ int32_t sp[PNB];
   if (threadIdx.x < nb) sp[threadIdx.x] = ipiv[j + threadIdx.x];
   __syncthreads();
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= j) c += nb;  // skip the panel's own columns
-  if (c >= n) return;
+  if (c >= n || c >= cmax) return;
   double* col = A + c * lda;
   for (int q = 0; q < nb; q++) {
     const int64_t r = j + q, p = sp[q];
@@ -656,15 +660,22 @@ void panel32(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t j, int 
   count_launch();
 }
 
-// Scratch for laswp (grown on demand, per device; stage two is stream ordered).
-struct SwapScratch {
-  int32_t* idx = nullptr;
-  double* tmp = nullptr;
-  size_t idx_n = 0, tmp_n = 0;
-};
-SwapScratch& swap_scratch() {
-  static SwapScratch s;
-  return s;
+// laswp scratch comes from the device's stream-ordered pool (cudaMallocAsync): stage two runs
+// laswp on two streams at once, and a pool kept warm (release threshold) makes it cheap.
+void* pool_alloc(size_t bytes, cudaStream_t st) {
+  static bool init[64] = {};
+  int dev = 0;
+  SLB_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev < 64 && !init[dev]) {
+    cudaMemPool_t pool;
+    SLB_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = 1ull << 30;  // keep up to 1 GiB of freed blocks for reuse
+    SLB_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    init[dev] = true;
+  }
+  void* p = nullptr;
+  SLB_CUDA_CHECK(cudaMallocAsync(&p, bytes, st));
+  return p;
 }
 
 // Apply ipiv[k1..k2) to columns [c0, c1) of the n-row matrix A: replay the
@@ -673,28 +684,19 @@ void laswp(cudaStream_t st, double* A, int64_t lda, int64_t c0, int64_t c1, cons
            int64_t k2, int64_t n) {
   if (c1 <= c0 || k2 <= k1) return;
   const int64_t m = n - k1, nc = c1 - c0;
-  SwapScratch& S = swap_scratch();
-  if (S.idx_n < (size_t)m) {
-    SLB_CUDA_CHECK(cudaStreamSynchronize(st));
-    if (S.idx) cudaFree(S.idx);
-    SLB_CUDA_CHECK(cudaMalloc(&S.idx, m * sizeof(int32_t)));
-    S.idx_n = m;
-  }
-  if (S.tmp_n < (size_t)(m * nc)) {
-    SLB_CUDA_CHECK(cudaStreamSynchronize(st));
-    if (S.tmp) cudaFree(S.tmp);
-    SLB_CUDA_CHECK(cudaMalloc(&S.tmp, m * nc * sizeof(double)));
-    S.tmp_n = m * nc;
-  }
-  swap_perm_kernel<<<1, 1024, (m + (k2 - k1)) * sizeof(int16_t), st>>>(ipiv, n, k1, k2, S.idx); count_launch();
+  int32_t* idx = static_cast<int32_t*>(pool_alloc(m * sizeof(int32_t), st));
+  double* tmp = static_cast<double*>(pool_alloc(m * nc * sizeof(double), st));
+  swap_perm_kernel<<<1, 1024, (m + (k2 - k1)) * sizeof(int16_t), st>>>(ipiv, n, k1, k2, idx); count_launch();
   SLB_CUDA_CHECK(cudaGetLastError());
   for (int64_t cb = 0; cb < nc; cb += 65535) {
     const int64_t ncb = std::min<int64_t>(65535, nc - cb);
     dim3 grid((unsigned)std::min<int64_t>(cdiv(m, 256), 16), (unsigned)ncb);
-    gather_rows_kernel<<<grid, 256, 0, st>>>(A, lda, c0 + cb, c0 + cb + ncb, k1, m, S.idx, S.tmp + cb * m); count_launch();
-    scatter_rows_kernel<<<grid, 256, 0, st>>>(A, lda, c0 + cb, k1, m, S.tmp + cb * m); count_launch();
+    gather_rows_kernel<<<grid, 256, 0, st>>>(A, lda, c0 + cb, c0 + cb + ncb, k1, m, idx, tmp + cb * m); count_launch();
+    scatter_rows_kernel<<<grid, 256, 0, st>>>(A, lda, c0 + cb, k1, m, tmp + cb * m); count_launch();
   }
   SLB_CUDA_CHECK(cudaGetLastError());
+  SLB_CUDA_CHECK(cudaFreeAsync(idx, st));
+  SLB_CUDA_CHECK(cudaFreeAsync(tmp, st));
 }
 
 // X = L^{-1} B (unit lower) or U^{-1} B (upper), L is m x m.
@@ -722,32 +724,34 @@ void trsm(cudaStream_t st, bool lower, const double* L, int64_t ldl, int64_t m, 
 }
 
 // Recursive LU of columns [c0, c1) (rows c0..n) of the n x n matrix A.
+// cmax: columns >= cmax are not touched (their interchanges are applied later by laswp).
 void getrf_rec(cudaStream_t st, double* A, int64_t n, int64_t c0, int64_t c1, int32_t* ipiv,
-               DevStatus* status, int block_index, int32_t* swl) {
+               DevStatus* status, int block_index, int32_t* swl, int64_t cmax) {
   const int64_t w = c1 - c0;
   if (w <= PNB) {
     if (swl && !panel_v1()) {
       panel32(st, A, n, n, c0, (int)w, ipiv, status, block_index, swl);
       // interchanges on every other column now (so the recursion needs no laswp) and the later
       // steps' interchanges on the panel's own L columns
-      panel_swaps_list_kernel<<<(unsigned)cdiv(n, 8), 256, 0, st>>>(A, n, n, c0, (int)w, swl, ipiv); count_launch();
+      panel_swaps_list_kernel<<<(unsigned)cdiv(n, 8), 256, 0, st>>>(A, n, n, c0, (int)w, swl, ipiv, cmax);
+      count_launch();
       SLB_CUDA_CHECK(cudaGetLastError());
       return;
     }
     panel(st, A, n, n, c0, (int)w, ipiv, status, block_index);
     if (n - w > 0) {  // interchanges on every other column now, so the recursion needs no laswp
-      panel_swaps_kernel<<<(unsigned)cdiv(n - w, 128), 128, 0, st>>>(A, n, n, c0, (int)w, ipiv); count_launch();
+      panel_swaps_kernel<<<(unsigned)cdiv(n - w, 128), 128, 0, st>>>(A, n, n, c0, (int)w, ipiv, cmax); count_launch();
       SLB_CUDA_CHECK(cudaGetLastError());
     }
     return;
   }
   int64_t h = round_up(w / 2, PNB);
   if (h >= w) h = w - PNB;
-  getrf_rec(st, A, n, c0, c0 + h, ipiv, status, block_index, swl);
+  getrf_rec(st, A, n, c0, c0 + h, ipiv, status, block_index, swl, cmax);
   trsm(st, true, A + c0 * n + c0, n, h, A + (c0 + h) * n + c0, n, w - h);
   dgemm_batched(st, n - c0 - h, w - h, h, -1.0, A + c0 * n + c0 + h, n, 0, A + (c0 + h) * n + c0, n, 0, 1.0,
                 A + (c0 + h) * n + c0 + h, n, 0, 1);
-  getrf_rec(st, A, n, c0 + h, c1, ipiv, status, block_index, swl);
+  getrf_rec(st, A, n, c0 + h, c1, ipiv, status, block_index, swl, cmax);
 }
 
 }  // namespace
@@ -756,7 +760,27 @@ void dgetrf(cudaStream_t st, int64_t n, double* a, int32_t* ipiv, double* /*work
             int block_index) {
   int32_t* swl = nullptr;  // swap list of the current panel (stream ordered, reused by every panel)
   SLB_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&swl), SWL * sizeof(int32_t), st));
-  getrf_rec(st, a, n, 0, n, ipiv, status, block_index, swl);
+  getrf_rec(st, a, n, 0, n, ipiv, status, block_index, swl, n);
+  SLB_CUDA_CHECK(cudaFreeAsync(swl, st));
+}
+
+// The same LU with columns [h, n) not ready yet: columns [0, h) are factored first (their
+// interchanges kept off the right part), then the stream waits for right_ready, applies the
+// left part's interchanges to columns [h, n) (LAPACK's deferred laswp), and finishes with the
+// triangular solve, the trailing update and the LU of the right part.
+void dgetrf_split(cudaStream_t st, int64_t n, double* a, int32_t* ipiv, DevStatus* status, int block_index,
+                  int64_t h, cudaEvent_t right_ready) {
+  h = std::min<int64_t>(round_up(std::max<int64_t>(h, PNB), PNB), n);
+  int32_t* swl = nullptr;
+  SLB_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&swl), SWL * sizeof(int32_t), st));
+  getrf_rec(st, a, n, 0, h, ipiv, status, block_index, swl, h);
+  SLB_CUDA_CHECK(cudaStreamWaitEvent(st, right_ready, 0));
+  if (h < n) {
+    laswp(st, a, n, h, n, ipiv, 0, h, n);
+    trsm(st, true, a, n, h, a + h * n, n, n - h);
+    dgemm_batched(st, n - h, n - h, h, -1.0, a + h, n, 0, a + h * n, n, 0, 1.0, a + h * n + h, n, 0, 1);
+    getrf_rec(st, a, n, h, n, ipiv, status, block_index, swl, n);
+  }
   SLB_CUDA_CHECK(cudaFreeAsync(swl, st));
 }
 

@@ -400,9 +400,14 @@ struct slablu_gpu_fact {
   double* Tdiag() const { return T.p; }
   double* Tsup() const { return T.p + (size_t)K * n2 * n2; }
   double* Tsub() const { return T.p + (size_t)(2 * K - 1) * n2 * n2; }
+  cudaStream_t stream2 = nullptr;  // stage two: the right half of X_j / S_{j+1} beside the LU
   ~slablu_gpu_fact() {
+    if (stream || stream2) cudaSetDevice(device);
+    if (stream2) {
+      cudaStreamSynchronize(stream2);
+      cudaStreamDestroy(stream2);
+    }
     if (stream) {
-      cudaSetDevice(device);
       cudaStreamSynchronize(stream);
       cudaStreamDestroy(stream);
     }
@@ -462,19 +467,57 @@ void factor_S(slablu_gpu_fact* F, int j) {
 
 // The sweep over the interfaces [ia, ib) started fresh at ia: S_ia = T_{ia ia},
 // X_{j-1} = S_{j-1}^{-1} super_{j-1}, S_j = T_jj - sub_{j-1} X_{j-1}.
+//
+// Overlap: the LU of S_j factors its left half first; the right half of X_{j-1} and of S_j
+// (getrs + GEMM on columns [h, n2)) is computed meanwhile on a second stream, and the LU waits
+// for it only when it reaches those columns (dgetrf_split).  SLB_STAGE2_SERIAL=1 disables it.
 void stage_two_range(slablu_gpu_fact* F, int ia, int ib) {
   cudaStream_t st = F->stream;
-  const int64_t n2 = F->n2, bs = n2 * n2;
+  const int64_t n2 = F->n2, bs = n2 * n2, dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
+  static const bool serial = getenv("SLB_STAGE2_SERIAL") != nullptr;
+  const bool overlap = !serial && n2 >= 512;
+  cudaEvent_t ev_in = nullptr, ev_right = nullptr;
+  if (overlap) {
+    if (!F->stream2) {
+      int least = 0, greatest = 0;
+      SLB_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      SLB_CUDA_CHECK(cudaStreamCreateWithPriority(&F->stream2, cudaStreamNonBlocking, least));
+    }
+    SLB_CUDA_CHECK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    SLB_CUDA_CHECK(cudaEventCreateWithFlags(&ev_right, cudaEventDisableTiming));
+  }
+  const int64_t h = round_up(n2 / 2, 32);
   for (int j = ia; j < ib; j++) {
     if (j > ia) {
       double* X = F->Xup.p + (size_t)(j - 1) * bs;
+      const double* LUp = F->Tdiag() + (j - 1) * bs;
+      const int32_t* ip = F->ipivT.p + (size_t)(j - 1) * n2;
+      double* Sj = F->Tdiag() + j * bs;
+      const double* sub = F->Tsub() + (j - 1) * bs;
       SLB_CUDA_CHECK(cudaMemcpyAsync(X, F->Tsup() + (j - 1) * bs, bs * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      dgetrs(st, n2, n2, F->Tdiag() + (j - 1) * bs, F->ipivT.p + (size_t)(j - 1) * n2, X, n2, nullptr);
-      dgemm_batched(st, n2, n2, n2, -1.0, F->Tsub() + (j - 1) * bs, n2, 0, X, n2, 0, 1.0, F->Tdiag() + j * bs, n2, 0,
-                    1);
+      if (overlap) {
+        SLB_CUDA_CHECK(cudaEventRecord(ev_in, st));
+        SLB_CUDA_CHECK(cudaStreamWaitEvent(F->stream2, ev_in, 0));
+        {
+          StreamScope s2(F->stream2);
+          dgetrs(F->stream2, n2, n2 - h, LUp, ip, X + h * n2, n2, nullptr);
+          dgemm_batched(F->stream2, n2, n2 - h, n2, -1.0, sub, n2, 0, X + h * n2, n2, 0, 1.0, Sj + h * n2, n2, 0, 1);
+        }
+        SLB_CUDA_CHECK(cudaEventRecord(ev_right, F->stream2));
+        dgetrs(st, n2, h, LUp, ip, X, n2, nullptr);
+        dgemm_batched(st, n2, h, n2, -1.0, sub, n2, 0, X, n2, 0, 1.0, Sj, n2, 0, 1);
+        dgetrf_split(st, n2, Sj, F->ipivT.p + (size_t)j * n2, F->status.p, j, h, ev_right);
+        getrs_prepare(st, n2, Sj, F->ipivT.p + (size_t)j * n2, F->permT.p + (size_t)j * n2,
+                      F->dinvT.p + (size_t)j * dinv_sz);
+        continue;
+      }
+      dgetrs(st, n2, n2, LUp, ip, X, n2, nullptr);
+      dgemm_batched(st, n2, n2, n2, -1.0, sub, n2, 0, X, n2, 0, 1.0, Sj, n2, 0, 1);
     }
     factor_S(F, j);
   }
+  if (ev_in) cudaEventDestroy(ev_in);
+  if (ev_right) cudaEventDestroy(ev_right);
 }
 
 void stage_two_build(slablu_gpu_fact* F) {

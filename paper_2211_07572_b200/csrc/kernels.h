@@ -167,6 +167,9 @@ void assemble_T(cudaStream_t st, int64_t n2, int nifc, int nstrips, const StripD
 // In-place LU with partial pivoting of an n x n column-major matrix (ld = n).
 void dgetrf(cudaStream_t st, int64_t n, double* a, int32_t* ipiv, double* work, DevStatus* status,
             int block_index);
+// dgetrf with columns [h, n) produced concurrently on another stream (event right_ready).
+void dgetrf_split(cudaStream_t st, int64_t n, double* a, int32_t* ipiv, DevStatus* status, int block_index,
+                  int64_t h, cudaEvent_t right_ready);
 // Solve A X = B with the dgetrf factors, B is n x nrhs (ld ldb), in place.
 void dgetrs(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, const int32_t* ipiv,
             double* b, int64_t ldb, double* work);
