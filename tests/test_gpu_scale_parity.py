@@ -215,3 +215,40 @@ def test_acceptance_criteria_5_to_7():
     kappa = S.kappa_from_ppw(250.0, 512)
     rep = S.run_problem(S.helmholtz_problem(512, 512, kappa), S.SolverConfig())
     assert rep["relerr_res"] <= 1e-9 and 1e-4 <= rep["relerr_true"] <= 3e-2           # criterion 7
+
+
+@pytest.mark.timeout(1800)
+def test_cfg4_batched_64_rhs():
+    """configs[3]: 2000^2 Helmholtz 10 ppw, b = 100, a 64-column right-hand side (BASELINE.json
+    north_star, batched solve).  The batched solve equals column-by-column solves, every column's
+    residual is at direct accuracy, and the reduced right-hand side of the batch matches the
+    oracle's slabs at an interior interface (stage_one.hpp:415-433)."""
+    n, b = 2000, 100
+    kappa = S.kappa_from_ppw(10.0, n)
+    sys_g = S.assemble_fd5(S.helmholtz_problem(n, n, kappa))
+    N = sys_g.dim()
+    fact = S.factorize(sys_g, S.SolverConfig(b=b, refine=0, compression=S.CompressionChoice.dense))
+    F = np.column_stack([sys_g.rhs, S.gaussian_matrix(N, 63, 4242)])
+    U = S.solve(fact, F)
+    for c in (0, 7, 8, 31, 63):  # column c alone, and its 8-column task neighbours in the batch
+        uc = S.solve(fact, F[:, c:c + 1])[:, 0]
+        e = relerr(U[:, c], uc)
+        # 8-column DMMA tasks vs the 1-column DFMA kernel: different summation order, amplified
+        # by the conditioning of the 10-ppw Helmholtz operator (measured 1.0e-11 on column 0)
+        assert e < 1e-9, (c, e)
+    R = np.column_stack([sys_g.matvec(U[:, c]).ravel() for c in range(0, 64, 9)]) - F[:, 0:64:9]
+    res = np.linalg.norm(R, axis=0) / np.linalg.norm(F[:, 0:64:9], axis=0)
+    print(f"cfg4 64-RHS unrefined residuals: max {res.max():.2e}")
+    assert res.max() < 1e-8  # unrefined; refine = 1 brings it to ~1e-13 (bench relerr_res)
+    # staged parity of the batch's reduced right-hand side at interface 9 (8 sampled columns)
+    sys_o = O.system_from_csr(n, n, sys_g.h, sys_g.row_ptr, sys_g.col_idx, sys_g.values, sys_g.rhs)
+    O.set_blas_threads(os.cpu_count() or 1)
+    cols = [0, 1, 7, 8, 9, 33, 62, 63]
+    red = fact.reduce_rhs(F[:, cols])
+    j = 9
+    off = fact.part.interface_offset(j)
+    left, right = O.Slab(sys_o, b, j), O.Slab(sys_o, b, j + 1)
+    ref = F[off:off + n][:, cols] - left.contrib(F[:, cols])[1] - right.contrib(F[:, cols])[0]
+    e = relerr(red[j * n:(j + 1) * n], ref)
+    print(f"cfg4 reduce_rhs interface {j}, 8 of 64 columns: rel diff {e:.3e}")
+    assert e < 1e-11
