@@ -37,8 +37,9 @@ CONFIGS = {
     "cfg3": (2, 4000, 4000, 150, 10.0, "5-point FD bump Helmholtz 4000x4000 (N=16M), 10 ppw, b=150 (dense)"),
     "cfg4": (1, 2000, 2000, 100, 10.0, "5-point FD Helmholtz 2000x2000 (rectangle stand-in), 10 ppw, b=100, 64 RHS"),
 }
-# DRAM bytes of one Schur-sweep launch (ncu --set full capture, profiles/ncu_schur_cfg3_r01.txt)
-SCHUR_DRAM_BYTES = {"cfg3": 1.833542e12 + 0.521007e12}
+# DRAM bytes of one Schur-sweep launch (ncu --set full capture of the current kernel,
+# profiles/ncu_schur_cfg3_r02.txt)
+SCHUR_DRAM_BYTES = {"cfg3": 1.912814e12 + 0.521009e12}
 FP64_PEAK_TFLOPS = 37.067  # measured DMMA peak on this pool's B200 (profiles/fp64_peak_r01.json)
 
 
