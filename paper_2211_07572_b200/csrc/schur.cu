@@ -19,6 +19,8 @@
 // A operands stream from HBM/L2 in fragment order (16-byte cp.async, 3-stage
 // ring, continuous across levels); B operands stay in shared memory; y_l is
 // spilled to a per-CTA HBM slab between the two sweeps.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -45,6 +47,31 @@ struct Lay {
   static constexpr int BWM = 16 / BWN;                // backward m groups
   static constexpr int BNT = NT / BWN;                // backward n tiles per warp
 };
+
+// Calls f with the warp's m-tile count as a compile-time constant (1..MTMAX): the DMMA loops
+// then have no per-tile exit branches, and every A fragment of a k4 step is loaded up front.
+template <int MTMAX, class F>
+__device__ __forceinline__ void dispatch_mt(int cnt, F&& f) {
+  switch (cnt) {
+    case 5:
+      if constexpr (MTMAX >= 5) f(std::integral_constant<int, 5>{});
+      break;
+    case 4:
+      if constexpr (MTMAX >= 4) f(std::integral_constant<int, 4>{});
+      break;
+    case 3:
+      if constexpr (MTMAX >= 3) f(std::integral_constant<int, 3>{});
+      break;
+    case 2:
+      if constexpr (MTMAX >= 2) f(std::integral_constant<int, 2>{});
+      break;
+    case 1:
+      f(std::integral_constant<int, 1>{});
+      break;
+    default:
+      break;
+  }
+}
 
 template <int C>
 __device__ __forceinline__ int swz(int r, int n) {
@@ -325,40 +352,44 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
         const double* A = acquire();
 #endif
         if (sc) {  // Ainv rows only: SNT n tiles per warp
+          const int cnt = min(fmt, MTH - fm * fmt);
+          dispatch_mt<MTMAX>(cnt, [&](auto MTc) {
+            constexpr int MT = decltype(MTc)::value;
 #pragma unroll
-          for (int kk = 0; kk < SK; kk++) {
-            const int k = j * 4 * SK + kk * 4 + t;  // B row
-            double bf[L::SNT];
+            for (int kk = 0; kk < SK; kk++) {
+              const int k = j * 4 * SK + kk * 4 + t;  // B row
+              double bf[L::SNT], af[MT];
 #pragma unroll
-            for (int nj = 0; nj < L::SNT; nj++) bf[nj] = tb[swz<C>(k, (fnb + nj) * 8 + g)];
-            const double* Ak = A + kk * MTH * 32 + lane;
+              for (int nj = 0; nj < L::SNT; nj++) bf[nj] = tb[swz<C>(k, (fnb + nj) * 8 + g)];
+              const double* Ak = A + kk * MTH * 32 + (fm * fmt) * 32 + lane;
 #pragma unroll
-            for (int mi = 0; mi < MTMAX; mi++) {
-              const int mt = fm * fmt + mi;
-              if (mi >= fmt || mt >= MTH) break;  // warp-uniform exit (see below)
-              const double af = Ak[mt * 32];
+              for (int mi = 0; mi < MT; mi++) af[mi] = Ak[mi * 32];
 #pragma unroll
-              for (int nj = 0; nj < L::SNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
+              for (int mi = 0; mi < MT; mi++)
+#pragma unroll
+                for (int nj = 0; nj < L::SNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af[mi], bf[nj]);
             }
-          }
+          });
         } else {
+          // predicated-off DMMAs would still occupy the pipe: the tile count is a template constant
+          const int cnt = min(fmt, MTH - fm * fmt);
+          dispatch_mt<MTMAX>(cnt, [&](auto MTc) {
+            constexpr int MT = decltype(MTc)::value;
 #pragma unroll
-          for (int kk = 0; kk < SK; kk++) {
-            const int k = j * 4 * SK + kk * 4 + t;  // B row
-            double bf[L::FNT];
+            for (int kk = 0; kk < SK; kk++) {
+              const int k = j * 4 * SK + kk * 4 + t;  // B row
+              double bf[L::FNT], af[MT];
 #pragma unroll
-            for (int nj = 0; nj < L::FNT; nj++) bf[nj] = tb[swz<C>(k, (fwn * L::FNT + nj) * 8 + g)];
-            const double* Ak = A + kk * (2 * MTH) * 32 + hf * MTH * 32 + lane;
+              for (int nj = 0; nj < L::FNT; nj++) bf[nj] = tb[swz<C>(k, (fwn * L::FNT + nj) * 8 + g)];
+              const double* Ak = A + kk * (2 * MTH) * 32 + hf * MTH * 32 + (fm * fmt) * 32 + lane;
 #pragma unroll
-            for (int mi = 0; mi < MTMAX; mi++) {
-              const int mt = fm * fmt + mi;
-              // warp-uniform exit, not a predicate: predicated-off DMMAs still occupy the pipe
-              if (mi >= fmt || mt >= MTH) break;
-              const double af = Ak[mt * 32];
+              for (int mi = 0; mi < MT; mi++) af[mi] = Ak[mi * 32];
 #pragma unroll
-              for (int nj = 0; nj < L::FNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
+              for (int mi = 0; mi < MT; mi++)
+#pragma unroll
+                for (int nj = 0; nj < L::FNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af[mi], bf[nj]);
             }
-          }
+          });
         }
         release();
       }
@@ -507,22 +538,23 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
         const int kj = j * 4 * SK;
         const double* xs = (kj < Wp) ? xp : xq;
         const int kbase = (kj < Wp) ? kj : kj - Wp;
+        dispatch_mt<MTMAX>(min(BMT, MTH - bwm * BMT), [&](auto MTc) {
+          constexpr int MT = decltype(MTc)::value;
 #pragma unroll
-        for (int kk = 0; kk < SK; kk++) {
-          const int k = kbase + kk * 4 + t;
-          double bf[L::BNT];
+          for (int kk = 0; kk < SK; kk++) {
+            const int k = kbase + kk * 4 + t;
+            double bf[L::BNT], af[MT];
 #pragma unroll
-          for (int nj = 0; nj < L::BNT; nj++) bf[nj] = xs[swz<C>(k, (bwn * L::BNT + nj) * 8 + g)];
-          const double* Ak = A + kk * MTH * 32 + lane;
+            for (int nj = 0; nj < L::BNT; nj++) bf[nj] = xs[swz<C>(k, (bwn * L::BNT + nj) * 8 + g)];
+            const double* Ak = A + kk * MTH * 32 + (bwm * BMT) * 32 + lane;
 #pragma unroll
-          for (int mi = 0; mi < MTMAX; mi++) {
-            const int mt = bwm * BMT + mi;
-            if (mi >= BMT || mt >= MTH) break;  // warp-uniform exit (see the forward loop)
-            const double af = Ak[mt * 32];
+            for (int mi = 0; mi < MT; mi++) af[mi] = Ak[mi * 32];
 #pragma unroll
-            for (int nj = 0; nj < L::BNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af, bf[nj]);
+            for (int mi = 0; mi < MT; mi++)
+#pragma unroll
+              for (int nj = 0; nj < L::BNT; nj++) dmma884(acc[mi][nj][0], acc[mi][nj][1], af[mi], bf[nj]);
           }
-        }
+        });
         release();
       }
       if (nhc > 0) {  // acc (= -x) += H[:, r] x_{l+2}[r, :] for the columns r of the rows pivoted up
