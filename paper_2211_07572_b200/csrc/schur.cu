@@ -28,6 +28,9 @@ namespace slb {
 namespace {
 
 constexpr int THREADS = 512;
+// The operand-ring producer thread: lane 0 of the last warp, whose m group holds the fewest row
+// tiles (19 = 5 + 5 + 5 + 4 at Wp = 152), so the issue work lands on the least-loaded warp.
+constexpr int PRODUCER = THREADS - 32;
 
 // Compile-time layout of a sweep kernel with C right-hand-side columns.
 template <int C>
@@ -101,10 +104,10 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
   __shared__ __align__(8) uint64_t full_bar[L::STAGES];
   __shared__ __align__(8) uint64_t empty_bar[L::STAGES];
   // Ring state persists across tasks: slot = global slice counter % STAGES.
-  // The producer (thread 0) fills slot s for slice q after all warps released
+  // The producer (thread PRODUCER) fills slot s for slice q after all warps released
   // slice q - STAGES from it; consumers wait on full_bar[s] with parity
   // (q / STAGES) & 1 and release with one arrive per warp.
-  // ring positions + phases (producer state lives in thread 0 only)
+  // ring positions + phases (producer state lives in thread PRODUCER only)
   int p_slot = 0, c_slot = 0;
   uint32_t p_round = 0, c_phase = 0;  // p_round: completed passes over the ring (producer)
 
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
 
     // Slice stream: forward levels l0..n2-1 (kf slices each), then backward
     // levels n2-1..lstop (kb slices, or kb/2 when U13 = 0 on that level).
-    // The producer (thread 0) walks it with an incremental cursor; the U13
+    // The producer (thread PRODUCER) walks it with an incremental cursor; the U13
     // flags of the strip sit in shared memory (loaded at task start).
     const double* p_src = fac + (int64_t)T.l0 * lvl_stride;
     int p_len = fslice, p_left = kf;
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
       return (f & 1) && !(a.bsc && !(f & 64) && ((f >> 2) & 15) <= 8);
     };
     auto issue = [&]() {
-      if (tid != 0 || p_done) return;
+      if (tid != PRODUCER || p_done) return;
       const double* src = p_src;
       const int len = p_len;
       // shortcut level (flags == 0): only the Ainv half of each k4 block of [Ainv ; Fbot]
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(THREADS, 1) sweep_kernel(SchurArgs a) {
     }
 
 #ifdef SLB_SCHUR_PROF
-    if ((tid == 0 || tid == 160) && blockIdx.x == 0)
+    if ((tid == 0 || tid == 160 || tid == PRODUCER) && blockIdx.x == 0)
       printf("SCHUR tid %d task %d levels %lld: topsync %lld build %lld presync %lld kloop %lld (issue %lld acquire-wait %lld) epi %lld [ystore %lld zcomp %lld bar1 %lld] shortcut-levels %lld\n",
              tid, task, (long long)(n2 - T.l0), sp[0], sp[1], sp[2], sp[3], sp[5], wacq, sp[4], ep[0], ep[1], ep[2], nsc);
 #endif
