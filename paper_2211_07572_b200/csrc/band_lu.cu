@@ -192,10 +192,13 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   if (tid == 0) s_sing = -1;
 
   const int init_rows = rows_total < NW ? rows_total : NW;
+  // the window's first rows: asynchronous 8-byte copies (transposing gather), so every thread has
+  // many loads in flight instead of one load-store pair at a time
   for (int idx = tid; idx < init_rows * Wp; idx += blockDim.x) {
     const int j = idx / init_rows, p = idx % init_rows;
-    rowp(p)[j] = Pval(p, j);
+    cp_async8(rowp(p) + j, p < Wp ? SV + (int64_t)j * Wp + p : NX + (int64_t)j * Wp + (p - Wp), true);
   }
+  cp_async_commit();
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm[p] = p;
   __syncthreads();
 
@@ -534,10 +537,13 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
   };
   if (tid == 0) s_sing = -1;
   const int init_rows = rows_total < NW ? rows_total : NW;
+  // the window's first rows: asynchronous 8-byte copies (transposing gather), so every thread has
+  // many loads in flight instead of one load-store pair at a time
   for (int idx = tid; idx < init_rows * Wp; idx += blockDim.x) {
     const int j = idx / init_rows, p = idx % init_rows;
-    rowp(p)[j] = Pval(p, j);
+    cp_async8(rowp(p) + j, p < Wp ? SV + (int64_t)j * Wp + p : NX + (int64_t)j * Wp + (p - Wp), true);
   }
+  cp_async_commit();
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm[p] = p;
 
   auto prefetch = [&](int kb_in, int buf) {  // rows entering at positions kb_in + Wp + q
@@ -741,7 +747,12 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
     }
   };
 
-  if (8 < Wp) prefetch(8, 0);
+  if (8 < Wp) {
+    prefetch(8, 0);
+    cp_async_wait<1>();  // the window (the entering rows of block 8 may still be in flight)
+  } else {
+    cp_async_wait<0>();
+  }
   __syncthreads();
   if (warp < PW) panel(0, nullptr);  // block 0: every row is in the window
   __syncthreads();

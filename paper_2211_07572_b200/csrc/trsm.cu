@@ -290,10 +290,14 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
   const int mt = warp >> 2, nt = warp & 3;
   for (int i = tid; i < 2 * Wp; i += 256) sperm[i] = perm[i];
   __syncthreads();
-  for (int idx = tid; idx < m * TN; idx += 256) {
+  for (int idx = tid; idx < m * TN; idx += 256) {  // asynchronous gather (many loads in flight)
     const int n = idx / m, r = idx % m;
-    X[sw32(r, n)] = n < ncol ? Rval(sperm[r], c0 + n) : 0.0;
+    const int p = sperm[r], c = c0 + n;
+    double* dst = &X[sw32(r, n)];
+    if (n >= ncol || (p < Wp && c >= Wp)) *dst = 0.0;
+    else cp_async8(dst, p < Wp ? V + (int64_t)c * Wp + p : NX + (int64_t)(Wp + c) * Wp + (p - Wp), true);
   }
+  cp_async_commit();
   for (int idx = m * TN + tid; idx < nb * RB * TN; idx += 256) X[idx] = 0.0;
   diag_inverses<true, true>(LU11, Wp, m, nb, Dv, tid, 256);
   UP(0)
