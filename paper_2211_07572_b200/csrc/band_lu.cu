@@ -194,8 +194,9 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
   const int init_rows = rows_total < NW ? rows_total : NW;
   // the window's first rows: asynchronous 8-byte copies (transposing gather), so every thread has
   // many loads in flight instead of one load-store pair at a time
+  const float inv_ir = 1.0f / (float)init_rows, inv_wp = 1.0f / (float)Wp;
   for (int idx = tid; idx < init_rows * Wp; idx += blockDim.x) {
-    const int j = idx / init_rows, p = idx % init_rows;
+    const int j = qdiv(idx, inv_ir), p = idx - j * init_rows;
     cp_async8(rowp(p) + j, p < Wp ? SV + (int64_t)j * Wp + p : NX + (int64_t)j * Wp + (p - Wp), true);
   }
   cp_async_commit();
@@ -539,8 +540,9 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
   const int init_rows = rows_total < NW ? rows_total : NW;
   // the window's first rows: asynchronous 8-byte copies (transposing gather), so every thread has
   // many loads in flight instead of one load-store pair at a time
+  const float inv_ir = 1.0f / (float)init_rows, inv_wp = 1.0f / (float)Wp;
   for (int idx = tid; idx < init_rows * Wp; idx += blockDim.x) {
-    const int j = idx / init_rows, p = idx % init_rows;
+    const int j = qdiv(idx, inv_ir), p = idx - j * init_rows;
     cp_async8(rowp(p) + j, p < Wp ? SV + (int64_t)j * Wp + p : NX + (int64_t)j * Wp + (p - Wp), true);
   }
   cp_async_commit();
@@ -548,7 +550,7 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
 
   auto prefetch = [&](int kb_in, int buf) {  // rows entering at positions kb_in + Wp + q
     for (int idx = tid; idx < 8 * Wp; idx += blockDim.x) {
-      const int q = idx / Wp, j = idx % Wp;
+      const int q = qdiv(idx, inv_wp), j = idx - q * Wp;
       const int pe = kb_in + Wp + q;
       if (pe < rows_total) cp_async8(ent + buf * 8 * Wp + idx, NX + (int64_t)j * Wp + (pe - Wp), true);
     }
@@ -774,7 +776,7 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
     }
     __syncthreads();
     for (int idx = tid; idx < 8 * Wp; idx += blockDim.x) {  // R
-      const int q = idx / Wp, j = idx % Wp;
+      const int q = qdiv(idx, inv_wp), j = idx - q * Wp;
       double* rr = rowp(kb + q);
       LU11[(int64_t)(kb + q) * Wp + j] = rr[j];
       if (kend + Wp + q < rows_total) rr[j] = ent[eb * 8 * Wp + idx];

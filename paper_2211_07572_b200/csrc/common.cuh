@@ -134,6 +134,11 @@ __device__ __forceinline__ int dsmem_ld_s32(uint32_t addr) {
   asm volatile("ld.shared::cluster.s32 %0, [%1];\n" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
+// idx / d for small quotients (idx < 2^20, idx / d <= 4096) via a float reciprocal: the hot
+// index loops of the chain kernels otherwise spend their issue slots on integer division.
+// (idx + 0.5) / d stays >= 0.5 / d away from the next integer, far above the float error.
+__device__ __forceinline__ int qdiv(int idx, float inv_d) { return (int)(((float)idx + 0.5f) * inv_d); }
+
 // 16-byte store into a peer CTA's shared memory, completion counted (bytes) on the peer's mbarrier
 __device__ __forceinline__ void st_async_v2(uint32_t raddr, double a, double b, uint32_t rbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),

@@ -272,8 +272,9 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
     const int h = min(m, r0 + RB) - r0;
     double* dst = sTb + buf * RB * KS;
     const int m2 = m / 2;  // Wp is a multiple of 8: rows are whole 16-byte pieces
+    const float inv_m2 = 1.0f / (float)m2;
     for (int idx = tid; idx < h * m2; idx += 256) {
-      const int rr = idx / m2, c = 2 * (idx % m2);
+      const int rr = qdiv(idx, inv_m2), c = 2 * (idx - rr * m2);
       cp_async16(dst + rr * KS + c, T + (int64_t)(r0 + rr) * m + c, true);
     }
   };
@@ -290,8 +291,9 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
   const int mt = warp >> 2, nt = warp & 3;
   for (int i = tid; i < 2 * Wp; i += 256) sperm[i] = perm[i];
   __syncthreads();
+  const float inv_m = 1.0f / (float)m;
   for (int idx = tid; idx < m * TN; idx += 256) {  // asynchronous gather (many loads in flight)
-    const int n = idx / m, r = idx % m;
+    const int n = qdiv(idx, inv_m), r = idx - n * m;
     const int p = sperm[r], c = c0 + n;
     double* dst = &X[sw32(r, n)];
     if (n >= ncol || (p < Wp && c >= Wp)) *dst = 0.0;
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
   UP(2)
   // ---- U1213 tile out
   for (int idx = tid; idx < m * ncol; idx += 256) {
-    const int n = idx / m, r = idx % m;
+    const int n = qdiv(idx, inv_m), r = idx - n * m;
     U1213[(int64_t)(c0 + n) * Wp + r] = X[sw32(r, n)];
   }
   // ---- GEMM: out = R2 - L21 X, row blocks of 16 of L21 staged like L11
