@@ -1,0 +1,10 @@
+# Round-end evidence: full GPU test suite, bench lines (cfg3 default, cfg4, reference arm),
+# and the ncu launch list of one factorization + solve at cfg3.
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
+python bench.py > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
+python bench.py --config cfg4 --no-cpu > gpurun_out/bench_cfg4.json 2> gpurun_out/bench_cfg4.err
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 40000 --csv --log-file gpurun_out/launches.csv \
+    python tools/profile_factor.py --config cfg3 --solve > gpurun_out/ncu_launch.log 2>&1
