@@ -25,7 +25,7 @@ namespace slb {
 namespace {
 
 constexpr int PNB = 32;          // panel width
-constexpr int PTHREADS = 256;    // rows per CTA of the panel cluster (<= 16 CTAs: n <= 4096)
+constexpr int PTHREADS = 256;    // threads per CTA of the panel cluster (<= 16 CTAs, 1 or 2 rows each: n <= 8192)
 
 // Factor rows [j, n) x cols [j, j + nb) of A in place.  Thread (rank, tid)
 // owns panel row i = rank * PTHREADS + tid in registers.  Per column one
@@ -231,6 +231,9 @@ __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_
 // replayed at the end into a swap list (row pos[s] <- original row org[s]) for
 // panel_swaps_list_kernel.
 constexpr int PNW = PTHREADS / 32;
+// RPT rows per thread (RPT = 2: panels of up to 8192 rows on the 16-CTA cluster): thread tid of
+// CTA rank owns rows rank * RPT * PTHREADS + tid + q * PTHREADS, q < RPT.
+template <int RPT>
 __global__ void __launch_bounds__(PTHREADS) panel32_kernel(double* A, int64_t lda, int64_t n, int64_t j, int nb,
                                                            int32_t* ipiv, DevStatus* status, int block_index,
                                                            int32_t* swl) {
@@ -239,8 +242,13 @@ __global__ void __launch_bounds__(PTHREADS) panel32_kernel(double* A, int64_t ld
   const int ncta = (int)cluster.num_blocks();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t m = n - j;
-  const int64_t i = (int64_t)rank * PTHREADS + tid;
-  const bool own = i < m;
+  int64_t iq[RPT];
+  bool ownq[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; q++) {
+    iq[q] = (int64_t)rank * RPT * PTHREADS + tid + q * PTHREADS;
+    ownq[q] = iq[q] < m;
+  }
   __shared__ __align__(16) double s_row[2][16][PNB];  // candidate rows of all CTAs (pushed)
   __shared__ __align__(16) double s_rec[2][16][2];    // {|a|, row index} of all CTAs (pushed)
   __shared__ __align__(16) double s_krow[2][PNB];     // row k (pushed by CTA 0)
@@ -253,9 +261,11 @@ __global__ void __launch_bounds__(PTHREADS) panel32_kernel(double* A, int64_t ld
   __shared__ int s_pos[2 * PNB], s_org[2 * PNB];
   __shared__ double s_urow[PNB][PNB + 1];  // retired U rows (CTA 0), shifted: [k][c] = U(k, k + c)
 
-  double r[PNB];
+  double rr[RPT][PNB];
 #pragma unroll
-  for (int c = 0; c < PNB; c++) r[c] = (own && c < nb) ? A[(j + c) * lda + j + i] : 0.0;
+  for (int q = 0; q < RPT; q++)
+#pragma unroll
+    for (int c = 0; c < PNB; c++) rr[q][c] = (ownq[q] && c < nb) ? A[(j + c) * lda + j + iq[q]] : 0.0;
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
@@ -280,19 +290,27 @@ __global__ void __launch_bounds__(PTHREADS) panel32_kernel(double* A, int64_t ld
 #pragma unroll 1
   for (int k = 0; k < nb; k++) {
     const int pb = k & 1;
-    const bool live = own && i >= k;  // rows above k have retired
+    bool liveq[RPT];  // rows above k have retired
+#pragma unroll
+    for (int q = 0; q < RPT; q++) liveq[q] = ownq[q] && iq[q] >= k;
     if (tid == 0) mbar_arrive_expect_tx(&s_bar[pb], xbytes);
     // (1) warp argmax (first max by row index); the warp winner stages its row
-    double v = live ? fabs(r[0]) : -1.0;
-    int vi = live ? (int)i : INT_MAX;
+    double v = -1.0;
+    int vi = INT_MAX;
+#pragma unroll
+    for (int q = 0; q < RPT; q++)
+      if (liveq[q]) better(v, vi, fabs(rr[q][0]), (int)iq[q]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) better(v, vi, __shfl_xor_sync(0xffffffffu, v, o), __shfl_xor_sync(0xffffffffu, vi, o));
-    if (live && i == vi)
 #pragma unroll
-      for (int c = 0; c < PNB; c++) s_wrow[pb][warp][c] = r[c];
-    if (live && i == k)
+    for (int q = 0; q < RPT; q++) {
+      if (liveq[q] && iq[q] == vi)
 #pragma unroll
-      for (int c = 0; c < PNB; c++) s_kst[pb][c] = r[c];
+        for (int c = 0; c < PNB; c++) s_wrow[pb][warp][c] = rr[q][c];
+      if (liveq[q] && iq[q] == k)
+#pragma unroll
+        for (int c = 0; c < PNB; c++) s_kst[pb][c] = rr[q][c];
+    }
     if (lane == 0) {
       s_wv[pb][warp] = v;
       s_wi[pb][warp] = vi;
@@ -374,21 +392,24 @@ __global__ void __launch_bounds__(PTHREADS) panel32_kernel(double* A, int64_t ld
       s_piv[k] = bi;
     }
     const double* prow = (bi == k) ? s_krow[pb] : s_row[pb][bc];
-    if (live) {
-      if (i == k) {  // row k retires as the U row: the pivot row (shifted: r[c] = column k + c)
+    const double pv = prow[0];
+    const double pinv = pv != 0.0 ? 1.0 / pv : 0.0;
+#pragma unroll
+    for (int q = 0; q < RPT; q++) {
+      if (!liveq[q]) continue;
+      if (iq[q] == k) {  // row k retires as the U row: the pivot row (shifted: r[c] = column k + c)
 #pragma unroll
         for (int c = 0; c < PNB; c++) s_urow[k][c] = prow[c];
       } else {
-        if (i == bi && bi != k)
+        if (iq[q] == bi && bi != k)
 #pragma unroll
-          for (int c = 0; c < PNB; c++) r[c] = s_krow[pb][c];
+          for (int c = 0; c < PNB; c++) rr[q][c] = s_krow[pb][c];
         // (5) scale, store L, rank-1 update shifted down one column
-        const double pv = prow[0];
-        const double l = r[0] * (pv != 0.0 ? 1.0 / pv : 0.0);
-        A[(j + k) * lda + j + i] = l;
+        const double l = rr[q][0] * pinv;
+        A[(j + k) * lda + j + iq[q]] = l;
 #pragma unroll
-        for (int c = 1; c < PNB; c++) r[c - 1] = fma(-l, prow[c], r[c]);
-        r[PNB - 1] = 0.0;
+        for (int c = 1; c < PNB; c++) rr[q][c - 1] = fma(-l, prow[c], rr[q][c]);
+        rr[q][PNB - 1] = 0.0;
       }
     }
     PP(3)
@@ -637,12 +658,14 @@ bool panel_v1() {
 void panel32(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t j, int nb, int32_t* ipiv,
              DevStatus* status, int block_index, int32_t* swl) {
   const int64_t m = n - j;
-  const int ncta = (int)cdiv(m, PTHREADS);
+  const int rpt = m > 16 * PTHREADS ? 2 : 1;
+  const int ncta = (int)cdiv(m, (int64_t)PTHREADS * rpt);
   if (ncta > 16)
-    throw CudaFailure(cudaErrorInvalidValue, "dgetrf: block dimension > 4096 unsupported", __FILE__, __LINE__);
+    throw CudaFailure(cudaErrorInvalidValue, "dgetrf: block dimension > 8192 unsupported", __FILE__, __LINE__);
   static bool attr = false;
   if (!attr) {
-    SLB_CUDA_CHECK(cudaFuncSetAttribute(panel32_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(panel32_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SLB_CUDA_CHECK(cudaFuncSetAttribute(panel32_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -656,7 +679,8 @@ void panel32(cudaStream_t st, double* A, int64_t lda, int64_t n, int64_t j, int 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel32_kernel, A, lda, n, j, nb, ipiv, status, block_index, swl));
+  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, rpt == 2 ? panel32_kernel<2> : panel32_kernel<1>, A, lda, n, j, nb, ipiv,
+                                    status, block_index, swl));
   count_launch();
 }
 
@@ -953,8 +977,10 @@ __global__ void __launch_bounds__(64) diag_inverse_kernel(int n, const double* _
   for (int r = 0; r < CT; r++) out[(int64_t)c * CT + r] = X[r];
 }
 
-template <int NR>
-__global__ void __launch_bounds__(256) getrs_chain_kernel(int n, int nb, const double* __restrict__ lu,
+// MINB = 2 (two CTAs per SM, registers capped at 128, a few spills) only for blocks beyond
+// 4096 rows, whose chains (2 * n / 64 CTAs) need more than one resident CTA per SM.
+template <int NR, int MINB>
+__global__ void __launch_bounds__(256, MINB) getrs_chain_kernel(int n, int nb, const double* __restrict__ lu,
                                                           const double* __restrict__ dinv,
                                                           const int32_t* __restrict__ perm, const double* b,
                                                           int64_t ldb, double* x, int64_t ldx, double alpha,
@@ -1117,19 +1143,23 @@ void getrs_chain(cudaStream_t st, int64_t n, int64_t nrhs, const double* lu, con
   const int64_t set = 16 * n * cdiv(nrhs, 8);
   double* cur = yz + (epoch & 1) * set;
   double* nxt = yz + ((epoch + 1) & 1) * set;
-  static int resident = 0;  // CTAs of getrs_chain_kernel<8> resident at once on this device
-  if (resident == 0) {
+  static int resident1 = 0, resident2 = 0;  // CTAs of getrs_chain_kernel<8, MINB> resident at once
+  if (resident1 == 0) {
     int dev = 0, sms = 0, per = 0;
     SLB_CUDA_CHECK(cudaGetDevice(&dev));
     SLB_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SLB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, getrs_chain_kernel<8>, 256, 0));
-    resident = std::max(1, sms * per);
+    SLB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, getrs_chain_kernel<8, 1>, 256, 0));
+    resident1 = std::max(1, sms * per);
+    SLB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, getrs_chain_kernel<8, 2>, 256, 0));
+    resident2 = std::max(1, sms * per);
   }
+  const bool two = 2 * nb > resident1;
+  const int resident = two ? resident2 : resident1;
   if (2 * nb > resident)
     throw CudaFailure(cudaErrorInvalidValue, "getrs_chain: block too large for one resident chain", __FILE__, __LINE__);
   const int64_t per_launch = std::max<int64_t>(1, resident / (2 * nb));
 #define SLB_CHAIN(NR, NCH, OFF)                                                                          \
-  getrs_chain_kernel<NR><<<(unsigned)(2 * nb * (NCH)), 256, 0, st>>>(                                    \
+  (two ? getrs_chain_kernel<NR, 2> : getrs_chain_kernel<NR, 1>)<<<(unsigned)(2 * nb * (NCH)), 256, 0, st>>>( \
       (int)n, nb, lu, dinv, perm, b + (OFF) * 8 * ldb, ldb, x + (OFF) * 8 * ldx, ldx, alpha, beta,       \
       cur + (OFF) * 16 * n, nxt + (OFF) * 16 * n, status);                                               \
   count_launch()

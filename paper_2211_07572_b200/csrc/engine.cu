@@ -324,7 +324,7 @@ cudaStream_t green_partition_stream(int dev, int conv_sms) {
   return made[dev];
 }
 
-constexpr int64_t kMaxIfc = 4096;  // stage-two block dimension limit (dgetrf panel cluster, dense.cu)
+constexpr int64_t kMaxIfc = 8192;  // stage-two block dimension limit (dgetrf panel cluster: 16 CTAs x 256 threads x 2 rows, dense.cu)
 
 int sm_count(int dev) {
   int v = 0;

@@ -79,3 +79,18 @@ def test_malformed_rejected():  # :194-216
         t.super[0][1, 2] = bad
         with pytest.raises(S.Error, match="non-finite"):
             S.sweep_build(t)
+
+
+def test_blocks_beyond_4096_rows():
+    """Stage-two envelope: blocks of 5000 rows (the panel cluster holds two rows per thread beyond
+    4096).  Residual of the block-tridiagonal solve, computed blockwise."""
+    k, m = 2, 5000
+    rng = np.random.default_rng(71)
+    diag = [rng.standard_normal((m, m)) + 2.0 * np.sqrt(m) * np.eye(m) for _ in range(k)]
+    sup = [rng.standard_normal((m, m)) for _ in range(k - 1)]
+    sub = [rng.standard_normal((m, m)) for _ in range(k - 1)]
+    t = S.BlockTridiagonal(diag, sup, sub)
+    f = rng.standard_normal(k * m)
+    u = S.sweep_build(t).solve(f)[:, 0]
+    r = np.concatenate([diag[0] @ u[:m] + sup[0] @ u[m:] - f[:m], sub[0] @ u[:m] + diag[1] @ u[m:] - f[m:]])
+    assert np.linalg.norm(r) <= 1e-10 * np.linalg.norm(f)
