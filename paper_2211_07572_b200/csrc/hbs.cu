@@ -259,36 +259,63 @@ __device__ int cta_jacobi_basis(double* M, int64_t ldm, int m, double floor_tol,
     if (threadIdx.x == 0) *sflag = 0;
     __syncthreads();
     for (int s = 0; s < mp - 1; s++) {
-      for (int k = w; k < mp / 2; k += HW) {
-        int p, q;
-        if (k == 0) {
-          p = mp - 1;
-          q = s;
-        } else {
-          p = (s + k) % (mp - 1);
-          q = (s - k + mp - 1) % (mp - 1);
+      // two pairs per warp at a time (their reductions and rotation arithmetic interleave)
+      for (int k0 = w; k0 < mp / 2; k0 += 2 * HW) {
+        double* cp[2];
+        double* cq[2];
+        bool ok[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int k = k0 + h * HW;
+          int p = 0, q = 0;
+          if (k == 0) {
+            p = mp - 1;
+            q = s;
+          } else {
+            p = (s + k) % (mp - 1);
+            q = (s - k + mp - 1) % (mp - 1);
+          }
+          ok[h] = k < mp / 2 && p < m && q < m;
+          cp[h] = M + (int64_t)(ok[h] ? p : 0) * ldm;
+          cq[h] = M + (int64_t)(ok[h] ? q : 0) * ldm;
         }
-        if (p >= m || q >= m) continue;
-        double* cp = M + (int64_t)p * ldm;
-        double* cq = M + (int64_t)q * ldm;
-        double a = 0.0, b = 0.0, c = 0.0;
+        double a[2] = {0.0, 0.0}, b[2] = {0.0, 0.0}, c[2] = {0.0, 0.0};
         for (int r = lane; r < m; r += 32) {
-          const double x = cp[r], y = cq[r];
-          a += x * x;
-          b += y * y;
-          c += x * y;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const double x = cp[h][r], y = cq[h][r];
+            a[h] += x * x;
+            b[h] += y * y;
+            c[h] += x * y;
+          }
         }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        c = warp_sum(c);
-        if (c != 0.0 && fabs(c) > 1e-15 * sqrt(a * b)) {
-          const double zeta = (b - a) / (2.0 * c);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            a[h] += __shfl_xor_sync(0xffffffffu, a[h], o);
+            b[h] += __shfl_xor_sync(0xffffffffu, b[h], o);
+            c[h] += __shfl_xor_sync(0xffffffffu, c[h], o);
+          }
+        double cs[2], sn[2];
+        bool rot[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          rot[h] = ok[h] && c[h] != 0.0 && c[h] * c[h] > 1e-30 * a[h] * b[h];
+          const double zeta = rot[h] ? (b[h] - a[h]) / (2.0 * c[h]) : 0.0;
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          cs[h] = rsqrt(1.0 + t * t);
+          sn[h] = cs[h] * t;
+        }
+        if (rot[0] || rot[1]) {
           for (int r = lane; r < m; r += 32) {
-            const double x = cp[r], y = cq[r];
-            cp[r] = cs * x - sn * y;
-            cq[r] = sn * x + cs * y;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              if (!rot[h]) continue;
+              const double x = cp[h][r], y = cq[h][r];
+              cp[h][r] = cs[h] * x - sn[h] * y;
+              cq[h][r] = sn[h] * x + cs[h] * y;
+            }
           }
           if (lane == 0) *sflag = 1;
         }
