@@ -12,6 +12,8 @@
 // into shared memory with cp.async one block ahead (double buffer), the
 // off-diagonal update is a DMMA GEMM, the 16 x 16 diagonal block is solved
 // per column.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -373,6 +375,155 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
            ph[0], ph[1], ph[2], ph[3], ph[4]);
 #endif
 }
+// Version 2 of the level update, right-looking: per 16-row block b of the TRSM the diagonal
+// block is applied (precomputed inverse) and ALL rows below take the rank-16 update at once
+// (independent 8x8 tiles over the 8 warps), so the sequential depth is one small step per
+// block instead of a left-looking dot product over the growing k range; the GEMM
+// R2 - L21 U1213 accumulates in registers over 16-column blocks of L21 (no per-row-block
+// round trip through shared memory).  L11 / L21 column blocks are staged with cp.async one
+// block ahead.  SLB_UPD_V1=1 selects the left-looking kernel above (A/B).
+constexpr int LCS = RB + 4;  // staged column-block row stride (doubles)
+constexpr int UT = 10;       // output tiles per warp in the GEMM (Wp <= 160: 20 x 4 tiles / 8 warps)
+__global__ void __launch_bounds__(256) level_update2_kernel(LevelArgs a) {
+  extern __shared__ double sm[];
+  const int Wp = a.Wp, s = blockIdx.y;
+  double* X = sm;                  // MMAX * TN   (U1213 tile, swizzled)
+  double* Lc = sm + MMAX * TN;     // 2 x MMAX x LCS (staged column block of L11 / L21)
+  double* Dv = Lc + 2 * MMAX * LCS;  // inverses of L11's 16 x 16 diagonal blocks
+  int* sperm = reinterpret_cast<int*>(Dv + MMAX * RB);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int c0 = blockIdx.x * TN;
+  const double* V = a.sv_in + s * a.sSV + (int64_t)Wp * Wp;
+  const double* NX = a.nx + s * a.sNX;
+  const int32_t* perm = a.perm + s * a.sP;
+  double* slot = a.slot + s * a.sF;
+  const double* LU11 = slot;
+  const double* L21 = slot + (int64_t)Wp * Wp;
+  double* U1213 = slot + 2LL * Wp * Wp;
+  double* svo = a.sv_out + s * a.sSV;
+  const int m = Wp;
+  const int nb = (m + RB - 1) / RB;
+  const int mt_all = m / 8;  // Wp is a multiple of 8
+  const int ncol = min(TN, 2 * Wp - c0);
+  // rows [rlo, m) of column block kb of a row-major m x m matrix -> Lc[buf][row][0..16)
+  auto stage_cols = [&](const double* T, int kb, int rlo, int buf) {
+    const int k0 = kb * RB, kw = min(m, k0 + RB) - k0;  // kw is a multiple of 8
+    const int pieces = kw / 2;                           // 16-byte pieces per row
+    double* dst = Lc + buf * MMAX * LCS;
+    const int total = (m - rlo) * pieces;
+    const float inv_p = 1.0f / (float)pieces;
+    for (int idx = tid; idx < total; idx += 256) {
+      const int rr = qdiv(idx, inv_p), c = 2 * (idx - rr * pieces);
+      const int row = rlo + rr;
+      cp_async16(dst + row * LCS + c, T + (int64_t)row * m + k0 + c, true);
+    }
+    cp_async_commit();
+  };
+  // ---- R1 tile -> X (gathered through perm, asynchronous), diagonal-block inverses
+  for (int i = tid; i < 2 * Wp; i += 256) sperm[i] = perm[i];
+  __syncthreads();
+  const float inv_m = 1.0f / (float)m;
+  for (int idx = tid; idx < m * TN; idx += 256) {
+    const int n = qdiv(idx, inv_m), r = idx - n * m;
+    const int p = sperm[r], c = c0 + n;
+    double* dst = &X[sw32(r, n)];
+    if (n >= ncol || (p < Wp && c >= Wp)) *dst = 0.0;
+    else cp_async8(dst, p < Wp ? V + (int64_t)c * Wp + p : NX + (int64_t)(Wp + c) * Wp + (p - Wp), true);
+  }
+  cp_async_commit();
+  for (int idx = m * TN + tid; idx < nb * RB * TN; idx += 256) X[idx] = 0.0;
+#ifdef SLB_UPD_PROF
+  long long Q0 = clock64(), qh[4] = {0, 0, 0, 0};
+#define UQ(k_) { const long long q_ = clock64(); qh[k_] += q_ - Q0; Q0 = q_; }
+#else
+#define UQ(k_)
+#endif
+  stage_cols(LU11, 0, min(m, RB), 0);
+  diag_inverses<true, true>(LU11, Wp, m, nb, Dv, tid, 256);
+  UQ(0)
+  // ---- TRSM, right-looking: X = L11^{-1} X (unit lower)
+  for (int b = 0; b < nb; b++) {
+    const int r0 = b * RB, r1 = min(m, r0 + RB);
+    cp_async_wait<0>();
+    __syncthreads();  // X (gather, previous trailing updates) and column block b staged
+    apply_diag_inverse(Dv + b * RB * RB, X, r0, r1, warp, g, t);
+    __syncthreads();
+    if (b + 1 < nb) stage_cols(LU11, b + 1, min(m, r1 + RB), (b + 1) & 1);
+    // X[r1:m] -= L11[r1:m, r0:r1] X[r0:r1]: (rows below) x 4 column tiles over the 8 warps
+    const double* lc = Lc + (b & 1) * MMAX * LCS;
+    const int mt0 = r1 / 8, ntile = (mt_all - mt0) * 4;
+    for (int tile = warp; tile < ntile; tile += 8) {
+      const int mt = mt0 + (tile >> 2), nt = tile & 3;
+      const int row = mt * 8 + g;
+      double d0 = X[sw32(row, nt * 8 + 2 * t)], d1 = X[sw32(row, nt * 8 + 2 * t + 1)];
+#pragma unroll
+      for (int kk = 0; kk < RB / 4; kk++) {
+        const int k = kk * 4 + t;
+        if (r0 + kk * 4 < r1)
+          dmma884(d0, d1, -lc[row * LCS + k], X[sw32(r0 + k, nt * 8 + g)]);
+      }
+      X[sw32(row, nt * 8 + 2 * t)] = d0;
+      X[sw32(row, nt * 8 + 2 * t + 1)] = d1;
+    }
+  }
+  __syncthreads();
+  UQ(1)
+  // ---- U1213 tile out; the GEMM's first L21 column block
+  stage_cols(L21, 0, 0, 0);
+  for (int idx = tid; idx < m * ncol; idx += 256) {
+    const int n = qdiv(idx, inv_m), r = idx - n * m;
+    U1213[(int64_t)(c0 + n) * Wp + r] = X[sw32(r, n)];
+  }
+  // ---- GEMM: out = R2 - L21 X, accumulated over column blocks of L21
+  double acc[UT][2];
+  double r2v[UT][2];
+  const int ntiles = mt_all * 4;
+#pragma unroll
+  for (int i = 0; i < UT; i++) {
+    acc[i][0] = acc[i][1] = 0.0;
+    r2v[i][0] = r2v[i][1] = 0.0;
+    const int tile = warp + 8 * i;
+    if (tile < ntiles) {
+      const int row = (tile >> 2) * 8 + g, col = c0 + (tile & 3) * 8 + 2 * t;
+      const int p = sperm[Wp + row];
+      if (col < 2 * Wp) r2v[i][0] = p < Wp ? (col < Wp ? V[(int64_t)col * Wp + p] : 0.0)
+                                           : NX[(int64_t)(Wp + col) * Wp + (p - Wp)];
+      if (col + 1 < 2 * Wp) r2v[i][1] = p < Wp ? (col + 1 < Wp ? V[(int64_t)(col + 1) * Wp + p] : 0.0)
+                                               : NX[(int64_t)(Wp + col + 1) * Wp + (p - Wp)];
+    }
+  }
+  for (int kb = 0; kb < nb; kb++) {
+    cp_async_wait<0>();
+    __syncthreads();
+    if (kb + 1 < nb) stage_cols(L21, kb + 1, 0, (kb + 1) & 1);
+    const double* lc = Lc + (kb & 1) * MMAX * LCS;
+    const int k0 = kb * RB, kw = min(m, k0 + RB) - k0;
+#pragma unroll
+    for (int i = 0; i < UT; i++) {
+      const int tile = warp + 8 * i;
+      if (tile >= ntiles) break;
+      const int row = (tile >> 2) * 8 + g, nt = tile & 3;
+#pragma unroll
+      for (int kk = 0; kk < RB / 4; kk++)
+        if (kk * 4 < kw)
+          dmma884(acc[i][0], acc[i][1], lc[row * LCS + kk * 4 + t], X[sw32(k0 + kk * 4 + t, nt * 8 + g)]);
+    }
+  }
+  UQ(2)
+#ifdef SLB_UPD_PROF
+  if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && (a.level % 1000) == 1)
+    printf("UPD2 l=%d: gather+inverses %lld trsm %lld gemm %lld (cycles)\n", a.level, qh[0], qh[1], qh[2]);
+#endif
+#pragma unroll
+  for (int i = 0; i < UT; i++) {
+    const int tile = warp + 8 * i;
+    if (tile >= ntiles) break;
+    const int row = (tile >> 2) * 8 + g, col = c0 + (tile & 3) * 8 + 2 * t;
+    if (col < 2 * Wp) svo[(int64_t)col * Wp + row] = r2v[i][0] - acc[i][0];
+    if (col + 1 < 2 * Wp) svo[(int64_t)(col + 1) * Wp + row] = r2v[i][1] - acc[i][1];
+  }
+}
 }  // namespace
 
 void level_update(cudaStream_t st, const LevelArgs& a) {
@@ -383,7 +534,18 @@ void level_update(cudaStream_t st, const LevelArgs& a) {
     attr = true;
   }
   dim3 grid((unsigned)cdiv(2 * a.Wp, TN), (unsigned)a.nstrips);
-  level_update_kernel<<<grid, 256, smem, st>>>(a); count_launch();
+  static const bool v1 = getenv("SLB_UPD_V1") != nullptr;
+  if (v1) {
+    level_update_kernel<<<grid, 256, smem, st>>>(a); count_launch();
+  } else {
+    const size_t smem2 = (size_t)(MMAX * TN + 2 * MMAX * LCS + MMAX * RB) * sizeof(double) + 2 * MMAX * sizeof(int);
+    static bool attr2 = false;
+    if (!attr2) {
+      SLB_CUDA_CHECK(cudaFuncSetAttribute(level_update2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      attr2 = true;
+    }
+    level_update2_kernel<<<grid, 256, smem2, st>>>(a); count_launch();
+  }
   SLB_CUDA_CHECK(cudaGetLastError());
 }
 }  // namespace slb
