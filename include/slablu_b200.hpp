@@ -221,6 +221,43 @@ inline SlabPartition partition(int64_t n1, int64_t n2, int64_t b) {
   return p;
 }
 
+// ---- randomized HBS compression of a dense operator (hbs_compress.hpp:21-311) ---
+struct CompressOptions {
+  double tol = 1e-10;
+  double trunc_rel = 1e-12;
+  uint64_t seed = 0;
+};
+struct CompressStats {
+  int64_t products_normal = 0, products_adjoint = 0;
+  int rounds = 0;
+  int64_t final_rank = 0;
+  double residual_estimate = 0.0;
+};
+namespace detail {
+inline std::vector<double> hbs_run(const std::vector<double>& m, int64_t n, int64_t leaf, int64_t r_start,
+                                   int64_t r_max, int adaptive, const CompressOptions& o, CompressStats* st) {
+  if ((int64_t)m.size() != n * n) throw Error("hbs_compress: dimension mismatch");
+  std::vector<double> out((size_t)(n * n));
+  slablu_gpu_hbs_stats s{};
+  check(slablu_gpu_hbs_compress(n, m.data(), leaf, r_start, r_max, adaptive, o.tol, o.trunc_rel, o.seed, 0,
+                                out.data(), &s));
+  if (st) *st = CompressStats{s.products_normal, s.products_adjoint, s.rounds, s.final_rank, s.residual_estimate};
+  return out;
+}
+}  // namespace detail
+// hbs_compress with the dense sampler (test_hbs.cpp:64-68) on a column-major n x n operator;
+// returns the dense materialization of the compressed operator (HbsMatrix::to_dense).
+inline std::vector<double> hbs_compress(const std::vector<double>& m, int64_t n, int64_t leaf_size,
+                                        int64_t rank_bound, const CompressOptions& o = {},
+                                        CompressStats* stats = nullptr) {
+  return detail::hbs_run(m, n, leaf_size, 0, rank_bound, 0, o, stats);
+}
+inline std::vector<double> hbs_compress_adaptive(const std::vector<double>& m, int64_t n, int64_t leaf_size,
+                                                 int64_t r_start, int64_t r_max, const CompressOptions& o = {},
+                                                 CompressStats* stats = nullptr) {
+  return detail::hbs_run(m, n, leaf_size, r_start, r_max, 1, o, stats);
+}
+
 // ---- factorize / solve (driver.hpp:72-179) -----------------------------------
 class Factorization {
  public:

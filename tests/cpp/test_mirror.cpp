@@ -90,9 +90,46 @@ static void gpu_checks() {
   CHECK(threw);
 }
 
+static void hbs_checks() {
+  // hbs_compress of a diagonal-plus-rank-5 operator (test_hbs.cpp:307-341) and the failure at
+  // the rank ceiling (:343-359), through the C++ mirror
+  const int64_t n = 96;
+  std::vector<double> m((size_t)(n * n), 0.0);
+  for (int64_t j = 0; j < n; j++)
+    for (int64_t i = 0; i < n; i++) {
+      double v = i == j ? 20.0 : 0.0;
+      for (int k = 0; k < 5; k++) v += std::sin(0.3 * double(i + 1) * (k + 1)) * std::cos(0.7 * double(j + 2) * (k + 1));
+      m[(size_t)(i + j * n)] = v;
+    }
+  S::CompressStats st;
+  const std::vector<double> h = S::hbs_compress_adaptive(m, n, 12, 2, 64, S::CompressOptions{1e-10, 1e-12, 37}, &st);
+  double num = 0, den = 0;
+  for (size_t e = 0; e < m.size(); e++) {
+    num += (h[e] - m[e]) * (h[e] - m[e]);
+    den += m[e] * m[e];
+  }
+  CHECK(std::sqrt(num / den) <= 1e-10);
+  CHECK(st.final_rank <= 10 && st.rounds <= 3);
+  bool threw = false;
+  try {
+    S::hbs_compress(m, n, 12, 2, S::CompressOptions{1e-10, 1e-12, 43});
+  } catch (const S::CompressionError& e) {
+    threw = e.residual_estimate > 1e-10;
+  }
+  CHECK(threw);
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::strcmp(argv[1], "sizes") == 0) {  // struct layouts for the ctypes mirror
+    std::printf("%zu %zu %zu %zu\n", sizeof(slablu_gpu_config), sizeof(slablu_gpu_status), sizeof(slablu_gpu_stats_t),
+                sizeof(slablu_gpu_hbs_stats));
+    return 0;
+  }
   host_checks();
-  if (argc > 1 && std::strcmp(argv[1], "gpu") == 0) gpu_checks();
+  if (argc > 1 && std::strcmp(argv[1], "gpu") == 0) {
+    gpu_checks();
+    hbs_checks();
+  }
   std::printf("%s (%d failures)\n", failures ? "FAIL" : "OK", failures);
   return failures ? 1 : 0;
 }

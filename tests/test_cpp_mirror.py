@@ -24,6 +24,17 @@ def test_mirror_host():
     assert r.returncode == 0, r.stderr + r.stdout
 
 
+def test_ctypes_struct_layouts_match_the_header():
+    """The Python mirror's ctypes structs have the C header's sizes (config, status, stats)."""
+    from paper_2211_07572_b200 import _lib
+    b = build_binary()
+    r = subprocess.run([b, "sizes"], capture_output=True, text=True, check=True)
+    cfg, st, stats, hbs = (int(x) for x in r.stdout.split())
+    import ctypes
+    assert (cfg, st, stats, hbs) == (ctypes.sizeof(_lib.Config), ctypes.sizeof(_lib.Status),
+                                     ctypes.sizeof(_lib.Stats), ctypes.sizeof(_lib.HbsStatsT))
+
+
 @pytest.mark.gpu
 def test_mirror_gpu():
     b = build_binary()
