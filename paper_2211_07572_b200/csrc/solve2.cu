@@ -1010,7 +1010,9 @@ int strip_solve2_cluster(int Wp, int64_t n2, int ntasks) {
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   const int MTH = Wp / 8;
-  int best = std::min(4, MTH);
+  // no size fits every task at once (many right-hand sides: tasks run in waves): 3-CTA clusters,
+  // more of them resident per wave (measured at cfg4, 64 RHS: 1.42 vs 1.56 ms per RHS with 4)
+  int best = strip_solve2_fits(Wp, n2, 3) ? 3 : std::min(4, MTH);
   for (int G : {8, 6, 5, 4}) {
     if (!strip_solve2_fits(Wp, n2, G)) continue;
     const size_t smem = (size_t)lay2(Wp, G, n2).bytes;
