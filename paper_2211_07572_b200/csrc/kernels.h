@@ -147,8 +147,8 @@ void strip_solve(cudaStream_t st, const SchurArgs& a, int ntasks);  // launches 
 void strip_rhs_pack(cudaStream_t st, const SchurArgs& a, int ntasks);
 // Version 2 (solve2.cu): TMA tensor slices + st.async level exchange, cluster size chosen at run
 // time (2..8 CTAs); ybuf as for strip_solve.
-bool strip_solve2_fits(int Wp, int64_t n2, int G);
-int strip_solve2_cluster(int Wp, int64_t n2, int ntasks);
+bool strip_solve2_fits(int Wp, int64_t n2, int G, bool dmma_only = false);
+int strip_solve2_cluster(int Wp, int64_t n2, int ntasks, bool dmma = false);
 void strip_solve2(cudaStream_t st, const SchurArgs& a, int ntasks);
 
 // T block assembly from per-strip G buffers (reference order: direct, left strip, right strip).

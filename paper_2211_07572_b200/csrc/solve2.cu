@@ -991,28 +991,31 @@ CUtensorMap make_map(const double* base, int mt, int tile_stride, int k4rows, in
 }
 
 
-bool strip_solve2_fits(int Wp, int64_t n2, int G) {
+bool strip_solve2_fits(int Wp, int64_t n2, int G, bool dmma_only) {
   const int MTH = Wp / 8;
   if (G < 1 || G > 8 || G > MTH || (MTH + G - 1) / G > MNMAX) return false;
-  if ((MTH + G - 1) / G > NCW_DFMA) return false;  // the DFMA variants' row-tile warps
+  if (!dmma_only && (MTH + G - 1) / G > NCW_DFMA) return false;  // the DFMA variants' row-tile warps
   return lay2(Wp, G, n2).bytes <= 227 * 1024 - 1024;
 }
 
 // Cluster size for ntasks concurrent tasks: the largest G in {8, 6, 5, 4} whose clusters all fit at
 // once (cudaOccupancyMaxActiveClusters), else 4.
-int strip_solve2_cluster(int Wp, int64_t n2, int ntasks) {
+int strip_solve2_cluster(int Wp, int64_t n2, int ntasks, bool dmma) {
   static std::mutex mu;
   static std::map<std::pair<int, int64_t>, int> cache;  // (Wp, n2 * 1024 + ntasks) -> G
   const char* e = getenv("SLB_SOLVE_G");
   if (e) return std::min(atoi(e), Wp / 8);
+  const char* e2 = getenv("SLB_SOLVE_G_WAVES");  // cluster size when the tasks run in waves (A/B)
   std::lock_guard<std::mutex> lk(mu);
-  const auto key = std::make_pair(Wp, n2 * 1024 + ntasks);
+  const auto key = std::make_pair(Wp * 2 + (dmma ? 1 : 0), n2 * 1024 + ntasks);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   const int MTH = Wp / 8;
-  // no size fits every task at once (many right-hand sides: tasks run in waves): 3-CTA clusters,
-  // more of them resident per wave (measured at cfg4, 64 RHS: 1.42 vs 1.56 ms per RHS with 4)
-  int best = strip_solve2_fits(Wp, n2, 3) ? 3 : std::min(4, MTH);
+  // no size fits every task at once (many right-hand sides: tasks run in waves): small clusters,
+  // more of them resident per wave (cfg4, 64 RHS on the DMMA variant: 1.31 ms per RHS with 2-CTA
+  // clusters, 1.42 with 3, 1.56 with 4)
+  int best = (dmma && strip_solve2_fits(Wp, n2, 2, true)) ? 2 : strip_solve2_fits(Wp, n2, 3) ? 3 : std::min(4, MTH);
+  if (e2) best = std::min(atoi(e2), MTH);
   for (int G : {8, 6, 5, 4}) {
     if (!strip_solve2_fits(Wp, n2, G)) continue;
     const size_t smem = (size_t)lay2(Wp, G, n2).bytes;
@@ -1047,8 +1050,9 @@ int strip_solve2_cluster(int Wp, int64_t n2, int ntasks) {
 
 void strip_solve2(cudaStream_t st, const SchurArgs& a, int ntasks) {
   const int Wp = a.Wp;
-  const int G = strip_solve2_cluster(Wp, a.n2, ntasks);
-  if (!strip_solve2_fits(Wp, a.n2, G))
+  const bool dmma = a.nrhs > 4 || getenv("SLB_SOLVE_DMMA") != nullptr;
+  const int G = strip_solve2_cluster(Wp, a.n2, ntasks, dmma);
+  if (!strip_solve2_fits(Wp, a.n2, G, dmma))
     throw CudaFailure(cudaErrorInvalidValue, "strip_solve2: slab too wide for the cluster split", __FILE__, __LINE__);
   strip_rhs_pack(st, a, ntasks);
   const Lay2 Ly = lay2(Wp, G, a.n2);
