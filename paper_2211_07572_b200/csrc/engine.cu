@@ -560,6 +560,15 @@ void hbs_reduce(slablu_gpu_fact* F, const slablu_gpu_config& c) {
     jk.push_back({j + 1, j});
   }
   std::vector<HbsStats> stats(blocks.size());
+  {
+    // the compression works in stream-ordered allocations sized by the free memory: blocks the
+    // exact-size pool keeps from earlier factorizations would shrink its batches to one block
+    size_t fr = 0, tot = 0;
+    SLB_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+    const HbsFootprint fp = hbs_footprint(n2, o);
+    const double want = fp.densify + fp.per_block * (double)blocks.size();
+    if (0.6 * (double)fr < want && pool().cached_bytes(F->device) > 0) pool().trim(F->device);
+  }
   cudaEvent_t h0, h1;
   SLB_CUDA_CHECK(cudaEventCreate(&h0));
   SLB_CUDA_CHECK(cudaEventCreate(&h1));

@@ -769,6 +769,20 @@ const size_t kSmemBytes = (2 * 16 * 65 + 32 + 8) * sizeof(double);
 
 }  // namespace
 
+// Device bytes one block needs at the largest round (pools + arenas), and the densify temporaries.
+HbsFootprint hbs_footprint(int64_t n, const HbsOptions& o) {
+  Tree tt = build_tree((int)n, std::max(1, std::min<int>(o.leaf, (int)n)));
+  const int64_t r_top = o.fixed_rank ? o.r_max : std::max<int64_t>(o.r_max, 2);
+  const int64_t S_top = sample_count(r_top) + 4 * 64;
+  const Layout Lt = plan_layout(tt, (int)r_top, (int)S_top);
+  HbsFootprint f;
+  f.per_block = 8.0 * (double)(4 * n * S_top + Lt.persist + Lt.work + Lt.hats[0] + Lt.hats[1] + 24 * n);
+  int64_t sum_rcap = 0;
+  for (const NodeDesc& nd : tt.nodes) sum_rcap += nd.rcap;
+  f.densify = 8.0 * (double)(n * n + 2 * sum_rcap * n);
+  return f;
+}
+
 // Compress nb dense n x n blocks (device, column major, ld n) in place: each becomes the dense
 // materialization of its HBS approximation.  seeds[i] is the block's CompressOptions.seed.
 // fixed_rank: hbs_compress with rank bound r_max (one round); else hbs_compress_adaptive.
@@ -793,20 +807,12 @@ void hbs_compress_blocks(cudaStream_t st, int64_t n, int nb, double* const* bloc
     attr = true;
   }
   // blocks per group from the largest round's footprint (pools + arenas + the densify temporaries)
-  const int64_t r_top = o.fixed_rank ? o.r_max : std::max<int64_t>(o.r_max, 2);
-  const int64_t S_top = sample_count(r_top) + 4 * 64;
   {
-    Tree tt = tree;
-    const Layout Lt = plan_layout(tt, (int)r_top, (int)S_top);
-    const double per_block =
-        8.0 * (double)(4 * n * S_top + Lt.persist + Lt.work + Lt.hats[0] + Lt.hats[1] + 24 * n);
-    int64_t sum_rcap = 0;
-    for (const NodeDesc& nd : tt.nodes) sum_rcap += nd.rcap;
-    const double densify = 8.0 * (double)(n * n + 2 * sum_rcap * n);
+    const HbsFootprint fp = hbs_footprint(n, o);
     size_t fr = 0, tot = 0;
     SLB_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
-    const double budget = 0.6 * (double)fr - densify;
-    const int group = (int)std::max<double>(1.0, std::min<double>(256.0, budget / per_block));
+    const double budget = 0.6 * (double)fr - fp.densify;
+    const int group = (int)std::max<double>(1.0, std::min<double>(256.0, budget / fp.per_block));
     if (group < nb) {
       for (int g0 = 0; g0 < nb; g0 += group) {
         const int ng = std::min(group, nb - g0);
@@ -815,6 +821,34 @@ void hbs_compress_blocks(cudaStream_t st, int64_t n, int nb, double* const* bloc
       return;
     }
   }
+  const int64_t r_top = o.fixed_rank ? o.r_max : std::max<int64_t>(o.r_max, 2);
+  const int64_t S_top = sample_count(r_top) + 4 * 64;
+  // the rounds allocate and free their arenas stream-ordered: keep the pool's memory mapped across
+  // rounds (a release threshold of 0 would unmap and remap gigabytes at every synchronization)
+  // and hand it back to the device once the compression is done
+  struct PoolKeep {
+    cudaMemPool_t pool = nullptr;
+    uint64_t old = 0;
+    cudaStream_t st;
+    explicit PoolKeep(cudaStream_t s) : st(s) {
+      int dev = 0;
+      if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) {
+        cudaGetLastError();
+        pool = nullptr;
+        return;
+      }
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &old);
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    ~PoolKeep() {
+      if (!pool) return;
+      cudaStreamSynchronize(st);
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &old);
+      cudaMemPoolTrimTo(pool, (size_t)old);
+      cudaGetLastError();
+    }
+  } keep_pool(st);
   DevMem mem{st, {}};
   const int B = nb;
   // per block pools (OM | Y | PS | Z), n x Smax each

@@ -216,5 +216,9 @@ struct HbsStats {
 // Throws HostError (SLABLU_ERR_COMPRESSION with the residual, or SLABLU_ERR_CONFIG).
 void hbs_compress_blocks(cudaStream_t st, int64_t n, int nb, double* const* blocks, const uint64_t* seeds,
                          const HbsOptions& o, HbsStats* stats);
+struct HbsFootprint {
+  double per_block, densify;  // bytes
+};
+HbsFootprint hbs_footprint(int64_t n, const HbsOptions& o);
 
 }  // namespace slb
