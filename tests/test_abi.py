@@ -105,3 +105,10 @@ def test_no_cpu_fallback_without_device():
     sysm = S.assemble_fd5(S.poisson_log_problem(16, 16))
     with pytest.raises(S.Error, match="no CUDA device"):
         S.factorize(sysm, S.SolverConfig(b=4))
+    # the other compute entry points fail the same way (HBS compression, stage two on caller
+    # blocks): no CPU path behind any of them
+    with pytest.raises(S.Error, match="no CUDA device"):
+        S.hbs_compress(np.eye(32), 8, 4)
+    eye = np.eye(4)
+    with pytest.raises(S.Error, match="no CUDA device"):
+        S.sweep_build(S.BlockTridiagonal([eye] * 2, [eye], [eye]))
