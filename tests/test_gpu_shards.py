@@ -129,3 +129,19 @@ def test_engine_multiprocess_gloo(tmp_path):
     so = O.assemble_canned(2, n1, n2, kappa)
     uo = O.factorize(so, b=b).solve(so.rhs)[:, 0]
     assert np.linalg.norm(u - uo) / np.linalg.norm(uo) < 1e-10
+
+
+def test_shards_compression_choice():
+    """A shard holds partial separator blocks, so it cannot compress them: compression = hbs is
+    rejected (UnsupportedError) and automatic resolves to dense even on long interfaces."""
+    n1 = n2 = 512
+    sysm = S.assemble_fd5(S.poisson_log_problem(n1, n2))
+    dev = torch.device("cuda", 0)
+    rp = torch.from_numpy(sysm.row_ptr).to(dev)
+    ci = torch.from_numpy(sysm.col_idx).to(dev)
+    v = torch.from_numpy(sysm.values).to(dev)
+    with pytest.raises(S.UnsupportedError):
+        D.Shard(n1, n2, rp, ci, v, S.SolverConfig(b=40, compression=S.CompressionChoice.hbs), 0, 2)
+    sh = D.Shard(n1, n2, rp, ci, v, S.SolverConfig(b=40), 0, 2)  # automatic, n2 >= 512, b >= 16
+    assert int(sh.stats.compression) == 1
+    sh.close()
