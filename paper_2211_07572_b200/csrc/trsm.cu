@@ -153,10 +153,19 @@ __global__ void __launch_bounds__(256) trsm_small_kernel(int m, const double* __
   };
   stage(0, 0);
   cp_async_commit();
+  bool nz = false;
   for (int idx = tid; idx < m * TN; idx += 256) {
     const int n = idx / m, r = idx % m;
     const int64_t c = c0 + n;
-    X[sw32(r, n)] = c < ncols ? B[c * ldb + r] : 0.0;
+    const double v = c < ncols ? B[c * ldb + r] : 0.0;
+    nz |= v != 0.0;
+    X[sw32(r, n)] = v;
+  }
+  // an all-zero right-hand-side tile has the zero solution, already in place (the U13 columns of
+  // the level conversion are zero but for the few rows pivoted up from the next level)
+  if (!__syncthreads_or(nz)) {
+    cp_async_wait<0>();
+    return;
   }
   for (int idx = m * TN + tid; idx < nb * RB * TN; idx += 256) X[idx] = 0.0;  // padding rows of the last block
   diag_inverses<LOWER, ROWMAJOR>(T, ldt, m, nb, Dv, tid, 256);
