@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <vector>
 #include <climits>
 #include <cstdlib>
 #include <cooperative_groups.h>
@@ -541,6 +542,95 @@ __global__ void __launch_bounds__(256) panel_swaps_list_kernel(double* A, int64_
   if (a1) col[s_pos[lane + 32]] = v1;
 }
 
+// The same interchanges restricted to column ranges (the look-ahead LU splits them between its
+// two streams): warps [0, own) fix the panel's own L columns, the next ones take the columns
+// [a0, a1) and then [b0, b1).
+__global__ void __launch_bounds__(256) panel_swaps_range_kernel(double* A, int64_t lda, int64_t j, int nb,
+                                                               const int32_t* swl, const int32_t* ipiv, int own,
+                                                               int64_t a0, int64_t a1, int64_t b0, int64_t b1) {
+  __shared__ int s_cnt;
+  __shared__ int s_pos[2 * PNB], s_org[2 * PNB];
+  if (threadIdx.x == 0) s_cnt = swl[0];
+  if (threadIdx.x < 2 * PNB) {
+    s_pos[threadIdx.x] = swl[1 + threadIdx.x];
+    s_org[threadIdx.x] = swl[1 + 2 * PNB + threadIdx.x];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (w < own) {
+    panel_column_swaps(A + (j + w) * lda, j, nb, (int)w, ipiv, lane);
+    return;
+  }
+  w -= own;
+  int64_t c;
+  if (w < a1 - a0) {
+    c = a0 + w;
+  } else {
+    w -= a1 - a0;
+    if (w >= b1 - b0) return;
+    c = b0 + w;
+  }
+  double* col = A + c * lda;
+  const int cnt = s_cnt;
+  const bool f0 = lane < cnt && s_pos[lane] != s_org[lane];
+  const bool f1 = lane + 32 < cnt && s_pos[lane + 32] != s_org[lane + 32];
+  const double v0 = f0 ? col[s_org[lane]] : 0.0;
+  const double v1 = f1 ? col[s_org[lane + 32]] : 0.0;
+  __syncwarp();
+  if (f0) col[s_pos[lane]] = v0;
+  if (f1) col[s_pos[lane + 32]] = v1;
+}
+
+// The interchanges of nl consecutive panels (their swap lists, in order) on the columns
+// [a0, a1) and [b0, b1): one warp per column replays the lists one after the other.
+constexpr int MAXL = 8;  // panels per look-ahead block (<= 256 columns)
+__global__ void __launch_bounds__(256) swaps_multi_kernel(double* A, int64_t lda, const int32_t* lists, int nl,
+                                                         int64_t a0, int64_t a1, int64_t b0, int64_t b1) {
+  __shared__ int s_cnt[MAXL];
+  __shared__ int s_pos[MAXL][2 * PNB], s_org[MAXL][2 * PNB];
+  for (int i = threadIdx.x; i < nl * 2 * PNB; i += blockDim.x) {
+    const int l = i / (2 * PNB), e = i % (2 * PNB);
+    const int32_t* sl = lists + l * SWL;
+    s_pos[l][e] = sl[1 + e];
+    s_org[l][e] = sl[1 + 2 * PNB + e];
+    if (e == 0) s_cnt[l] = sl[0];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  int64_t c;
+  if (w < a1 - a0) {
+    c = a0 + w;
+  } else {
+    w -= a1 - a0;
+    if (w >= b1 - b0) return;
+    c = b0 + w;
+  }
+  double* col = A + c * lda;
+  for (int l = 0; l < nl; l++) {
+    const int cnt = s_cnt[l];
+    const bool f0 = lane < cnt && s_pos[l][lane] != s_org[l][lane];
+    const bool f1 = lane + 32 < cnt && s_pos[l][lane + 32] != s_org[l][lane + 32];
+    const double v0 = f0 ? col[s_org[l][lane]] : 0.0;
+    const double v1 = f1 ? col[s_org[l][lane + 32]] : 0.0;
+    __syncwarp();
+    if (f0) col[s_pos[l][lane]] = v0;
+    if (f1) col[s_pos[l][lane + 32]] = v1;
+    __syncwarp();
+  }
+}
+
+void swaps_multi(cudaStream_t st, double* A, int64_t lda, const int32_t* lists, int nl, int64_t a0, int64_t a1,
+                 int64_t b0, int64_t b1) {
+  const int64_t tot = std::max<int64_t>(0, a1 - a0) + std::max<int64_t>(0, b1 - b0);
+  if (tot <= 0 || nl <= 0) return;
+  swaps_multi_kernel<<<(unsigned)cdiv(tot, (int64_t)8), 256, 0, st>>>(A, lda, lists, nl, a0, std::max(a0, a1), b0,
+                                                                     std::max(b0, b1));
+  count_launch();
+  SLB_CUDA_CHECK(cudaGetLastError());
+}
+
 // Row interchanges ipiv[k1..k2) (LAPACK order) as one permutation of rows
 // [k1, n): idx[r - k1] = source row of row r.  One CTA, swaps replayed in
 // shared memory by one thread (n - k1 <= 8192).
@@ -778,10 +868,161 @@ void getrf_rec(cudaStream_t st, double* A, int64_t n, int64_t c0, int64_t c1, in
   getrf_rec(st, A, n, c0 + h, c1, ipiv, status, block_index, swl, cmax);
 }
 
+// Streams of the look-ahead LU (per host thread and device): the panel chain on a
+// greatest-priority stream, the trailing updates on a least-priority one.
+struct LaStreams {
+  cudaStream_t hi = nullptr, lo = nullptr;
+  cudaEvent_t ev[4] = {};
+};
+LaStreams& la_streams() {
+  thread_local std::map<int, LaStreams> per_dev;
+  int dev = 0;
+  SLB_CUDA_CHECK(cudaGetDevice(&dev));
+  LaStreams& s = per_dev[dev];
+  if (!s.hi) {
+    int least = 0, greatest = 0;
+    SLB_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    SLB_CUDA_CHECK(cudaStreamCreateWithPriority(&s.hi, cudaStreamNonBlocking, greatest));
+    SLB_CUDA_CHECK(cudaStreamCreateWithPriority(&s.lo, cudaStreamNonBlocking, least));
+    for (auto& e : s.ev) SLB_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  return s;
+}
+
+bool getrf_rec_only() {
+  static const bool v = [] {
+    const char* e = getenv("SLB_GETRF_REC");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+// Recursive LU of the block [c0, c1) inside the look-ahead LU: like getrf_rec, but the
+// interchanges touch only the block's own columns (the caller applies them elsewhere from the
+// swap lists, kept one per 32-column panel at lists + ((j - cb) / 32) * SWL).
+void getrf_blk(cudaStream_t st, double* A, int64_t n, int64_t c0, int64_t c1, int64_t cb, int64_t ce,
+               int32_t* ipiv, DevStatus* status, int block_index, int32_t* lists) {
+  const int64_t w = c1 - c0;
+  if (w <= PNB) {
+    int32_t* sw = lists + ((c0 - cb) / PNB) * SWL;
+    panel32(st, A, n, n, c0, (int)w, ipiv, status, block_index, sw);
+    const int64_t tot = w + (c0 - cb) + (ce - c1);
+    panel_swaps_range_kernel<<<(unsigned)cdiv(tot, (int64_t)8), 256, 0, st>>>(A, n, c0, (int)w, sw, ipiv, (int)w, cb,
+                                                                             c0, c1, ce);
+    count_launch();
+    SLB_CUDA_CHECK(cudaGetLastError());
+    return;
+  }
+  int64_t h = round_up(w / 2, PNB);
+  if (h >= w) h = w - PNB;
+  getrf_blk(st, A, n, c0, c0 + h, cb, ce, ipiv, status, block_index, lists);
+  trsm(st, true, A + c0 * n + c0, n, h, A + (c0 + h) * n + c0, n, w - h);
+  dgemm_batched(st, n - c0 - h, w - h, h, -1.0, A + c0 * n + c0 + h, n, 0, A + (c0 + h) * n + c0, n, 0, 1.0,
+                A + (c0 + h) * n + c0 + h, n, 0, 1);
+  getrf_blk(st, A, n, c0 + h, c1, cb, ce, ipiv, status, block_index, lists);
+}
+
+// LU of columns [c0, c1) (rows c0..n) of the n x n matrix A with look-ahead: blocks of NBW
+// columns, each factored recursively (getrf_blk) on a greatest-priority stream; then the same
+// stream applies the block's interchanges, TRSM and update to the NEXT block only, so that
+// block's factorization starts at once, while a least-priority stream applies the interchanges
+// to the columns left of the block and right of the next one and the rank-NBW update to the
+// trailing columns [p + 2 NBW, c1) (cmax as in getrf_rec).  The trailing GEMM of one block
+// (K = NBW) hides behind the next block's latency-bound panels.
+//   panel stream:    LU block k | wait T(k-1) | swaps+TRSM+GEMM on block k+1
+//   trailing stream: wait | swaps on [0, p) and [p + 2 NBW, cmax) | TRSM+GEMM on [p + 2 NBW, c1)
+// T(k-1) is waited for before block k+1 is touched: it wrote those columns.  The swap lists
+// alternate between two sets (T(k) reads set k while block k + 1 writes the other).
+void getrf_la(cudaStream_t st, double* A, int64_t n, int64_t c0, int64_t c1, int32_t* ipiv, DevStatus* status,
+              int block_index, int64_t cmax) {
+  if (c1 <= c0) return;
+  static const int64_t NBW = [] {
+    const char* e = getenv("SLB_GETRF_NBW");
+    const int v = e ? atoi(e) : 64;  // cfg3 stage two: 64 0.677 s, 128 0.685, 256 0.695 (recursive 0.720)
+    return (int64_t)std::min(std::max(PNB, v / PNB * PNB), MAXL * PNB);
+  }();
+  LaStreams& S = la_streams();
+  cudaStream_t sa = S.hi, sb = S.lo;
+  cudaEvent_t evP = S.ev[0], evB[2] = {S.ev[1], S.ev[2]}, evJ = S.ev[3];
+  SLB_CUDA_CHECK(cudaEventRecord(evJ, st));
+  SLB_CUDA_CHECK(cudaStreamWaitEvent(sa, evJ, 0));
+  SLB_CUDA_CHECK(cudaStreamWaitEvent(sb, evJ, 0));
+  const int64_t lset = (NBW / PNB) * SWL;
+  int32_t* swl = nullptr;
+  SLB_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&swl), 2 * lset * sizeof(int32_t), sa));
+  const int64_t nbk = cdiv(c1 - c0, NBW);
+  // SLB_GETRF_TRACE=1 (measurement): timed events per block, printed for a few blocks
+  static const bool trace = getenv("SLB_GETRF_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t s) {
+    if (!trace) return;
+    cudaEvent_t e;
+    SLB_CUDA_CHECK(cudaEventCreate(&e));
+    SLB_CUDA_CHECK(cudaEventRecord(e, s));
+    tev.push_back(e);
+  };
+  mark(sa);
+  for (int64_t k = 0; k < nbk; k++) {
+    const int64_t p = c0 + k * NBW;
+    const int64_t w = std::min(NBW, c1 - p);
+    const int nl = (int)cdiv(w, (int64_t)PNB);
+    const int64_t q = p + w;                                      // next block [q, q + wn)
+    const int64_t wn = std::max<int64_t>(0, std::min(NBW, c1 - q));
+    const int64_t r = q + wn;                                     // trailing columns [r, c1)
+    int32_t* ls = swl + (k & 1) * lset;
+    getrf_blk(sa, A, n, p, q, p, q, ipiv, status, block_index, ls);
+    mark(sa);
+    if (k > 0) SLB_CUDA_CHECK(cudaStreamWaitEvent(sa, evB[(k - 1) & 1], 0));
+    mark(sa);
+    SLB_CUDA_CHECK(cudaEventRecord(evP, sa));
+    SLB_CUDA_CHECK(cudaStreamWaitEvent(sb, evP, 0));
+    if (wn > 0) {
+      swaps_multi(sa, A, n, ls, nl, q, q + wn, 0, 0);
+      trsm(sa, true, A + p * n + p, n, w, A + q * n + p, n, wn);
+      dgemm_batched(sa, n - q, wn, w, -1.0, A + p * n + q, n, 0, A + q * n + p, n, 0, 1.0, A + q * n + q, n, 0, 1);
+    }
+    mark(sa);
+    swaps_multi(sb, A, n, ls, nl, 0, p, std::min(r, cmax), cmax);
+    if (r < c1) {
+      trsm(sb, true, A + p * n + p, n, w, A + r * n + p, n, c1 - r);
+      dgemm_batched(sb, n - q, c1 - r, w, -1.0, A + p * n + q, n, 0, A + r * n + p, n, 0, 1.0, A + r * n + q, n, 0, 1);
+    }
+    mark(sb);
+    SLB_CUDA_CHECK(cudaEventRecord(evB[k & 1], sb));
+  }
+  SLB_CUDA_CHECK(cudaStreamWaitEvent(sa, evB[(nbk - 1) & 1], 0));
+  SLB_CUDA_CHECK(cudaFreeAsync(swl, sa));
+  SLB_CUDA_CHECK(cudaEventRecord(evJ, sa));
+  SLB_CUDA_CHECK(cudaStreamWaitEvent(st, evJ, 0));
+  if (trace) {
+    // per block: LU end, T(k-1) wait end, next-block update end (sa), T(k) end (sb); us from the block start
+    SLB_CUDA_CHECK(cudaStreamSynchronize(st));
+    double sum[3] = {0, 0, 0};
+    for (int64_t k = 0; k < nbk; k++) {
+      float t[4];
+      cudaEvent_t e0 = tev[k == 0 ? 0 : 4 * k - 1];
+      for (int i = 0; i < 4; i++) SLB_CUDA_CHECK(cudaEventElapsedTime(&t[i], e0, tev[4 * k + 1 + i]));
+      sum[0] += t[0];
+      sum[1] += t[1] - t[0];
+      sum[2] += t[2] - t[1];
+      if (k % 8 == 0 || k == nbk - 1)
+        fprintf(stderr, "[getrf_la] block %lld: LU %.1f us, wait %.1f us, next-block update %.1f us; trailing done at %.1f us\n",
+                (long long)k, 1e3 * t[0], 1e3 * (t[1] - t[0]), 1e3 * (t[2] - t[1]), 1e3 * t[3]);
+    }
+    fprintf(stderr, "[getrf_la] n=%lld cols [%lld,%lld) NBW %lld: block LU %.2f ms, wait %.2f ms, next-block %.2f ms\n",
+            (long long)n, (long long)c0, (long long)c1, (long long)NBW, sum[0], sum[1], sum[2]);
+    for (auto e : tev) cudaEventDestroy(e);
+  }
+}
+
 }  // namespace
 
 void dgetrf(cudaStream_t st, int64_t n, double* a, int32_t* ipiv, double* /*work*/, DevStatus* status,
             int block_index) {
+  if (!panel_v1() && !getrf_rec_only()) {
+    getrf_la(st, a, n, 0, n, ipiv, status, block_index, n);
+    return;
+  }
   int32_t* swl = nullptr;  // swap list of the current panel (stream ordered, reused by every panel)
   SLB_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&swl), SWL * sizeof(int32_t), st));
   getrf_rec(st, a, n, 0, n, ipiv, status, block_index, swl, n);
@@ -795,6 +1036,17 @@ void dgetrf(cudaStream_t st, int64_t n, double* a, int32_t* ipiv, double* /*work
 void dgetrf_split(cudaStream_t st, int64_t n, double* a, int32_t* ipiv, DevStatus* status, int block_index,
                   int64_t h, cudaEvent_t right_ready) {
   h = std::min<int64_t>(round_up(std::max<int64_t>(h, PNB), PNB), n);
+  if (!panel_v1() && !getrf_rec_only()) {
+    getrf_la(st, a, n, 0, h, ipiv, status, block_index, h);
+    SLB_CUDA_CHECK(cudaStreamWaitEvent(st, right_ready, 0));
+    if (h < n) {
+      laswp(st, a, n, h, n, ipiv, 0, h, n);
+      trsm(st, true, a, n, h, a + h * n, n, n - h);
+      dgemm_batched(st, n - h, n - h, h, -1.0, a + h, n, 0, a + h * n, n, 0, 1.0, a + h * n + h, n, 0, 1);
+      getrf_la(st, a, n, h, n, ipiv, status, block_index, n);
+    }
+    return;
+  }
   int32_t* swl = nullptr;
   SLB_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&swl), SWL * sizeof(int32_t), st));
   getrf_rec(st, a, n, 0, h, ipiv, status, block_index, swl, h);

@@ -261,7 +261,8 @@ def test_backward_columns_match_full_operator(monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,nrhs", [(1, 1), (37, 3), (64, 1), (100, 8), (333, 2), (1000, 5), (4000, 1), (700, 12), (129, 16), (2000, 64)])
+@pytest.mark.parametrize("n,nrhs", [(1, 1), (37, 3), (64, 1), (100, 8), (333, 2), (1000, 5), (4000, 1), (700, 12), (129, 16), (2000, 64),
+                                    (257, 2), (4500, 2)])
 def test_stage_two_getrs_vs_numpy(n, nrhs):
     """The stage-two solve applies S_j^{-1} from its LU factors (stage_two.hpp:176-186,
     DenseLU::solve dense.hpp:48-61): chained getrs, 8-column chains (+ a remainder chain).
