@@ -539,11 +539,21 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
   if (tid == 0) s_sing = -1;
   const int init_rows = rows_total < NW ? rows_total : NW;
   // the window's first rows: asynchronous 8-byte copies (transposing gather), so every thread has
-  // many loads in flight instead of one load-store pair at a time
-  const float inv_ir = 1.0f / (float)init_rows, inv_wp = 1.0f / (float)Wp;
-  for (int idx = tid; idx < init_rows * Wp; idx += blockDim.x) {
-    const int j = qdiv(idx, inv_ir), p = idx - j * init_rows;
-    cp_async8(rowp(p) + j, p < Wp ? SV + (int64_t)j * Wp + p : NX + (int64_t)j * Wp + (p - Wp), true);
+  // many loads in flight instead of one load-store pair at a time.  The rows of level l + 1 (NX,
+  // extracted long before) are requested before the wait for the previous level's update (PDL).
+  const float inv_wp = 1.0f / (float)Wp;
+  if (init_rows > Wp) {
+    const int nxr = init_rows - Wp;
+    const float inv_n = 1.0f / (float)nxr;
+    for (int idx = tid; idx < nxr * Wp; idx += blockDim.x) {
+      const int j = qdiv(idx, inv_n), p = idx - j * nxr;
+      cp_async8(rowp(Wp + p) + j, NX + (int64_t)j * Wp + p, true);
+    }
+  }
+  pdl_wait();
+  for (int idx = tid; idx < Wp * Wp; idx += blockDim.x) {
+    const int j = qdiv(idx, inv_wp), p = idx - j * Wp;
+    cp_async8(rowp(p) + j, SV + (int64_t)j * Wp + p, true);
   }
   cp_async_commit();
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm[p] = p;
@@ -792,6 +802,7 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
     eb ^= 1;
   }
 
+  pdl_trigger();  // the level update may start launching (it waits for this grid's completion)
   int32_t* perm_out = a.perm + s * a.sP;
   for (int p = tid; p < 2 * Wp; p += blockDim.x) perm_out[p] = perm[p];
   {
@@ -920,7 +931,7 @@ void level_lu(cudaStream_t st, const LevelArgs& a) {
       SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_la_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
       attr2 = smem2;
     }
-    level_lu_la_kernel<<<a.nstrips, 512, smem2, st>>>(a); count_launch();
+    launch_pdl(level_lu_la_kernel, dim3(a.nstrips), dim3(512), smem2, st, a);
   }
   SLB_CUDA_CHECK(cudaGetLastError());
 }

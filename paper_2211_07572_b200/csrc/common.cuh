@@ -5,6 +5,8 @@
 // written for that pipe: m8n8k4 fragments, cp.async staging, padded shared
 // tiles (row stride == 4 mod 16 doubles so a fragment load is 2 wavefronts).
 #pragma once
+#include <cstdlib>
+#include <utility>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
@@ -64,6 +66,26 @@ namespace slb {
 // gpu_launches / solve_launches).
 extern std::atomic<long long> g_kernel_count;
 inline void count_launch() { g_kernel_count.fetch_add(1, std::memory_order_relaxed); }
+
+// Launch with programmatic stream serialization (the kernel may begin before the previous grid
+// of the stream completes; it calls pdl_wait() before reading that grid's results).
+// SLB_NO_PDL=1 launches it plainly.
+template <class... P, class... A>
+inline void launch_pdl(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  static const bool off = getenv("SLB_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = off ? 0 : 1;
+  SLB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...));
+  count_launch();
+}
 // ---- mbarrier + TMA bulk copy (cp.async.bulk) helpers ----------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
@@ -113,6 +135,11 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
 }
 // Distributed shared memory: address of `local` in CTA `rank` of the cluster, and 32-bit loads
 // through the shared::cluster window (cheaper than generic loads of a mapped pointer).
+// Programmatic dependent launch: wait for the preceding grid's completion (a no-op for a grid
+// launched without the attribute) / let the next grid of the stream start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t dsmem_map(const void* local, int rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));

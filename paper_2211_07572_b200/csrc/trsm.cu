@@ -296,6 +296,8 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs a) {
 #else
 #define UP(k_)
 #endif
+  pdl_wait();     // the level's LU (and, transitively, everything before it) is complete
+  pdl_trigger();  // the next level's LU may start launching
   stage_rows(LU11, 0, 0);
   cp_async_commit();
   const int ncol = min(TN, 2 * Wp - c0);
@@ -547,7 +549,7 @@ void level_update(cudaStream_t st, const LevelArgs& a) {
   // cfg3 1.9e-11 vs 5.3e-11 for version 2, which is 2.5 % faster); SLB_UPD_V2=1 selects version 2
   static const bool v1 = getenv("SLB_UPD_V2") == nullptr;
   if (v1) {
-    level_update_kernel<<<grid, 256, smem, st>>>(a); count_launch();
+    launch_pdl(level_update_kernel, grid, dim3(256), smem, st, a);
   } else {
     const size_t smem2 = (size_t)(MMAX * TN + 2 * MMAX * LCS + MMAX * RB) * sizeof(double) + 2 * MMAX * sizeof(int);
     static bool attr2 = false;
