@@ -468,9 +468,9 @@ void factor_S(slablu_gpu_fact* F, int j) {
 // The sweep over the interfaces [ia, ib) started fresh at ia: S_ia = T_{ia ia},
 // X_{j-1} = S_{j-1}^{-1} super_{j-1}, S_j = T_jj - sub_{j-1} X_{j-1}.
 //
-// Overlap: the LU of S_j factors its left half first; the right half of X_{j-1} and of S_j
-// (getrs + GEMM on columns [h, n2)) is computed meanwhile on a second stream, and the LU waits
-// for it only when it reaches those columns (dgetrf_split).  SLB_STAGE2_SERIAL=1 disables it.
+// Overlap: the LU of S_j factors its left part (columns [0, h), h = n2 / 5) first; the right part
+// of X_{j-1} and of S_j (getrs + GEMM on columns [h, n2)) is computed meanwhile on a second
+// stream, and the LU waits for it only when it reaches those columns (dgetrf_split).  SLB_STAGE2_SERIAL=1 disables it.
 void stage_two_range(slablu_gpu_fact* F, int ia, int ib) {
   cudaStream_t st = F->stream;
   const int64_t n2 = F->n2, bs = n2 * n2, dinv_sz = cdiv(n2, 64) * 2 * 64 * 64;
@@ -486,7 +486,15 @@ void stage_two_range(slablu_gpu_fact* F, int ia, int ib) {
     SLB_CUDA_CHECK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
     SLB_CUDA_CHECK(cudaEventCreateWithFlags(&ev_right, cudaEventDisableTiming));
   }
-  const int64_t h = round_up(n2 / 2, 32);
+  // split column of the overlap (SLB_S2_SPLIT: fraction of n2).  A narrow left part starts the
+  // LU early and leaves most of the getrs / GEMM to run beside it: cfg3 stage two 0.679 s at
+  // 0.5, 0.671 at 0.3, 0.650 at 0.2, 0.658 at 0.16, 0.678 at 0.1
+  static const double split = [] {
+    const char* e = getenv("SLB_S2_SPLIT");
+    const double v = e ? atof(e) : 0.2;
+    return v > 0.05 && v < 0.95 ? v : 0.2;
+  }();
+  const int64_t h = std::min(n2, round_up((int64_t)(split * (double)n2), 64));
   for (int j = ia; j < ib; j++) {
     if (j > ia) {
       double* X = F->Xup.p + (size_t)(j - 1) * bs;
