@@ -70,6 +70,23 @@ __device__ __forceinline__ void better(double& v, int& vi, double ov, int oi) {
   }
 }
 
+// Warp-wide first maximum of (v, vi) with three hardware reductions on the bit pattern of v
+// (non-negative doubles order like their bit patterns): the maximum v, ties to the smallest vi.
+// Candidates with v < 0 or NaN never win (key 0; a 0.0 maximum is the singular case anyway).
+// Returns the lanes holding the winner.
+__device__ __forceinline__ unsigned warp_argmax(double& v, int& vi) {
+  const unsigned long long key = (v >= 0.0) ? (unsigned long long)__double_as_longlong(v) : 0ull;
+  const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, khi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
+  const bool ismax = khi == mhi && klo == mlo;
+  const int mi = (int)__reduce_min_sync(0xffffffffu, ismax ? (unsigned)vi : 0x7fffffffu);
+  const unsigned who = __ballot_sync(0xffffffffu, ismax && vi == mi);
+  vi = mi;
+  v = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+  return who;
+}
+
 template <bool RELAXED>
 __global__ void __launch_bounds__(PTHREADS) panel_getrf_kernel(double* A, int64_t lda, int64_t n, int64_t j, int nb,
                                                                int32_t* ipiv, DevStatus* status, int block_index) {
@@ -301,8 +318,7 @@ __global__ void __launch_bounds__(PTHREADS) panel32_kernel(double* A, int64_t ld
 #pragma unroll
     for (int q = 0; q < RPT; q++)
       if (liveq[q]) better(v, vi, fabs(rr[q][0]), (int)iq[q]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) better(v, vi, __shfl_xor_sync(0xffffffffu, v, o), __shfl_xor_sync(0xffffffffu, vi, o));
+    warp_argmax(v, vi);
 #pragma unroll
     for (int q = 0; q < RPT; q++) {
       if (liveq[q] && iq[q] == vi)
@@ -319,23 +335,10 @@ __global__ void __launch_bounds__(PTHREADS) panel32_kernel(double* A, int64_t ld
     __syncthreads();
     PP(0)
     // (2) CTA winner (every warp, redundantly), then push to this warp's two destinations
-    int wb = lane < PNW ? lane : 0;
     v = lane < PNW ? s_wv[pb][lane] : -1.0;
     vi = lane < PNW ? s_wi[pb][lane] : INT_MAX;
-#pragma unroll
-    for (int o = PNW / 2; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
-      const int ob = __shfl_xor_sync(0xffffffffu, wb, o);
-      if (ov > v || (ov == v && oi < vi)) {
-        v = ov;
-        vi = oi;
-        wb = ob;
-      }
-    }
-    v = __shfl_sync(0xffffffffu, v, 0);
-    vi = __shfl_sync(0xffffffffu, vi, 0);
-    wb = __shfl_sync(0xffffffffu, wb, 0);
+    const unsigned wwho = warp_argmax(v, vi) & ((1u << PNW) - 1);
+    const int wb = wwho ? __ffs(wwho) - 1 : 0;  // the winning warp (its row is staged)
     {
       const uint32_t boff = (uint32_t)(pb * 8);
       const uint32_t roff = (uint32_t)(pb * 16 * PNB * 8);
@@ -360,26 +363,13 @@ __global__ void __launch_bounds__(PTHREADS) panel32_kernel(double* A, int64_t ld
     PP(2)
     // (4) resolve the pivot from the local copies
     double bv = -1.0;
-    int bi = INT_MAX, bc = 0;
+    int bi = INT_MAX;
     if (lane < ncta) {
       bv = s_rec[pb][lane][0];
       bi = (int)s_rec[pb][lane][1];
-      bc = lane;
     }
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {  // ncta <= 16
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-      if (ov > bv || (ov == bv && oi < bi)) {
-        bv = ov;
-        bi = oi;
-        bc = oc;
-      }
-    }
-    bv = __shfl_sync(0xffffffffu, bv, 0);
-    bi = __shfl_sync(0xffffffffu, bi, 0);
-    bc = __shfl_sync(0xffffffffu, bc, 0);
+    const unsigned cwho = warp_argmax(bv, bi) & (ncta >= 32 ? 0xffffffffu : ((1u << ncta) - 1));
+    int bc = cwho ? __ffs(cwho) - 1 : 0;  // the CTA holding the pivot row
     if (!(bv > 0.0)) {  // exactly singular column: no interchange
       bi = k;
       bc = 0;
@@ -394,7 +384,7 @@ __global__ void __launch_bounds__(PTHREADS) panel32_kernel(double* A, int64_t ld
     }
     const double* prow = (bi == k) ? s_krow[pb] : s_row[pb][bc];
     const double pv = prow[0];
-    const double pinv = pv != 0.0 ? 1.0 / pv : 0.0;
+    const double pinv = pv != 0.0 ? __drcp_rn(pv) : 0.0;  // == 1.0 / pv (both correctly rounded)
 #pragma unroll
     for (int q = 0; q < RPT; q++) {
       if (!liveq[q]) continue;
