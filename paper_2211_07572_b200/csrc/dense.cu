@@ -378,19 +378,23 @@ __global__ void __launch_bounds__(PTHREADS) panel32_kernel(double* A, int64_t ld
         atomicMin(&status->singular_block, block_index);
       }
     }
-    if (tid == 0 && rank == 0) {
-      ipiv[j + k] = (int32_t)(j + bi);
-      s_piv[k] = bi;
-    }
     const double* prow = (bi == k) ? s_krow[pb] : s_row[pb][bc];
+    // bookkeeping on CTA 0's last warp (warp 0 holds the panel's own rows and is the busiest):
+    // the pivot index, and row k retiring as the U row = the pivot row (shifted: r[c] = column
+    // k + c), one element per lane
+    if (rank == 0 && warp == PNW - 1) {
+      if (lane == 0) {
+        ipiv[j + k] = (int32_t)(j + bi);
+        s_piv[k] = bi;
+      }
+      s_urow[k][lane] = prow[lane];  // PNB == 32
+    }
     const double pv = prow[0];
     const double pinv = pv != 0.0 ? __drcp_rn(pv) : 0.0;  // == 1.0 / pv (both correctly rounded)
 #pragma unroll
     for (int q = 0; q < RPT; q++) {
       if (!liveq[q]) continue;
-      if (iq[q] == k) {  // row k retires as the U row: the pivot row (shifted: r[c] = column k + c)
-#pragma unroll
-        for (int c = 0; c < PNB; c++) s_urow[k][c] = prow[c];
+      if (iq[q] == k) {  // row k retires (copied to s_urow above)
       } else {
         if (iq[q] == bi && bi != k)
 #pragma unroll
