@@ -759,6 +759,12 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
     }
   };
 
+#ifdef SLB_LU_PROF
+  long long Q0 = clock64(), lq[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define LQ(k_) { const long long q_ = clock64(); lq[k_] += q_ - Q0; Q0 = q_; }
+#else
+#define LQ(k_)
+#endif
   if (8 < Wp) {
     prefetch(8, 0);
     cp_async_wait<1>();  // the window (the entering rows of block 8 may still be in flight)
@@ -766,12 +772,14 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
     cp_async_wait<0>();
   }
   __syncthreads();
+  LQ(0)
   if (warp < PW) panel(0, nullptr);  // block 0: every row is in the window
   __syncthreads();
   swaps(0);
   __syncthreads();
   ublock(0);
   __syncthreads();
+  LQ(1)
   int eb = 0;
   for (int kb = 0; kb < Wp; kb += 8) {
     const int kend = kb + 8;
@@ -779,12 +787,15 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
     if (more) trailing(kb, kend, kend + 8, 0, nwarps);  // X
     cp_async_wait<0>();
     __syncthreads();
+    LQ(2)
     if (warp < PW) {  // Y
       if (more) panel(kend, ent + eb * 8 * Wp);
     } else {
       trailing(kb, more ? kend + 8 : kend, Wp, PW, nwarps - PW);
     }
+    LQ(3)
     __syncthreads();
+    LQ(4)
     for (int idx = tid; idx < 8 * Wp; idx += blockDim.x) {  // R
       const int q = qdiv(idx, inv_wp), j = idx - q * Wp;
       double* rr = rowp(kb + q);
@@ -792,6 +803,7 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
       if (kend + Wp + q < rows_total) rr[j] = ent[eb * 8 * Wp + idx];
     }
     __syncthreads();
+    LQ(5)
     if (more) {
       if (kend + 8 < Wp) prefetch(kend + 8, eb ^ 1);
       swaps(kend);  // S
@@ -799,8 +811,14 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
       ublock(kend);  // U
       __syncthreads();
     }
+    LQ(6)
     eb ^= 1;
   }
+#ifdef SLB_LU_PROF
+  if ((tid == 0 || tid == 511) && s == 0 && (a.level % 1000) == 1)
+    printf("LEVEL_LU_LA l=%d tid %d: prologue %lld block0 %lld X %lld Y %lld Ywait %lld R %lld SU %lld (cycles)\n", a.level,
+           tid, lq[0], lq[1], lq[2], lq[3], lq[4], lq[5], lq[6]);
+#endif
 
   pdl_trigger();  // the level update may start launching (it waits for this grid's completion)
   int32_t* perm_out = a.perm + s * a.sP;
