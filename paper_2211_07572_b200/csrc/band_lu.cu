@@ -781,6 +781,10 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
   __syncthreads();
   LQ(1)
   int eb = 0;
+  // first warp of the trailing update beside the panel: 8 of the 12 non-panel warps suffice
+  // (trailing ~81k vs panel ~147k cycles per level) and leave the panel warps more issue slots
+  // on their SMSPs: cfg3 chain 0.823 -> 0.816 s (SLB_LU_TW0 overrides, measurement)
+  const int tw0 = a.tw0 > PW ? a.tw0 : 8;
   for (int kb = 0; kb < Wp; kb += 8) {
     const int kend = kb + 8;
     const bool more = kend < Wp;
@@ -790,8 +794,8 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
     LQ(2)
     if (warp < PW) {  // Y
       if (more) panel(kend, ent + eb * 8 * Wp);
-    } else {
-      trailing(kb, more ? kend + 8 : kend, Wp, PW, nwarps - PW);
+    } else if (warp >= tw0) {
+      trailing(kb, more ? kend + 8 : kend, Wp, tw0, nwarps - tw0);
     }
     LQ(3)
     __syncthreads();
@@ -949,7 +953,10 @@ void level_lu(cudaStream_t st, const LevelArgs& a) {
       SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_la_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
       attr2 = smem2;
     }
-    launch_pdl(level_lu_la_kernel, dim3(a.nstrips), dim3(512), smem2, st, a);
+    static const int tw0 = getenv("SLB_LU_TW0") ? atoi(getenv("SLB_LU_TW0")) : 0;
+    LevelArgs a2 = a;
+    a2.tw0 = tw0;
+    launch_pdl(level_lu_la_kernel, dim3(a.nstrips), dim3(512), smem2, st, a2);
   }
   SLB_CUDA_CHECK(cudaGetLastError());
 }

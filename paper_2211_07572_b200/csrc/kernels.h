@@ -87,6 +87,7 @@ struct LevelArgs {
   const uint8_t* lnd;    // Lsub_{l+1} off-diagonal flag (per strip stride n2), level l+1
   DevStatus* status;
   int32_t level;
+  int tw0 = 0;  // measurement knob of level_lu_la_kernel (first trailing warp beside the panel)
 };
 void level_lu(cudaStream_t st, const LevelArgs& a);
 // U1213 = L11^{-1} R1 and [S|V]_{l+1} = R2 - L21 U1213 in one launch (trsm.cu).
