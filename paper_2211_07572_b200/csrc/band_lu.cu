@@ -800,21 +800,55 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
     LQ(3)
     __syncthreads();
     LQ(4)
-    for (int idx = tid; idx < 8 * Wp; idx += blockDim.x) {  // R
-      const int q = qdiv(idx, inv_wp), j = idx - q * Wp;
-      double* rr = rowp(kb + q);
-      LU11[(int64_t)(kb + q) * Wp + j] = rr[j];
-      if (kend + Wp + q < rows_total) rr[j] = ent[eb * 8 * Wp + idx];
+    if (more && kend + 8 < Wp) prefetch(kend + 8, eb ^ 1);
+    // R, S and U fused per column (one thread per column, no barrier between them): rows
+    // kb..kb+7 retire and the entering rows take their slots (R); panel kend's interchanges (S)
+    // and its U block (U) on the column.  Column j touches only column j of the window, and
+    // reads the panel's L values, final since the barrier above.
+    if (more && tid == blockDim.x - 1)
+      for (int q = 0; q < 8; q++) {  // pivot-order bookkeeping of panel kend
+        const int c = kend + q, r = s_piv[q];
+        if (r != c) {
+          const int tp = perm[c];
+          perm[c] = perm[r];
+          perm[r] = tp;
+        }
+      }
+    for (int j = tid; j < Wp; j += blockDim.x) {
+#pragma unroll
+      for (int q = 0; q < 8; q++) {  // R
+        double* rr = rowp(kb + q);
+        LU11[(int64_t)(kb + q) * Wp + j] = rr[j];
+        if (kend + Wp + q < rows_total) rr[j] = ent[eb * 8 * Wp + q * Wp + j];
+      }
+      if (!more || (j >= kend && j < kend + 8)) continue;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {  // S
+        const int c = kend + q, r = s_piv[q];
+        if (r != c) {
+          double* rc = rowp(c);
+          double* rw = rowp(r);
+          const double tv = rc[j];
+          rc[j] = rw[j];
+          rw[j] = tv;
+        }
+      }
+      if (j < kend + 8) continue;
+      double u[8];  // U
+#pragma unroll
+      for (int q = 0; q < 8; q++) u[q] = rowp(kend + q)[j];
+#pragma unroll
+      for (int q = 1; q < 8; q++) {
+        const double* lq = rowp(kend + q);
+#pragma unroll
+        for (int p2 = 0; p2 < 8; p2++)
+          if (p2 < q) u[q] = fma(-lq[kend + p2], u[p2], u[q]);
+      }
+#pragma unroll
+      for (int q = 1; q < 8; q++) rowp(kend + q)[j] = u[q];
     }
     __syncthreads();
     LQ(5)
-    if (more) {
-      if (kend + 8 < Wp) prefetch(kend + 8, eb ^ 1);
-      swaps(kend);  // S
-      __syncthreads();
-      ublock(kend);  // U
-      __syncthreads();
-    }
     LQ(6)
     eb ^= 1;
   }
