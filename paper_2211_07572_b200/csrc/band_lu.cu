@@ -511,6 +511,7 @@ __global__ void __launch_bounds__(512) level_lu_kernel(LevelArgs a) {
 //   R  rows kb..kb+7 retire to LU11, the entering rows take their physical rows
 //   S  panel kb+8's interchanges on the other columns;  U  its U block
 // so the serial pivot search of panel kb+8 runs beside the DMMA update of block kb.
+template <int PW>  // warps factoring the panel: 4 (two rows per lane) or 2 (three rows per lane)
 __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
   extern __shared__ double smem[];
   const int Wp = a.Wp, NW = Wp + 8;
@@ -521,7 +522,7 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
   int* perm = reinterpret_cast<int*>(ent + 16 * Wp);
   __shared__ int s_sing;
   __shared__ int s_piv[8];
-  constexpr int PW = 4, NT = PW * 32, RPL = 2;
+  constexpr int NT = PW * 32, RPL = PW == 4 ? 2 : 3;  // NT * RPL >= Wp + 8 (Wp <= 160)
 
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -783,8 +784,9 @@ __global__ void __launch_bounds__(512) level_lu_la_kernel(LevelArgs a) {
   int eb = 0;
   // first warp of the trailing update beside the panel: 8 of the 12 non-panel warps suffice
   // (trailing ~81k vs panel ~147k cycles per level) and leave the panel warps more issue slots
-  // on their SMSPs: cfg3 chain 0.823 -> 0.816 s (SLB_LU_TW0 overrides, measurement)
-  const int tw0 = a.tw0 > PW ? a.tw0 : 8;
+  // on their SMSPs: cfg3 chain 0.823 -> 0.816 s; with two panel warps, 10 trailing warps
+  // (SLB_LU_TW0 overrides, measurement)
+  const int tw0 = a.tw0 > PW ? a.tw0 : (PW == 2 ? 6 : 8);
   for (int kb = 0; kb < Wp; kb += 8) {
     const int kend = kb + 8;
     const bool more = kend < Wp;
@@ -984,13 +986,18 @@ void level_lu(cudaStream_t st, const LevelArgs& a) {
     const size_t smem2 = (size_t)((Wp + 8) * RS + 32 + 16 * Wp) * sizeof(double) + 2 * Wp * sizeof(int);
     static size_t attr2 = 0;
     if (smem2 > attr2) {
-      SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_la_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_la_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      SLB_CUDA_CHECK(cudaFuncSetAttribute(level_lu_la_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
       attr2 = smem2;
     }
     static const int tw0 = getenv("SLB_LU_TW0") ? atoi(getenv("SLB_LU_TW0")) : 0;
     LevelArgs a2 = a;
     a2.tw0 = tw0;
-    launch_pdl(level_lu_la_kernel, dim3(a.nstrips), dim3(512), smem2, st, a2);
+    // two panel warps with three rows per lane (cfg3 chain 0.793 -> 0.789 s; the per-column
+    // critical path barely depends on the panel's warp count), SLB_LU_PW=4 selects four
+    static const int pw = getenv("SLB_LU_PW") ? atoi(getenv("SLB_LU_PW")) : 2;
+    if (pw == 2) launch_pdl(level_lu_la_kernel<2>, dim3(a.nstrips), dim3(512), smem2, st, a2);
+    else launch_pdl(level_lu_la_kernel<4>, dim3(a.nstrips), dim3(512), smem2, st, a2);
   }
   SLB_CUDA_CHECK(cudaGetLastError());
 }
