@@ -749,7 +749,10 @@ slablu_gpu_fact* factorize_impl(int64_t n1, int64_t n2, int64_t nnz, const int32
   init_sv(st, S, Wp, nx.p, sNX, svb[0], sSV);
   // LU-form -> GEMM-form conversion runs behind the chain on a low-priority
   // stream, one chunk of CCH levels at a time (idle SMs during the chain).
-  const int64_t CCH = std::min<int64_t>(n2, 256);
+  // levels per conversion chunk (SLB_CONV_CHUNK, measurement): cfg3 chain 0.835 / 0.794 / 0.781 /
+  // 0.787 / 0.812 s at 64 / 96 / 128 / 256 / 512
+  static const int64_t cch_env = getenv("SLB_CONV_CHUNK") ? atoi(getenv("SLB_CONV_CHUNK")) : 128;
+  const int64_t CCH = std::min<int64_t>(n2, std::max<int64_t>(64, cch_env));
   // conversion stream: a green-context partition that leaves the chain (one CTA per strip)
   // SMs of its own (SLB_NO_GREEN=1 disables; SLB_GREEN_SMS sets the partition), else a
   // least-priority stream.  cfg3: chain phase 0.981 -> 0.959 s with 120 of 148 SMs for the
