@@ -6,7 +6,7 @@ echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
 python bench.py > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
 python bench.py --config cfg4 --no-cpu > gpurun_out/bench_cfg4.json 2> gpurun_out/bench_cfg4.err
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 40000 --csv --log-file gpurun_out/launches.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 50000 --csv --log-file gpurun_out/launches.csv \
     python tools/profile_factor.py --config cfg3 --solve > gpurun_out/ncu_launch.log 2>&1
 python -m pytest tests/test_gpu_scale_parity.py tests/test_gpu_hbs.py -q -s > gpurun_out/scale_parity.txt 2>&1
 python tools/hbs_bench.py poisson1000_b60 helm1000_10ppw poisson2000 helm2000_10ppw > gpurun_out/hbs_bench.txt 2>&1
